@@ -1,0 +1,162 @@
+"""Seeded synthetic inputs for DPG record retrieval (shared by both sides).
+
+Holds none of the method's arithmetic: only record bytes, rid sequences and
+foreign keys, produced by the counter-based generators of ``datagen/gen.c``
+(reading A12 in DESIGN.md).  Seeds are 0 everywhere (reading A13); every
+array has its own stream id, listed in :data:`STREAMS` and echoed in the
+bench JSON.
+
+Workloads (BASELINE.json ``configs``):
+
+* ``c1``  65,536 x 100 B, rids = uniform random permutation (uint32)
+* ``c2``  1,048,576 x 100 B Datamation-shaped records (10-byte key at offset 0
+  ++ 90-byte payload, all random bytes); rids = stable argsort of the keys
+  (ties by ascending rid, reading A10) -- the sort's phase 3
+* ``c3a`` 16,777,216 x rec, rec in {8,16,32,64,128,256}, rids = permutation
+* ``c3b`` same, rids iid uniform with replacement
+* ``c4``  dimension 16,777,216 x 64 B; fact 67,108,864 x (uint32 fk uniform in
+  [0, 2^24) ++ 16-byte payload) -- the DPG-Move join
+* ``c5``  2^30 x 100 B, rids = Feistel permutation (uint64), evaluated pointwise
+
+These synthetic inputs stand in for the paper's workloads (Datamation
+benchmark records, the record-size sweep, uniform foreign keys); no benchmark
+item or dataset is reproduced.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gen.c")
+_LIB = os.path.join(_HERE, "libdpggen.so")
+_lib = None
+
+SEED = 0
+# stream ids: (config, array) -> sid
+STREAMS = {
+    ("c1", "src"): 0x101, ("c1", "rids"): 0x102,
+    ("c2", "src"): 0x201,
+    ("c3", "src"): 0x301, ("c3a", "rids"): 0x302, ("c3b", "rids"): 0x303,
+    ("c4", "dim"): 0x401, ("c4", "fact"): 0x402, ("c4", "fk"): 0x403,
+    ("c5", "src"): 0x501, ("c5", "rids"): 0x502,
+    ("test", "src"): 0x901, ("test", "rids"): 0x902,
+}
+
+C3_RECS = (8, 16, 32, 64, 128, 256)
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-std=c11", "-fopenmp", "-shared", "-fPIC",
+                               _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        U, P = ctypes.c_uint64, ctypes.c_void_p
+        lib.gen_word.argtypes = [U, U, U]
+        lib.gen_word.restype = U
+        lib.gen_bytes.argtypes = [U, U, U, U, P]
+        lib.gen_permutation_u32.argtypes = [U, U, U, P]
+        lib.gen_uniform_u32.argtypes = [U, U, U, U, P]
+        lib.gen_feistel_u64.argtypes = [U, U, ctypes.c_uint, ctypes.c_uint, U, U, U, P]
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def word(sid: int, k: int, seed: int = SEED) -> int:
+    return int(_load().gen_word(seed, sid, k))
+
+
+def random_bytes(n: int, sid: int, seed: int = SEED, offset: int = 0, out=None) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint8) if out is None else out
+    assert out.dtype == np.uint8 and out.flags.c_contiguous and out.size == n
+    _load().gen_bytes(seed, sid, offset, n, _p(out))
+    return out
+
+
+def records(n: int, rec: int, sid: int, seed: int = SEED, out=None) -> np.ndarray:
+    """n records of rec uniformly random bytes: uint8 [n, rec]."""
+    flat = random_bytes(n * rec, sid, seed, out=None if out is None else out.reshape(-1))
+    return flat.reshape(n, rec)
+
+
+def permutation(n: int, sid: int, seed: int = SEED) -> np.ndarray:
+    """Uniformly random permutation of [0, n) as uint32 (Fisher-Yates)."""
+    assert n < 2 ** 32
+    out = np.empty(n, dtype=np.uint32)
+    _load().gen_permutation_u32(seed, sid, n, _p(out))
+    return out
+
+
+def uniform(n: int, bound: int, sid: int, seed: int = SEED) -> np.ndarray:
+    """n iid uniform draws in [0, bound) as uint32 (with replacement)."""
+    assert 0 < bound <= 2 ** 32
+    out = np.empty(n, dtype=np.uint32)
+    _load().gen_uniform_u32(seed, sid, n, bound, _p(out))
+    return out
+
+
+def feistel(n: int, first: int, count: int, sid: int, seed: int = SEED,
+            rounds: int = 6) -> np.ndarray:
+    """Elements [first, first+count) of a keyed Feistel permutation of [0, n), uint64."""
+    bits = max(2, (n - 1).bit_length())
+    bits += bits & 1
+    out = np.empty(count, dtype=np.uint64)
+    _load().gen_feistel_u64(seed, sid, bits, rounds, n, first, count, _p(out))
+    return out
+
+
+def stable_key_argsort(recs: np.ndarray, key_len: int = 10) -> np.ndarray:
+    """Stable argsort of the records' key bytes (offset 0, unsigned
+    lexicographic), ties by ascending rid (reading A10).  Part of the input
+    generator for config 2: the sort's phases 1-2 are not the
+    retrieval path; only their result (the rid sequence) is an input."""
+    assert key_len <= 10
+    keys = np.zeros((recs.shape[0], 10), dtype=np.uint8)
+    keys[:, :key_len] = recs[:, :key_len]
+    hi = keys[:, :8].copy().view(">u8").reshape(-1)
+    lo = keys[:, 8:10].copy().view(">u2").reshape(-1)
+    return np.lexsort((lo, hi)).astype(np.uint32)
+
+
+def make(config: str, rec: int | None = None, scale: int = 1) -> dict:
+    """Build a named workload.  ``scale`` > 1 divides the sizes (tests)."""
+    if config == "c1":
+        n = 65536 // scale
+        return {"src": records(n, 100, STREAMS[("c1", "src")]),
+                "rids": permutation(n, STREAMS[("c1", "rids")])}
+    if config == "c2":
+        n = 1048576 // scale
+        src = records(n, 100, STREAMS[("c2", "src")])
+        return {"src": src, "rids": stable_key_argsort(src, 10)}
+    if config in ("c3a", "c3b"):
+        assert rec in C3_RECS
+        n = 16777216 // scale
+        src = records(n, rec, STREAMS[("c3", "src")])
+        if config == "c3a":
+            rids = permutation(n, STREAMS[("c3a", "rids")])
+        else:
+            rids = uniform(n, n, STREAMS[("c3b", "rids")])
+        return {"src": src, "rids": rids}
+    if config == "c4":
+        n_dim = 16777216 // scale
+        n_fact = 67108864 // scale
+        return {"dim": records(n_dim, 64, STREAMS[("c4", "dim")]),
+                "fact": records(n_fact, 16, STREAMS[("c4", "fact")]),
+                "fk": uniform(n_fact, n_dim, STREAMS[("c4", "fk")])}
+    raise KeyError(config)

@@ -1,0 +1,200 @@
+/*
+ * oracle/oracle.c -- CPU ORACLE for DPG record retrieval (arXiv cs/0308004).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load, call or execute
+ * anything under oracle/.  The product path (paper_cs_0308004_b200/) never
+ * does, and shares no code, header, table or helper with this file.
+ *
+ * Everything here is plain, slow, single-threaded C with no blocking, fusion
+ * or reordering beyond what the cited passage states.  Citations:
+ *   P:n  = /root/reference/PAPER.md line n (LaTeX body of the paper)
+ *   S:n  = /root/reference/SPEC.md line n   (interfaces / test ideas only)
+ *
+ * Pins (tests/test_oracle.py, run with -m "not gpu"): the Fig. 2 worked
+ * example (golden fixture tests/golden/fig2_example.txt),
+ * brute force over all permutations n<=6 via an independent inverse-scatter
+ * formulation, all rid sequences of length <= 4 over n <= 3 against numpy
+ * fancy indexing, identity / multiset / sorted-key invariants, the join's
+ * nested-loop cross-check.  No function here is "parity unpinned".
+ *
+ * Return convention (reading A6 of DESIGN.md): 0 on success; -1 on an invalid
+ * argument; 1 if some rid >= n_src, in which case *bad_index receives the
+ * SMALLEST offending position i and dst row i is left unwritten (every other
+ * row is still written).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ *
+ * (1) The record-retrieval problem, by definition:             *
+ *         for each i,  D[i] = R[S_rid[i]]                                   *
+ *     with records of rec bytes laid out back to back and rids    *
+ *     dense, 0-based, in [0, n_src) (reading A2).                *
+ * ------------------------------------------------------------------------ */
+int oracle_retrieve(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                    const uint32_t *rids, uint64_t n_out, uint8_t *dst,
+                    uint64_t *bad_index)
+{
+    int status = 0;
+    if (rec == 0) return -1;
+    for (uint64_t i = 0; i < n_out; ++i) {
+        uint64_t r = rids[i];
+        if (r >= n_src) {
+            if (status == 0) { status = 1; if (bad_index) *bad_index = i; }
+            continue;
+        }
+        memcpy(dst + i * rec, src + r * rec, rec);
+    }
+    return status;
+}
+
+/* Same definition with 64-bit rids (the multi-GPU configuration uses them). */
+int oracle_retrieve_u64(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                        const uint64_t *rids, uint64_t n_out, uint8_t *dst,
+                        uint64_t *bad_index)
+{
+    int status = 0;
+    if (rec == 0) return -1;
+    for (uint64_t i = 0; i < n_out; ++i) {
+        uint64_t r = rids[i];
+        if (r >= n_src) {
+            if (status == 0) { status = 1; if (bad_index) *bad_index = i; }
+            continue;
+        }
+        memcpy(dst + i * rec, src + r * rec, rec);
+    }
+    return status;
+}
+
+/* ------------------------------------------------------------------------ *
+ * (2) The DPG algorithm exactly as Fig. 1 writes it, in the     *
+ *     paper's order and notation, with INTERNAL (RECORD_RUN) materialised.  *
+ *     Used to pin the intermediates of the method (RID runs, INTERNAL runs) *
+ *     and to show that the three phases reach the definition (1).           *
+ *                                                                          *
+ *     L      run length in records.  Fig. 1 sets L from the     *
+ *            cache size; here it is a parameter (reading A3).      *
+ *     run of rid r = floor(r / L) (0-based; Fig. 1 writes ceil(r/L) with    *
+ *            1-based runs, reading A1).                             *
+ *                                                                          *
+ *   Optional outputs (any may be NULL):                                     *
+ *     run_start[NUM_RUNS+1]  offsets of each RID run inside rid_runs        *
+ *     rid_runs[n_out]        RID_RUN[0] ++ RID_RUN[1] ++ ...       *
+ *     rid_pos[n_out]         for each entry of rid_runs, the position i in  *
+ *                            RID it came from (the "i-th step" of P:313)    *
+ *     record_runs[n_out*rec] RECORD_RUN[0] ++ ... = INTERNAL        *
+ *   Sizes: NUM_RUNS = ceil(n_src / L).  INTERNAL holds n_out records        *
+ *   (reading A4: "same size as the data file" only for permutations).      *
+ * ------------------------------------------------------------------------ */
+int oracle_dpg_fig1(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                    const uint32_t *rids, uint64_t n_out, uint64_t L,
+                    uint8_t *dst, uint64_t *run_start_out,
+                    uint32_t *rid_runs_out, uint64_t *rid_pos_out,
+                    uint8_t *record_runs_out, uint64_t *bad_index)
+{
+    if (rec == 0 || L == 0) return -1;
+    /* Range check first (reading A6): the paper assumes valid rids. */
+    for (uint64_t i = 0; i < n_out; ++i) {
+        if ((uint64_t)rids[i] >= n_src) { if (bad_index) *bad_index = i; return 1; }
+    }
+    uint64_t num_runs = (n_src + L - 1) / L;          /* NUM_RUNS <- N/L */
+    uint64_t *run_len = calloc(num_runs + 1, sizeof(uint64_t));
+    uint64_t *run_start = calloc(num_runs + 1, sizeof(uint64_t));
+    uint64_t *cursor = calloc(num_runs + 1, sizeof(uint64_t));
+    uint32_t *RID_RUN = malloc((n_out ? n_out : 1) * sizeof(uint32_t));
+    uint64_t *RID_POS = malloc((n_out ? n_out : 1) * sizeof(uint64_t));
+    uint8_t *RECORD_RUN = malloc((n_out ? n_out : 1) * rec);
+    if (!run_len || !run_start || !cursor || !RID_RUN || !RID_POS || !RECORD_RUN) {
+        free(run_len); free(run_start); free(cursor); free(RID_RUN); free(RID_POS); free(RECORD_RUN);
+        return -1;
+    }
+    /* The runs are growable lists in Fig. 1 ("Append r to RID_RUN[run_num]");
+     * they are stored back to back here, sized by a counting pass. */
+    for (uint64_t i = 0; i < n_out; ++i) run_len[rids[i] / L] += 1;
+    for (uint64_t b = 0; b < num_runs; ++b) run_start[b + 1] = run_start[b] + run_len[b];
+
+    /* Phase I: Distribute RID array into runs. */
+    for (uint64_t b = 0; b < num_runs; ++b) cursor[b] = run_start[b];
+    for (uint64_t i = 0; i < n_out; ++i) {
+        uint32_t r = rids[i];
+        uint64_t run_num = r / L;                      /* run_num = ceil(r/L), 1-based */
+        RID_RUN[cursor[run_num]] = r;                  /* Append r to RID_RUN[run_num] */
+        RID_POS[cursor[run_num]] = i;
+        cursor[run_num] += 1;
+    }
+
+    /* Phase II: Probe partitions of INPUT_REC.  Run i of INPUT is
+     * records [(i-1)L+1, iL] in 1-based notation = [iL, (i+1)L) 0-based. */
+    for (uint64_t i = 0; i < num_runs; ++i) {
+        const uint8_t *input_run = src + i * L * rec;  /* "Read into memory all records" */
+        uint64_t out = run_start[i];                   /* RECORD_RUN[i] */
+        for (uint64_t j = run_start[i]; j < run_start[i + 1]; ++j) {
+            uint32_t r = RID_RUN[j];                   /* For each rid r in RID_RUN[i] */
+            memcpy(RECORD_RUN + out * rec,             /* Append INPUT_REC[r] to RECORD_RUN[i] */
+                   input_run + (r - i * L) * rec, rec);
+            out += 1;
+        }
+    }
+
+    /* Phase III: Gather records from RECORD_RUN[] into OUTPUT_REC in the same
+     * order as RID[]: read the NEXT record of run floor(r/L). */
+    for (uint64_t b = 0; b < num_runs; ++b) cursor[b] = run_start[b];
+    for (uint64_t i = 0; i < n_out; ++i) {
+        uint32_t r = rids[i];
+        uint64_t run_num = r / L;
+        memcpy(dst + i * rec, RECORD_RUN + cursor[run_num] * rec, rec);
+        cursor[run_num] += 1;
+    }
+
+    if (run_start_out) memcpy(run_start_out, run_start, (num_runs + 1) * sizeof(uint64_t));
+    if (rid_runs_out) memcpy(rid_runs_out, RID_RUN, n_out * sizeof(uint32_t));
+    if (rid_pos_out) memcpy(rid_pos_out, RID_POS, n_out * sizeof(uint64_t));
+    if (record_runs_out) memcpy(record_runs_out, RECORD_RUN, n_out * rec);
+    free(run_len); free(run_start); free(cursor); free(RID_RUN); free(RID_POS); free(RECORD_RUN);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ *
+ * (3) DPG-Move foreign-key join, with the join triple  *
+ *     (k, rid_R, rid_F) of P:565-567.  The fact relation R is scanned in    *
+ *     file order, so rid_R = i; the foreign key k names the     *
+ *     dimension record directly (dense key, reading A11), so rid_F = fk[i]. *
+ *     Output row i = R-part ++ F[rid_F] ("join the temporary file with the  *
+ *     remaining relation"): fact payload (fact_bytes) followed   *
+ *     by the dimension record (rec bytes), in fact order.                   *
+ * ------------------------------------------------------------------------ */
+int oracle_fk_join(const uint8_t *fact, uint64_t fact_bytes, uint64_t n_fact,
+                   const uint32_t *fk, const uint8_t *dim, uint64_t rec,
+                   uint64_t n_dim, uint8_t *out, uint64_t *bad_index)
+{
+    int status = 0;
+    if (rec == 0) return -1;
+    uint64_t row = fact_bytes + rec;
+    for (uint64_t i = 0; i < n_fact; ++i) {
+        uint64_t rid_F = fk[i];
+        if (rid_F >= n_dim) {                          /* referential integrity */
+            if (status == 0) { status = 1; if (bad_index) *bad_index = i; }
+            continue;
+        }
+        memcpy(out + i * row, fact + i * fact_bytes, fact_bytes);
+        memcpy(out + i * row + fact_bytes, dim + rid_F * rec, rec);
+    }
+    return status;
+}
+
+/* Sampled oracle: the definition evaluated at selected output positions only
+ * (for parity at full sizes, where the whole output is large). out row j is
+ * D[idx[j]]. */
+int oracle_retrieve_at(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                       const uint32_t *rids, const uint64_t *idx, uint64_t n_idx,
+                       uint8_t *out)
+{
+    for (uint64_t j = 0; j < n_idx; ++j) {
+        uint64_t r = rids[idx[j]];
+        if (r >= n_src) return 1;
+        memcpy(out + j * rec, src + r * rec, rec);
+    }
+    return 0;
+}
