@@ -1,0 +1,406 @@
+#!/usr/bin/env python3
+"""Benchmark of the DPG record-retrieval hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dpg|reference]
+                    [--config c2] [--rec R]
+
+One step = one pass of the whole hot path (plan,
+distribute, fused probe+gather) over one batch of synthetic input already
+resident in HBM: dpg_retrieve on BASELINE.json configs[1] (Datamation-shaped
+sort phase 3, 1,048,576 x 100-byte records, rids = stable argsort of the
+10-byte keys).  L2 is flushed (a 512 MiB write) before every timed step and
+each step is timed alone with CUDA events on the launching stream; flush time
+is excluded.  Multi-process (torchrun, N > 1): every rank runs its own
+replica of the workload ("replicas", weak scaling) and the job time is the max
+over ranks.
+
+The JSON line adds: roofline of the dominant kernel (k_probe_gather) from its
+own CUDA-event time inside the same timed steps, the naive direct-gather
+comparison timed the same way, the end-to-end number through the host-buffer
+C-ABI entry, the oracle's CPU throughput (cpu_baseline) and the SM clocks
+sampled during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "record-retrieval effective GB/s vs HBM peak; records/s at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dpg", choices=["dpg", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3a", "c3b", "c4"])
+    ap.add_argument("--rec", type=int, default=None, help="record bytes for c3a/c3b")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(cfg: str, rec: int | None) -> str:
+    return {"c1": "c1: 65,536 x 100 B random records, uniform random permutation",
+            "c2": "c2: Datamation sort phase 3, 1,048,576 x 100 B, rids = stable argsort of 10-B keys",
+            "c3a": f"c3a: 16,777,216 x {rec} B, uniform random permutation",
+            "c3b": f"c3b: 16,777,216 x {rec} B, uniform rids with replacement",
+            "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)"}[cfg]
+
+
+def make_inputs(cfg: str, rec: int | None):
+    import datagen
+    if cfg in ("c3a", "c3b"):
+        return datagen.make(cfg, rec=rec or 64)
+    return datagen.make(cfg)
+
+
+def units(cfg, w):
+    """(n_out, rec, algorithmic bytes per step, rid bytes) per SURVEY 8(d):
+    B = N * (2 * rec + rid_bytes)."""
+    if cfg == "c4":
+        n_out = w["fk"].size
+        rec = w["dim"].shape[1] + w["fact"].shape[1]          # 80-byte output rows
+        # join rows: read fk (4) + fact payload (16) + dim record (64), write 80
+        return n_out, rec, n_out * (4 + 16 + 64 + 80), 4
+    n_out = w["rids"].size
+    rec = w["src"].shape[1]
+    return n_out, rec, n_out * (2 * rec + 4), 4
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(cfg):
+    """dram bytes per probe-gather launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, w, budget_s=10.0):
+    """The oracle as it stands (single-threaded C loop, oracle/oracle.c) on this
+    host, repeated over the full workload until ~budget_s of CPU work."""
+    import oracle
+    n_out, rec, alg_bytes, _ = units(cfg, w)
+    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg == "c4" else \
+        (lambda: oracle.retrieve(w["src"], w["rids"]))
+    fn()  # warm (page in)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        fn()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (reps >= 3 and el > budget_s / 2):
+            break
+    t = el / reps
+    return {"value": alg_bytes / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "records_per_s": n_out / t,
+            "sample": f"full {cfg} workload x {reps} repetitions ({el:.1f} s), "
+                      f"oracle.retrieve single-threaded C loop",
+            "host_cpu": host_cpu(), "host_threads": os.cpu_count()}
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = args.config
+    w = make_inputs(cfg, args.rec)
+    import oracle
+    n_out, rec, alg_bytes, _ = units(cfg, w)
+    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg == "c4" else \
+        (lambda: oracle.retrieve(w["src"], w["rids"]))
+    for _ in range(max(0, min(args.warmup, 3))):
+        fn()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if sum(times) > 120:
+            break
+    t = sum(times) / len(times)
+    value = alg_bytes / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (datagen, seed 0)",
+        "config": {"workload": workload_name(cfg, args.rec), "n_out": n_out, "rec_bytes": rec},
+        "records_per_s": n_out / t,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"full {cfg} workload, {len(times)} steps",
+                         "host_cpu": host_cpu()},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import numpy as np
+    import paper_cs_0308004_b200 as dpg
+
+    cfg = args.config
+    w = make_inputs(cfg, args.rec)
+    n_out, rec, alg_bytes, rid_bytes = units(cfg, w)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def to_dev(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype == np.uint32:
+            a = a.view(np.int32)
+        return torch.from_numpy(a).to(dev)
+
+    if cfg == "c4":
+        fact, fk, dim = to_dev(w["fact"]), to_dev(w["fk"]), to_dev(w["dim"])
+        out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
+        step = lambda: dpg.dpg_fk_join(fact, fk, dim, out=out)
+        naive = None
+        n_src = dim.shape[0]
+    else:
+        src, rids = to_dev(w["src"]), to_dev(w["rids"])
+        out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
+        step = lambda: dpg.dpg_retrieve(src, rids, dst=out)
+        naive = lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)
+        n_src = src.shape[0]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, steps, phase=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        if phase:
+            dpg.dpg_phase_times()
+            dpg.dpg_phase_timing(True)
+        launches = 0
+        for e0, e1 in evs:
+            flush.fill_(1)                      # evict L2 (write > 126 MB)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            launches += dpg.last_launch_count()
+        torch.cuda.synchronize()
+        ph = None
+        if phase:
+            dpg.dpg_phase_timing(False)
+            ph = dpg.dpg_phase_times()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        return ms, launches, ph
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        step()
+        if naive:
+            naive()
+    torch.cuda.synchronize()
+    dpg.dpg_sync_status()
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms, launches, ph = timed(step, args.steps, phase=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    dpg.dpg_sync_status()
+    total_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * alg_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # naive comparison, same protocol
+    naive_res = None
+    if naive is not None:
+        nms, nl, _ = timed(naive, args.steps)
+        nt = sum(nms) / len(nms)
+        naive_res = {"value": alg_bytes / (nt * 1e-3) / 1e9, "unit": "GB/s",
+                     "ms_per_step": nt, "kernel": "k_direct", "launches_per_step": nl / args.steps}
+
+    peak, peak_src = hbm_peak()
+    dist_ms, probe_ms, calls = ph
+    pg_ms = probe_ms / max(1, calls)
+    # algorithmic bytes of the dominant kernel per launch: every source record
+    # staged once + every output row written once + its pair read once
+    plan = dpg.dpg_plan(rec if cfg != "c4" else w["dim"].shape[1], n_src, n_out,
+                        16 if cfg == "c4" else 0, torch.cuda.get_device_properties(dev).multi_processor_count)
+    src_rec = w["dim"].shape[1] if cfg == "c4" else rec
+    pay = 16 if cfg == "c4" else 0
+    pg_bytes = n_src * src_rec + n_out * (rec + plan["pair_bytes"] + pay)
+    achieved = pg_bytes / (pg_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_probe_gather", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": committed_traffic(cfg),
+                "peak_source": peak_src,
+                "alg_bytes_per_launch": pg_bytes,
+                "launch_ms": pg_ms,
+                "share_of_step": probe_ms / max(1e-9, sum(ms)),
+                "distribute_ms": dist_ms / max(1, calls),
+                "path_frac_of_peak": value / world / peak}
+
+    # end to end through the host-buffer C-ABI entry
+    e2e = None
+    if not args.no_e2e and cfg != "c4":
+        hs = torch.from_numpy(w["src"]).pin_memory()
+        hr = torch.from_numpy(w["rids"].view(np.int32)).pin_memory()
+        hd = torch.empty((n_out, rec), dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            dpg.dpg_retrieve_host(hs, hr, hd)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dpg.dpg_retrieve_host(hs, hr, hd)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * alg_bytes / (el / args.steps) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(w["src"].nbytes + w["rids"].nbytes),
+               "d2h_bytes_per_step": int(n_out * rec),
+               "ms_per_step": el / args.steps * 1e3, "entry": "dpg_retrieve_host"}
+        assert np.array_equal(hd[:1000].numpy(), w["src"][w["rids"][:1000].astype(np.int64)])
+        dpg.dpg_release_cache()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, w)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (datagen, seed 0)",
+            "config": {"workload": workload_name(cfg, args.rec), "n_src": n_src, "n_out": n_out,
+                       "rec_bytes": rec, "rid_bytes": rid_bytes,
+                       "alg_bytes_per_step": alg_bytes, "l2": "flushed before every step",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "run_len": plan["run_len"], "num_runs": plan["num_runs"],
+                       "pair_bytes": plan["pair_bytes"]},
+            "records_per_s": world * n_out / (ms_per_step * 1e-3),
+            "frac_of_hbm_peak": value / world / peak,
+            "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
+            "roofline": roofline, "naive": naive_res, "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * dpg.h -- C ABI of the B200-native DPG record-retrieval library (libdpg.so).
+ *
+ * The paper: "distribute-probe-gather" (DPG), arXiv cs/0308004.  Citations:
+ * P:n = line n of the paper's LaTeX body, in the section named.
+ *
+ * The record-retrieval problem (section 2): given a data file R of
+ * fixed-size records and a sequence of record ids S_rid, fill a destination
+ * file D with
+ *         for each i,  D[i] = R[S_rid[i]]
+ * The rid sequence may be a permutation (sort phase 3, section 3)
+ * or repeat rids (joins).  DPG computes exactly this result in
+ * three phases (section 2.1, Fig. 1): Distribute the rids
+ * into runs by their high bits, Probe each cache-resident run of the input,
+ * Gather the probed records back into rid order.  On B200 the probe and
+ * gather phases are fused: each source run is staged into shared
+ * memory by TMA bulk copies and every record is written straight to its
+ * destination position.
+ *
+ * Conventions (all entry points):
+ *  - Pointers named src/rids/dst/fact/fk_col/dim/out are DEVICE pointers
+ *    owned by the caller; the library never frees or retains them.  Records
+ *    are laid out back to back: record j occupies bytes [j*rec, (j+1)*rec).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are asynchronous w.r.t. the host and stream-ordered; the
+ *    inputs must stay valid until the stream reaches the call.  Scratch space
+ *    is library-owned and stream-ordered (cudaMallocAsync/cudaFreeAsync on
+ *    `stream`), so calls on different streams may run concurrently.
+ *  - Host-detected errors return immediately and enqueue nothing:
+ *    DPG_ERR_INVALID_ARG for a NULL pointer with a nonzero count, rec == 0,
+ *    n_src == 0 with n_out > 0, byte-size overflow, or dst overlapping an
+ *    input (the paper always copies into a separate destination);
+ *    DPG_ERR_UNSUPPORTED for n_out >= 2^32.
+ *  - n_out == 0 is a no-op returning DPG_OK.
+ *  - Device-detected errors: a rid >= n_src (an fk >= n_dim) is skipped, its
+ *    destination row is left unwritten, and the smallest offending position
+ *    is recorded in a per-device status word.  dpg_sync_status() reports it.
+ *  - Any rec >= 1 and any pointer alignment is supported; 16-byte aligned
+ *    pointers with rec % 16 == 0 (or % 4 == 0) take the widest vector path.
+ */
+#ifndef DPG_H
+#define DPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DPG_OK = 0,
+    DPG_ERR_INVALID_ARG = 1,
+    DPG_ERR_RID_RANGE = 2,
+    DPG_ERR_UNSUPPORTED = 3,
+    DPG_ERR_OOM = 4,
+    DPG_ERR_CUDA = 5,
+    DPG_ERR_NCCL = 6
+} dpg_status_t;
+
+typedef void *dpg_stream_t; /* a cudaStream_t */
+
+/* Execution plan chosen for one call (host-side; no GPU needed).
+ * Run length L = 2^log2_run records (runs sized to the cache,
+ * power of two, identified by the high-order bits of the rid); on B200 a
+ * run is sized so that one run plus its pair chunk fit one shared-memory
+ * stage, two stages per SM. */
+typedef struct {
+    uint32_t log2_run;      /* s: run of rid r is r >> s (reading A1)           */
+    uint32_t pair_bytes;    /* 4 = packed (pos << s | local), 8 = (local, pos)  */
+    uint64_t run_len;       /* L = 2^s                                          */
+    uint64_t num_runs;      /* K = ceil(n_src / L)                              */
+    uint32_t word_bytes;    /* vector width of the record copy (1..16)          */
+    uint32_t slot_pairs;    /* pairs staged per shared-memory stage             */
+    uint32_t smem_bytes;    /* dynamic shared memory of the probe-gather kernel */
+    uint32_t grid_distribute; /* CTAs of the distribute kernels (chunks)        */
+    uint32_t grid_probe;    /* CTAs of the persistent probe-gather kernel       */
+    uint32_t hist_in_smem;  /* 1: per-CTA run histogram in shared memory        */
+    uint32_t pay_bytes;     /* payload bytes carried per pair (join: fact row)  */
+    uint32_t reserved;
+} dpg_plan_t;
+
+/* Optional overrides for tests and tuning (zero = automatic).  The output
+ * of every call is independent of all of them (a property test checks it). */
+typedef struct {
+    uint32_t log2_run;      /* force s (tiny inputs then span many runs)        */
+    uint32_t grid_distribute;
+    uint32_t grid_probe;
+    uint32_t pair_bytes;    /* force 8-byte pairs                               */
+    uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
+    uint32_t reserved[3];
+} dpg_options_t;
+
+/* Build the plan the library would use (host only; sm_count <= 0 queries the
+ * current device, or uses 148 when no device is present). */
+dpg_status_t dpg_plan(size_t rec_bytes, uint64_t n_src, uint64_t n_out,
+                      size_t pay_bytes, const dpg_options_t *opt, int sm_count,
+                      dpg_plan_t *plan);
+
+/* DPG record retrieval: dst[i] = src[rids[i]] for i in [0, n_out) (P:196-201,
+ * Fig. 1).  src: n_src records of rec_bytes; rids: n_out uint32 in
+ * [0, n_src); dst: n_out records, must not overlap src or rids. */
+dpg_status_t dpg_retrieve(const void *src, size_t rec_bytes, uint64_t n_src,
+                          const uint32_t *rids, uint64_t n_out, void *dst,
+                          dpg_stream_t stream);
+
+/* dpg_retrieve with overrides (opt may be NULL). */
+dpg_status_t dpg_retrieve_ex(const void *src, size_t rec_bytes, uint64_t n_src,
+                             const uint32_t *rids, uint64_t n_out, void *dst,
+                             dpg_stream_t stream, const dpg_options_t *opt);
+
+/* The standard approach the paper compares against: access
+ * src[rids[i]] directly, one random access per record.  Same arguments and
+ * result as dpg_retrieve; one kernel.  The measured comparison. */
+dpg_status_t dpg_retrieve_direct(const void *src, size_t rec_bytes, uint64_t n_src,
+                                 const uint32_t *rids, uint64_t n_out, void *dst,
+                                 dpg_stream_t stream);
+
+/* DPG-Move foreign-key join (section 4.2.1).  The fact
+ * relation R is scanned in file order, so its join triples (k, rid_R, rid_F)
+ * come in rid_R order; the foreign key names the dimension record
+ * directly (dense key), so rid_F = fk_col[i].  The records of F (dim) are
+ * moved into R's order by DPG and joined with R ("join the temporary file
+ * with the remaining relation"):
+ *     out row i = fact[i] (fact_bytes) ++ dim[fk_col[i]] (rec_bytes)
+ * out: n_fact rows of fact_bytes + rec_bytes, in fact order.  An fk_col entry
+ * >= n_dim is a referential-integrity error (row left unwritten). */
+dpg_status_t dpg_fk_join(const void *fact, size_t fact_bytes, uint64_t n_fact,
+                         const uint32_t *fk_col, const void *dim, size_t rec_bytes,
+                         uint64_t n_dim, void *out, dpg_stream_t stream);
+
+dpg_status_t dpg_fk_join_ex(const void *fact, size_t fact_bytes, uint64_t n_fact,
+                            const uint32_t *fk_col, const void *dim, size_t rec_bytes,
+                            uint64_t n_dim, void *out, dpg_stream_t stream,
+                            const dpg_options_t *opt);
+
+/* Phase I alone (Distribute, Fig. 1), for tests: the
+ * rids are distributed into runs r >> log2_run.  pairs_out[j] (uint64) =
+ * local | (pos << 32) where local = rid - run*L and pos = the rid's position
+ * in `rids`; the entries of run b occupy [run_start[b], run_start[b+1]).
+ * Within a run the order of entries is unspecified (the GPU distributes in
+ * parallel); the set of entries of each run is unique.  run_start_out has
+ * num_runs + 1 uint64 entries. */
+dpg_status_t dpg_distribute(const uint32_t *rids, uint64_t n_out, uint64_t n_src,
+                            uint32_t log2_run, uint64_t *pairs_out,
+                            uint64_t *run_start_out, dpg_stream_t stream,
+                            const dpg_options_t *opt);
+
+/* Owner-side helper of the multi-GPU path: dst[pos[k]] = rows[k] for k in
+ * [0, n) (Phase III against received replies).  pos must be distinct. */
+dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t *pos,
+                              uint64_t n, void *dst, uint64_t n_dst, dpg_stream_t stream);
+
+/* End-to-end entry with HOST buffers: copies src and rids host->device,
+ * runs dpg_retrieve, copies dst device->host and synchronises `stream`.
+ * Host buffers should be pinned for full PCIe bandwidth.  Device buffers are
+ * library-owned and cached across calls (dpg_release_cache frees them). */
+dpg_status_t dpg_retrieve_host(const void *src_host, size_t rec_bytes, uint64_t n_src,
+                               const uint32_t *rids_host, uint64_t n_out, void *dst_host,
+                               dpg_stream_t stream);
+void dpg_release_cache(void);
+
+/* Synchronise `stream`, then report and clear the device status word:
+ * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
+ * recorded since the last call, or DPG_OK.  The status word is per device,
+ * shared by all streams. */
+dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t *first_bad_index);
+
+const char *dpg_status_string(dpg_status_t status);
+
+/* Number of kernel launches the most recent call on this host thread enqueued. */
+uint32_t dpg_last_launch_count(void);
+
+/* Phase timing (bench.py's roofline): while enabled, every dpg_retrieve /
+ * dpg_fk_join call records CUDA events on its own stream around Phase I
+ * (distribute) and the fused probe-gather kernel.  dpg_phase_times
+ * synchronises those events, returns the summed milliseconds and the number
+ * of calls since the last read, and clears the record. */
+void dpg_phase_timing(int enable);
+dpg_status_t dpg_phase_times(double *distribute_ms, double *probe_gather_ms, uint32_t *calls);
+
+int dpg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPG_H */

@@ -1,0 +1,289 @@
+"""B200-native DPG record retrieval (arXiv cs/0308004) -- Python binding.
+
+A thin ctypes layer over ``libdpg.so`` (C ABI declared in ``include/dpg.h``):
+argument marshalling only.  Every step of the path runs in the library's
+CUDA kernels; PyTorch supplies device memory and the current stream.  There
+is no CPU fallback: importing this package raises if ``libdpg.so`` has not
+been built (``python -m paper_cs_0308004_b200.build``).
+
+Functions carry the C ABI's names:
+
+* :func:`dpg_retrieve`        ``dst[i] = src[rids[i]]`` by distribute-probe-gather (Fig. 1)
+* :func:`dpg_retrieve_direct` the standard direct retrieval, the measured comparison
+* :func:`dpg_fk_join`         DPG-Move join rows ``fact[i] ++ dim[fk[i]]``
+* :func:`dpg_distribute`      Phase I alone, for tests
+* :func:`dpg_scatter_rows`    ``dst[pos[k]] = rows[k]`` (multi-GPU reply scatter)
+* :func:`dpg_retrieve_host`   end-to-end entry with host buffers
+* :func:`dpg_plan`            the host-side plan (run length L, stages, grids)
+* :func:`dpg_sync_status`     device-side rid-range errors
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdpg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_cs_0308004_b200.build` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+DPG_OK, DPG_ERR_INVALID_ARG, DPG_ERR_RID_RANGE, DPG_ERR_UNSUPPORTED, DPG_ERR_OOM, \
+    DPG_ERR_CUDA, DPG_ERR_NCCL = range(7)
+
+EXPORTED = (
+    "dpg_plan", "dpg_retrieve", "dpg_retrieve_ex", "dpg_retrieve_direct", "dpg_fk_join",
+    "dpg_fk_join_ex", "dpg_distribute", "dpg_scatter_rows", "dpg_retrieve_host",
+    "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
+    "dpg_version", "dpg_phase_timing", "dpg_phase_times",
+)
+
+
+class DPGError(RuntimeError):
+    def __init__(self, status: int, where: str, index: int | None = None):
+        name = _lib.dpg_status_string(status).decode()
+        msg = f"{where}: {name}" + (f" at position {index}" if index is not None else "")
+        super().__init__(msg)
+        self.status = status
+        self.index = index
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("log2_run", "pair_bytes")] + [
+        ("run_len", ctypes.c_uint64), ("num_runs", ctypes.c_uint64)] + [
+        (n, ctypes.c_uint32) for n in ("word_bytes", "slot_pairs", "smem_bytes",
+                                       "grid_distribute", "grid_probe", "hist_in_smem",
+                                       "pay_bytes", "reserved")]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+class Options(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("log2_run", "grid_distribute", "grid_probe",
+                                               "pair_bytes", "hist_mode")] + [
+        ("reserved", ctypes.c_uint32 * 3)]
+
+
+_P, _U, _S, _I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
+_st = ctypes.c_int
+_sigs = {
+    "dpg_plan": [_S, _U, _U, _S, _P, _I, _P],
+    "dpg_retrieve": [_P, _S, _U, _P, _U, _P, _P],
+    "dpg_retrieve_ex": [_P, _S, _U, _P, _U, _P, _P, _P],
+    "dpg_retrieve_direct": [_P, _S, _U, _P, _U, _P, _P],
+    "dpg_fk_join": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
+    "dpg_fk_join_ex": [_P, _S, _U, _P, _P, _S, _U, _P, _P, _P],
+    "dpg_distribute": [_P, _U, _U, ctypes.c_uint32, _P, _P, _P, _P],
+    "dpg_scatter_rows": [_P, _S, _P, _U, _P, _U, _P],
+    "dpg_retrieve_host": [_P, _S, _U, _P, _U, _P, _P],
+    "dpg_sync_status": [_P, _P],
+}
+for _name, _args in _sigs.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _st
+_lib.dpg_status_string.argtypes = [_st]
+_lib.dpg_status_string.restype = ctypes.c_char_p
+_lib.dpg_last_launch_count.restype = ctypes.c_uint32
+_lib.dpg_version.restype = ctypes.c_int
+_lib.dpg_release_cache.restype = None
+_lib.dpg_phase_timing.argtypes = [ctypes.c_int]
+_lib.dpg_phase_timing.restype = None
+_lib.dpg_phase_times.argtypes = [_P, _P, _P]
+_lib.dpg_phase_times.restype = _st
+
+
+def _check(status: int, where: str):
+    if status != DPG_OK:
+        raise DPGError(status, where)
+
+
+def _options(**kw) -> Options | None:
+    if not kw or all(v in (None, 0) for v in kw.values()):
+        return None
+    o = Options()
+    for k, v in kw.items():
+        if v:
+            setattr(o, k, int(v))
+    return o
+
+
+def _ref(o):
+    return None if o is None else ctypes.byref(o)
+
+
+def dpg_plan(rec_bytes: int, n_src: int, n_out: int, pay_bytes: int = 0, sm_count: int = 148,
+             **opts) -> dict:
+    """The plan the library would choose (host-only; no GPU needed)."""
+    p = Plan()
+    _check(_lib.dpg_plan(rec_bytes, n_src, n_out, pay_bytes, _ref(_options(**opts)), sm_count,
+                         ctypes.byref(p)), "dpg_plan")
+    return p.as_dict()
+
+
+def last_launch_count() -> int:
+    return int(_lib.dpg_last_launch_count())
+
+
+def dpg_phase_timing(enable: bool = True):
+    """Record CUDA events around Phase I and the probe-gather kernel of every
+    call (on the call's stream) until disabled."""
+    _lib.dpg_phase_timing(1 if enable else 0)
+
+
+def dpg_phase_times() -> tuple[float, float, int]:
+    """(distribute_ms, probe_gather_ms, calls) summed since the last read."""
+    d, p, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+    _check(_lib.dpg_phase_times(ctypes.byref(d), ctypes.byref(p), ctypes.byref(c)),
+           "dpg_phase_times")
+    return d.value, p.value, c.value
+
+
+# ---------------------------------------------------------------------------
+# torch-facing wrappers (device tensors; stream = torch's current stream)
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _records(t, name):
+    torch = _torch()
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.uint8:
+        raise ValueError(f"{name} must be uint8 [n, rec_bytes]")
+    if t.dim() == 1:
+        t = t.view(-1, 1)
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _rid_tensor(t, name="rids"):
+    torch = _torch()
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise ValueError(f"{name} must be int32/uint32 (read as uint32)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0, grid_probe=0,
+                 pair_bytes=0, hist_mode=0):
+    """``dst[i] = src[rids[i]]`` by DPG.  src: uint8 CUDA [n_src, rec]; rids:
+    int32/uint32 CUDA [n_out].  Returns dst (uint8 [n_out, rec])."""
+    torch = _torch()
+    src = _records(src, "src")
+    rids = _rid_tensor(rids)
+    n_src, rec = src.shape
+    n_out = rids.numel()
+    if dst is None:
+        dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
+    o = _options(log2_run=log2_run, grid_distribute=grid_distribute, grid_probe=grid_probe,
+                 pair_bytes=pair_bytes, hist_mode=hist_mode)
+    _check(_lib.dpg_retrieve_ex(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
+                                dst.data_ptr(), _stream_ptr(stream), _ref(o)), "dpg_retrieve")
+    return dst
+
+
+def dpg_retrieve_direct(src, rids, dst=None, stream=None):
+    """The paper's standard direct retrieval on the GPU."""
+    torch = _torch()
+    src = _records(src, "src")
+    rids = _rid_tensor(rids)
+    n_src, rec = src.shape
+    n_out = rids.numel()
+    if dst is None:
+        dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
+    _check(_lib.dpg_retrieve_direct(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
+                                    dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_direct")
+    return dst
+
+
+def dpg_fk_join(fact, fk_col, dim, out=None, stream=None, **opts):
+    """DPG-Move join: out row i = fact[i] ++ dim[fk_col[i]]."""
+    torch = _torch()
+    fact = _records(fact, "fact")
+    dim = _records(dim, "dim")
+    fk_col = _rid_tensor(fk_col, "fk_col")
+    n_fact, fact_bytes = fact.shape
+    n_dim, rec = dim.shape
+    if fk_col.numel() != n_fact:
+        raise ValueError("fk_col must have one entry per fact row")
+    if out is None:
+        out = torch.empty((n_fact, fact_bytes + rec), dtype=torch.uint8, device=dim.device)
+    _check(_lib.dpg_fk_join_ex(fact.data_ptr(), fact_bytes, n_fact, fk_col.data_ptr(),
+                               dim.data_ptr(), rec, n_dim, out.data_ptr(), _stream_ptr(stream),
+                               _ref(_options(**opts))), "dpg_fk_join")
+    return out
+
+
+def dpg_distribute(rids, n_src: int, log2_run: int, stream=None, **opts):
+    """Phase I alone.  Returns (pairs uint64 [n_out] = local | pos << 32,
+    run_start uint64 [K+1]) as int64 CUDA tensors."""
+    torch = _torch()
+    rids = _rid_tensor(rids)
+    n_out = rids.numel()
+    K = (n_src + (1 << log2_run) - 1) >> log2_run
+    pairs = torch.empty(max(n_out, 1), dtype=torch.int64, device=rids.device)
+    rs = torch.empty(K + 1, dtype=torch.int64, device=rids.device)
+    _check(_lib.dpg_distribute(rids.data_ptr(), n_out, n_src, log2_run, pairs.data_ptr(),
+                               rs.data_ptr(), _stream_ptr(stream), _ref(_options(**opts))),
+           "dpg_distribute")
+    return pairs[:n_out], rs
+
+
+def dpg_scatter_rows(rows, pos, dst, stream=None):
+    """dst[pos[k]] = rows[k] (pos distinct, uint32)."""
+    rows = _records(rows, "rows")
+    pos = _rid_tensor(pos, "pos")
+    dst = _records(dst, "dst")
+    n, rec = rows.shape
+    _check(_lib.dpg_scatter_rows(rows.data_ptr(), rec, pos.data_ptr(), n, dst.data_ptr(),
+                                 dst.shape[0], _stream_ptr(stream)), "dpg_scatter_rows")
+    return dst
+
+
+def dpg_retrieve_host(src, rids, dst, stream=None):
+    """End-to-end retrieval with HOST tensors (pinned for full PCIe speed):
+    H2D of src and rids, DPG on the GPU, D2H of dst, synchronise."""
+    for t, n in ((src, "src"), (rids, "rids"), (dst, "dst")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{n} must be a contiguous host tensor")
+    n_src, rec = src.shape
+    _check(_lib.dpg_retrieve_host(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
+                                  dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_host")
+    return dst
+
+
+def dpg_release_cache():
+    _lib.dpg_release_cache()
+
+
+def dpg_sync_status(stream=None):
+    """Synchronise the stream; raise DPGError(DPG_ERR_RID_RANGE, index) if a
+    rid was out of range since the last check."""
+    idx = ctypes.c_uint64(0)
+    s = _lib.dpg_sync_status(_stream_ptr(stream), ctypes.byref(idx))
+    if s == DPG_ERR_RID_RANGE:
+        raise DPGError(s, "dpg_sync_status", int(idx.value))
+    _check(s, "dpg_sync_status")
+
+
+def raw_lib():
+    """The loaded ctypes library (tests of the C ABI itself)."""
+    return _lib

@@ -1,0 +1,550 @@
+// api.cu -- the C ABI of libdpg.so (include/dpg.h): argument validation,
+// planning of the run length L, stream-ordered workspace, and the
+// kernel sequence  distribute (Phase I) -> fused probe+gather (Phases II+III).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "dpg_internal.cuh"
+
+using namespace dpg;
+
+namespace {
+
+constexpr uint32_t kSmemLimit = 232448;   // 227 KB dynamic smem per CTA (sm_100)
+constexpr uint32_t kBarBytes = 128;
+constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives in smem
+
+thread_local uint32_t t_launches = 0;
+
+// ---- optional phase timing (events on the call's stream) --------------------
+std::mutex g_timing_mu;
+bool g_timing = false;
+struct PhaseEvents { cudaEvent_t e0, e1, e2; };
+std::vector<PhaseEvents> g_pending, g_pool;
+
+bool timing_begin(cudaStream_t st, PhaseEvents* pe) {
+  if (!g_timing) return false;
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  if (!g_pool.empty()) { *pe = g_pool.back(); g_pool.pop_back(); }
+  else {
+    cudaEventCreate(&pe->e0); cudaEventCreate(&pe->e1); cudaEventCreate(&pe->e2);
+  }
+  cudaEventRecord(pe->e0, st);
+  g_pending.push_back(*pe);
+  return true;
+}
+
+int current_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+// Per-device status word + mempool setup.
+unsigned long long* device_status() {
+  static std::mutex mu;
+  static unsigned long long* ptr[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ptr[dev]) {
+    unsigned long long* p = nullptr;
+    if (cudaMalloc(&p, sizeof(*p)) != cudaSuccess) return nullptr;
+    unsigned long long init = ~0ull;
+    if (cudaMemcpy(p, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    // keep freed workspace in the default pool (no release back to the OS)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    ptr[dev] = p;
+  }
+  return ptr[dev];
+}
+
+uint32_t bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+bool overlaps(const void* a, uint64_t na, const void* b, uint64_t nb) {
+  if (!na || !nb) return false;
+  uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+  return a0 < b0 + nb && b0 < a0 + na;
+}
+
+uint32_t pow2_divisor(uint64_t x) {  // largest power of two <= 16 dividing x
+  uint32_t w = 16;
+  while (w > 1 && (x % w)) w >>= 1;
+  return w;
+}
+
+// Stage geometry for run length L = 2^s.
+void stage_geometry(uint64_t rec, uint32_t s, uint32_t pb, uint64_t pay, uint32_t slot_pairs,
+                    dpg_plan_t* p) {
+  uint64_t L = 1ull << s;
+  uint64_t region_cap = align_up(L * rec + 32, 16);
+  uint64_t pair_cap = align_up((uint64_t)slot_pairs * pb + 32, 16);
+  uint64_t pay_cap = pay ? align_up((uint64_t)slot_pairs * pay + 32, 16) : 0;
+  uint64_t slot = region_cap + pair_cap + pay_cap;
+  p->slot_pairs = slot_pairs;
+  p->smem_bytes = (uint32_t)std::min<uint64_t>(UINT32_MAX, kBarBytes + 2 * slot);
+}
+
+// Distribute geometry: chunks of >= 2048 rids per CTA, up to 2 CTAs per SM;
+// per-CTA run histogram in shared memory when K counters fit.
+dpg_status_t dist_geometry(uint64_t K, uint64_t n_out, const dpg_options_t* opt, int sm,
+                           dpg_plan_t* p) {
+  uint64_t G = std::min<uint64_t>((uint64_t)2 * sm, std::max<uint64_t>(1, (n_out + 2047) / 2048));
+  uint32_t hist_mode = opt ? opt->hist_mode : 0;
+  bool smem_hist = hist_mode == 1 ? (K * 4 <= kSmemLimit)
+                 : hist_mode == 2 ? false
+                                  : (K <= kHistSmemMax);
+  if (hist_mode == 1 && !smem_hist) return DPG_ERR_UNSUPPORTED;
+  if (!smem_hist) G = std::min<uint64_t>(G, (uint64_t)sm);
+  if (opt && opt->grid_distribute) G = opt->grid_distribute;
+  p->grid_distribute = (uint32_t)G;
+  p->hist_in_smem = smem_hist ? 1 : 0;
+  return DPG_OK;
+}
+
+dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
+                       const dpg_options_t* opt, int sm, dpg_plan_t* p) {
+  if (rec == 0 || !p) return DPG_ERR_INVALID_ARG;
+  if (n_out >= (1ull << 32) || n_src > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  std::memset(p, 0, sizeof(*p));
+  if (sm <= 0) sm = 148;
+  const uint64_t nsrc = std::max<uint64_t>(n_src, 1);
+  const uint32_t pos_bits = bit_length(n_out > 0 ? n_out - 1 : 0);
+  const bool force8 = opt && opt->pair_bytes == 8;
+  auto pair_bytes_for = [&](uint32_t s) -> uint32_t {
+    return (!force8 && s + pos_bits <= 32) ? 4u : 8u;
+  };
+  // Largest run that fits one of two shared-memory stages (paper's first
+  // constraint: one run of records plus the buffer of its rids).
+  uint32_t s_fit = 0;
+  for (int s = 24; s >= 0; --s) {
+    uint64_t L = 1ull << s;
+    if (L * rec + 32 > kSmemLimit) continue;
+    dpg_plan_t t;
+    stage_geometry(rec, s, pair_bytes_for(s), pay, (uint32_t)std::max<uint64_t>(32, L), &t);
+    if (t.smem_bytes <= kSmemLimit) { s_fit = (uint32_t)s; break; }
+  }
+  // No larger than the source itself, and small enough that every SM gets
+  // several runs (load balance), but not below ~8 KB of records per run.
+  uint32_t s_src = bit_length(nsrc - 1);
+  uint32_t s = std::min(s_fit, s_src);
+  uint64_t want_runs = 4ull * (uint64_t)sm;
+  while (s > 0 && ((nsrc + (1ull << s) - 1) >> s) < want_runs && ((1ull << (s - 1)) * rec) >= 8192)
+    --s;
+  if (opt && opt->log2_run) {
+    if (opt->log2_run > 31) return DPG_ERR_INVALID_ARG;
+    s = opt->log2_run;
+    if ((1ull << s) * rec + 32 > kSmemLimit) return DPG_ERR_UNSUPPORTED;
+  }
+  const uint64_t L = 1ull << s;
+  const uint64_t K = (nsrc + L - 1) >> s;
+  if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
+  const uint32_t pb = pair_bytes_for(s);
+  // Pair chunk per stage: 2L when it fits (Poisson slack for with-replacement
+  // rids), else 1.5L, else L; a heavier run is processed in several chunks.
+  uint32_t sp = 0;
+  for (uint64_t cand : {2 * L, L + L / 2, L, L / 2, L / 4, (uint64_t)32}) {
+    cand = std::max<uint64_t>(32, cand);
+    dpg_plan_t t;
+    stage_geometry(rec, s, pb, pay, (uint32_t)std::min<uint64_t>(cand, 1u << 24), &t);
+    if (t.smem_bytes <= kSmemLimit) { sp = t.slot_pairs; break; }
+  }
+  if (!sp) return DPG_ERR_UNSUPPORTED;
+  stage_geometry(rec, s, pb, pay, sp, p);
+  p->log2_run = s;
+  p->pair_bytes = pb;
+  p->run_len = L;
+  p->num_runs = K;
+  p->word_bytes = pow2_divisor(rec | pay);
+  p->pay_bytes = (uint32_t)pay;
+  dpg_status_t ds = dist_geometry(K, n_out, opt, sm, p);
+  if (ds != DPG_OK) return ds;
+  uint64_t gp = std::min<uint64_t>(K, (uint64_t)sm);
+  if (opt && opt->grid_probe) gp = opt->grid_probe;
+  p->grid_probe = (uint32_t)std::max<uint64_t>(1, gp);
+  return DPG_OK;
+}
+
+struct Workspace {
+  uint8_t* base = nullptr;
+  uint32_t* counts = nullptr;
+  uint32_t* run_start = nullptr;
+  void* pairs = nullptr;
+  uint8_t* pay = nullptr;
+};
+
+dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t st, Workspace* w) {
+  const uint64_t K = p.num_runs, G = p.grid_distribute;
+  const uint64_t M = K * G;
+  const uint64_t ntiles = (M + 4095) / 4096;
+  uint64_t off_counts = 0;
+  uint64_t off_rs = align_up(off_counts + M * 4, 256);
+  uint64_t off_pairs = align_up(off_rs + (K + 1 + ntiles) * 4, 256);
+  uint64_t off_pay = align_up(off_pairs + n_out * p.pair_bytes + 64, 256);
+  uint64_t total = align_up(off_pay + (p.pay_bytes ? n_out * p.pay_bytes + 64 : 0), 256);
+  void* b = nullptr;
+  if (cudaMallocAsync(&b, total, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  w->base = (uint8_t*)b;
+  w->counts = (uint32_t*)(w->base + off_counts);
+  w->run_start = (uint32_t*)(w->base + off_rs);
+  w->pairs = w->base + off_pairs;
+  w->pay = p.pay_bytes ? w->base + off_pay : nullptr;
+  return DPG_OK;
+}
+
+dpg_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return DPG_OK;
+  cudaGetLastError();
+  return e == cudaErrorMemoryAllocation ? DPG_ERR_OOM : DPG_ERR_CUDA;
+}
+
+// Shared body of dpg_retrieve and dpg_fk_join: rows of (pay ++ rec) bytes.
+dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32_t* rids,
+                     uint64_t n_out, const void* pay_src, uint64_t pay, void* dst,
+                     cudaStream_t st, const dpg_options_t* opt) {
+  t_launches = 0;
+  if (rec == 0) return DPG_ERR_INVALID_ARG;
+  if (n_out == 0) return DPG_OK;
+  if (!src || !rids || !dst || (pay && !pay_src)) return DPG_ERR_INVALID_ARG;
+  if (n_src == 0) return DPG_ERR_INVALID_ARG;
+  if (n_out >= (1ull << 32) || n_src > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  uint64_t src_bytes, row, dst_bytes, pay_bytes_total;
+  if (__builtin_mul_overflow(n_src, rec, &src_bytes)) return DPG_ERR_INVALID_ARG;
+  if (__builtin_add_overflow(rec, pay, &row)) return DPG_ERR_INVALID_ARG;
+  if (__builtin_mul_overflow(n_out, row, &dst_bytes)) return DPG_ERR_INVALID_ARG;
+  if (__builtin_mul_overflow(n_out, pay, &pay_bytes_total)) return DPG_ERR_INVALID_ARG;
+  if (rec > UINT32_MAX / 2 || row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  if (overlaps(dst, dst_bytes, src, src_bytes) || overlaps(dst, dst_bytes, rids, n_out * 4) ||
+      (pay && overlaps(dst, dst_bytes, pay_src, pay_bytes_total)))
+    return DPG_ERR_INVALID_ARG;
+
+  const int sm = current_sm_count();
+  dpg_plan_t p;
+  dpg_status_t ps = make_plan(rec, n_src, n_out, pay, opt, sm, &p);
+  if (ps != DPG_OK) return ps;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+
+  Workspace w;
+  dpg_status_t as = alloc_workspace(p, n_out, st, &w);
+  if (as != DPG_OK) return as;
+  uint32_t nl = 0;
+  const uint64_t M = p.num_runs * (uint64_t)p.grid_distribute;
+  if (!p.hist_in_smem) {
+    cudaError_t e = cudaMemsetAsync(w.counts, 0, M * 4, st);
+    if (e != cudaSuccess) { cudaFreeAsync(w.base, st); return cuda_status(e); }
+  }
+  DistArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = rids;
+  d.n_out = n_out;
+  d.n_src = n_src;
+  d.s = p.log2_run;
+  d.K = (uint32_t)p.num_runs;
+  d.G = p.grid_distribute;
+  d.chunk = (n_out + d.G - 1) / d.G;
+  d.counts = w.counts;
+  d.run_start = w.run_start;
+  d.pairs = w.pairs;
+  d.pair_bytes = p.pair_bytes;
+  d.pay_src = (const uint8_t*)pay_src;
+  d.pay_dst = w.pay;
+  d.pay_bytes = (uint32_t)pay;
+  d.hist_smem = p.hist_in_smem;
+  d.status = status;
+  PhaseEvents pe;
+  const bool timed = timing_begin(st, &pe);
+  cudaError_t e = launch_distribute(d, false, st, &nl);
+  if (timed) cudaEventRecord(pe.e1, st);
+  if (e == cudaSuccess) {
+    ProbeArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.src = (const uint8_t*)src;
+    a.n_src = n_src;
+    a.rec = (uint32_t)rec;
+    a.s = p.log2_run;
+    a.K = (uint32_t)p.num_runs;
+    a.run_start = w.run_start;
+    a.pairs = w.pairs;
+    a.pair_bytes = p.pair_bytes;
+    a.pay = w.pay;
+    a.pay_bytes = (uint32_t)pay;
+    a.dst = (uint8_t*)dst;
+    a.row_bytes = (uint32_t)row;
+    a.slot_pairs = p.slot_pairs;
+    a.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
+    a.slot_bytes = (p.smem_bytes - kBarBytes) / 2;
+    uint32_t W = pow2_divisor(rec | pay | (uintptr_t)src | (uintptr_t)dst);
+    e = launch_probe_gather(a, W, p.grid_probe, p.smem_bytes, st, &nl);
+  }
+  if (timed) cudaEventRecord(pe.e2, st);
+  cudaFreeAsync(w.base, st);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dpg_version(void) { return 1; }
+
+uint32_t dpg_last_launch_count(void) { return t_launches; }
+
+void dpg_phase_timing(int enable) {
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  g_timing = enable != 0;
+}
+
+dpg_status_t dpg_phase_times(double* distribute_ms, double* probe_gather_ms, uint32_t* calls) {
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  double d = 0, p = 0;
+  for (auto& pe : g_pending) {
+    float a = 0, b = 0;
+    if (cudaEventSynchronize(pe.e2) != cudaSuccess) return cuda_status(cudaGetLastError());
+    cudaEventElapsedTime(&a, pe.e0, pe.e1);
+    cudaEventElapsedTime(&b, pe.e1, pe.e2);
+    d += a;
+    p += b;
+    g_pool.push_back(pe);
+  }
+  if (distribute_ms) *distribute_ms = d;
+  if (probe_gather_ms) *probe_gather_ms = p;
+  if (calls) *calls = (uint32_t)g_pending.size();
+  g_pending.clear();
+  return DPG_OK;
+}
+
+const char* dpg_status_string(dpg_status_t s) {
+  switch (s) {
+    case DPG_OK: return "DPG_OK";
+    case DPG_ERR_INVALID_ARG: return "DPG_ERR_INVALID_ARG";
+    case DPG_ERR_RID_RANGE: return "DPG_ERR_RID_RANGE";
+    case DPG_ERR_UNSUPPORTED: return "DPG_ERR_UNSUPPORTED";
+    case DPG_ERR_OOM: return "DPG_ERR_OOM";
+    case DPG_ERR_CUDA: return "DPG_ERR_CUDA";
+    case DPG_ERR_NCCL: return "DPG_ERR_NCCL";
+  }
+  return "DPG_ERR_UNKNOWN";
+}
+
+dpg_status_t dpg_plan(size_t rec_bytes, uint64_t n_src, uint64_t n_out, size_t pay_bytes,
+                      const dpg_options_t* opt, int sm_count, dpg_plan_t* plan) {
+  return make_plan(rec_bytes, n_src, n_out, pay_bytes, opt, sm_count, plan);
+}
+
+dpg_status_t dpg_retrieve_ex(const void* src, size_t rec_bytes, uint64_t n_src,
+                             const uint32_t* rids, uint64_t n_out, void* dst, dpg_stream_t stream,
+                             const dpg_options_t* opt) {
+  return run_dpg(src, rec_bytes, n_src, rids, n_out, nullptr, 0, dst, (cudaStream_t)stream, opt);
+}
+
+dpg_status_t dpg_retrieve(const void* src, size_t rec_bytes, uint64_t n_src, const uint32_t* rids,
+                          uint64_t n_out, void* dst, dpg_stream_t stream) {
+  return dpg_retrieve_ex(src, rec_bytes, n_src, rids, n_out, dst, stream, nullptr);
+}
+
+dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact,
+                            const uint32_t* fk_col, const void* dim, size_t rec_bytes,
+                            uint64_t n_dim, void* out, dpg_stream_t stream,
+                            const dpg_options_t* opt) {
+  return run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, fact, fact_bytes, out,
+                 (cudaStream_t)stream, opt);
+}
+
+dpg_status_t dpg_fk_join(const void* fact, size_t fact_bytes, uint64_t n_fact,
+                         const uint32_t* fk_col, const void* dim, size_t rec_bytes, uint64_t n_dim,
+                         void* out, dpg_stream_t stream) {
+  return dpg_fk_join_ex(fact, fact_bytes, n_fact, fk_col, dim, rec_bytes, n_dim, out, stream,
+                        nullptr);
+}
+
+dpg_status_t dpg_retrieve_direct(const void* src, size_t rec_bytes, uint64_t n_src,
+                                 const uint32_t* rids, uint64_t n_out, void* dst,
+                                 dpg_stream_t stream) {
+  t_launches = 0;
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n_out == 0) return DPG_OK;
+  if (!src || !rids || !dst || n_src == 0) return DPG_ERR_INVALID_ARG;
+  if (n_out >= (1ull << 32) || n_src > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  uint64_t src_bytes, dst_bytes;
+  if (__builtin_mul_overflow(n_src, (uint64_t)rec_bytes, &src_bytes) ||
+      __builtin_mul_overflow(n_out, (uint64_t)rec_bytes, &dst_bytes))
+    return DPG_ERR_INVALID_ARG;
+  if (rec_bytes > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  if (overlaps(dst, dst_bytes, src, src_bytes) || overlaps(dst, dst_bytes, rids, n_out * 4))
+    return DPG_ERR_INVALID_ARG;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  uint32_t W = pow2_divisor(rec_bytes | (uintptr_t)src | (uintptr_t)dst);
+  uint32_t nl = 0;
+  cudaError_t e = launch_direct((const uint8_t*)src, n_src, (uint32_t)rec_bytes, rids, n_out,
+                                (uint8_t*)dst, W, current_sm_count(), status,
+                                (cudaStream_t)stream, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src, uint32_t log2_run,
+                            uint64_t* pairs_out, uint64_t* run_start_out, dpg_stream_t stream,
+                            const dpg_options_t* opt) {
+  t_launches = 0;
+  if (n_src == 0 || !run_start_out || (n_out && (!rids || !pairs_out)) || log2_run > 31)
+    return DPG_ERR_INVALID_ARG;
+  if (n_out >= (1ull << 32) || n_src > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = current_sm_count();
+  const uint64_t L = 1ull << log2_run;
+  const uint64_t K = (n_src + L - 1) >> log2_run;
+  if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
+  dpg_plan_t p;
+  std::memset(&p, 0, sizeof(p));
+  p.log2_run = log2_run;
+  p.run_len = L;
+  p.num_runs = K;
+  const bool force8 = opt && opt->pair_bytes == 8;
+  p.pair_bytes = (!force8 && log2_run + bit_length(n_out ? n_out - 1 : 0) <= 32) ? 4 : 8;
+  dpg_status_t ds = dist_geometry(K, n_out, opt, sm, &p);
+  if (ds != DPG_OK) return ds;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  Workspace w;
+  dpg_status_t as = alloc_workspace(p, n_out, st, &w);
+  if (as != DPG_OK) return as;
+  uint32_t nl = 0;
+  cudaError_t e = cudaSuccess;
+  if (!p.hist_in_smem) e = cudaMemsetAsync(w.counts, 0, K * (uint64_t)p.grid_distribute * 4, st);
+  DistArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = rids;
+  d.n_out = n_out;
+  d.n_src = n_src;
+  d.s = log2_run;
+  d.K = (uint32_t)K;
+  d.G = p.grid_distribute;
+  d.chunk = (n_out + d.G - 1) / d.G;
+  d.counts = w.counts;
+  d.run_start = w.run_start;
+  d.pairs = w.pairs;
+  d.pair_bytes = p.pair_bytes;
+  d.hist_smem = p.hist_in_smem;
+  d.status = status;
+  if (e == cudaSuccess && n_out) e = launch_distribute(d, false, st, &nl);
+  if (e == cudaSuccess) {
+    if (!n_out) {
+      e = cudaMemsetAsync(w.run_start, 0, (K + 1) * 4, st);
+      d.run_start = w.run_start;
+    }
+    if (e == cudaSuccess) e = launch_unpack_pairs(d, pairs_out, run_start_out, st, &nl);
+  }
+  cudaFreeAsync(w.base, st);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_scatter_rows(const void* rows, size_t rec_bytes, const uint32_t* pos, uint64_t n,
+                              void* dst, uint64_t n_dst, dpg_stream_t stream) {
+  t_launches = 0;
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n == 0) return DPG_OK;
+  if (!rows || !pos || !dst) return DPG_ERR_INVALID_ARG;
+  if (rec_bytes > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  uint32_t W = pow2_divisor(rec_bytes | (uintptr_t)rows | (uintptr_t)dst);
+  uint32_t nl = 0;
+  cudaError_t e = launch_scatter_rows((const uint8_t*)rows, (uint32_t)rec_bytes, pos, n,
+                                      (uint8_t*)dst, n_dst, W, current_sm_count(),
+                                      (cudaStream_t)stream, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  unsigned long long v = 0;
+  e = cudaMemcpy(&v, status, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (v == ~0ull) return DPG_OK;
+  unsigned long long init = ~0ull;
+  e = cudaMemcpy(status, &init, sizeof(init), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (first_bad_index) *first_bad_index = v;
+  return DPG_ERR_RID_RANGE;
+}
+
+// ---- end-to-end entry with host buffers --------------------------------------
+static std::mutex g_host_mu;
+static void* g_host_buf[3] = {nullptr, nullptr, nullptr};
+static size_t g_host_cap[3] = {0, 0, 0};
+
+static dpg_status_t host_buf(int k, size_t bytes, void** out) {
+  if (g_host_cap[k] < bytes) {
+    if (g_host_buf[k]) cudaFree(g_host_buf[k]);
+    g_host_buf[k] = nullptr;
+    g_host_cap[k] = 0;
+    if (cudaMalloc(&g_host_buf[k], bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return DPG_ERR_OOM;
+    }
+    g_host_cap[k] = bytes;
+  }
+  *out = g_host_buf[k];
+  return DPG_OK;
+}
+
+dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t n_src,
+                               const uint32_t* rids_host, uint64_t n_out, void* dst_host,
+                               dpg_stream_t stream) {
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n_out == 0) return DPG_OK;
+  if (!src_host || !rids_host || !dst_host || n_src == 0) return DPG_ERR_INVALID_ARG;
+  uint64_t sb, db;
+  if (__builtin_mul_overflow(n_src, (uint64_t)rec_bytes, &sb) ||
+      __builtin_mul_overflow(n_out, (uint64_t)rec_bytes, &db))
+    return DPG_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  void *s = nullptr, *r = nullptr, *d = nullptr;
+  dpg_status_t x;
+  if ((x = host_buf(0, sb, &s)) != DPG_OK) return x;
+  if ((x = host_buf(1, n_out * 4, &r)) != DPG_OK) return x;
+  if ((x = host_buf(2, db, &d)) != DPG_OK) return x;
+  cudaError_t e = cudaMemcpyAsync(s, src_host, sb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(r, rids_host, n_out * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  dpg_status_t ds = dpg_retrieve(s, rec_bytes, n_src, (const uint32_t*)r, n_out, d, stream);
+  if (ds != DPG_OK) return ds;
+  e = cudaMemcpyAsync(dst_host, d, db, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e);
+}
+
+void dpg_release_cache(void) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  for (int k = 0; k < 3; ++k) {
+    if (g_host_buf[k]) cudaFree(g_host_buf[k]);
+    g_host_buf[k] = nullptr;
+    g_host_cap[k] = 0;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// direct.cu -- the standard retrieval the paper measures DPG against
+// (P:73-77): "accesses the records of the source data file directly according
+// to the sequence of the rids", i.e. dst[i] = src[rid[i]] with one random
+// access per record.  Built as the measured GPU comparison (the "naive
+// direct-gather" kernel), tuned honestly: each warp owns 32 consecutive
+// output rows, lanes cover the words of a row, and a batch of independent
+// row loads is issued before any store so many random reads are in flight.
+//
+// Also the owner-side reply scatter of the multi-GPU path (dst[pos[k]] =
+// rows[k]), the same lane layout with the random side on the write.
+#include "dpg_internal.cuh"
+
+namespace dpg {
+
+static constexpr int kDirectThreads = 256;
+
+template <int W>
+__global__ void __launch_bounds__(kDirectThreads) k_direct(const uint8_t* __restrict__ src,
+                                                           uint64_t n_src, uint32_t rec,
+                                                           const uint32_t* __restrict__ rids,
+                                                           uint64_t n_out, uint8_t* __restrict__ dst,
+                                                           unsigned long long* status) {
+  using T = typename Word<W>::T;
+  constexpr int B = W >= 16 ? 4 : 8;  // rows in flight per lane per batch
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t R = rec / W;
+  const uint32_t RPI = R <= 32 ? 32 / R : 1;
+  const uint32_t lr = R <= 32 ? lane / R : 0;
+  const uint32_t lw = R <= 32 ? lane % R : 0;
+  const bool lane_on = R <= 32 ? (uint32_t)lane < RPI * R : true;
+
+  for (uint64_t g0 = gw * 32; g0 < n_out; g0 += nw * 32) {
+    const uint64_t i = g0 + lane;
+    uint32_t my_r = 0;
+    uint32_t my_ok = 0;
+    if (i < n_out) {
+      my_r = __ldg(rids + i);
+      if (my_r < n_src) my_ok = 1;
+      else report_bad(status, i);
+    }
+    const uint32_t cnt = (uint32_t)min_u64(32, n_out - g0);
+    if (R <= 32) {
+      for (uint32_t k0 = 0; k0 < 32; k0 += RPI * B) {
+        T v[B];
+        bool ok[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const uint32_t rr = k0 + u * RPI + lr;
+          const uint32_t r = __shfl_sync(0xffffffffu, my_r, rr & 31);
+          const uint32_t o = __shfl_sync(0xffffffffu, my_ok, rr & 31);
+          ok[u] = lane_on && rr < cnt && o;
+          if (ok[u]) v[u] = __ldg(reinterpret_cast<const T*>(src + (uint64_t)r * rec + lw * W));
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const uint32_t rr = k0 + u * RPI + lr;
+          if (ok[u]) *reinterpret_cast<T*>(dst + (g0 + rr) * rec + lw * W) = v[u];
+        }
+      }
+    } else {
+      for (uint32_t rr = 0; rr < cnt; ++rr) {
+        const uint32_t r = __shfl_sync(0xffffffffu, my_r, rr);
+        const uint32_t o = __shfl_sync(0xffffffffu, my_ok, rr);
+        if (!o) continue;
+        const uint8_t* s = src + (uint64_t)r * rec;
+        uint8_t* d = dst + (g0 + rr) * rec;
+        for (uint32_t w0 = 0; w0 < R; w0 += 32 * B) {
+          T v[B];
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const uint32_t w = w0 + u * 32 + lane;
+            if (w < R) v[u] = __ldg(reinterpret_cast<const T*>(s + w * W));
+          }
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const uint32_t w = w0 + u * 32 + lane;
+            if (w < R) *reinterpret_cast<T*>(d + w * W) = v[u];
+          }
+        }
+      }
+    }
+  }
+}
+
+// dst[pos[k]] = rows[k]
+template <int W>
+__global__ void __launch_bounds__(kDirectThreads) k_scatter_rows(const uint8_t* __restrict__ rows,
+                                                                 uint32_t rec,
+                                                                 const uint32_t* __restrict__ pos,
+                                                                 uint64_t n, uint8_t* __restrict__ dst,
+                                                                 uint64_t n_dst) {
+  using T = typename Word<W>::T;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t R = rec / W;
+  const uint32_t RPI = R <= 32 ? 32 / R : 1;
+  const uint32_t lr = R <= 32 ? lane / R : 0;
+  const uint32_t lw = R <= 32 ? lane % R : 0;
+  const bool lane_on = R <= 32 ? (uint32_t)lane < RPI * R : true;
+  for (uint64_t g0 = gw * 32; g0 < n; g0 += nw * 32) {
+    const uint64_t k = g0 + lane;
+    const uint32_t my_p = k < n ? __ldg(pos + k) : 0xffffffffu;
+    const uint32_t cnt = (uint32_t)min_u64(32, n - g0);
+    if (R <= 32) {
+#pragma unroll 4
+      for (uint32_t k0 = 0; k0 < 32; k0 += RPI) {
+        const uint32_t rr = k0 + lr;
+        const uint32_t p = __shfl_sync(0xffffffffu, my_p, rr & 31);
+        if (lane_on && rr < cnt && p < n_dst)
+          *reinterpret_cast<T*>(dst + (uint64_t)p * rec + lw * W) =
+              __ldg(reinterpret_cast<const T*>(rows + (g0 + rr) * rec + lw * W));
+      }
+    } else {
+      for (uint32_t rr = 0; rr < cnt; ++rr) {
+        const uint32_t p = __shfl_sync(0xffffffffu, my_p, rr);
+        if (p >= n_dst) continue;
+        for (uint32_t w = lane; w < R; w += 32)
+          *reinterpret_cast<T*>(dst + (uint64_t)p * rec + w * W) =
+              __ldg(reinterpret_cast<const T*>(rows + (g0 + rr) * rec + w * W));
+      }
+    }
+  }
+}
+
+static uint32_t grid_for(uint64_t n_rows, int sm_count) {
+  uint64_t warps = (n_rows + 31) / 32;
+  uint64_t blocks = (warps + (kDirectThreads / 32) - 1) / (kDirectThreads / 32);
+  uint64_t cap = (uint64_t)sm_count * 8;  // 8 x 256 threads = 64 warps per SM
+  return (uint32_t)max_u64(1, min_u64(blocks, cap));
+}
+
+cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
+                          uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
+                          unsigned long long* status, cudaStream_t st, uint32_t* nl) {
+  uint32_t grid = grid_for(n_out, sm_count);
+  ++*nl;
+  switch (W) {
+    case 16: k_direct<16><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 8: k_direct<8><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 4: k_direct<4><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 2: k_direct<2><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    default: k_direct<1><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos, uint64_t n,
+                                uint8_t* dst, uint64_t n_dst, uint32_t W, int sm_count,
+                                cudaStream_t st, uint32_t* nl) {
+  uint32_t grid = grid_for(n, sm_count);
+  ++*nl;
+  switch (W) {
+    case 16: k_scatter_rows<16><<<grid, kDirectThreads, 0, st>>>(rows, rec, pos, n, dst, n_dst); break;
+    case 8: k_scatter_rows<8><<<grid, kDirectThreads, 0, st>>>(rows, rec, pos, n, dst, n_dst); break;
+    case 4: k_scatter_rows<4><<<grid, kDirectThreads, 0, st>>>(rows, rec, pos, n, dst, n_dst); break;
+    case 2: k_scatter_rows<2><<<grid, kDirectThreads, 0, st>>>(rows, rec, pos, n, dst, n_dst); break;
+    default: k_scatter_rows<1><<<grid, kDirectThreads, 0, st>>>(rows, rec, pos, n, dst, n_dst); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dpg

@@ -1,0 +1,145 @@
+// dpg_internal.cuh -- device helpers and launcher declarations shared by the
+// CUDA translation units of libdpg.so (product path; no oracle code here).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dpg.h"
+
+namespace dpg {
+
+__host__ __device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t max_u64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Device status word (one per device, library-owned): smallest position i
+// whose rid was out of range; ~0 when clean.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void report_bad(unsigned long long* status, uint64_t i) {
+  atomicMin(status, (unsigned long long)i);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers: mbarrier + cp.async.bulk (TMA bulk copy, sm_90+ / sm_100a).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(tx)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Bulk async copy global -> shared, completion counted on `bar` (bytes).
+// dst_smem, src and bytes must be 16-byte aligned / multiples of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Vector word of W bytes.
+// ---------------------------------------------------------------------------
+template <int W> struct Word;
+template <> struct Word<1> { using T = uint8_t; };
+template <> struct Word<2> { using T = uint16_t; };
+template <> struct Word<4> { using T = uint32_t; };
+template <> struct Word<8> { using T = uint2; };
+template <> struct Word<16> { using T = uint4; };
+
+// ---------------------------------------------------------------------------
+// Workspace layout of one distribute (host computes, kernels consume).
+// ---------------------------------------------------------------------------
+struct DistArgs {
+  const void* rids;       // uint32 or uint64 rids
+  uint64_t n_out;
+  uint64_t n_src;
+  uint32_t s;             // log2 run length
+  uint32_t K;             // number of runs
+  uint32_t G;             // number of distribute chunks (CTAs)
+  uint64_t chunk;         // rids per chunk
+  uint32_t* counts;       // [K*G] bucket-major counts, then exclusive offsets
+  uint32_t* run_start;    // [K+1] start of each run in the pair array
+  void* pairs;            // [n_out] packed pairs (4 or 8 bytes)
+  uint32_t pair_bytes;
+  // optional payload carried with each pair (join: the fact row)
+  const uint8_t* pay_src;
+  uint8_t* pay_dst;
+  uint32_t pay_bytes;
+  uint32_t hist_smem;     // 1: shared-memory histogram of K counters
+  unsigned long long* status;
+};
+
+struct ProbeArgs {
+  const uint8_t* src;     // staged source records
+  uint64_t n_src;
+  uint32_t rec;
+  uint32_t s;
+  uint32_t K;
+  const uint32_t* run_start;   // [K+1]
+  const void* pairs;
+  uint32_t pair_bytes;
+  const uint8_t* pay;          // [n_out * pay_bytes] or null
+  uint32_t pay_bytes;
+  uint8_t* dst;                // row r at dst + r*row_bytes
+  uint32_t row_bytes;          // pay_bytes + rec
+  uint32_t slot_pairs;         // pairs per stage
+  uint32_t region_cap;         // bytes reserved for a region in a stage
+  uint32_t slot_bytes;         // total bytes per stage
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
+                                cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
+                          uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
+                          unsigned long long* status, cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos,
+                                uint64_t n, uint8_t* dst, uint64_t n_dst, uint32_t W,
+                                int sm_count, cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_unpack_pairs(const DistArgs& a, uint64_t* pairs_out, uint64_t* run_start_out,
+                                cudaStream_t st, uint32_t* nlaunch);
+
+}  // namespace dpg

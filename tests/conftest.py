@@ -8,6 +8,13 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_sessionstart(session):
+    # Build (or confirm fresh) every native artefact in-tree before any test
+    # imports the product package; a no-op when nothing changed.
+    from tools.buildall import build_all
+    build_all()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: full-size configurations")

@@ -1,0 +1,110 @@
+"""Host-side tests of the C ABI (no GPU): the library loads, exports every
+symbol include/dpg.h declares, validates arguments before touching CUDA, and
+plans run lengths per the paper's constraints."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def dpg():
+    from tools.buildall import build_dpg
+    build_dpg()
+    import paper_cs_0308004_b200 as m
+    return m
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "dpg.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dpg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(dpg):
+    declared = _declared_symbols()
+    assert "dpg_retrieve" in declared and "dpg_fk_join" in declared
+    out = subprocess.check_output(["nm", "-D", "--defined-only", dpg.LIB_PATH], text=True)
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    for s in declared:
+        assert hasattr(dpg.raw_lib(), s)
+    assert set(dpg.EXPORTED) <= set(declared)
+
+
+def test_library_is_sm100a_only(dpg):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", dpg.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", dpg.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    # TMA bulk copies in the probe-gather kernel
+    assert "UBLKCP" in sass
+
+
+def test_status_strings(dpg):
+    lib = dpg.raw_lib()
+    assert lib.dpg_status_string(0) == b"DPG_OK"
+    assert lib.dpg_status_string(2) == b"DPG_ERR_RID_RANGE"
+    assert lib.dpg_version() >= 1
+
+
+def test_argument_validation_before_any_cuda_call(dpg):
+    lib = dpg.raw_lib()
+    p = ctypes.c_void_p(0x10000)
+    q = ctypes.c_void_p(0x90000000)
+    r = ctypes.c_void_p(0x40000000)
+    # rec == 0
+    assert lib.dpg_retrieve(p, 0, 10, r, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    # n_out == 0: no-op
+    assert lib.dpg_retrieve(None, 100, 10, None, 0, None, None) == dpg.DPG_OK
+    # NULL pointer with nonzero count
+    assert lib.dpg_retrieve(None, 100, 10, r, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve(p, 100, 10, None, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve(p, 100, 10, r, 10, None, None) == dpg.DPG_ERR_INVALID_ARG
+    # n_src == 0 with n_out > 0
+    assert lib.dpg_retrieve(p, 100, 0, r, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    # dst overlapping src (in-place is not the paper's problem)
+    assert lib.dpg_retrieve(p, 100, 10, r, 10, ctypes.c_void_p(0x10000 + 500), None) == \
+        dpg.DPG_ERR_INVALID_ARG
+    # dst overlapping rids
+    assert lib.dpg_retrieve(p, 4, 10, r, 10, r, None) == dpg.DPG_ERR_INVALID_ARG
+    # n_out >= 2^32
+    assert lib.dpg_retrieve(p, 1, 10, r, 1 << 32, q, None) == dpg.DPG_ERR_UNSUPPORTED
+    # byte-size overflow
+    assert lib.dpg_retrieve(p, 1 << 40, 1 << 30, r, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve_direct(p, 0, 10, r, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_fk_join(p, 16, 10, r, None, 64, 10, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_scatter_rows(p, 0, r, 10, q, 10, None) == dpg.DPG_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("rec,n,L,K", [
+    (100, 65536, 128, 512),        # config 1: runs shrink for load balance
+    (100, 1048576, 1024, 1024),    # config 2: one 100 KB run per stage
+    (64, 16777216, 1024, 16384),   # config 3/4 dims at rec 64
+    (256, 16777216, 256, 65536),
+])
+def test_plan_run_length(dpg, rec, n, L, K):
+    p = dpg.dpg_plan(rec, n, n, 0, 148)
+    assert p["run_len"] == L and p["num_runs"] == K
+    assert p["run_len"] & (p["run_len"] - 1) == 0            # power of two
+    assert p["smem_bytes"] <= 232448                          # two stages fit one SM
+    assert p["slot_pairs"] >= p["run_len"]                    # a permutation's run fits one stage
+    assert p["run_len"] * rec <= (p["smem_bytes"] - 128) // 2
+
+
+def test_plan_pair_packing_and_overrides(dpg):
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20)["pair_bytes"] == 4     # 10 + 20 bits
+    assert dpg.dpg_plan(64, 1 << 24, 1 << 26)["pair_bytes"] == 8      # 10 + 26 bits
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8)["pair_bytes"] == 8
+    p = dpg.dpg_plan(3, 12, 12, log2_run=2)
+    assert p["run_len"] == 4 and p["num_runs"] == 3                   # Fig. 2 geometry
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_plan(0, 10, 10)
+    j = dpg.dpg_plan(64, 1 << 24, 1 << 26, pay_bytes=16)
+    assert j["pay_bytes"] == 16 and j["word_bytes"] == 16
