@@ -77,6 +77,9 @@ typedef struct {
     uint32_t grid_probe;    /* CTAs of the persistent probe-gather kernel       */
     uint32_t hist_in_smem;  /* 1: per-CTA run histogram in shared memory        */
     uint32_t pay_bytes;     /* payload bytes carried per pair (join: fact row)  */
+    uint32_t path;          /* 1 = one persistent cooperative kernel (fused.cu)
+                               2 = distribute kernels + probe-gather kernel     */
+    uint32_t nstages;       /* shared-memory stages of the probe-gather pipeline */
     uint32_t reserved;
 } dpg_plan_t;
 
@@ -88,7 +91,8 @@ typedef struct {
     uint32_t grid_probe;
     uint32_t pair_bytes;    /* force 8-byte pairs                               */
     uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
-    uint32_t reserved[3];
+    uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel */
+    uint32_t reserved[2];
 } dpg_options_t;
 
 /* Build the plan the library would use (host only; sm_count <= 0 queries the

@@ -57,7 +57,7 @@ class Plan(ctypes.Structure):
         ("run_len", ctypes.c_uint64), ("num_runs", ctypes.c_uint64)] + [
         (n, ctypes.c_uint32) for n in ("word_bytes", "slot_pairs", "smem_bytes",
                                        "grid_distribute", "grid_probe", "hist_in_smem",
-                                       "pay_bytes", "reserved")]
+                                       "pay_bytes", "path", "nstages", "reserved")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -65,8 +65,8 @@ class Plan(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("log2_run", "grid_distribute", "grid_probe",
-                                               "pair_bytes", "hist_mode")] + [
-        ("reserved", ctypes.c_uint32 * 3)]
+                                               "pair_bytes", "hist_mode", "path")] + [
+        ("reserved", ctypes.c_uint32 * 2)]
 
 
 _P, _U, _S, _I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
@@ -183,7 +183,7 @@ def _rid_tensor(t, name="rids"):
 
 
 def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0, grid_probe=0,
-                 pair_bytes=0, hist_mode=0):
+                 pair_bytes=0, hist_mode=0, path=0):
     """``dst[i] = src[rids[i]]`` by DPG.  src: uint8 CUDA [n_src, rec]; rids:
     int32/uint32 CUDA [n_out].  Returns dst (uint8 [n_out, rec])."""
     torch = _torch()
@@ -194,7 +194,7 @@ def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0
     if dst is None:
         dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
     o = _options(log2_run=log2_run, grid_distribute=grid_distribute, grid_probe=grid_probe,
-                 pair_bytes=pair_bytes, hist_mode=hist_mode)
+                 pair_bytes=pair_bytes, hist_mode=hist_mode, path=path)
     _check(_lib.dpg_retrieve_ex(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
                                 dst.data_ptr(), _stream_ptr(stream), _ref(o)), "dpg_retrieve")
     return dst

@@ -116,12 +116,83 @@ dpg_status_t dist_geometry(uint64_t K, uint64_t n_out, const dpg_options_t* opt,
   return DPG_OK;
 }
 
+// Plan for the single persistent kernel (fused.cu): S = 4 stages of
+// (run records + 1.5 L pairs), bucket_start[K+1] resident in shared memory,
+// the last two stages doubling as Phase I scratch (16 warp histograms of K
+// u16 + K u32 CTA bases).  Eligible when that fits, the per-CTA rid chunk
+// fits u16 counters, and no payload rides with the pairs.
+constexpr uint32_t kFusedStages = 4;
+constexpr uint32_t kFusedHdr = 512;
+constexpr uint32_t kFusedWarps = 16;
+
+bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
+                const dpg_options_t* opt, int sm, dpg_plan_t* p) {
+  if (pay) return false;
+  const uint64_t chunk = (n_out + sm - 1) / sm;
+  if (chunk > 65535 || n_out == 0) return false;
+  const uint32_t pos_bits = bit_length(n_out - 1);
+  const bool force8 = opt && opt->pair_bytes == 8;
+  auto fits = [&](uint32_t s, dpg_plan_t* q) -> bool {
+    const uint64_t L = 1ull << s;
+    const uint64_t K = (n_src + L - 1) >> s;
+    const uint32_t pb = (!force8 && s + pos_bits <= 32) ? 4u : 8u;
+    const uint64_t sp = std::max<uint64_t>(32, L + L / 2);
+    const uint64_t region_cap = align_up(L * rec + 32, 16);
+    const uint64_t stage = align_up(region_cap + sp * pb + 32, 128);
+    const uint64_t bs = align_up((K + 1) * 4, 128);
+    const uint64_t smem = kFusedHdr + bs + kFusedStages * stage;
+    const uint64_t scratch = (uint64_t)kFusedWarps * K * 2 + K * 4;
+    if (smem > kSmemLimit || scratch > 2 * stage) return false;
+    q->log2_run = s;
+    q->run_len = L;
+    q->num_runs = K;
+    q->pair_bytes = pb;
+    q->slot_pairs = (uint32_t)sp;
+    q->smem_bytes = (uint32_t)smem;
+    q->nstages = kFusedStages;
+    q->reserved = (uint32_t)stage;  // stage bytes (internal)
+    return true;
+  };
+  dpg_plan_t q;
+  std::memset(&q, 0, sizeof(q));
+  const uint32_t s_src = bit_length(std::max<uint64_t>(n_src, 1) - 1);
+  int s = -1;
+  if (opt && opt->log2_run) {
+    if (!fits(opt->log2_run, &q)) return false;
+    s = (int)opt->log2_run;
+  } else {
+    for (int t = (int)std::min<uint32_t>(s_src, 24); t >= 0; --t)
+      if (fits((uint32_t)t, &q)) { s = t; break; }
+    if (s < 0) return false;
+    const uint64_t want_runs = 4ull * (uint64_t)sm;
+    while (s > 0 && ((n_src + (1ull << s) - 1) >> s) < want_runs &&
+           ((1ull << (s - 1)) * rec) >= 8192)
+      --s;
+    if (!fits((uint32_t)s, &q)) return false;
+  }
+  *p = q;
+  p->word_bytes = pow2_divisor(rec);
+  p->grid_distribute = (uint32_t)sm;
+  p->grid_probe = (uint32_t)sm;
+  p->hist_in_smem = 1;
+  p->path = 1;
+  return true;
+}
+
 dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                        const dpg_options_t* opt, int sm, dpg_plan_t* p) {
   if (rec == 0 || !p) return DPG_ERR_INVALID_ARG;
   if (n_out >= (1ull << 32) || n_src > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
   std::memset(p, 0, sizeof(*p));
   if (sm <= 0) sm = 148;
+  const uint32_t want_path = opt ? opt->path : 0;
+  if (want_path != 2 && !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
+      plan_fused(rec, n_src, n_out, pay, opt, sm, p))
+    return DPG_OK;
+  if (want_path == 1) return DPG_ERR_UNSUPPORTED;
+  std::memset(p, 0, sizeof(*p));
+  p->path = 2;
+  p->nstages = 2;
   const uint64_t nsrc = std::max<uint64_t>(n_src, 1);
   const uint32_t pos_bits = bit_length(n_out > 0 ? n_out - 1 : 0);
   const bool force8 = opt && opt->pair_bytes == 8;
@@ -209,6 +280,63 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
   return DPG_OK;
 }
 
+// Persistent per-(device, stream) workspace of the fused kernel:
+// [grid barrier (2 u32) | run totals (K u32) | pairs].  The kernel leaves the
+// barrier and the totals zero on exit, so they are zeroed once, at allocation.
+struct PersistWS {
+  uint8_t* base = nullptr;
+  uint64_t counters = 0;  // bytes of the zero-invariant prefix
+  uint64_t bytes = 0;
+};
+std::mutex g_ws_mu;
+std::vector<std::pair<std::pair<int, cudaStream_t>, PersistWS>> g_ws;
+
+dpg_status_t persist_ws(cudaStream_t st, uint64_t K, uint64_t pair_bytes_total, uint32_t** gbar,
+                        uint32_t** total, void** pairs) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return DPG_ERR_CUDA;
+  const uint64_t need_ctr = align_up(256 + K * 4, 256);
+  const uint64_t need = need_ctr + align_up(pair_bytes_total + 64, 256);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  PersistWS* w = nullptr;
+  for (auto& kv : g_ws)
+    if (kv.first.first == dev && kv.first.second == st) w = &kv.second;
+  if (!w) {
+    g_ws.push_back({{dev, st}, PersistWS()});
+    w = &g_ws.back().second;
+  }
+  const uint64_t need_pairs = need - need_ctr;
+  const uint64_t have_pairs = w->bytes - w->counters;
+  if (w->counters < need_ctr || have_pairs < need_pairs) {
+    const uint64_t ctr = std::max(need_ctr, w->counters);
+    const uint64_t bytes = ctr + std::max(need_pairs, have_pairs);
+    if (w->base) cudaFreeAsync(w->base, st);
+    w->base = nullptr;
+    w->bytes = w->counters = 0;
+    void* b = nullptr;
+    if (cudaMallocAsync(&b, bytes, st) != cudaSuccess) {
+      cudaGetLastError();
+      return DPG_ERR_OOM;
+    }
+    if (cudaMemsetAsync(b, 0, ctr, st) != cudaSuccess) return DPG_ERR_CUDA;
+    w->base = (uint8_t*)b;
+    w->counters = ctr;
+    w->bytes = bytes;
+  }
+  *gbar = (uint32_t*)w->base;
+  *total = (uint32_t*)(w->base + 256);
+  *pairs = w->base + w->counters;
+  return DPG_OK;
+}
+
+void release_persist_ws() {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto& kv : g_ws)
+    if (kv.second.base) cudaFreeAsync(kv.second.base, kv.first.second);
+  g_ws.clear();
+}
+
 dpg_status_t cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return DPG_OK;
   cudaGetLastError();
@@ -238,9 +366,54 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   const int sm = current_sm_count();
   dpg_plan_t p;
   dpg_status_t ps = make_plan(rec, n_src, n_out, pay, opt, sm, &p);
+  if (ps == DPG_ERR_UNSUPPORTED && pay == 0 && !(opt && opt->log2_run) &&
+      rec * 2 + 64 > kSmemLimit / 2) {
+    // A record larger than a shared-memory stage is itself one sequential
+    // stream; DPG's run staging has nothing left to win, so such
+    // records take the direct path.
+    return dpg_retrieve_direct(src, rec, n_src, rids, n_out, dst, (dpg_stream_t)st);
+  }
   if (ps != DPG_OK) return ps;
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
+
+  if (p.path == 1) {
+    FusedArgs f;
+    std::memset(&f, 0, sizeof(f));
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* pairs = nullptr;
+    dpg_status_t ws = persist_ws(st, p.num_runs, n_out * (uint64_t)p.pair_bytes, &gbar, &total,
+                                 &pairs);
+    if (ws != DPG_OK) return ws;
+    f.src = (const uint8_t*)src;
+    f.n_src = n_src;
+    f.rec = (uint32_t)rec;
+    f.s = p.log2_run;
+    f.K = (uint32_t)p.num_runs;
+    f.nstages = p.nstages;
+    f.rids = rids;
+    f.n_out = n_out;
+    f.chunk = (n_out + p.grid_distribute - 1) / p.grid_distribute;
+    f.total = total;
+    f.gbar = gbar;
+    f.pairs = pairs;
+    f.pair_bytes = p.pair_bytes;
+    f.dst = (uint8_t*)dst;
+    f.row_bytes = (uint32_t)row;
+    f.slot_pairs = p.slot_pairs;
+    f.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
+    f.stage_bytes = p.reserved;
+    f.status = status;
+    uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
+    uint32_t nl = 0;
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    if (timed) cudaEventRecord(pe.e1, st);  // Phase I runs inside the same kernel
+    cudaError_t e = launch_fused(f, W, p.grid_probe, p.smem_bytes, st, &nl);
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_launches = nl;
+    return cuda_status(e);
+  }
 
   Workspace w;
   dpg_status_t as = alloc_workspace(p, n_out, st, &w);
@@ -545,6 +718,7 @@ void dpg_release_cache(void) {
     g_host_buf[k] = nullptr;
     g_host_cap[k] = 0;
   }
+  release_persist_ws();
 }
 
 }  // extern "C"

@@ -61,6 +61,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -129,7 +143,32 @@ struct ProbeArgs {
   uint32_t slot_bytes;         // total bytes per stage
 };
 
+// One persistent cooperative kernel for the whole path (fused.cu).
+struct FusedArgs {
+  const uint8_t* src;
+  uint64_t n_src;
+  uint32_t rec;
+  uint32_t s;            // log2 run length
+  uint32_t K;            // runs
+  uint32_t nstages;      // shared-memory stages (<= kMaxStages)
+  const uint32_t* rids;
+  uint64_t n_out;
+  uint64_t chunk;        // rids per CTA in the distribute phases
+  uint32_t* total;       // [K] run totals; zero on entry, restored to zero on exit
+  uint32_t* gbar;        // [2] grid barrier (count, generation), persistent
+  void* pairs;           // [n_out] pairs (+ slack for 16-byte bulk copies)
+  uint32_t pair_bytes;
+  uint8_t* dst;
+  uint32_t row_bytes;
+  uint32_t slot_pairs;   // pairs per stage
+  uint32_t region_cap;   // bytes of a stage reserved for the run's records
+  uint32_t stage_bytes;  // bytes per stage
+  unsigned long long* status;
+};
+
 // Launchers (return cudaError_t of the launch).
+cudaError_t launch_fused(const FusedArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
+                         cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                                 cudaStream_t st, uint32_t* nlaunch);

@@ -83,27 +83,32 @@ def test_argument_validation_before_any_cuda_call(dpg):
     assert lib.dpg_scatter_rows(p, 0, r, 10, q, 10, None) == dpg.DPG_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("rec,n,L,K", [
-    (100, 65536, 128, 512),        # config 1: runs shrink for load balance
-    (100, 1048576, 1024, 1024),    # config 2: one 100 KB run per stage
-    (64, 16777216, 1024, 16384),   # config 3/4 dims at rec 64
-    (256, 16777216, 256, 65536),
+@pytest.mark.parametrize("rec,n,L,K,path", [
+    (100, 65536, 128, 512, 1),        # config 1: runs shrink for load balance
+    (100, 1048576, 512, 2048, 1),     # config 2: fused kernel, 4 stages of 50 KB runs
+    (64, 16777216, 1024, 16384, 2),   # config 3/4 dims at rec 64: multi-kernel path
+    (256, 16777216, 256, 65536, 2),
 ])
-def test_plan_run_length(dpg, rec, n, L, K):
+def test_plan_run_length(dpg, rec, n, L, K, path):
     p = dpg.dpg_plan(rec, n, n, 0, 148)
-    assert p["run_len"] == L and p["num_runs"] == K
+    assert p["run_len"] == L and p["num_runs"] == K and p["path"] == path
     assert p["run_len"] & (p["run_len"] - 1) == 0            # power of two
     assert p["smem_bytes"] <= 232448                          # two stages fit one SM
     assert p["slot_pairs"] >= p["run_len"]                    # a permutation's run fits one stage
-    assert p["run_len"] * rec <= (p["smem_bytes"] - 128) // 2
+    assert p["run_len"] * rec <= (p["smem_bytes"] - 128) // p["nstages"]
+    m = dpg.dpg_plan(rec, n, n, 0, 148, path=2)
+    assert m["path"] == 2 and m["nstages"] == 2
 
 
 def test_plan_pair_packing_and_overrides(dpg):
-    assert dpg.dpg_plan(100, 1 << 20, 1 << 20)["pair_bytes"] == 4     # 10 + 20 bits
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20)["pair_bytes"] == 4     # 9 + 20 bits
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26)["pair_bytes"] == 8      # 10 + 26 bits
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8)["pair_bytes"] == 8
     p = dpg.dpg_plan(3, 12, 12, log2_run=2)
     assert p["run_len"] == 4 and p["num_runs"] == 3                   # Fig. 2 geometry
+    assert dpg.dpg_plan(64, 1 << 24, 1 << 26, path=2)["path"] == 2
+    with pytest.raises(dpg.DPGError):                                 # chunk > u16 counters
+        dpg.dpg_plan(64, 1 << 24, 1 << 26, path=1)
     with pytest.raises(dpg.DPGError):
         dpg.dpg_plan(0, 10, 10)
     j = dpg.dpg_plan(64, 1 << 24, 1 << 26, pay_bytes=16)

@@ -97,7 +97,7 @@ def _sweep():
             n_out = int(rng.integers(0, n_src + 1))
         else:
             n_out = int(rng.integers(0, 2 * n_src + 2))
-        max_s = max(0, min(14, int(np.log2(200000 // rec))))
+        max_s = max(0, min(14, int(np.log2(90000 // rec))))
         log2_run = int(rng.integers(0, max_s + 1)) if k % 3 else 0
         cases.append((k, n_src, rec, n_out, kind, log2_run))
     return cases
@@ -122,6 +122,23 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
     dpg.dpg_sync_status()
 
 
+@pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
+@pytest.mark.parametrize("path", [1, 2])
+def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path):
+    """Both execution paths (one fused cooperative kernel; distribute kernels +
+    probe-gather kernel) on the same cases; path 1 is skipped where it does
+    not apply (its planner refuses with DPG_ERR_UNSUPPORTED)."""
+    src, rids = _case(k, n_src, rec, n_out, kind)
+    try:
+        p = dpg.dpg_plan(rec, n_src, n_out, log2_run=log2_run, path=path)
+    except dpg.DPGError:
+        pytest.skip("path not applicable")
+    assert p["path"] == path
+    got = host(dpg.dpg_retrieve(dev(src), dev(rids), log2_run=log2_run, path=path))
+    assert np.array_equal(got, oracle.retrieve(src, rids))
+    dpg.dpg_sync_status()
+
+
 @pytest.mark.parametrize("hist_mode", [1, 2])
 def test_histogram_modes_agree(dpg, hist_mode):
     src, rids = _case(7, 50000, 24, 70000, "repl")
@@ -137,6 +154,12 @@ def test_output_invariant_under_run_length_and_grid(dpg):
         for gp in (1, 5, 148):
             got = host(dpg.dpg_retrieve(s, r, log2_run=log2_run, grid_probe=gp))
             assert np.array_equal(got, want), (log2_run, gp)
+        try:
+            dpg.dpg_plan(20, 30000, 30000, log2_run=log2_run, path=1)
+        except dpg.DPGError:
+            continue
+        got = host(dpg.dpg_retrieve(s, r, log2_run=log2_run, path=1))
+        assert np.array_equal(got, want), (log2_run, "fused")
 
 
 @pytest.mark.parametrize("soff,doff", [(1, 0), (0, 3), (4, 8), (12, 5), (8, 8)])
