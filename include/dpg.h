@@ -80,6 +80,13 @@ typedef struct {
     uint32_t path;          /* 1 = one persistent cooperative kernel (fused.cu)
                                2 = distribute kernels + probe-gather kernel     */
     uint32_t nstages;       /* shared-memory stages of the probe-gather pipeline */
+    uint32_t stage_bytes;   /* bytes per stage                                  */
+    uint32_t gather;        /* 1 = probe writes rows straight to dst (rows are
+                               whole 32-B sectors); 2 = INTERNAL file + gather
+                               (Fig. 1 literally; rows straddle sectors)       */
+    uint32_t npre;          /* source runs prefetched before Phase I (fused)    */
+    uint32_t rid_cache;     /* 1: each CTA's rid chunk is staged in smem (fused) */
+    uint32_t hist_warps;    /* warps owning a private run histogram (fused)     */
     uint32_t reserved;
 } dpg_plan_t;
 
@@ -92,7 +99,8 @@ typedef struct {
     uint32_t pair_bytes;    /* force 8-byte pairs                               */
     uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
     uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel */
-    uint32_t reserved[2];
+    uint32_t gather;        /* 0 auto, 1 force direct-to-dst, 2 force INTERNAL  */
+    uint32_t reserved;
 } dpg_options_t;
 
 /* Build the plan the library would use (host only; sm_count <= 0 queries the
@@ -181,6 +189,12 @@ uint32_t dpg_last_launch_count(void);
  * synchronises those events, returns the summed milliseconds and the number
  * of calls since the last read, and clears the record. */
 void dpg_phase_timing(int enable);
+
+/* Profiling only: when device_buf (>= grid*8 uint64) is non-NULL, the fused
+ * kernel writes per-CTA %globaltimer stamps at its phase boundaries (start,
+ * Phase I count done, barrier 1, scatter done, barrier 2, end).  NULL turns
+ * it off. */
+void dpg_debug_phase_stamps(void *device_buf);
 dpg_status_t dpg_phase_times(double *distribute_ms, double *probe_gather_ms, uint32_t *calls);
 
 int dpg_version(void);

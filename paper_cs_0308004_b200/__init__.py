@@ -39,7 +39,7 @@ EXPORTED = (
     "dpg_plan", "dpg_retrieve", "dpg_retrieve_ex", "dpg_retrieve_direct", "dpg_fk_join",
     "dpg_fk_join_ex", "dpg_distribute", "dpg_scatter_rows", "dpg_retrieve_host",
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
-    "dpg_version", "dpg_phase_timing", "dpg_phase_times",
+    "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
 )
 
 
@@ -57,7 +57,9 @@ class Plan(ctypes.Structure):
         ("run_len", ctypes.c_uint64), ("num_runs", ctypes.c_uint64)] + [
         (n, ctypes.c_uint32) for n in ("word_bytes", "slot_pairs", "smem_bytes",
                                        "grid_distribute", "grid_probe", "hist_in_smem",
-                                       "pay_bytes", "path", "nstages", "reserved")]
+                                       "pay_bytes", "path", "nstages", "stage_bytes",
+                                       "gather", "npre", "rid_cache", "hist_warps",
+                                       "reserved")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -65,8 +67,8 @@ class Plan(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("log2_run", "grid_distribute", "grid_probe",
-                                               "pair_bytes", "hist_mode", "path")] + [
-        ("reserved", ctypes.c_uint32 * 2)]
+                                               "pair_bytes", "hist_mode", "path", "gather",
+                                               "reserved")]
 
 
 _P, _U, _S, _I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
@@ -183,7 +185,7 @@ def _rid_tensor(t, name="rids"):
 
 
 def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0, grid_probe=0,
-                 pair_bytes=0, hist_mode=0, path=0):
+                 pair_bytes=0, hist_mode=0, path=0, gather=0):
     """``dst[i] = src[rids[i]]`` by DPG.  src: uint8 CUDA [n_src, rec]; rids:
     int32/uint32 CUDA [n_out].  Returns dst (uint8 [n_out, rec])."""
     torch = _torch()
@@ -194,7 +196,7 @@ def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0
     if dst is None:
         dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
     o = _options(log2_run=log2_run, grid_distribute=grid_distribute, grid_probe=grid_probe,
-                 pair_bytes=pair_bytes, hist_mode=hist_mode, path=path)
+                 pair_bytes=pair_bytes, hist_mode=hist_mode, path=path, gather=gather)
     _check(_lib.dpg_retrieve_ex(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
                                 dst.data_ptr(), _stream_ptr(stream), _ref(o)), "dpg_retrieve")
     return dst

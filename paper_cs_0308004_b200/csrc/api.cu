@@ -17,6 +17,7 @@ constexpr uint32_t kBarBytes = 128;
 constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives in smem
 
 thread_local uint32_t t_launches = 0;
+unsigned long long* g_debug_ts = nullptr;  // profiling: per-CTA phase stamps of the fused kernel
 
 // ---- optional phase timing (events on the call's stream) --------------------
 std::mutex g_timing_mu;
@@ -128,21 +129,47 @@ constexpr uint32_t kFusedWarps = 16;
 bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                 const dpg_options_t* opt, int sm, dpg_plan_t* p) {
   if (pay) return false;
-  const uint64_t chunk = (n_out + sm - 1) / sm;
+  const uint64_t chunk = align_up((n_out + sm - 1) / sm, 4);
   if (chunk > 65535 || n_out == 0) return false;
   const uint32_t pos_bits = bit_length(n_out - 1);
   const bool force8 = opt && opt->pair_bytes == 8;
+  // Gather mode: rows that are whole 32-byte sectors go straight to dst;
+  // rows that straddle sectors go through INTERNAL (a scattered partial-sector
+  // write costs a DRAM read-modify-write on this HBM).
+  uint32_t gather = (rec % 32 == 0) ? 1u : 2u;
+  if (opt && opt->gather) gather = opt->gather;
+  if (gather == 2 && n_out * rec >= (1ull << 32) * 8) return false;
   auto fits = [&](uint32_t s, dpg_plan_t* q) -> bool {
     const uint64_t L = 1ull << s;
     const uint64_t K = (n_src + L - 1) >> s;
-    const uint32_t pb = (!force8 && s + pos_bits <= 32) ? 4u : 8u;
+    const uint32_t pb = gather == 2 ? (s <= 16 && !force8 ? 2u : 4u)
+                                    : ((!force8 && s + pos_bits <= 32) ? 4u : 8u);
     const uint64_t sp = std::max<uint64_t>(32, L + L / 2);
     const uint64_t region_cap = align_up(L * rec + 32, 16);
     const uint64_t stage = align_up(region_cap + sp * pb + 32, 128);
     const uint64_t bs = align_up((K + 1) * 4, 128);
     const uint64_t smem = kFusedHdr + bs + kFusedStages * stage;
-    const uint64_t scratch = (uint64_t)kFusedWarps * K * 2 + K * 4;
-    if (smem > kSmemLimit || scratch > 2 * stage) return false;
+    // Phase I scratch (warp histograms + CTA bases [+ the CTA's rid chunk])
+    // lives in the stages that are not prefetched into before Phase I.
+    // Fewer histogram warps when K is large (each owns K u16 counters).
+    if (smem > kSmemLimit) return false;
+    const uint64_t rcache = align_up(chunk, 4) * 4 + 16;
+    uint32_t npre = 0, rid_cache = 0, hwarps = 0;
+    for (uint32_t hwp : {kFusedWarps, kFusedWarps / 2, kFusedWarps / 4}) {
+      // a warp's u16 prefix must hold the CTA chunk share of the warps before it
+      if (chunk > 65535) break;
+      const uint64_t scratch = (uint64_t)hwp * K * 2 + align_up(K, 4) * 4;
+      if (scratch + rcache <= 2 * stage) { npre = 2; rid_cache = 1; }
+      else if (scratch <= 2 * stage) { npre = 2; }
+      else if (scratch + rcache <= kFusedStages * stage) { rid_cache = 1; }
+      else if (scratch > kFusedStages * stage) continue;
+      hwarps = hwp;
+      break;
+    }
+    if (!hwarps) return false;
+    q->npre = npre;
+    q->rid_cache = rid_cache;
+    q->hist_warps = hwarps;
     q->log2_run = s;
     q->run_len = L;
     q->num_runs = K;
@@ -150,7 +177,8 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     q->slot_pairs = (uint32_t)sp;
     q->smem_bytes = (uint32_t)smem;
     q->nstages = kFusedStages;
-    q->reserved = (uint32_t)stage;  // stage bytes (internal)
+    q->stage_bytes = (uint32_t)stage;
+    q->gather = gather;
     return true;
   };
   dpg_plan_t q;
@@ -382,9 +410,18 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     std::memset(&f, 0, sizeof(f));
     uint32_t *gbar = nullptr, *total = nullptr;
     void* pairs = nullptr;
-    dpg_status_t ws = persist_ws(st, p.num_runs, n_out * (uint64_t)p.pair_bytes, &gbar, &total,
+    // [pairs | inv | INTERNAL] (the last two only in gather mode 2)
+    const uint64_t pairs_sz = align_up(n_out * (uint64_t)p.pair_bytes + 64, 256);
+    const uint64_t inv_sz = p.gather == 2 ? align_up(n_out * 4, 256) : 0;
+    const uint64_t int_sz = p.gather == 2 ? align_up(n_out * rec + 64, 256) : 0;
+    dpg_status_t ws = persist_ws(st, p.num_runs, pairs_sz + inv_sz + int_sz, &gbar, &total,
                                  &pairs);
     if (ws != DPG_OK) return ws;
+    f.mode = p.gather == 2 ? 1 : 0;
+    if (f.mode == 1) {
+      f.inv = (uint32_t*)((uint8_t*)pairs + pairs_sz);
+      f.internal = (uint8_t*)pairs + pairs_sz + inv_sz;
+    }
     f.src = (const uint8_t*)src;
     f.n_src = n_src;
     f.rec = (uint32_t)rec;
@@ -393,7 +430,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.nstages = p.nstages;
     f.rids = rids;
     f.n_out = n_out;
-    f.chunk = (n_out + p.grid_distribute - 1) / p.grid_distribute;
+    f.chunk = align_up((n_out + p.grid_distribute - 1) / p.grid_distribute, 4);
     f.total = total;
     f.gbar = gbar;
     f.pairs = pairs;
@@ -402,14 +439,27 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.row_bytes = (uint32_t)row;
     f.slot_pairs = p.slot_pairs;
     f.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
-    f.stage_bytes = p.reserved;
+    f.stage_bytes = p.stage_bytes;
+    f.npre = p.npre;
+    f.rid_cache = (p.rid_cache && ((uintptr_t)rids % 16 == 0)) ? 1 : 0;
+    f.hist_warps = p.hist_warps;
     f.status = status;
-    uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
+    f.ts = g_debug_ts;
+    uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst |
+                              (f.mode == 1 ? (uintptr_t)f.internal : 0));
     uint32_t nl = 0;
     PhaseEvents pe;
     const bool timed = timing_begin(st, &pe);
     if (timed) cudaEventRecord(pe.e1, st);  // Phase I runs inside the same kernel
     cudaError_t e = launch_fused(f, W, p.grid_probe, p.smem_bytes, st, &nl);
+    if (e == cudaSuccess && f.mode == 1) {
+      // Phase III: gather "the next record from the j-th INTERNAL run",
+      // i.e. INTERNAL[inv[i]], writing the output rows sequentially; a full-
+      // occupancy launch of the direct-gather kernel over (INTERNAL, inv).
+      e = launch_direct(f.internal, n_out, (uint32_t)rec, f.inv, n_out, (uint8_t*)dst,
+                        pow2_divisor(rec | (uintptr_t)dst | (uintptr_t)f.internal), sm, status,
+                        st, &nl, /*streaming=*/true);
+    }
     if (timed) cudaEventRecord(pe.e2, st);
     t_launches = nl;
     return cuda_status(e);
@@ -480,6 +530,8 @@ extern "C" {
 int dpg_version(void) { return 1; }
 
 uint32_t dpg_last_launch_count(void) { return t_launches; }
+
+void dpg_debug_phase_stamps(void* device_buf) { g_debug_ts = (unsigned long long*)device_buf; }
 
 void dpg_phase_timing(int enable) {
   std::lock_guard<std::mutex> lk(g_timing_mu);

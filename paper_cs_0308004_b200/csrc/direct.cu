@@ -14,14 +14,18 @@ namespace dpg {
 
 static constexpr int kDirectThreads = 256;
 
-template <int W>
-__global__ void __launch_bounds__(kDirectThreads) k_direct(const uint8_t* __restrict__ src,
-                                                           uint64_t n_src, uint32_t rec,
-                                                           const uint32_t* __restrict__ rids,
-                                                           uint64_t n_out, uint8_t* __restrict__ dst,
-                                                           unsigned long long* status) {
+// STREAM: both sides are touched exactly once (the INTERNAL -> dst gather of
+// the three-phase DPG): loads and stores carry an L2 evict_first hint.
+template <int W, bool STREAM>
+__global__ void __launch_bounds__(kDirectThreads, 5) k_direct(const uint8_t* __restrict__ src,
+                                                              uint64_t n_src, uint32_t rec,
+                                                              const uint32_t* __restrict__ rids,
+                                                              uint64_t n_out,
+                                                              uint8_t* __restrict__ dst,
+                                                              unsigned long long* status) {
   using T = typename Word<W>::T;
-  constexpr int B = W >= 16 ? 4 : 8;  // rows in flight per lane per batch
+  const uint64_t pol = STREAM ? policy_evict_first() : 0;
+  constexpr int B = W >= 16 ? 2 : W == 8 ? 4 : 8;  // rows in flight per lane per batch
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -42,21 +46,29 @@ __global__ void __launch_bounds__(kDirectThreads) k_direct(const uint8_t* __rest
     }
     const uint32_t cnt = (uint32_t)min_u64(32, n_out - g0);
     if (R <= 32) {
-      for (uint32_t k0 = 0; k0 < 32; k0 += RPI * B) {
+      // bit rr of okm: row g0+rr exists and its rid is valid (lanes >= cnt have my_ok = 0)
+      const uint32_t okm = __ballot_sync(0xffffffffu, my_ok) & (lane_on ? 0xffffffffu : 0u);
+      const uint8_t* s_lw = src + lw * W;
+      uint8_t* d_row = dst + (g0 + lr) * rec + lw * W;
+      for (uint32_t k0 = 0; k0 < cnt; k0 += RPI * B) {
         T v[B];
-        bool ok[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
           const uint32_t rr = k0 + u * RPI + lr;
           const uint32_t r = __shfl_sync(0xffffffffu, my_r, rr & 31);
-          const uint32_t o = __shfl_sync(0xffffffffu, my_ok, rr & 31);
-          ok[u] = lane_on && rr < cnt && o;
-          if (ok[u]) v[u] = __ldg(reinterpret_cast<const T*>(src + (uint64_t)r * rec + lw * W));
+          if ((okm >> (rr & 31)) & (rr < 32)) {
+            const uint8_t* p = s_lw + (uint64_t)r * rec;
+            v[u] = STREAM ? HintIO<W>::ld(p, pol) : __ldg(reinterpret_cast<const T*>(p));
+          }
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
           const uint32_t rr = k0 + u * RPI + lr;
-          if (ok[u]) *reinterpret_cast<T*>(dst + (g0 + rr) * rec + lw * W) = v[u];
+          if ((okm >> (rr & 31)) & (rr < 32)) {
+            uint8_t* p = d_row + (uint64_t)(k0 + u * RPI) * rec;
+            if (STREAM) HintIO<W>::st(p, v[u], pol);
+            else *reinterpret_cast<T*>(p) = v[u];
+          }
         }
       }
     } else {
@@ -128,22 +140,31 @@ __global__ void __launch_bounds__(kDirectThreads) k_scatter_rows(const uint8_t* 
 static uint32_t grid_for(uint64_t n_rows, int sm_count) {
   uint64_t warps = (n_rows + 31) / 32;
   uint64_t blocks = (warps + (kDirectThreads / 32) - 1) / (kDirectThreads / 32);
-  uint64_t cap = (uint64_t)sm_count * 8;  // 8 x 256 threads = 64 warps per SM
+  uint64_t cap = (uint64_t)sm_count * 5;  // 5 x 256 threads = 40 warps per SM (launch bounds)
   return (uint32_t)max_u64(1, min_u64(blocks, cap));
+}
+
+template <bool STREAM>
+static void direct_w(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
+                     uint64_t n_out, uint8_t* dst, uint32_t W, uint32_t grid,
+                     unsigned long long* status, cudaStream_t st) {
+  switch (W) {
+    case 16: k_direct<16, STREAM><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 8: k_direct<8, STREAM><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 4: k_direct<4, STREAM><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    case 2: k_direct<2, STREAM><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+    default: k_direct<1, STREAM><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
+  }
 }
 
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
                           uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
-                          unsigned long long* status, cudaStream_t st, uint32_t* nl) {
+                          unsigned long long* status, cudaStream_t st, uint32_t* nl,
+                          bool streaming) {
   uint32_t grid = grid_for(n_out, sm_count);
   ++*nl;
-  switch (W) {
-    case 16: k_direct<16><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
-    case 8: k_direct<8><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
-    case 4: k_direct<4><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
-    case 2: k_direct<2><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
-    default: k_direct<1><<<grid, kDirectThreads, 0, st>>>(src, n_src, rec, rids, n_out, dst, status); break;
-  }
+  if (streaming) direct_w<true>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
+  else direct_w<false>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
   return cudaGetLastError();
 }
 

@@ -164,7 +164,69 @@ struct FusedArgs {
   uint32_t region_cap;   // bytes of a stage reserved for the run's records
   uint32_t stage_bytes;  // bytes per stage
   unsigned long long* status;
+  unsigned long long* ts;  // optional [grid * 8] %globaltimer stamps (profiling), or null
+  // mode 1 (three-phase, INTERNAL materialised as in Fig. 1):
+  uint32_t npre;         // stages whose source run is prefetched before Phase I (0..2)
+  uint32_t rid_cache;    // 1: the CTA's rid chunk is bulk-copied into shared memory
+  uint32_t hist_warps;   // warps owning a private run histogram in Phase I (4, 8 or 16)
+  uint32_t mode;         // 0: probe writes rows straight to dst; 1: probe -> INTERNAL -> gather
+  uint8_t* internal;     // [n_out * rec] INTERNAL file (mode 1)
+  uint32_t* inv;         // [n_out] INTERNAL slot of output row i (mode 1)
 };
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// W-byte global load / store with an L2 eviction-priority hint (W >= 4);
+// narrower words fall back to plain accesses.
+template <int W> struct HintIO {
+  using T = typename Word<W>::T;
+  static __device__ __forceinline__ T ld(const void* p, uint64_t) { return *reinterpret_cast<const T*>(p); }
+  static __device__ __forceinline__ void st(void* p, T v, uint64_t) { *reinterpret_cast<T*>(p) = v; }
+};
+template <> struct HintIO<4> {
+  static __device__ __forceinline__ uint32_t ld(const void* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+  }
+  static __device__ __forceinline__ void st(void* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+  }
+};
+template <> struct HintIO<8> {
+  static __device__ __forceinline__ uint2 ld(const void* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+  }
+  static __device__ __forceinline__ void st(void* p, uint2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "l"(pol) : "memory");
+  }
+};
+template <> struct HintIO<16> {
+  static __device__ __forceinline__ uint4 ld(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+  }
+  static __device__ __forceinline__ void st(void* p, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+  }
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_fused(const FusedArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
@@ -174,7 +236,8 @@ cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, u
                                 cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
                           uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
-                          unsigned long long* status, cudaStream_t st, uint32_t* nlaunch);
+                          unsigned long long* status, cudaStream_t st, uint32_t* nlaunch,
+                          bool streaming = false);
 cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos,
                                 uint64_t n, uint8_t* dst, uint64_t n_dst, uint32_t W,
                                 int sm_count, cudaStream_t st, uint32_t* nlaunch);

@@ -101,9 +101,13 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
 
 
 def test_plan_pair_packing_and_overrides(dpg):
-    assert dpg.dpg_plan(100, 1 << 20, 1 << 20)["pair_bytes"] == 4     # 9 + 20 bits
+    c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20)
+    assert c2["gather"] == 2 and c2["pair_bytes"] == 2                # INTERNAL mode: u16 locals
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, gather=1)["pair_bytes"] == 4   # 9 + 20 bits
+    assert dpg.dpg_plan(128, 1 << 20, 1 << 20)["gather"] == 1         # whole sectors
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26)["pair_bytes"] == 8      # 10 + 26 bits
-    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8)["pair_bytes"] == 8
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8, gather=1)["pair_bytes"] == 8
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8)["pair_bytes"] == 4   # u32 locals
     p = dpg.dpg_plan(3, 12, 12, log2_run=2)
     assert p["run_len"] == 4 and p["num_runs"] == 3                   # Fig. 2 geometry
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26, path=2)["path"] == 2

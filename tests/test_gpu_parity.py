@@ -123,18 +123,22 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
 
 
 @pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
-@pytest.mark.parametrize("path", [1, 2])
-def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path):
-    """Both execution paths (one fused cooperative kernel; distribute kernels +
-    probe-gather kernel) on the same cases; path 1 is skipped where it does
-    not apply (its planner refuses with DPG_ERR_UNSUPPORTED)."""
+@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0)])
+def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path, gather):
+    """Every execution path on the same cases: the fused cooperative kernel
+    writing rows straight to dst (gather 1) or through INTERNAL (gather 2),
+    and distribute kernels + probe-gather kernel (path 2).  A path is skipped
+    where its planner refuses with DPG_ERR_UNSUPPORTED."""
     src, rids = _case(k, n_src, rec, n_out, kind)
     try:
-        p = dpg.dpg_plan(rec, n_src, n_out, log2_run=log2_run, path=path)
+        p = dpg.dpg_plan(rec, n_src, n_out, log2_run=log2_run, path=path, gather=gather)
     except dpg.DPGError:
         pytest.skip("path not applicable")
     assert p["path"] == path
-    got = host(dpg.dpg_retrieve(dev(src), dev(rids), log2_run=log2_run, path=path))
+    if path == 1:
+        assert p["gather"] == gather
+    got = host(dpg.dpg_retrieve(dev(src), dev(rids), log2_run=log2_run, path=path,
+                                gather=gather))
     assert np.array_equal(got, oracle.retrieve(src, rids))
     dpg.dpg_sync_status()
 

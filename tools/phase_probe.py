@@ -1,0 +1,61 @@
+"""Profiling helper: per-CTA phase timeline of the fused DPG kernel from the
+%globaltimer stamps it writes when dpg_debug_phase_stamps() is set.
+
+    python tools/phase_probe.py [--config c2] [--reps 5]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--rec", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    import torch
+
+    import datagen
+    import paper_cs_0308004_b200 as dpg
+    w = datagen.make(args.config, rec=args.rec) if args.rec else datagen.make(args.config)
+    src = torch.from_numpy(w["src"]).cuda()
+    rids = torch.from_numpy(w["rids"].view(np.int32)).cuda()
+    out = torch.empty((rids.numel(), src.shape[1]), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    ts = torch.zeros(G * 8, dtype=torch.int64, device="cuda")
+    lib = dpg.raw_lib()
+    lib.dpg_debug_phase_stamps.argtypes = [ctypes.c_void_p]
+    lib.dpg_debug_phase_stamps.restype = None
+    for _ in range(3):
+        dpg.dpg_retrieve(src, rids, dst=out)
+    names = ["count", "barrier1", "scatter", "barrier2", "probe_gather"]
+    for rep in range(args.reps):
+        flush.fill_(1)
+        ts.zero_()
+        lib.dpg_debug_phase_stamps(ctypes.c_void_p(ts.data_ptr()))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dpg.dpg_retrieve(src, rids, dst=out)
+        e1.record()
+        torch.cuda.synchronize()
+        lib.dpg_debug_phase_stamps(None)
+        t = ts.view(G, 8)[:, :6].cpu().numpy().astype(np.float64)
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1e3  # us
+        line = [f"event {e0.elapsed_time(e1)*1e3:7.1f}us", f"start spread {rel[:,0].max():5.1f}"]
+        for k, n in enumerate(names):
+            d = rel[:, k + 1] - rel[:, k]
+            line.append(f"{n} med {np.median(d):6.1f} max {d.max():6.1f} (ends {rel[:, k+1].max():6.1f})")
+        print(" | ".join(line))
+    print("plan", dpg.dpg_plan(src.shape[1], src.shape[0], rids.numel(), sm_count=G))
+
+
+if __name__ == "__main__":
+    main()
