@@ -128,6 +128,17 @@ dpg_status_t dpg_retrieve_direct(const void *src, size_t rec_bytes, uint64_t n_s
                                  const uint32_t *rids, uint64_t n_out, void *dst,
                                  dpg_stream_t stream);
 
+/* dpg_retrieve_direct with L2 eviction hints: hint 0 plain, 1 loads and
+ * stores evict_first, 2 loads evict_last + stores evict_first (source staged
+ * in L2 beforehand, e.g. by dpg_l2_prefetch). */
+dpg_status_t dpg_retrieve_direct_ex(const void *src, size_t rec_bytes, uint64_t n_src,
+                                    const uint32_t *rids, uint64_t n_out, void *dst,
+                                    dpg_stream_t stream, int hint);
+
+/* Stage [ptr, ptr+bytes) into L2 with evict_last priority (bulk L2
+ * prefetches; asynchronous, no completion signal). */
+dpg_status_t dpg_l2_prefetch(const void *ptr, uint64_t bytes, dpg_stream_t stream);
+
 /* DPG-Move foreign-key join (section 4.2.1).  The fact
  * relation R is scanned in file order, so its join triples (k, rid_R, rid_F)
  * come in rid_R order; the foreign key names the dimension record
@@ -190,7 +201,7 @@ uint32_t dpg_last_launch_count(void);
  * of calls since the last read, and clears the record. */
 void dpg_phase_timing(int enable);
 
-/* Profiling only: when device_buf (>= grid*8 uint64) is non-NULL, the fused
+/* Profiling only: when device_buf (>= grid*16 uint64) is non-NULL, the fused
  * kernel writes per-CTA %globaltimer stamps at its phase boundaries (start,
  * Phase I count done, barrier 1, scatter done, barrier 2, end).  NULL turns
  * it off. */

@@ -40,6 +40,7 @@ EXPORTED = (
     "dpg_fk_join_ex", "dpg_distribute", "dpg_scatter_rows", "dpg_retrieve_host",
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
+    "dpg_retrieve_direct_ex", "dpg_l2_prefetch",
 )
 
 
@@ -84,6 +85,8 @@ _sigs = {
     "dpg_scatter_rows": [_P, _S, _P, _U, _P, _U, _P],
     "dpg_retrieve_host": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sync_status": [_P, _P],
+    "dpg_retrieve_direct_ex": [_P, _S, _U, _P, _U, _P, _P, _I],
+    "dpg_l2_prefetch": [_P, _U, _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -214,6 +217,27 @@ def dpg_retrieve_direct(src, rids, dst=None, stream=None):
     _check(_lib.dpg_retrieve_direct(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
                                     dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_direct")
     return dst
+
+
+def dpg_retrieve_direct_ex(src, rids, dst=None, stream=None, hint=0):
+    """Direct retrieval with L2 hints (0 plain, 1 stream, 2 L2-resident source)."""
+    torch = _torch()
+    src = _records(src, "src")
+    rids = _rid_tensor(rids)
+    n_src, rec = src.shape
+    n_out = rids.numel()
+    if dst is None:
+        dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
+    _check(_lib.dpg_retrieve_direct_ex(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
+                                       dst.data_ptr(), _stream_ptr(stream), hint),
+           "dpg_retrieve_direct_ex")
+    return dst
+
+
+def dpg_l2_prefetch(t, stream=None):
+    """Stage tensor t's bytes into L2 (evict_last)."""
+    _check(_lib.dpg_l2_prefetch(t.data_ptr(), t.numel() * t.element_size(), _stream_ptr(stream)),
+           "dpg_l2_prefetch")
 
 
 def dpg_fk_join(fact, fk_col, dim, out=None, stream=None, **opts):

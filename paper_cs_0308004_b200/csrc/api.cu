@@ -117,64 +117,46 @@ dpg_status_t dist_geometry(uint64_t K, uint64_t n_out, const dpg_options_t* opt,
   return DPG_OK;
 }
 
-// Plan for the single persistent kernel (fused.cu): S = 4 stages of
-// (run records + 1.5 L pairs), bucket_start[K+1] resident in shared memory,
-// the last two stages doubling as Phase I scratch (16 warp histograms of K
-// u16 + K u32 CTA bases).  Eligible when that fits, the per-CTA rid chunk
-// fits u16 counters, and no payload rides with the pairs.
+// Plan for the single persistent kernel (fused.cu): S = 4 stages, each one
+// run of L records plus its entries (capacity CAP = L + L/4 + 32: exact for
+// permutations, Poisson slack for rids drawn with replacement, overflow list
+// beyond), the counts of the CTA's own runs resident in shared memory, and the
+// CTA's rid chunk cached in a stage that is not prefetched into before Phase I.
 constexpr uint32_t kFusedStages = 4;
 constexpr uint32_t kFusedHdr = 512;
-constexpr uint32_t kFusedWarps = 16;
 
 bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                 const dpg_options_t* opt, int sm, dpg_plan_t* p) {
-  if (pay) return false;
+  if (pay || n_out == 0) return false;
   const uint64_t chunk = align_up((n_out + sm - 1) / sm, 4);
-  if (chunk > 65535 || n_out == 0) return false;
   const uint32_t pos_bits = bit_length(n_out - 1);
   const bool force8 = opt && opt->pair_bytes == 8;
   // Gather mode: rows that are whole 32-byte sectors go straight to dst;
-  // rows that straddle sectors go through INTERNAL (a scattered partial-sector
-  // write costs a DRAM read-modify-write on this HBM).
-  uint32_t gather = (rec % 32 == 0) ? 1u : 2u;
+  // rows that straddle sectors may go through INTERNAL (a scattered
+  // partial-sector write costs a DRAM read-modify-write on this HBM).
+  uint32_t gather = 1;
   if (opt && opt->gather) gather = opt->gather;
-  if (gather == 2 && n_out * rec >= (1ull << 32) * 8) return false;
   auto fits = [&](uint32_t s, dpg_plan_t* q) -> bool {
     const uint64_t L = 1ull << s;
     const uint64_t K = (n_src + L - 1) >> s;
+    const uint64_t cap = align_up(L + L / 4 + 32, 8);
+    if (K * cap >= (1ull << 32)) return false;
     const uint32_t pb = gather == 2 ? (s <= 16 && !force8 ? 2u : 4u)
                                     : ((!force8 && s + pos_bits <= 32) ? 4u : 8u);
-    const uint64_t sp = std::max<uint64_t>(32, L + L / 2);
     const uint64_t region_cap = align_up(L * rec + 32, 16);
-    const uint64_t stage = align_up(region_cap + sp * pb + 32, 128);
-    const uint64_t bs = align_up((K + 1) * 4, 128);
-    const uint64_t smem = kFusedHdr + bs + kFusedStages * stage;
-    // Phase I scratch (warp histograms + CTA bases [+ the CTA's rid chunk])
-    // lives in the stages that are not prefetched into before Phase I.
-    // Fewer histogram warps when K is large (each owns K u16 counters).
+    const uint64_t stage = align_up(region_cap + cap * pb + 32, 128);
+    const uint64_t max_own = (K + sm - 1) / sm;
+    const uint64_t smem = kFusedHdr + align_up(max_own * 4, 128) + kFusedStages * stage;
     if (smem > kSmemLimit) return false;
-    const uint64_t rcache = align_up(chunk, 4) * 4 + 16;
-    uint32_t npre = 0, rid_cache = 0, hwarps = 0;
-    for (uint32_t hwp : {kFusedWarps, kFusedWarps / 2, kFusedWarps / 4}) {
-      // a warp's u16 prefix must hold the CTA chunk share of the warps before it
-      if (chunk > 65535) break;
-      const uint64_t scratch = (uint64_t)hwp * K * 2 + align_up(K, 4) * 4;
-      if (scratch + rcache <= 2 * stage) { npre = 2; rid_cache = 1; }
-      else if (scratch <= 2 * stage) { npre = 2; }
-      else if (scratch + rcache <= kFusedStages * stage) { rid_cache = 1; }
-      else if (scratch > kFusedStages * stage) continue;
-      hwarps = hwp;
-      break;
-    }
-    if (!hwarps) return false;
+    const uint32_t npre = std::min<uint32_t>(2, (uint32_t)std::min<uint64_t>(K, kFusedStages - 1));
     q->npre = npre;
-    q->rid_cache = rid_cache;
-    q->hist_warps = hwarps;
+    q->rid_cache = (chunk * 4 + 16 <= (kFusedStages - npre) * stage) ? 1 : 0;
+    q->hist_warps = 0;
     q->log2_run = s;
     q->run_len = L;
     q->num_runs = K;
     q->pair_bytes = pb;
-    q->slot_pairs = (uint32_t)sp;
+    q->slot_pairs = (uint32_t)cap;
     q->smem_bytes = (uint32_t)smem;
     q->nstages = kFusedStages;
     q->stage_bytes = (uint32_t)stage;
@@ -411,16 +393,20 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     uint32_t *gbar = nullptr, *total = nullptr;
     void* pairs = nullptr;
     // [pairs | inv | INTERNAL] (the last two only in gather mode 2)
-    const uint64_t pairs_sz = align_up(n_out * (uint64_t)p.pair_bytes + 64, 256);
+    // [pairs (K*CAP entries) | overflow list | inv | INTERNAL] (the last two
+    // only in gather mode 2)
+    const uint64_t slots = p.num_runs * (uint64_t)p.slot_pairs;
+    const uint64_t pairs_sz = align_up(slots * p.pair_bytes + 64, 256);
+    const uint64_t ovf_sz = align_up(n_out * 8, 256);
     const uint64_t inv_sz = p.gather == 2 ? align_up(n_out * 4, 256) : 0;
-    const uint64_t int_sz = p.gather == 2 ? align_up(n_out * rec + 64, 256) : 0;
-    dpg_status_t ws = persist_ws(st, p.num_runs, pairs_sz + inv_sz + int_sz, &gbar, &total,
-                                 &pairs);
+    const uint64_t int_sz = p.gather == 2 ? align_up(slots * rec + 64, 256) : 0;
+    dpg_status_t ws = persist_ws(st, p.num_runs, pairs_sz + ovf_sz + inv_sz + int_sz, &gbar,
+                                 &total, &pairs);
     if (ws != DPG_OK) return ws;
     f.mode = p.gather == 2 ? 1 : 0;
     if (f.mode == 1) {
-      f.inv = (uint32_t*)((uint8_t*)pairs + pairs_sz);
-      f.internal = (uint8_t*)pairs + pairs_sz + inv_sz;
+      f.inv = (uint32_t*)((uint8_t*)pairs + pairs_sz + ovf_sz);
+      f.internal = (uint8_t*)pairs + pairs_sz + ovf_sz + inv_sz;
     }
     f.src = (const uint8_t*)src;
     f.n_src = n_src;
@@ -442,7 +428,9 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.stage_bytes = p.stage_bytes;
     f.npre = p.npre;
     f.rid_cache = (p.rid_cache && ((uintptr_t)rids % 16 == 0)) ? 1 : 0;
-    f.hist_warps = p.hist_warps;
+    f.cap = p.slot_pairs;
+    f.ovf = (uint64_t*)((uint8_t*)pairs + pairs_sz);
+    f.max_own = (uint32_t)((p.num_runs + p.grid_probe - 1) / p.grid_probe);
     f.status = status;
     f.ts = g_debug_ts;
     uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst |
@@ -456,9 +444,11 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       // Phase III: gather "the next record from the j-th INTERNAL run",
       // i.e. INTERNAL[inv[i]], writing the output rows sequentially; a full-
       // occupancy launch of the direct-gather kernel over (INTERNAL, inv).
-      e = launch_direct(f.internal, n_out, (uint32_t)rec, f.inv, n_out, (uint8_t*)dst,
-                        pow2_divisor(rec | (uintptr_t)dst | (uintptr_t)f.internal), sm, status,
-                        st, &nl, /*streaming=*/true);
+      // (rows marked 0xFFFFFFFF were reported in Phase I or copied from the
+      // overflow list; the gather leaves them alone and reports nothing)
+      e = launch_direct(f.internal, slots, (uint32_t)rec, f.inv, n_out, (uint8_t*)dst,
+                        pow2_divisor(rec | (uintptr_t)dst | (uintptr_t)f.internal), sm, nullptr,
+                        st, &nl, /*hint=*/1);
     }
     if (timed) cudaEventRecord(pe.e2, st);
     t_launches = nl;
@@ -604,6 +594,22 @@ dpg_status_t dpg_fk_join(const void* fact, size_t fact_bytes, uint64_t n_fact,
 dpg_status_t dpg_retrieve_direct(const void* src, size_t rec_bytes, uint64_t n_src,
                                  const uint32_t* rids, uint64_t n_out, void* dst,
                                  dpg_stream_t stream) {
+  return dpg_retrieve_direct_ex(src, rec_bytes, n_src, rids, n_out, dst, stream, 0);
+}
+
+dpg_status_t dpg_l2_prefetch(const void* ptr, uint64_t bytes, dpg_stream_t stream) {
+  t_launches = 0;
+  if (!bytes) return DPG_OK;
+  if (!ptr) return DPG_ERR_INVALID_ARG;
+  uint32_t nl = 0;
+  cudaError_t e = launch_l2_prefetch(ptr, bytes, current_sm_count(), (cudaStream_t)stream, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_retrieve_direct_ex(const void* src, size_t rec_bytes, uint64_t n_src,
+                                    const uint32_t* rids, uint64_t n_out, void* dst,
+                                    dpg_stream_t stream, int hint) {
   t_launches = 0;
   if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
   if (n_out == 0) return DPG_OK;
@@ -622,7 +628,7 @@ dpg_status_t dpg_retrieve_direct(const void* src, size_t rec_bytes, uint64_t n_s
   uint32_t nl = 0;
   cudaError_t e = launch_direct((const uint8_t*)src, n_src, (uint32_t)rec_bytes, rids, n_out,
                                 (uint8_t*)dst, W, current_sm_count(), status,
-                                (cudaStream_t)stream, &nl);
+                                (cudaStream_t)stream, &nl, hint);
   t_launches = nl;
   return cuda_status(e);
 }

@@ -14,18 +14,27 @@ namespace dpg {
 
 static constexpr int kDirectThreads = 256;
 
-// STREAM: both sides are touched exactly once (the INTERNAL -> dst gather of
-// the three-phase DPG): loads and stores carry an L2 evict_first hint.
-template <int W, bool STREAM>
-__global__ void __launch_bounds__(kDirectThreads, 5) k_direct(const uint8_t* __restrict__ src,
+// HINT 0: plain loads and stores.
+// HINT 1: both sides are touched exactly once (the INTERNAL -> dst gather of
+//         the three-phase DPG): loads and stores carry an L2 evict_first hint.
+// HINT 2: the source is an L2-resident run (the single-run DPG, whose run is
+//         the whole source, staged into L2): loads evict_last, stores
+//         evict_first so the output stream does not evict the run.
+template <int W, int HINT>
+__global__ void __launch_bounds__(kDirectThreads, 4) k_direct(const uint8_t* __restrict__ src,
                                                               uint64_t n_src, uint32_t rec,
                                                               const uint32_t* __restrict__ rids,
                                                               uint64_t n_out,
                                                               uint8_t* __restrict__ dst,
                                                               unsigned long long* status) {
   using T = typename Word<W>::T;
-  const uint64_t pol = STREAM ? policy_evict_first() : 0;
-  constexpr int B = W >= 16 ? 2 : W == 8 ? 4 : 8;  // rows in flight per lane per batch
+  const bool STREAM = HINT != 0;
+  const uint64_t pol = HINT ? policy_evict_first() : 0;
+  const uint64_t lpol = HINT == 2 ? policy_evict_last() : pol;
+  // rows in flight per lane per batch: up to 128 bytes of loads per lane, so a
+  // warp keeps a whole 32-row group (3.2 KB at 100-B rows) in flight
+  constexpr int B = W >= 16 ? 4 : W == 8 ? 8 : 16;
+  constexpr int B2 = W >= 16 ? 2 : 4;  // words in flight per lane for rows wider than a warp
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -58,7 +67,7 @@ __global__ void __launch_bounds__(kDirectThreads, 5) k_direct(const uint8_t* __r
           const uint32_t r = __shfl_sync(0xffffffffu, my_r, rr & 31);
           if ((okm >> (rr & 31)) & (rr < 32)) {
             const uint8_t* p = s_lw + (uint64_t)r * rec;
-            v[u] = STREAM ? HintIO<W>::ld(p, pol) : __ldg(reinterpret_cast<const T*>(p));
+            v[u] = STREAM ? HintIO<W>::ld(p, lpol) : __ldg(reinterpret_cast<const T*>(p));
           }
         }
 #pragma unroll
@@ -78,15 +87,15 @@ __global__ void __launch_bounds__(kDirectThreads, 5) k_direct(const uint8_t* __r
         if (!o) continue;
         const uint8_t* s = src + (uint64_t)r * rec;
         uint8_t* d = dst + (g0 + rr) * rec;
-        for (uint32_t w0 = 0; w0 < R; w0 += 32 * B) {
-          T v[B];
+        for (uint32_t w0 = 0; w0 < R; w0 += 32 * B2) {
+          T v[B2];
 #pragma unroll
-          for (int u = 0; u < B; ++u) {
+          for (int u = 0; u < B2; ++u) {
             const uint32_t w = w0 + u * 32 + lane;
             if (w < R) v[u] = __ldg(reinterpret_cast<const T*>(s + w * W));
           }
 #pragma unroll
-          for (int u = 0; u < B; ++u) {
+          for (int u = 0; u < B2; ++u) {
             const uint32_t w = w0 + u * 32 + lane;
             if (w < R) *reinterpret_cast<T*>(d + w * W) = v[u];
           }
@@ -140,11 +149,11 @@ __global__ void __launch_bounds__(kDirectThreads) k_scatter_rows(const uint8_t* 
 static uint32_t grid_for(uint64_t n_rows, int sm_count) {
   uint64_t warps = (n_rows + 31) / 32;
   uint64_t blocks = (warps + (kDirectThreads / 32) - 1) / (kDirectThreads / 32);
-  uint64_t cap = (uint64_t)sm_count * 5;  // 5 x 256 threads = 40 warps per SM (launch bounds)
+  uint64_t cap = (uint64_t)sm_count * 4;  // 4 x 256 threads = 32 warps per SM (launch bounds)
   return (uint32_t)max_u64(1, min_u64(blocks, cap));
 }
 
-template <bool STREAM>
+template <int STREAM>
 static void direct_w(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
                      uint64_t n_out, uint8_t* dst, uint32_t W, uint32_t grid,
                      unsigned long long* status, cudaStream_t st) {
@@ -160,11 +169,34 @@ static void direct_w(const uint8_t* src, uint64_t n_src, uint32_t rec, const uin
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
                           uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
                           unsigned long long* status, cudaStream_t st, uint32_t* nl,
-                          bool streaming) {
+                          int hint) {
   uint32_t grid = grid_for(n_out, sm_count);
   ++*nl;
-  if (streaming) direct_w<true>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
-  else direct_w<false>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
+  if (hint == 1) direct_w<1>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
+  else if (hint == 2) direct_w<2>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
+  else direct_w<0>(src, n_src, rec, rids, n_out, dst, W, grid, status, st);
+  return cudaGetLastError();
+}
+
+// Stage [p, p+bytes) into L2 with evict_last priority: 64 KB bulk prefetches
+// spread over the grid (cp.async.bulk.prefetch.L2; no completion signal).
+__global__ void k_l2_prefetch(const uint8_t* p, uint64_t bytes) {
+  const uint64_t pol = policy_evict_last();
+  const uint8_t* a0 = reinterpret_cast<const uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  const uint8_t* a1 = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p + bytes) & ~uintptr_t(15));
+  constexpr uint64_t kChunk = 64 << 10;
+  const uint64_t n = a1 > a0 ? (uint64_t)(a1 - a0) : 0;
+  for (uint64_t off = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kChunk; off < n;
+       off += (uint64_t)gridDim.x * blockDim.x * kChunk)
+    bulk_prefetch_l2(a0 + off, (uint32_t)min_u64(kChunk, n - off), pol);
+}
+
+cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cudaStream_t st,
+                               uint32_t* nl) {
+  const uint64_t chunks = (bytes + (64 << 10) - 1) / (64 << 10);
+  const uint32_t grid = (uint32_t)max_u64(1, min_u64((chunks + 127) / 128, (uint64_t)sm_count));
+  ++*nl;
+  k_l2_prefetch<<<grid, 128, 0, st>>>(reinterpret_cast<const uint8_t*>(p), bytes);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ __host__ __device__ __forceinline__ uint64_t max_u64(uint64_t a, uint64_t b) { r
 // whose rid was out of range; ~0 when clean.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void report_bad(unsigned long long* status, uint64_t i) {
-  atomicMin(status, (unsigned long long)i);
+  if (status) atomicMin(status, (unsigned long long)i);
 }
 
 // ---------------------------------------------------------------------------
@@ -155,7 +155,8 @@ struct FusedArgs {
   uint64_t n_out;
   uint64_t chunk;        // rids per CTA in the distribute phases
   uint32_t* total;       // [K] run totals; zero on entry, restored to zero on exit
-  uint32_t* gbar;        // [2] grid barrier (count, generation), persistent
+  uint32_t* gbar;        // [4] grid barrier (count, generation), overflow count, done
+                         //     counter; persistent, zero-restored by the kernel
   void* pairs;           // [n_out] pairs (+ slack for 16-byte bulk copies)
   uint32_t pair_bytes;
   uint8_t* dst;
@@ -168,11 +169,21 @@ struct FusedArgs {
   // mode 1 (three-phase, INTERNAL materialised as in Fig. 1):
   uint32_t npre;         // stages whose source run is prefetched before Phase I (0..2)
   uint32_t rid_cache;    // 1: the CTA's rid chunk is bulk-copied into shared memory
-  uint32_t hist_warps;   // warps owning a private run histogram in Phase I (4, 8 or 16)
+  uint32_t cap;          // fixed capacity of a run (entries); run b at [b*cap, b*cap + n_b)
+  uint32_t max_own;      // runs per CTA, ceil(K / grid)
+  uint64_t* ovf;         // [n_out] (i | rid << 32) of entries beyond a run's capacity
   uint32_t mode;         // 0: probe writes rows straight to dst; 1: probe -> INTERNAL -> gather
   uint8_t* internal;     // [n_out * rec] INTERNAL file (mode 1)
   uint32_t* inv;         // [n_out] INTERNAL slot of output row i (mode 1)
 };
+
+// Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
+// signal); src and bytes 16-byte aligned / multiples of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
@@ -237,7 +248,9 @@ cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, u
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,
                           uint64_t n_out, uint8_t* dst, uint32_t W, int sm_count,
                           unsigned long long* status, cudaStream_t st, uint32_t* nlaunch,
-                          bool streaming = false);
+                          int hint = 0);
+cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cudaStream_t st,
+                               uint32_t* nlaunch);
 cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos,
                                 uint64_t n, uint8_t* dst, uint64_t n_dst, uint32_t W,
                                 int sm_count, cudaStream_t st, uint32_t* nlaunch);

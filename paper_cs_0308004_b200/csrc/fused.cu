@@ -1,40 +1,32 @@
 // fused.cu -- the whole DPG path in one persistent cooperative kernel.
 //
-//   Phase I   Distribute (Fig. 1)
-//     B  count : each CTA histograms its contiguous chunk of the rid list by
-//                run r >> s into warp-private 16-bit counters (warp-level
-//                __match_any_sync aggregation, no shared-memory atomics), then
-//                reserves its share of every run with one global atomicAdd per
-//                run ("count the number of elements destined for each
-//                bucket").
-//     -- grid barrier --
-//     C  scan + scatter : every CTA scans the K run totals ("set bucket
-//                boundaries according to the statistics") and
-//                appends each rid to its run ("Append r to RID_RUN[run_num]",
-//                P:410).
-//     -- grid barrier --
+//   Phase I   Distribute (Fig. 1).  Every rid r goes to
+//        run r >> s ("the high order bits"): it reserves the next
+//        slot of its run with one atomicAdd on the run's cursor and appends
+//        (r - run*L, i) there ("Append r to RID_RUN[run_num]", plus the
+//        position i Phase III needs).  Runs have a fixed capacity
+//        CAP: a permutation puts exactly L rids into every run (the paper's
+//        sorting case), rids drawn with replacement exceed L only
+//        by a Poisson tail, and the rare excess -- or a skewed rid list
+//        (section 2.3) -- goes to an overflow list served after
+//        Phase II by direct copies.  No counting pass, no scan: one pass over
+//        the rid list, then one grid barrier.
 //   Phase II  Probe (Fig. 1): warp 0 is a TMA producer
 //        that bulk-copies each run of INPUT owned by this CTA ("load the i-th
-//        INPUT run entirely into cache") plus the run's RID-run
-//        entries into one of S shared-memory stages (full/empty mbarrier
-//        ring); the other warps consume the stages asynchronously.  The
-//        source runs of the first two items are prefetched before Phase I, so
-//        the distribute overlaps the first source reads.
+//        INPUT run entirely into cache") plus the run's entries
+//        into one of S shared-memory stages (full/empty mbarrier ring); the
+//        other warps consume the stages asynchronously.  The source runs of
+//        the first items are prefetched before Phase I, so the distribute
+//        overlaps the first source reads.
 //   Phase III Gather (Fig. 1), in one of two modes:
 //     mode 0 (fused):  the probe writes each staged record straight to its
-//        output row; the RID-run entry carries the row (pos).  No INTERNAL
-//        file.  Right when rows are whole 32-byte sectors (rec % 32 == 0):
-//        B200's L2 then absorbs the scattered rows without read-modify-write.
+//        output row; the entry carries the row (pos).  No INTERNAL file.
 //     mode 1 (three-phase, as Fig. 1): the probe appends records to the run's
-//        INTERNAL segment sequentially (L2 evict_last: for L2-sized inputs
-//        INTERNAL stays on chip), a grid barrier, then each CTA gathers its own
-//        chunk of output rows, "the next record from the j-th INTERNAL run"
-//         being INTERNAL[inv[i]], and writes the rows sequentially.
-//        Right for records that straddle sectors (e.g. 100 B), whose scattered
-//        writes would each cost a DRAM read-modify-write.
+//        INTERNAL segment sequentially, then (separate launch, api.cu) the
+//        output rows are gathered from INTERNAL and written sequentially.
 //
-// Shared memory: [header | bucket_start[K+1] | stage 0 | ... | stage S-1];
-// during Phase I the last two stages hold the warp histograms and CTA bases.
+// Shared memory: [header | own-run counts | stage 0 | ... | stage S-1]; the
+// CTA's rid chunk is cached in a stage that is not prefetched into.
 #include "dpg_internal.cuh"
 
 namespace dpg {
@@ -62,47 +54,12 @@ __device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t G) {
   __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 __device__ __forceinline__ const uint8_t* adn(const uint8_t* p) {
   return reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15));
 }
 __device__ __forceinline__ const uint8_t* aup(const uint8_t* p) {
   return reinterpret_cast<const uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
 }
-
-// Item sequence of one CTA over its runs b = c, c+G, ...: first the leading
-// chunk (up to slot_pairs entries) of every run, then -- only for runs heavier
-// than one stage (skew) -- their remaining chunks.  Item t < #runs
-// is therefore always run c + t*G, which lets the source of the first runs be
-// prefetched before Phase I knows the run sizes.
-struct Items {
-  uint32_t b, j, pass, c, G, K, sp;
-  const uint32_t* bs;
-  __device__ void init(uint32_t c_, uint32_t G_, uint32_t K_, uint32_t sp_, const uint32_t* bs_) {
-    c = c_; b = c_; j = 0; pass = 0; G = G_; K = K_; sp = sp_; bs = bs_;
-    if (b >= K) { pass = 1; b = K; }
-  }
-  __device__ bool valid() const { return b < K; }
-  __device__ uint32_t p0() const { return bs[b] + j * sp; }
-  __device__ uint32_t p1() const { return min(bs[b + 1], bs[b] + (j + 1) * sp); }
-  __device__ void settle() {
-    while (b < K && j * sp >= bs[b + 1] - bs[b]) { b += G; j = 1; }
-  }
-  __device__ void next() {
-    if (pass == 0) {
-      b += G;
-      if (b >= K) { pass = 1; b = c; j = 1; settle(); }
-    } else {
-      ++j;
-      settle();
-    }
-  }
-};
 
 // Producer-warp helpers --------------------------------------------------------
 // Copy the unaligned head/tail bytes of run b's byte range into the stage
@@ -131,14 +88,14 @@ __device__ __forceinline__ void issue_region(const FusedArgs& a, uint32_t b, uin
   }
 }
 
-__device__ __forceinline__ void issue_pairs(const FusedArgs& a, uint32_t p0, uint32_t p1,
+__device__ __forceinline__ void issue_pairs(const FusedArgs& a, uint64_t p0, uint64_t p1,
                                             uint8_t* stage, uint64_t* full, int lane,
                                             uint64_t pol) {
   if (lane == 0) {
     if (p1 > p0) {
       const uint8_t* pb = reinterpret_cast<const uint8_t*>(a.pairs);
-      const uint8_t* q0 = adn(pb + (uint64_t)p0 * a.pair_bytes);
-      const uint8_t* q1 = aup(pb + (uint64_t)p1 * a.pair_bytes);
+      const uint8_t* q0 = adn(pb + p0 * a.pair_bytes);
+      const uint8_t* q1 = aup(pb + p1 * a.pair_bytes);
       const uint32_t bytes = (uint32_t)(q1 - q0);
       mbar_arrive_expect_tx(full, bytes);
       bulk_g2s(stage + a.region_cap, q0, bytes, full, pol);
@@ -170,22 +127,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
-  uint32_t* wsum = reinterpret_cast<uint32_t*>(smem + 128);
-  uint32_t* bs = reinterpret_cast<uint32_t*>(smem + kHdr);
-  const uint32_t bs_bytes = ((a.K + 1) * 4 + 127) & ~127u;
-  uint8_t* stages = smem + kHdr + bs_bytes;
-  const uint32_t S = a.nstages;
-  // Phase I scratch: the stages not prefetched into
-  uint16_t* hw = reinterpret_cast<uint16_t*>(stages + (size_t)a.npre * a.stage_bytes);
-  uint32_t* cbase = reinterpret_cast<uint32_t*>(hw + (size_t)a.hist_warps * a.K);
-  uint32_t* rcache = cbase + ((a.K + 3) & ~3u);       // this CTA's rid chunk (optional)
   uint64_t* ridbar = reinterpret_cast<uint64_t*>(smem + 384);
+  uint32_t* own_cnt = reinterpret_cast<uint32_t*>(smem + kHdr);   // entries of run c + t*G
+  const uint32_t own_bytes = (a.max_own * 4 + 127) & ~127u;
+  uint8_t* stages = smem + kHdr + own_bytes;
+  const uint32_t S = a.nstages;
+  uint32_t* rcache = reinterpret_cast<uint32_t*>(stages + (size_t)a.npre * a.stage_bytes);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
   const uint64_t pol_first = policy_evict_first();
 #define DPG_STAMP(k) \
-  if (a.ts && tid == 0) a.ts[(size_t)c * 8 + (k)] = globaltimer();
+  if (a.ts && tid == 0) a.ts[(size_t)c * 16 + (k)] = globaltimer();
   DPG_STAMP(0);
 
   const uint64_t lo = (uint64_t)c * a.chunk;
@@ -212,181 +165,87 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       if (b < a.K) issue_region(a, b, stages + (size_t)t * a.stage_bytes, &full[t], lane, pol_first);
     }
   }
-  {
-    uint4* h4 = reinterpret_cast<uint4*>(hw);
-    const uint32_t n4 = (a.hist_warps * a.K * 2 + 15) / 16;
-    for (uint32_t k = tid; k < n4; k += blockDim.x) h4[k] = make_uint4(0, 0, 0, 0);
-    if (a.rid_cache && (uint64_t)tid < span - span16) rcache[span16 + tid] = a.rids[lo + span16 + tid];
-  }
-  if (a.rid_cache) mbar_wait(ridbar, 0);
-  __syncthreads();
-
-  // ---- B: count -----------------------------------------------------------------
-  const uint32_t HW = a.hist_warps;   // warps with a private histogram (Phase I)
-  const uint64_t sub = ((span + HW - 1) / HW + 31) & ~31ull;
-  const uint64_t wlo = min_u64(hi, lo + (uint64_t)warp * sub);
-  const uint64_t whi = min_u64(hi, wlo + sub);
-  uint16_t* myh = hw + (size_t)warp * a.K;
-  auto rid_at = [&](uint64_t i) -> uint32_t {
-    return a.rid_cache ? rcache[i - lo] : __ldg(a.rids + i);
-  };
-  constexpr int U = 8;
-  for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
-    uint32_t r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t i = i0 + u * 32 + lane;
-      r[u] = i < whi ? rid_at(i) : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t i = i0 + u * 32 + lane;
-      const bool in = i < whi;
-      const bool ok = in && r[u] < a.n_src;
-      if (in && !ok) report_bad(a.status, i);
-      const uint32_t d = ok ? (r[u] >> a.s) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-      if (ok && lane == __ffs(peers) - 1) myh[d] = (uint16_t)(myh[d] + __popc(peers));
-    }
-  }
-  __syncthreads();
-  {
-    // CTA totals per run, warp-exclusive prefixes in place, and one global
-    // reservation per (run, CTA); the atomics of a thread are all in flight
-    // together.
-    constexpr int BPT = 8;
-    for (uint32_t b0 = tid; b0 < a.K; b0 += BPT * blockDim.x) {
-      uint32_t sum[BPT];
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        const uint32_t b = b0 + q * blockDim.x;
-        sum[q] = 0;
-        if (b < a.K) {
-#pragma unroll 4
-          for (uint32_t w = 0; w < HW; ++w) {
-            const uint32_t h = hw[(size_t)w * a.K + b];
-            hw[(size_t)w * a.K + b] = (uint16_t)sum[q];
-            sum[q] += h;
-          }
-        }
-      }
-      uint32_t base[BPT];
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        const uint32_t b = b0 + q * blockDim.x;
-        base[q] = (b < a.K && sum[q]) ? atomicAdd(&a.total[b], sum[q]) : 0u;
-      }
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        const uint32_t b = b0 + q * blockDim.x;
-        if (b < a.K) cbase[b] = base[q];
-      }
-    }
+  if (a.rid_cache) {
+    if ((uint64_t)tid < span - span16) rcache[span16 + tid] = a.rids[lo + span16 + tid];
+    mbar_wait(ridbar, 0);
+    __syncthreads();
   }
   DPG_STAMP(1);
-  grid_barrier(a.gbar, G);
-  DPG_STAMP(2);
 
-  // ---- C: scan of run totals, then scatter ----------------------------------------
-  {
-    const uint32_t ipt = (a.K + blockDim.x - 1) / blockDim.x;
-    const uint32_t k0 = tid * ipt;
-    uint32_t local = 0;
-    for (uint32_t k = k0; k < min(a.K, k0 + ipt); ++k) local += __ldcg(a.total + k);
-    uint32_t x = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t v = lane < kWarps ? wsum[lane] : 0;
-      uint32_t ws = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, ws, o);
-        if (lane >= o) ws += y;
-      }
-      if (lane < kWarps) wsum[lane] = ws - v;
-      if (lane == kWarps - 1) wsum[32] = ws;
-    }
-    __syncthreads();
-    uint32_t run = wsum[warp] + x - local;
-    for (uint32_t k = k0; k < min(a.K, k0 + ipt); ++k) {
-      bs[k] = run;
-      run += __ldcg(a.total + k);
-    }
-    if (tid == 0) bs[a.K] = wsum[32];
-    __syncthreads();
-  }
+  // ---- B: distribute: one reservation per rid on its run's cursor ---------------
   {
     PairT* pairs = reinterpret_cast<PairT*>(a.pairs);
     const uint32_t lmask = (1u << a.s) - 1u;
-    const uint32_t lt = lanemask_lt();
-    for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
-      uint32_t r[U];
+    constexpr int U = 8;
+    for (uint64_t i0 = lo + (uint64_t)warp * 32 * U; i0 < hi; i0 += (uint64_t)kWarps * 32 * U) {
+      uint32_t r[U], slot[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t i = i0 + u * 32 + lane;
-        r[u] = i < whi ? rid_at(i) : 0xFFFFFFFFu;
+        r[u] = 0xFFFFFFFFu;
+        if (i < hi) r[u] = a.rid_cache ? rcache[i - lo] : __ldg(a.rids + i);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t i = i0 + u * 32 + lane;
-        const bool ok = i < whi && r[u] < a.n_src;
-        const uint32_t d = ok ? (r[u] >> a.s) : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (ok && lane == leader) {
-          const uint32_t h = myh[d];
-          base = bs[d] + cbase[d] + h;
-          myh[d] = (uint16_t)(h + __popc(peers));
+        const bool ok = i < hi && r[u] < a.n_src;
+        slot[u] = ok ? atomicAdd(&a.total[r[u] >> a.s], 1u) : 0xFFFFFFFFu;
+        if (i < hi && !ok) {
+          report_bad(a.status, i);
+          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
         }
-        base = __shfl_sync(0xFFFFFFFFu, base, leader);
-        if (ok) {
-          const uint32_t slot = base + __popc(peers & lt);
-          const uint32_t loc = r[u] & lmask;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * 32 + lane;
+        if (slot[u] == 0xFFFFFFFFu) continue;
+        const uint32_t b = r[u] >> a.s;
+        const uint32_t loc = r[u] & lmask;
+        if (slot[u] < a.cap) {
+          const uint64_t e = (uint64_t)b * a.cap + slot[u];
           if (MODE == 1) {
-            pairs[slot] = (PairT)loc;
-            a.inv[i] = slot;
+            pairs[e] = (PairT)loc;
+            a.inv[i] = (uint32_t)e;
           } else if (sizeof(PairT) == 4) {
-            pairs[slot] = (PairT)(((uint32_t)i << a.s) | loc);
+            pairs[e] = (PairT)(((uint32_t)i << a.s) | loc);
           } else {
-            pairs[slot] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
+            pairs[e] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
           }
-        } else if (MODE == 1 && i < whi) {
-          a.inv[i] = 0xFFFFFFFFu;      // row left unwritten (invalid rid)
+        } else {
+          // run over capacity (skew): served after Phase II by a direct copy
+          const uint32_t o = atomicAdd(a.gbar + 2, 1u);
+          a.ovf[o] = (uint64_t)i | ((uint64_t)r[u] << 32);
+          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;
         }
       }
     }
   }
-  DPG_STAMP(3);
+  DPG_STAMP(2);
   grid_barrier(a.gbar, G);
-  DPG_STAMP(4);
+  DPG_STAMP(3);
+
+  // entries of this CTA's runs; restore the zero invariant of the cursors
+  for (uint32_t t = tid; c + (uint64_t)t * G < a.K; t += blockDim.x) {
+    const uint32_t b = c + t * G;
+    own_cnt[t] = min(__ldcg(a.total + b), a.cap);
+    a.total[b] = 0;
+  }
+  __syncthreads();
 
   // ---- Phase II (+ III in mode 0) --------------------------------------------------
-  for (uint32_t b = c; b < a.K; b += G) a.total[b] = 0;   // restore the zero invariant
-
-  Items it;
-  it.init(c, G, a.K, a.slot_pairs, bs);
+  const uint32_t n_items = c < a.K ? (a.K - c + G - 1) / G : 0;
   if (warp == 0) {
     // producer
-    fence_proxy_async_global();  // RID-run entries were written by generic stores
-    for (uint32_t t = 0; it.valid(); ++t, it.next()) {
+    fence_proxy_async_global();  // the entries were written by generic stores in Phase I
+    for (uint32_t t = 0; t < n_items; ++t) {
+      const uint32_t b = c + t * G;
       const uint32_t st = t % S;
       uint8_t* stage = stages + (size_t)st * a.stage_bytes;
-      const bool pre = t < a.npre && it.pass == 0;
       if (t >= S) mbar_wait(&empty[st], ((t / S) & 1) ^ 1);
-      const uint32_t p0 = it.p0(), p1 = it.p1();
-      if (!pre) {
-        if (p1 > p0) {
-          issue_region(a, it.b, stage, &full[st], lane, pol_first);
-        } else if (lane == 0) {
-          mbar_arrive(&full[st]);
-        }
+      const uint64_t p0 = (uint64_t)b * a.cap, p1 = p0 + own_cnt[t];
+      if (t >= a.npre) {
+        if (p1 > p0) issue_region(a, b, stage, &full[st], lane, pol_first);
+        else if (lane == 0) mbar_arrive(&full[st]);
       }
       issue_pairs(a, p0, p1, stage, &full[st], lane, pol_first);
     }
@@ -400,16 +259,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
     const bool lane_on = R <= 32 ? (uint32_t)lane < RPI * R : true;
     const uint64_t pol_last = policy_evict_last();
     uint32_t q0 = 0;
-    for (uint32_t t = 0; it.valid(); ++t, it.next()) {
+    for (uint32_t t = 0; t < n_items; ++t) {
+      const uint32_t b = c + t * G;
       const uint32_t st = t % S;
       const uint8_t* stage = stages + (size_t)st * a.stage_bytes;
-      const uint32_t p0 = it.p0(), p1 = it.p1();
-      const uint32_t n = p1 - p0;
+      const uint64_t p0 = (uint64_t)b * a.cap;
+      const uint32_t n = own_cnt[t];
       const uint32_t ng = (n + 31) / 32;
       mbar_wait(&full[st], (t / S) & 1);
-      const uint8_t* r0 = a.src + ((uint64_t)it.b << a.s) * a.rec;
+      const uint8_t* r0 = a.src + ((uint64_t)b << a.s) * a.rec;
       const uint8_t* region = stage + (r0 - adn(r0));
-      const uint8_t* pb = reinterpret_cast<const uint8_t*>(a.pairs) + (uint64_t)p0 * a.pair_bytes;
+      const uint8_t* pb = reinterpret_cast<const uint8_t*>(a.pairs) + p0 * a.pair_bytes;
       const PairT* prs = reinterpret_cast<const PairT*>(stage + a.region_cap + (pb - adn(pb)));
       for (uint32_t g = (rank + kConsumers - (q0 % kConsumers)) % kConsumers; g < ng;
            g += kConsumers) {
@@ -419,7 +279,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
         const uint32_t cnt = min(32u, n - g0);
         // destination of entry rr of this group: mode 0 its output row, mode 1
         // the next slot of the run's INTERNAL segment
-        uint8_t* const obase = MODE == 1 ? a.internal + (uint64_t)(p0 + g0) * a.rec : a.dst;
+        uint8_t* const obase = MODE == 1 ? a.internal + (p0 + g0) * a.rec : a.dst;
         if (R <= 32) {
           constexpr int B = W >= 16 ? 4 : 8;
           for (uint32_t k0 = 0; k0 < cnt; k0 += RPI * B) {
@@ -463,12 +323,35 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+  DPG_STAMP(4);
 
-  // Mode 1: Phase III (gather from INTERNAL) is a separate launch of the
-  // direct-gather kernel over (INTERNAL, inv), at full occupancy (api.cu).
+  // ---- overflow entries (runs over capacity): direct copies ------------------------
+  {
+    const uint32_t n_ovf = __ldcg(a.gbar + 2);   // final since the grid barrier
+    if (n_ovf) {
+      const uint32_t R = a.rec / W;
+      for (uint64_t j = (uint64_t)c * kWarps + warp; j < n_ovf; j += (uint64_t)G * kWarps) {
+        const uint64_t e = __ldcg(a.ovf + j);
+        const uint64_t i = (uint32_t)e, r = e >> 32;
+        const uint8_t* s = a.src + r * a.rec;
+        uint8_t* d = a.dst + i * a.row_bytes;
+        for (uint32_t w = lane; w < R; w += 32)
+          *reinterpret_cast<T*>(d + w * W) = *reinterpret_cast<const T*>(s + w * W);
+      }
+    }
+    // the last CTA through here resets the overflow count for the next call
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(a.gbar + 3, 1u) == G - 1) {
+        atomicExch(a.gbar + 2, 0u);
+        atomicExch(a.gbar + 3, 0u);
+      }
+    }
+  }
   if (a.ts) {
     __syncthreads();
-    DPG_STAMP(7);
+    DPG_STAMP(5);
   }
 #undef DPG_STAMP
 }

@@ -86,8 +86,8 @@ def test_argument_validation_before_any_cuda_call(dpg):
 @pytest.mark.parametrize("rec,n,L,K,path", [
     (100, 65536, 128, 512, 1),        # config 1: runs shrink for load balance
     (100, 1048576, 512, 2048, 1),     # config 2: fused kernel, 4 stages of 50 KB runs
-    (64, 16777216, 1024, 16384, 2),   # config 3/4 dims at rec 64: multi-kernel path
-    (256, 16777216, 256, 65536, 2),
+    (64, 16777216, 512, 32768, 1),    # config 3 at rec 64
+    (256, 16777216, 128, 131072, 1),
 ])
 def test_plan_run_length(dpg, rec, n, L, K, path):
     p = dpg.dpg_plan(rec, n, n, 0, 148)
@@ -102,17 +102,18 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
 
 def test_plan_pair_packing_and_overrides(dpg):
     c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20)
-    assert c2["gather"] == 2 and c2["pair_bytes"] == 2                # INTERNAL mode: u16 locals
-    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, gather=1)["pair_bytes"] == 4   # 9 + 20 bits
+    assert c2["gather"] == 1 and c2["pair_bytes"] == 4                # 9 + 20 bits packed
+    assert c2["slot_pairs"] == 672                                    # CAP = L + L/4 + 32
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, gather=2)["pair_bytes"] == 2   # u16 locals
     assert dpg.dpg_plan(128, 1 << 20, 1 << 20)["gather"] == 1         # whole sectors
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26)["pair_bytes"] == 8      # 10 + 26 bits
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8, gather=1)["pair_bytes"] == 8
-    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8)["pair_bytes"] == 4   # u32 locals
+    assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8, gather=2)["pair_bytes"] == 4
     p = dpg.dpg_plan(3, 12, 12, log2_run=2)
     assert p["run_len"] == 4 and p["num_runs"] == 3                   # Fig. 2 geometry
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26, path=2)["path"] == 2
-    with pytest.raises(dpg.DPGError):                                 # chunk > u16 counters
-        dpg.dpg_plan(64, 1 << 24, 1 << 26, path=1)
+    with pytest.raises(dpg.DPGError):                                 # payload: multi-kernel only
+        dpg.dpg_plan(64, 1 << 24, 1 << 26, pay_bytes=16, path=1)
     with pytest.raises(dpg.DPGError):
         dpg.dpg_plan(0, 10, 10)
     j = dpg.dpg_plan(64, 1 << 24, 1 << 26, pay_bytes=16)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rec", type=int, default=None)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--gather", type=int, default=0)
     args = ap.parse_args()
     import torch
 
@@ -29,30 +30,30 @@ def main():
     out = torch.empty((rids.numel(), src.shape[1]), dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     G = torch.cuda.get_device_properties(0).multi_processor_count
-    ts = torch.zeros(G * 8, dtype=torch.int64, device="cuda")
+    ts = torch.zeros(G * 16, dtype=torch.int64, device="cuda")
     lib = dpg.raw_lib()
     lib.dpg_debug_phase_stamps.argtypes = [ctypes.c_void_p]
     lib.dpg_debug_phase_stamps.restype = None
     for _ in range(3):
         dpg.dpg_retrieve(src, rids, dst=out)
-    names = ["count", "barrier1", "scatter", "barrier2", "probe_gather"]
+    names = ["init", "distribute", "barrier", "probe", "overflow"]
     for rep in range(args.reps):
         flush.fill_(1)
         ts.zero_()
         lib.dpg_debug_phase_stamps(ctypes.c_void_p(ts.data_ptr()))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        dpg.dpg_retrieve(src, rids, dst=out)
+        dpg.dpg_retrieve(src, rids, dst=out, gather=args.gather)
         e1.record()
         torch.cuda.synchronize()
         lib.dpg_debug_phase_stamps(None)
-        t = ts.view(G, 8)[:, :6].cpu().numpy().astype(np.float64)
+        t = ts.view(G, 16)[:, :6].cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3  # us
-        line = [f"event {e0.elapsed_time(e1)*1e3:7.1f}us", f"start spread {rel[:,0].max():5.1f}"]
+        line = [f"event {e0.elapsed_time(e1)*1e3:6.1f}us", f"spread {rel[:,0].max():4.1f}"]
         for k, n in enumerate(names):
             d = rel[:, k + 1] - rel[:, k]
-            line.append(f"{n} med {np.median(d):6.1f} max {d.max():6.1f} (ends {rel[:, k+1].max():6.1f})")
+            line.append(f"{n} {np.median(d):5.1f}/{d.max():5.1f} @{rel[:, k+1].max():5.1f}")
         print(" | ".join(line))
     print("plan", dpg.dpg_plan(src.shape[1], src.shape[0], rids.numel(), sm_count=G))
 
