@@ -86,8 +86,8 @@ typedef struct {
                                (Fig. 1 literally; rows straddle sectors)       */
     uint32_t npre;          /* source runs prefetched before Phase I (fused)    */
     uint32_t rid_cache;     /* 1: each CTA's rid chunk is staged in smem (fused) */
-    uint32_t hist_warps;    /* warps owning a private run histogram (fused)     */
-    uint32_t reserved;
+    uint32_t hist_warps;    /* warps owning private 16-bit run counters (fused) */
+    uint32_t tile;          /* rids per Phase I tile of a CTA (fused)           */
 } dpg_plan_t;
 
 /* Optional overrides for tests and tuning (zero = automatic).  The output

@@ -60,7 +60,7 @@ class Plan(ctypes.Structure):
                                        "grid_distribute", "grid_probe", "hist_in_smem",
                                        "pay_bytes", "path", "nstages", "stage_bytes",
                                        "gather", "npre", "rid_cache", "hist_warps",
-                                       "reserved")]
+                                       "tile")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}

@@ -149,9 +149,30 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     const uint64_t smem = kFusedHdr + align_up(max_own * 4, 128) + kFusedStages * stage;
     if (smem > kSmemLimit) return false;
     const uint32_t npre = std::min<uint32_t>(2, (uint32_t)std::min<uint64_t>(K, kFusedStages - 1));
+    // Phase I scratch in the stages not prefetched into: 16-bit counters per
+    // (warp, run), the CTA's run bases, and (optionally) the current rid tile.
+    const uint64_t scratch = (uint64_t)(kFusedStages - npre) * stage;
+    const uint64_t max_tile = std::min<uint64_t>(align_up(chunk, 4), 65532);
+    uint32_t hwarps = 0, tile = 0, rc_words = 0;
+    for (uint32_t hwp : {16u, 8u, 4u, 2u, 1u}) {
+      const uint64_t fixed = align_up((uint64_t)hwp * K * 2, 16) + K * 4 + 64;
+      if (fixed > scratch) continue;
+      const uint64_t room = ((scratch - fixed) / 4) & ~3ull;
+      if (room >= std::min<uint64_t>(max_tile, 1024)) {          // rid tile cached
+        tile = (uint32_t)std::min<uint64_t>(max_tile, room);
+        rc_words = tile;
+      } else {
+        tile = (uint32_t)max_tile;
+        rc_words = 0;
+      }
+      hwarps = hwp;
+      break;
+    }
+    if (!hwarps) return false;
     q->npre = npre;
-    q->rid_cache = (chunk * 4 + 16 <= (kFusedStages - npre) * stage) ? 1 : 0;
-    q->hist_warps = 0;
+    q->rid_cache = rc_words ? 1 : 0;
+    q->hist_warps = hwarps;
+    q->tile = tile;
     q->log2_run = s;
     q->run_len = L;
     q->num_runs = K;
@@ -428,6 +449,9 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.stage_bytes = p.stage_bytes;
     f.npre = p.npre;
     f.rid_cache = (p.rid_cache && ((uintptr_t)rids % 16 == 0)) ? 1 : 0;
+    f.hist_warps = p.hist_warps;
+    f.tile = p.tile;
+    f.rcache_words = p.rid_cache ? p.tile : 0;
     f.cap = p.slot_pairs;
     f.ovf = (uint64_t*)((uint8_t*)pairs + pairs_sz);
     f.max_own = (uint32_t)((p.num_runs + p.grid_probe - 1) / p.grid_probe);

@@ -171,6 +171,9 @@ struct FusedArgs {
   uint32_t rid_cache;    // 1: the CTA's rid chunk is bulk-copied into shared memory
   uint32_t cap;          // fixed capacity of a run (entries); run b at [b*cap, b*cap + n_b)
   uint32_t max_own;      // runs per CTA, ceil(K / grid)
+  uint32_t hist_warps;   // warps owning a private 16-bit counter per run (Phase I)
+  uint32_t tile;         // rids per Phase I tile (multiple of 4, <= 65535)
+  uint32_t rcache_words; // shared-memory words reserved for a cached tile (0: no cache)
   uint64_t* ovf;         // [n_out] (i | rid << 32) of entries beyond a run's capacity
   uint32_t mode;         // 0: probe writes rows straight to dst; 1: probe -> INTERNAL -> gather
   uint8_t* internal;     // [n_out * rec] INTERNAL file (mode 1)

@@ -153,70 +153,143 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  // ---- A: one bulk copy of this CTA's rid chunk; prefetch of its first runs -----
-  const uint64_t span16 = a.rid_cache ? (span & ~3ull) : 0;   // 16-byte multiple
-  if (tid == 0 && a.rid_cache) {
-    mbar_arrive_expect_tx(ridbar, (uint32_t)(span16 * 4));
-    if (span16) bulk_g2s(rcache, a.rids + lo, (uint32_t)(span16 * 4), ridbar, pol_first);
-  }
+  // ---- A: prefetch the source runs of this CTA's first items --------------------
   if (warp == 0) {
     for (uint32_t t = 0; t < a.npre; ++t) {
       const uint32_t b = c + t * G;
       if (b < a.K) issue_region(a, b, stages + (size_t)t * a.stage_bytes, &full[t], lane, pol_first);
     }
   }
-  if (a.rid_cache) {
-    if ((uint64_t)tid < span - span16) rcache[span16 + tid] = a.rids[lo + span16 + tid];
-    mbar_wait(ridbar, 0);
-    __syncthreads();
-  }
-  DPG_STAMP(1);
 
-  // ---- B: distribute: one reservation per rid on its run's cursor ---------------
-  {
-    PairT* pairs = reinterpret_cast<PairT*>(a.pairs);
-    const uint32_t lmask = (1u << a.s) - 1u;
-    constexpr int U = 8;
-    for (uint64_t i0 = lo + (uint64_t)warp * 32 * U; i0 < hi; i0 += (uint64_t)kWarps * 32 * U) {
-      uint32_t r[U], slot[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        r[u] = 0xFFFFFFFFu;
-        if (i < hi) r[u] = a.rid_cache ? rcache[i - lo] : __ldg(a.rids + i);
+  // ---- B: distribute ---------------------------------------------------------------
+  // The CTA's chunk of the rid list is processed in tiles (each staged into
+  // shared memory by one bulk copy when rid_cache is set).  Each warp owns a
+  // contiguous slice of the tile and a private 16-bit counter per run.  Equal
+  // runs within a warp are found with one ballot per bit of the run id (a
+  // warp-level multisplit; no shared-memory atomics): the lowest lane of each
+  // group updates the warp's counter, the others take their rank inside the
+  // group.  Pass 1 counts; the CTA then reserves its share of every run with
+  // one global atomicAdd per run; pass 2 writes the entries (stable within the
+  // CTA).
+  const uint32_t HW = a.hist_warps;
+  uint16_t* hw = reinterpret_cast<uint16_t*>(rcache + a.rcache_words);
+  uint32_t* cbase = reinterpret_cast<uint32_t*>(hw + (((size_t)HW * a.K + 7) & ~(size_t)7));
+  uint16_t* myh = hw + (size_t)warp * a.K;
+  const uint32_t kbits = 32 - __clz(a.K);     // bits of the run id (key K marks "invalid")
+  const uint32_t lt = (1u << lane) - 1u;
+  auto group = [&](uint32_t key) -> uint32_t {   // lanes holding the same key
+    uint32_t peers = 0xFFFFFFFFu;
+    for (uint32_t j = 0; j < kbits; ++j) {
+      const uint32_t bit = (key >> j) & 1u;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+    return peers;
+  };
+  PairT* pairs = reinterpret_cast<PairT*>(a.pairs);
+  const uint32_t lmask = (1u << a.s) - 1u;
+  uint32_t tile_no = 0;
+  for (uint64_t tlo = lo; tlo < hi; tlo += a.tile, ++tile_no) {
+    const uint64_t thi = min_u64(hi, tlo + a.tile);
+    const uint64_t tspan = thi - tlo;
+    if (a.rid_cache) {
+      const uint64_t t16 = tspan & ~3ull;          // 16-byte multiple (tlo % 4 == 0)
+      __syncthreads();                             // previous tile fully consumed
+      if (tid == 0) {
+        mbar_arrive_expect_tx(ridbar, (uint32_t)(t16 * 4));
+        if (t16) bulk_g2s(rcache, a.rids + tlo, (uint32_t)(t16 * 4), ridbar, pol_first);
       }
+      if ((uint64_t)tid < tspan - t16) rcache[t16 + tid] = a.rids[tlo + t16 + tid];
+    }
+    {
+      uint4* h4 = reinterpret_cast<uint4*>(hw);
+      for (uint32_t k = tid; k < (HW * a.K * 2 + 15) / 16; k += blockDim.x) h4[k] = make_uint4(0, 0, 0, 0);
+    }
+    if (a.rid_cache) mbar_wait(ridbar, tile_no & 1);
+    __syncthreads();
+    if (tile_no == 0) DPG_STAMP(1);
+    const uint64_t sub = ((tspan + HW - 1) / HW + 31) & ~31ull;
+    const uint64_t wlo = min_u64(thi, tlo + (uint64_t)warp * sub);
+    const uint64_t whi = warp < (int)HW ? min_u64(thi, wlo + sub) : wlo;
+    auto rid_at = [&](uint64_t i) -> uint32_t {
+      return a.rid_cache ? rcache[i - tlo] : __ldg(a.rids + i);
+    };
+    // pass 1: count
+    for (uint64_t i0 = wlo; i0 < whi; i0 += 32) {
+      const uint64_t i = i0 + lane;
+      const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
+      const bool ok = i < whi && r < a.n_src;
+      if (i < whi && !ok) {
+        report_bad(a.status, i);
+        if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
+      }
+      const uint32_t key = ok ? (r >> a.s) : a.K;
+      const uint32_t peers = group(key);
+      if (ok && (peers & lt) == 0) myh[key] = (uint16_t)(myh[key] + __popc(peers));
+    }
+    __syncthreads();
+    // warp-exclusive prefixes per run, CTA totals, one reservation per run
+    for (uint32_t b = tid; b < a.K; b += blockDim.x) {
+      uint32_t sum = 0;
+      for (uint32_t w = 0; w < HW; ++w) {
+        const uint32_t h = hw[(size_t)w * a.K + b];
+        hw[(size_t)w * a.K + b] = (uint16_t)sum;
+        sum += h;
+      }
+      cbase[b] = sum;
+    }
+    __syncthreads();
+    {
+      constexpr int BPT = 8;    // a thread's reservations are all in flight together
+      for (uint32_t b0 = tid; b0 < a.K; b0 += BPT * blockDim.x) {
+        uint32_t base[BPT];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        const bool ok = i < hi && r[u] < a.n_src;
-        slot[u] = ok ? atomicAdd(&a.total[r[u] >> a.s], 1u) : 0xFFFFFFFFu;
-        if (i < hi && !ok) {
-          report_bad(a.status, i);
-          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
+        for (int q = 0; q < BPT; ++q) {
+          const uint32_t b = b0 + q * blockDim.x;
+          const uint32_t n = b < a.K ? cbase[b] : 0u;
+          base[q] = n ? atomicAdd(&a.total[b], n) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < BPT; ++q) {
+          const uint32_t b = b0 + q * blockDim.x;
+          if (b < a.K) cbase[b] = base[q];
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        if (slot[u] == 0xFFFFFFFFu) continue;
-        const uint32_t b = r[u] >> a.s;
-        const uint32_t loc = r[u] & lmask;
-        if (slot[u] < a.cap) {
-          const uint64_t e = (uint64_t)b * a.cap + slot[u];
-          if (MODE == 1) {
-            pairs[e] = (PairT)loc;
-            a.inv[i] = (uint32_t)e;
-          } else if (sizeof(PairT) == 4) {
-            pairs[e] = (PairT)(((uint32_t)i << a.s) | loc);
-          } else {
-            pairs[e] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
-          }
+    }
+    __syncthreads();
+    // pass 2: append each rid to its run
+    for (uint64_t i0 = wlo; i0 < whi; i0 += 32) {
+      const uint64_t i = i0 + lane;
+      const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
+      const bool ok = i < whi && r < a.n_src;
+      const uint32_t key = ok ? (r >> a.s) : a.K;
+      const uint32_t peers = group(key);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (ok && lane == leader) {
+        const uint32_t h = myh[key];
+        base = cbase[key] + h;
+        myh[key] = (uint16_t)(h + __popc(peers));
+      }
+      base = __shfl_sync(0xFFFFFFFFu, base, leader);
+      if (!ok) continue;
+      const uint32_t slot = base + __popc(peers & lt);
+      const uint32_t loc = r & lmask;
+      if (slot < a.cap) {
+        const uint64_t e = (uint64_t)key * a.cap + slot;
+        if (MODE == 1) {
+          pairs[e] = (PairT)loc;
+          a.inv[i] = (uint32_t)e;
+        } else if (sizeof(PairT) == 4) {
+          pairs[e] = (PairT)(((uint32_t)i << a.s) | loc);
         } else {
-          // run over capacity (skew): served after Phase II by a direct copy
-          const uint32_t o = atomicAdd(a.gbar + 2, 1u);
-          a.ovf[o] = (uint64_t)i | ((uint64_t)r[u] << 32);
-          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;
+          pairs[e] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
         }
+      } else {
+        // run over capacity (skew): served after Phase II by a direct copy
+        const uint32_t o = atomicAdd(a.gbar + 2, 1u);
+        a.ovf[o] = (uint64_t)i | ((uint64_t)r << 32);
+        if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;
       }
     }
   }
