@@ -330,15 +330,22 @@ def main():
     peak, peak_src = hbm_peak()
     dist_ms, probe_ms, calls = ph
     pg_ms = probe_ms / max(1, calls)
-    # algorithmic bytes of the dominant kernel per launch: every source record
-    # staged once + every output row written once + its pair read once
     plan = dpg.dpg_plan(rec if cfg != "c4" else w["dim"].shape[1], n_src, n_out,
                         16 if cfg == "c4" else 0, torch.cuda.get_device_properties(dev).multi_processor_count)
     src_rec = w["dim"].shape[1] if cfg == "c4" else rec
     pay = 16 if cfg == "c4" else 0
-    pg_bytes = n_src * src_rec + n_out * (rec + plan["pair_bytes"] + pay)
+    if plan["path"] == 1:
+        # one persistent kernel runs the whole path: its algorithmic bytes are
+        # the path's, N * (2 * rec + rid_bytes)
+        kernel = "k_dpg_fused" + (" + k_direct(INTERNAL)" if plan["gather"] == 2 else "")
+        pg_bytes = alg_bytes
+    else:
+        # probe-gather kernel: every source record staged once + every output
+        # row written once + its entry (and payload) read once
+        kernel = "k_probe_gather"
+        pg_bytes = n_src * src_rec + n_out * (rec + plan["pair_bytes"] + pay)
     achieved = pg_bytes / (pg_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_probe_gather", "achieved": achieved, "peak": peak,
+    roofline = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": committed_traffic(cfg),
                 "peak_source": peak_src,
                 "alg_bytes_per_launch": pg_bytes,

@@ -21,7 +21,7 @@ static constexpr int kDirectThreads = 256;
 //         the whole source, staged into L2): loads evict_last, stores
 //         evict_first so the output stream does not evict the run.
 template <int W, int HINT>
-__global__ void __launch_bounds__(kDirectThreads, 4) k_direct(const uint8_t* __restrict__ src,
+__global__ void __launch_bounds__(kDirectThreads, 5) k_direct(const uint8_t* __restrict__ src,
                                                               uint64_t n_src, uint32_t rec,
                                                               const uint32_t* __restrict__ rids,
                                                               uint64_t n_out,
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kDirectThreads, 4) k_direct(const uint8_t* __r
   const uint64_t lpol = HINT == 2 ? policy_evict_last() : pol;
   // rows in flight per lane per batch: up to 128 bytes of loads per lane, so a
   // warp keeps a whole 32-row group (3.2 KB at 100-B rows) in flight
-  constexpr int B = W >= 16 ? 4 : W == 8 ? 8 : 16;
+  constexpr int B = W >= 16 ? 2 : W == 8 ? 4 : 8;
   constexpr int B2 = W >= 16 ? 2 : 4;  // words in flight per lane for rows wider than a warp
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kDirectThreads) k_scatter_rows(const uint8_t* 
 static uint32_t grid_for(uint64_t n_rows, int sm_count) {
   uint64_t warps = (n_rows + 31) / 32;
   uint64_t blocks = (warps + (kDirectThreads / 32) - 1) / (kDirectThreads / 32);
-  uint64_t cap = (uint64_t)sm_count * 4;  // 4 x 256 threads = 32 warps per SM (launch bounds)
+  uint64_t cap = (uint64_t)sm_count * 5;  // 5 x 256 threads = 40 warps per SM (launch bounds)
   return (uint32_t)max_u64(1, min_u64(blocks, cap));
 }
 

@@ -153,13 +153,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  // ---- A: prefetch the source runs of this CTA's first items --------------------
-  if (warp == 0) {
-    for (uint32_t t = 0; t < a.npre; ++t) {
-      const uint32_t b = c + t * G;
-      if (b < a.K) issue_region(a, b, stages + (size_t)t * a.stage_bytes, &full[t], lane, pol_first);
+  // ---- A: prefetch of the source runs of this CTA's first items: issued right
+  // after the first rid tile's bulk copy (below), so that copy is not queued
+  // behind them.
+  auto prefetch_runs = [&]() {
+    if (warp == 0) {
+      for (uint32_t t = 0; t < a.npre; ++t) {
+        const uint32_t b = c + t * G;
+        if (b < a.K) issue_region(a, b, stages + (size_t)t * a.stage_bytes, &full[t], lane, pol_first);
+      }
     }
-  }
+  };
+  if (lo >= hi) prefetch_runs();
 
   // ---- B: distribute ---------------------------------------------------------------
   // The CTA's chunk of the rid list is processed in tiles (each staged into
@@ -177,14 +182,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   uint16_t* myh = hw + (size_t)warp * a.K;
   const uint32_t kbits = 32 - __clz(a.K);     // bits of the run id (key K marks "invalid")
   const uint32_t lt = (1u << lane) - 1u;
-  auto group = [&](uint32_t key) -> uint32_t {   // lanes holding the same key
-    uint32_t peers = 0xFFFFFFFFu;
+  // lanes holding the same key, for U independent key groups at once (the
+  // ballot chains interleave, hiding the vote latency)
+  constexpr int U = 4;
+  auto group = [&](const uint32_t (&key)[U], uint32_t (&peers)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) peers[u] = 0xFFFFFFFFu;
     for (uint32_t j = 0; j < kbits; ++j) {
-      const uint32_t bit = (key >> j) & 1u;
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-      peers &= bit ? bal : ~bal;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t bit = (key[u] >> j) & 1u;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+        peers[u] &= bit ? bal : ~bal;
+      }
     }
-    return peers;
   };
   PairT* pairs = reinterpret_cast<PairT*>(a.pairs);
   const uint32_t lmask = (1u << a.s) - 1u;
@@ -201,6 +212,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       }
       if ((uint64_t)tid < tspan - t16) rcache[t16 + tid] = a.rids[tlo + t16 + tid];
     }
+    if (tile_no == 0) prefetch_runs();
     {
       uint4* h4 = reinterpret_cast<uint4*>(hw);
       for (uint32_t k = tid; k < (HW * a.K * 2 + 15) / 16; k += blockDim.x) h4[k] = make_uint4(0, 0, 0, 0);
@@ -215,19 +227,27 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       return a.rid_cache ? rcache[i - tlo] : __ldg(a.rids + i);
     };
     // pass 1: count
-    for (uint64_t i0 = wlo; i0 < whi; i0 += 32) {
-      const uint64_t i = i0 + lane;
-      const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
-      const bool ok = i < whi && r < a.n_src;
-      if (i < whi && !ok) {
-        report_bad(a.status, i);
-        if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
+    for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
+      uint32_t key[U], peers[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * 32 + lane;
+        const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
+        const bool ok = i < whi && r < a.n_src;
+        if (i < whi && !ok) {
+          report_bad(a.status, i);
+          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
+        }
+        key[u] = ok ? (r >> a.s) : a.K;
       }
-      const uint32_t key = ok ? (r >> a.s) : a.K;
-      const uint32_t peers = group(key);
-      if (ok && (peers & lt) == 0) myh[key] = (uint16_t)(myh[key] + __popc(peers));
+      group(key, peers);
+#pragma unroll
+      for (int u = 0; u < U; ++u)   // in order: a later group may lead the same run
+        if (key[u] < a.K && (peers[u] & lt) == 0)
+          myh[key[u]] = (uint16_t)(myh[key[u]] + __popc(peers[u]));
     }
     __syncthreads();
+    if (tile_no == 0) DPG_STAMP(6);
     // warp-exclusive prefixes per run, CTA totals, one reservation per run
     for (uint32_t b = tid; b < a.K; b += blockDim.x) {
       uint32_t sum = 0;
@@ -239,6 +259,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       cbase[b] = sum;
     }
     __syncthreads();
+    if (tile_no == 0) DPG_STAMP(7);
     {
       constexpr int BPT = 8;    // a thread's reservations are all in flight together
       for (uint32_t b0 = tid; b0 < a.K; b0 += BPT * blockDim.x) {
@@ -257,39 +278,48 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       }
     }
     __syncthreads();
+    if (tile_no == 0) DPG_STAMP(8);
     // pass 2: append each rid to its run
-    for (uint64_t i0 = wlo; i0 < whi; i0 += 32) {
-      const uint64_t i = i0 + lane;
-      const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
-      const bool ok = i < whi && r < a.n_src;
-      const uint32_t key = ok ? (r >> a.s) : a.K;
-      const uint32_t peers = group(key);
-      const int leader = __ffs(peers) - 1;
-      uint32_t base = 0;
-      if (ok && lane == leader) {
-        const uint32_t h = myh[key];
-        base = cbase[key] + h;
-        myh[key] = (uint16_t)(h + __popc(peers));
+    for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
+      uint32_t key[U], peers[U], r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * 32 + lane;
+        r[u] = i < whi ? rid_at(i) : 0xFFFFFFFFu;
+        key[u] = (i < whi && r[u] < a.n_src) ? (r[u] >> a.s) : a.K;
       }
-      base = __shfl_sync(0xFFFFFFFFu, base, leader);
-      if (!ok) continue;
-      const uint32_t slot = base + __popc(peers & lt);
-      const uint32_t loc = r & lmask;
-      if (slot < a.cap) {
-        const uint64_t e = (uint64_t)key * a.cap + slot;
-        if (MODE == 1) {
-          pairs[e] = (PairT)loc;
-          a.inv[i] = (uint32_t)e;
-        } else if (sizeof(PairT) == 4) {
-          pairs[e] = (PairT)(((uint32_t)i << a.s) | loc);
-        } else {
-          pairs[e] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
+      group(key, peers);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * 32 + lane;
+        const bool ok = key[u] < a.K;
+        const int leader = __ffs(peers[u]) - 1;
+        uint32_t base = 0;
+        if (ok && lane == leader) {
+          const uint32_t h = myh[key[u]];
+          base = cbase[key[u]] + h;
+          myh[key[u]] = (uint16_t)(h + __popc(peers[u]));
         }
-      } else {
-        // run over capacity (skew): served after Phase II by a direct copy
-        const uint32_t o = atomicAdd(a.gbar + 2, 1u);
-        a.ovf[o] = (uint64_t)i | ((uint64_t)r << 32);
-        if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
+        if (!ok) continue;
+        const uint32_t slot = base + __popc(peers[u] & lt);
+        const uint32_t loc = r[u] & lmask;
+        if (slot < a.cap) {
+          const uint64_t e = (uint64_t)key[u] * a.cap + slot;
+          if (MODE == 1) {
+            pairs[e] = (PairT)loc;
+            a.inv[i] = (uint32_t)e;
+          } else if (sizeof(PairT) == 4) {
+            pairs[e] = (PairT)(((uint32_t)i << a.s) | loc);
+          } else {
+            pairs[e] = (PairT)((uint64_t)loc | ((uint64_t)i << 32));
+          }
+        } else {
+          // run over capacity (skew): served after Phase II by a direct copy
+          const uint32_t o = atomicAdd(a.gbar + 2, 1u);
+          a.ovf[o] = (uint64_t)i | ((uint64_t)r[u] << 32);
+          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;
+        }
       }
     }
   }

@@ -54,6 +54,9 @@ def main():
         for k, n in enumerate(names):
             d = rel[:, k + 1] - rel[:, k]
             line.append(f"{n} {np.median(d):5.1f}/{d.max():5.1f} @{rel[:, k+1].max():5.1f}")
+        d = (ts.view(G, 16).cpu().numpy().astype(np.float64) - t0) / 1e3
+        sub = [("count", 1, 6), ("prefix", 6, 7), ("reserve", 7, 8), ("scatter", 8, 2)]
+        line.append("  [" + " ".join(f"{n} {np.median(d[:, b] - d[:, a]):.1f}" for n, a, b in sub) + "]")
         print(" | ".join(line))
     print("plan", dpg.dpg_plan(src.shape[1], src.shape[0], rids.numel(), sm_count=G))
 
