@@ -148,27 +148,32 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     const uint64_t max_own = (K + sm - 1) / sm;
     const uint64_t smem = kFusedHdr + align_up(max_own * 4, 128) + kFusedStages * stage;
     if (smem > kSmemLimit) return false;
-    const uint32_t npre = std::min<uint32_t>(2, (uint32_t)std::min<uint64_t>(K, kFusedStages - 1));
-    // Phase I scratch in the stages not prefetched into: 16-bit counters per
-    // (warp, run), the CTA's run bases, and (optionally) the current rid tile.
-    const uint64_t scratch = (uint64_t)(kFusedStages - npre) * stage;
-    const uint64_t max_tile = std::min<uint64_t>(align_up(chunk, 4), 65532);
-    uint32_t hwarps = 0, tile = 0, rc_words = 0;
-    for (uint32_t hwp : {16u, 8u, 4u, 2u, 1u}) {
-      const uint64_t fixed = align_up((uint64_t)hwp * K * 2, 16) + K * 4 + 64;
-      if (fixed > scratch) continue;
-      const uint64_t room = ((scratch - fixed) / 4) & ~3ull;
-      if (room >= std::min<uint64_t>(max_tile, 1024)) {          // rid tile cached
-        tile = (uint32_t)std::min<uint64_t>(max_tile, room);
-        rc_words = tile;
-      } else {
-        tile = (uint32_t)max_tile;
-        rc_words = 0;
+    // Phase I scratch in the stages not prefetched into: the CTA's run
+    // counters (K u32), the ranks of the current tile (u16), and (preferably)
+    // the tile's rids (one bulk copy, one DRAM round trip).  A tile is the
+    // CTA's chunk up to 65532 rids (the 16-bit ranks' range); the
+    // K-proportional work of Phase I is paid once per tile, so tiles are not
+    // shrunk to fit -- rather fewer stages are prefetched, or the rids are
+    // read twice from L2.
+    uint64_t tile = std::min<uint64_t>(align_up(chunk, 4), 65532);
+    const uint32_t max_pre = (uint32_t)std::min<uint64_t>(2, std::min<uint64_t>(K, kFusedStages - 1));
+    const uint64_t kfix = align_up(K, 4) * 4 + 64;
+    uint32_t npre = 0, rc_words = 0;
+    bool found = false;
+    for (int pre = (int)max_pre; pre >= 0 && !found; --pre)
+      if (kfix + tile * 6 + 16 <= (uint64_t)(kFusedStages - pre) * stage) {
+        npre = (uint32_t)pre; rc_words = (uint32_t)tile; found = true;
       }
-      hwarps = hwp;
-      break;
+    for (int pre = (int)max_pre; pre >= 0 && !found; --pre)
+      if (kfix + tile * 2 <= (uint64_t)(kFusedStages - pre) * stage) { npre = (uint32_t)pre; found = true; }
+    if (!found) {
+      // many runs: smaller tiles (rids read from L2), all stages as scratch
+      const uint64_t room = (uint64_t)kFusedStages * stage;
+      if (kfix + 2 * 1024 > room) return false;
+      tile = std::min<uint64_t>(tile, ((room - kfix) / 2) & ~3ull);
+      npre = 0;
     }
-    if (!hwarps) return false;
+    const uint32_t hwarps = 0;
     q->npre = npre;
     q->rid_cache = rc_words ? 1 : 0;
     q->hist_warps = hwarps;

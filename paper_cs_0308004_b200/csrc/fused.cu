@@ -168,98 +168,61 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
 
   // ---- B: distribute ---------------------------------------------------------------
   // The CTA's chunk of the rid list is processed in tiles (each staged into
-  // shared memory by one bulk copy when rid_cache is set).  Each warp owns a
-  // contiguous slice of the tile and a private 16-bit counter per run.  Equal
-  // runs within a warp are found with one ballot per bit of the run id (a
-  // warp-level multisplit; no shared-memory atomics): the lowest lane of each
-  // group updates the warp's counter, the others take their rank inside the
-  // group.  Pass 1 counts; the CTA then reserves its share of every run with
-  // one global atomicAdd per run; pass 2 writes the entries (stable within the
-  // CTA).
-  const uint32_t HW = a.hist_warps;
-  uint16_t* hw = reinterpret_cast<uint16_t*>(rcache + a.rcache_words);
-  uint32_t* cbase = reinterpret_cast<uint32_t*>(hw + (((size_t)HW * a.K + 7) & ~(size_t)7));
-  uint16_t* myh = hw + (size_t)warp * a.K;
-  const uint32_t kbits = 32 - __clz(a.K);     // bits of the run id (key K marks "invalid")
-  const uint32_t lt = (1u << lane) - 1u;
-  // lanes holding the same key, for U independent key groups at once (the
-  // ballot chains interleave, hiding the vote latency)
-  constexpr int U = 4;
-  auto group = [&](const uint32_t (&key)[U], uint32_t (&peers)[U]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) peers[u] = 0xFFFFFFFFu;
-    for (uint32_t j = 0; j < kbits; ++j) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t bit = (key[u] >> j) & 1u;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-        peers[u] &= bit ? bal : ~bal;
-      }
-    }
-  };
+  // shared memory by one bulk copy when rid_cache is set).  Pass 1: every rid
+  // takes its rank inside (this CTA, its run) from a shared-memory atomicAdd on
+  // the run's counter ("count the number of elements destined for each
+  // bucket").  The CTA then reserves its share of every run with one
+  // global atomicAdd per run ("set bucket boundaries according to the
+  // statistics").  Pass 2 appends each rid to its run at base +
+  // rank ("Append r to RID_RUN[run_num]"); no further atomics.
+  uint32_t* hc = rcache + a.rcache_words;                        // [K] counts, then bases
+  uint16_t* rank = reinterpret_cast<uint16_t*>(hc + ((a.K + 3) & ~3u));   // [tile]
   PairT* pairs = reinterpret_cast<PairT*>(a.pairs);
   const uint32_t lmask = (1u << a.s) - 1u;
+  constexpr int U = 8;
   uint32_t tile_no = 0;
   for (uint64_t tlo = lo; tlo < hi; tlo += a.tile, ++tile_no) {
     const uint64_t thi = min_u64(hi, tlo + a.tile);
-    const uint64_t tspan = thi - tlo;
+    const uint32_t tspan = (uint32_t)(thi - tlo);
     if (a.rid_cache) {
-      const uint64_t t16 = tspan & ~3ull;          // 16-byte multiple (tlo % 4 == 0)
+      const uint32_t t16 = tspan & ~3u;            // 16-byte multiple (tlo % 4 == 0)
       __syncthreads();                             // previous tile fully consumed
       if (tid == 0) {
-        mbar_arrive_expect_tx(ridbar, (uint32_t)(t16 * 4));
-        if (t16) bulk_g2s(rcache, a.rids + tlo, (uint32_t)(t16 * 4), ridbar, pol_first);
+        mbar_arrive_expect_tx(ridbar, t16 * 4);
+        if (t16) bulk_g2s(rcache, a.rids + tlo, t16 * 4, ridbar, pol_first);
       }
-      if ((uint64_t)tid < tspan - t16) rcache[t16 + tid] = a.rids[tlo + t16 + tid];
+      if ((uint32_t)tid < tspan - t16) rcache[t16 + tid] = a.rids[tlo + t16 + tid];
     }
     if (tile_no == 0) prefetch_runs();
-    {
-      uint4* h4 = reinterpret_cast<uint4*>(hw);
-      for (uint32_t k = tid; k < (HW * a.K * 2 + 15) / 16; k += blockDim.x) h4[k] = make_uint4(0, 0, 0, 0);
-    }
+    for (uint32_t b = tid; b < a.K; b += blockDim.x) hc[b] = 0;
     if (a.rid_cache) mbar_wait(ridbar, tile_no & 1);
     __syncthreads();
     if (tile_no == 0) DPG_STAMP(1);
-    const uint64_t sub = ((tspan + HW - 1) / HW + 31) & ~31ull;
-    const uint64_t wlo = min_u64(thi, tlo + (uint64_t)warp * sub);
-    const uint64_t whi = warp < (int)HW ? min_u64(thi, wlo + sub) : wlo;
-    auto rid_at = [&](uint64_t i) -> uint32_t {
-      return a.rid_cache ? rcache[i - tlo] : __ldg(a.rids + i);
+    auto rid_at = [&](uint32_t j) -> uint32_t {
+      return a.rid_cache ? rcache[j] : __ldg(a.rids + tlo + j);
     };
-    // pass 1: count
-    for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
-      uint32_t key[U], peers[U];
+    // pass 1: rank within (CTA, run)
+    for (uint32_t j0 = tid; j0 < tspan; j0 += U * blockDim.x) {
+      uint32_t r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        const uint32_t r = i < whi ? rid_at(i) : 0xFFFFFFFFu;
-        const bool ok = i < whi && r < a.n_src;
-        if (i < whi && !ok) {
-          report_bad(a.status, i);
-          if (MODE == 1) a.inv[i] = 0xFFFFFFFFu;      // row left unwritten
-        }
-        key[u] = ok ? (r >> a.s) : a.K;
+        const uint32_t j = j0 + u * blockDim.x;
+        r[u] = j < tspan ? rid_at(j) : 0xFFFFFFFFu;
       }
-      group(key, peers);
 #pragma unroll
-      for (int u = 0; u < U; ++u)   // in order: a later group may lead the same run
-        if (key[u] < a.K && (peers[u] & lt) == 0)
-          myh[key[u]] = (uint16_t)(myh[key[u]] + __popc(peers[u]));
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j >= tspan) continue;
+        if (r[u] < a.n_src) {
+          rank[j] = (uint16_t)atomicAdd(&hc[r[u] >> a.s], 1u);
+        } else {
+          report_bad(a.status, tlo + j);
+          if (MODE == 1) a.inv[tlo + j] = 0xFFFFFFFFu;   // row left unwritten
+        }
+      }
     }
     __syncthreads();
     if (tile_no == 0) DPG_STAMP(6);
-    // warp-exclusive prefixes per run, CTA totals, one reservation per run
-    for (uint32_t b = tid; b < a.K; b += blockDim.x) {
-      uint32_t sum = 0;
-      for (uint32_t w = 0; w < HW; ++w) {
-        const uint32_t h = hw[(size_t)w * a.K + b];
-        hw[(size_t)w * a.K + b] = (uint16_t)sum;
-        sum += h;
-      }
-      cbase[b] = sum;
-    }
-    __syncthreads();
-    if (tile_no == 0) DPG_STAMP(7);
     {
       constexpr int BPT = 8;    // a thread's reservations are all in flight together
       for (uint32_t b0 = tid; b0 < a.K; b0 += BPT * blockDim.x) {
@@ -267,45 +230,36 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
           const uint32_t b = b0 + q * blockDim.x;
-          const uint32_t n = b < a.K ? cbase[b] : 0u;
+          const uint32_t n = b < a.K ? hc[b] : 0u;
           base[q] = n ? atomicAdd(&a.total[b], n) : 0u;
         }
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
           const uint32_t b = b0 + q * blockDim.x;
-          if (b < a.K) cbase[b] = base[q];
+          if (b < a.K) hc[b] = base[q];
         }
       }
     }
     __syncthreads();
-    if (tile_no == 0) DPG_STAMP(8);
+    if (tile_no == 0) DPG_STAMP(7);
     // pass 2: append each rid to its run
-    for (uint64_t i0 = wlo; i0 < whi; i0 += 32 * U) {
-      uint32_t key[U], peers[U], r[U];
+    for (uint32_t j0 = tid; j0 < tspan; j0 += U * blockDim.x) {
+      uint32_t r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        r[u] = i < whi ? rid_at(i) : 0xFFFFFFFFu;
-        key[u] = (i < whi && r[u] < a.n_src) ? (r[u] >> a.s) : a.K;
+        const uint32_t j = j0 + u * blockDim.x;
+        r[u] = j < tspan ? rid_at(j) : 0xFFFFFFFFu;
       }
-      group(key, peers);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t i = i0 + u * 32 + lane;
-        const bool ok = key[u] < a.K;
-        const int leader = __ffs(peers[u]) - 1;
-        uint32_t base = 0;
-        if (ok && lane == leader) {
-          const uint32_t h = myh[key[u]];
-          base = cbase[key[u]] + h;
-          myh[key[u]] = (uint16_t)(h + __popc(peers[u]));
-        }
-        base = __shfl_sync(0xFFFFFFFFu, base, leader);
-        if (!ok) continue;
-        const uint32_t slot = base + __popc(peers[u] & lt);
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j >= tspan || r[u] >= a.n_src) continue;
+        const uint64_t i = tlo + j;
+        const uint32_t b = r[u] >> a.s;
+        const uint32_t slot = hc[b] + rank[j];
         const uint32_t loc = r[u] & lmask;
         if (slot < a.cap) {
-          const uint64_t e = (uint64_t)key[u] * a.cap + slot;
+          const uint64_t e = (uint64_t)b * a.cap + slot;
           if (MODE == 1) {
             pairs[e] = (PairT)loc;
             a.inv[i] = (uint32_t)e;
@@ -322,6 +276,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
         }
       }
     }
+    if (tile_no == 0) DPG_STAMP(8);
   }
   DPG_STAMP(2);
   grid_barrier(a.gbar, G);

@@ -86,8 +86,8 @@ def test_argument_validation_before_any_cuda_call(dpg):
 @pytest.mark.parametrize("rec,n,L,K,path", [
     (100, 65536, 128, 512, 1),        # config 1: runs shrink for load balance
     (100, 1048576, 512, 2048, 1),     # config 2: fused kernel, 4 stages of 50 KB runs
-    (64, 16777216, 1024, 16384, 2),   # config 3 at rec 64: K too large for the fused kernel
-    (256, 16777216, 256, 65536, 2),
+    (64, 16777216, 512, 32768, 1),    # config 3 at rec 64: smaller Phase I tiles
+    (256, 16777216, 256, 65536, 2),   # too many runs for the fused kernel
 ])
 def test_plan_run_length(dpg, rec, n, L, K, path):
     p = dpg.dpg_plan(rec, n, n, 0, 148)

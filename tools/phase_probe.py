@@ -19,14 +19,21 @@ def main():
     ap.add_argument("--rec", type=int, default=None)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--gather", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0, help="synthetic permutation of n records of --rec bytes")
     args = ap.parse_args()
     import torch
 
     import datagen
     import paper_cs_0308004_b200 as dpg
-    w = datagen.make(args.config, rec=args.rec) if args.rec else datagen.make(args.config)
-    src = torch.from_numpy(w["src"]).cuda()
-    rids = torch.from_numpy(w["rids"].view(np.int32)).cuda()
+    if args.n:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(0)
+        src = torch.randint(0, 256, (args.n, args.rec or 100), dtype=torch.uint8, device="cuda")
+        rids = torch.randperm(args.n, device="cuda", generator=g).to(torch.int32)
+    else:
+        w = datagen.make(args.config, rec=args.rec) if args.rec else datagen.make(args.config)
+        src = torch.from_numpy(w["src"]).cuda()
+        rids = torch.from_numpy(w["rids"].view(np.int32)).cuda()
     out = torch.empty((rids.numel(), src.shape[1]), dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     G = torch.cuda.get_device_properties(0).multi_processor_count
