@@ -184,9 +184,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   for (uint64_t tlo = lo; tlo < hi; tlo += a.tile, ++tile_no) {
     const uint64_t thi = min_u64(hi, tlo + a.tile);
     const uint32_t tspan = (uint32_t)(thi - tlo);
+    if (tile_no) __syncthreads();                  // previous tile fully consumed
     if (a.rid_cache) {
       const uint32_t t16 = tspan & ~3u;            // 16-byte multiple (tlo % 4 == 0)
-      __syncthreads();                             // previous tile fully consumed
       if (tid == 0) {
         mbar_arrive_expect_tx(ridbar, t16 * 4);
         if (t16) bulk_g2s(rcache, a.rids + tlo, t16 * 4, ridbar, pol_first);
