@@ -1,16 +1,17 @@
 // fused.cu -- the whole DPG path in one persistent cooperative kernel.
 //
 //   Phase I   Distribute (Fig. 1).  Every rid r goes to
-//        run r >> s ("the high order bits"): it reserves the next
-//        slot of its run with one atomicAdd on the run's cursor and appends
-//        (r - run*L, i) there ("Append r to RID_RUN[run_num]", plus the
-//        position i Phase III needs).  Runs have a fixed capacity
-//        CAP: a permutation puts exactly L rids into every run (the paper's
-//        sorting case), rids drawn with replacement exceed L only
-//        by a Poisson tail, and the rare excess -- or a skewed rid list
-//        (section 2.3) -- goes to an overflow list served after
-//        Phase II by direct copies.  No counting pass, no scan: one pass over
-//        the rid list, then one grid barrier.
+//        run r >> s ("the high order bits").  Per tile of the CTA's
+//        chunk: each rid takes its rank inside (CTA, run) from a shared-memory
+//        atomicAdd, the CTA reserves its share of every run with one global
+//        atomicAdd per run, and each rid appends (r - run*L, i) at base + rank
+//        ("Append r to RID_RUN[run_num]", plus the position i Phase
+//        III needs).  Runs have a fixed capacity CAP: a
+//        permutation puts exactly L rids into every run (the paper's sorting
+//        case), rids drawn with replacement exceed L only by a
+//        Poisson tail, and the rare excess -- or a skewed rid list (section
+//        2.3) -- goes to an overflow list served after Phase II by
+//        direct copies.  No scan: one grid barrier ends Phase I.
 //   Phase II  Probe (Fig. 1): warp 0 is a TMA producer
 //        that bulk-copies each run of INPUT owned by this CTA ("load the i-th
 //        INPUT run entirely into cache") plus the run's entries
