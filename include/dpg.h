@@ -169,6 +169,18 @@ dpg_status_t dpg_distribute(const uint32_t *rids, uint64_t n_out, uint64_t n_src
                             uint64_t *run_start_out, dpg_stream_t stream,
                             const dpg_options_t *opt);
 
+/* Multi-GPU Phase I by owner: rids (uint32 or uint64,
+ * rid_bytes = 4 or 8, device) are distributed to owners r >> log2_span
+ * (parts owners, each owning 2^log2_span consecutive source records of the
+ * n_src_total).  Outputs (device): local_out[j] = rid - owner * 2^log2_span
+ * and pos_out[j] = the rid's position, grouped by owner (owner 0 first; order
+ * inside an owner unspecified); counts_out[parts] (uint64) = requests per
+ * owner.  Invalid rids (>= n_src_total) are reported as in dpg_retrieve and
+ * dropped.  Requires n_src_total <= parts << log2_span. */
+dpg_status_t dpg_partition(const void *rids, uint32_t rid_bytes, uint64_t n, uint64_t n_src_total,
+                           uint32_t log2_span, uint32_t parts, uint32_t *local_out,
+                           uint32_t *pos_out, uint64_t *counts_out, dpg_stream_t stream);
+
 /* Owner-side helper of the multi-GPU path: dst[pos[k]] = rows[k] for k in
  * [0, n) (Phase III against received replies).  pos must be distinct. */
 dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t *pos,

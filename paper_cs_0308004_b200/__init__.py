@@ -40,7 +40,7 @@ EXPORTED = (
     "dpg_fk_join_ex", "dpg_distribute", "dpg_scatter_rows", "dpg_retrieve_host",
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
-    "dpg_retrieve_direct_ex", "dpg_l2_prefetch",
+    "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition",
 )
 
 
@@ -87,6 +87,8 @@ _sigs = {
     "dpg_sync_status": [_P, _P],
     "dpg_retrieve_direct_ex": [_P, _S, _U, _P, _U, _P, _P, _I],
     "dpg_l2_prefetch": [_P, _U, _P],
+    "dpg_partition": [_P, ctypes.c_uint32, _U, _U, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _P,
+                      _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -271,6 +273,26 @@ def dpg_distribute(rids, n_src: int, log2_run: int, stream=None, **opts):
                                rs.data_ptr(), _stream_ptr(stream), _ref(_options(**opts))),
            "dpg_distribute")
     return pairs[:n_out], rs
+
+
+def dpg_partition(rids, n_src_total: int, log2_span: int, parts: int, stream=None):
+    """Distribute rids (CUDA int32/uint32/int64/uint64) to owners rid >> log2_span.
+    Returns (local int32 [m], pos int32 [m], counts int64 [parts]) as CUDA
+    tensors, grouped by owner (m = number of valid rids)."""
+    torch = _torch()
+    if not rids.is_cuda or not rids.is_contiguous():
+        raise ValueError("rids must be a contiguous CUDA tensor (no CPU fallback)")
+    rb = rids.element_size()
+    if rb not in (4, 8):
+        raise ValueError("rids must be 32- or 64-bit")
+    n = rids.numel()
+    local = torch.empty(max(n, 1), dtype=torch.int32, device=rids.device)
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=rids.device)
+    counts = torch.empty(parts, dtype=torch.int64, device=rids.device)
+    _check(_lib.dpg_partition(rids.data_ptr(), rb, n, n_src_total, log2_span, parts,
+                              local.data_ptr(), pos.data_ptr(), counts.data_ptr(),
+                              _stream_ptr(stream)), "dpg_partition")
+    return local, pos, counts
 
 
 def dpg_scatter_rows(rows, pos, dst, stream=None):

@@ -719,6 +719,57 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   return cuda_status(e);
 }
 
+dpg_status_t dpg_partition(const void* rids, uint32_t rid_bytes, uint64_t n, uint64_t n_src_total,
+                           uint32_t log2_span, uint32_t parts, uint32_t* local_out,
+                           uint32_t* pos_out, uint64_t* counts_out, dpg_stream_t stream) {
+  t_launches = 0;
+  if ((rid_bytes != 4 && rid_bytes != 8) || parts == 0 || log2_span > 32 || !counts_out)
+    return DPG_ERR_INVALID_ARG;
+  if (n && (!rids || !local_out || !pos_out)) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  if (n_src_total == 0 || (((n_src_total - 1) >> log2_span) >= parts)) return DPG_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  if (n == 0) return cuda_status(cudaMemsetAsync(counts_out, 0, parts * sizeof(uint64_t), st));
+  const int sm = current_sm_count();
+  dpg_plan_t p;
+  std::memset(&p, 0, sizeof(p));
+  p.log2_run = log2_span;
+  p.num_runs = parts;
+  p.pair_bytes = 8;
+  dpg_options_t o;
+  std::memset(&o, 0, sizeof(o));
+  o.hist_mode = 1;                      // parts counters always fit shared memory
+  if (parts * 4 > kSmemLimit) return DPG_ERR_UNSUPPORTED;
+  dpg_status_t ds = dist_geometry(parts, n, &o, sm, &p);
+  if (ds != DPG_OK) return ds;
+  Workspace w;
+  dpg_status_t as = alloc_workspace(p, n, st, &w);
+  if (as != DPG_OK) return as;
+  DistArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = rids;
+  d.n_out = n;
+  d.n_src = n_src_total;
+  d.s = log2_span;
+  d.K = parts;
+  d.G = p.grid_distribute;
+  d.chunk = (n + d.G - 1) / d.G;
+  d.counts = w.counts;
+  d.run_start = w.run_start;
+  d.pairs = w.pairs;
+  d.pair_bytes = 8;
+  d.hist_smem = 1;
+  d.status = status;
+  uint32_t nl = 0;
+  cudaError_t e = launch_distribute(d, rid_bytes == 8, st, &nl);
+  if (e == cudaSuccess) e = launch_split_entries(d, local_out, pos_out, counts_out, st, &nl);
+  cudaFreeAsync(w.base, st);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
 dpg_status_t dpg_scatter_rows(const void* rows, size_t rec_bytes, const uint32_t* pos, uint64_t n,
                               void* dst, uint64_t n_dst, dpg_stream_t stream) {
   t_launches = 0;

@@ -271,4 +271,28 @@ cudaError_t launch_unpack_pairs(const DistArgs& a, uint64_t* pairs_out, uint64_t
   return cudaGetLastError();
 }
 
+// Owner partition (multi-GPU): 8-byte entries (local | pos << 32) grouped by
+// owner -> separate request (local) and position arrays + per-owner counts.
+__global__ void k_split_entries(const uint64_t* pairs, const uint32_t* rs, uint32_t K,
+                                uint32_t* local_out, uint32_t* pos_out, uint64_t* counts) {
+  const uint64_t n = rs[K];
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = t; j < n; j += stride) {
+    const uint64_t p = pairs[j];
+    local_out[j] = (uint32_t)p;
+    pos_out[j] = (uint32_t)(p >> 32);
+  }
+  for (uint64_t b = t; b < K; b += stride) counts[b] = rs[b + 1] - rs[b];
+}
+
+cudaError_t launch_split_entries(const DistArgs& a, uint32_t* local_out, uint32_t* pos_out,
+                                 uint64_t* counts, cudaStream_t st, uint32_t* nl) {
+  const uint32_t grid = (uint32_t)min_u64(4096, max_u64(1, (a.n_out + 255) / 256));
+  k_split_entries<<<grid, 256, 0, st>>>((const uint64_t*)a.pairs, a.run_start, a.K, local_out,
+                                        pos_out, counts);
+  ++*nl;
+  return cudaGetLastError();
+}
+
 }  // namespace dpg

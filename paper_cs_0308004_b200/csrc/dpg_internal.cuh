@@ -257,6 +257,8 @@ cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cuda
 cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos,
                                 uint64_t n, uint8_t* dst, uint64_t n_dst, uint32_t W,
                                 int sm_count, cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_split_entries(const DistArgs& a, uint32_t* local_out, uint32_t* pos_out,
+                                 uint64_t* counts, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_unpack_pairs(const DistArgs& a, uint64_t* pairs_out, uint64_t* run_start_out,
                                 cudaStream_t st, uint32_t* nlaunch);
 

@@ -1,0 +1,63 @@
+"""The multi-GPU path's GPU pieces on one GPU: the owner partition kernel
+against a plain definition, and the whole exchange (NCCL, world size 1)
+against the oracle.  Multi-rank exchanges are covered on CPU by
+tests/test_dist_gloo.py (no second GPU in this environment)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dpg():
+    import paper_cs_0308004_b200 as m
+    return m
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("parts,log2_span,n_total", [(4, 10, 4096), (8, 7, 1000), (1, 12, 3000)])
+def test_partition_groups_by_owner(dpg, dtype, parts, log2_span, n_total):
+    rng = np.random.default_rng(parts * 100 + log2_span)
+    rids = rng.integers(0, n_total, 5000).astype(dtype)
+    local, pos, counts = dpg.dpg_partition(torch.from_numpy(rids).cuda(), n_total, log2_span, parts)
+    torch.cuda.synchronize()
+    counts = counts.cpu().numpy()
+    m = int(counts.sum())
+    local = local[:m].cpu().numpy().astype(np.int64)
+    pos = pos[:m].cpu().numpy().astype(np.int64)
+    owner = rids.astype(np.int64) >> log2_span
+    assert np.array_equal(counts, np.bincount(owner, minlength=parts))
+    start = np.concatenate([[0], np.cumsum(counts)])
+    for o in range(parts):
+        seg_pos = pos[start[o]:start[o + 1]]
+        seg_loc = local[start[o]:start[o + 1]]
+        want = np.nonzero(owner == o)[0]
+        assert np.array_equal(np.sort(seg_pos), want)
+        assert np.array_equal(seg_loc + (o << log2_span), rids[seg_pos].astype(np.int64))
+
+
+def test_retrieve_dist_single_rank_nccl(dpg):
+    import torch.distributed as dist
+    from paper_cs_0308004_b200.dist import retrieve_dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(3)
+        src = rng.integers(0, 256, (50000, 100), dtype=np.uint8)
+        rids = rng.integers(0, 50000, 70000).astype(np.int64)
+        out = retrieve_dist(torch.from_numpy(src).cuda(), torch.from_numpy(rids).cuda(), 50000,
+                            max_rows_per_round=30000)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+    finally:
+        dist.destroy_process_group()
