@@ -10,11 +10,13 @@ resident in HBM: dpg_retrieve on BASELINE.json configs[1] (Datamation-shaped
 sort phase 3, 1,048,576 x 100-byte records, rids = stable argsort of the
 10-byte keys).  L2 is flushed (a 512 MiB write) before every timed step and
 each step is timed alone with CUDA events on the launching stream; flush time
-is excluded.  Multi-process (torchrun, N > 1): every rank runs its own
-replica of the workload ("replicas", weak scaling) and the job time is the max
-over ranks.
+is excluded.  Multi-process (torchrun, N > 1): BASELINE.json config 5 --
+2^30 x 100-byte records range-partitioned over the ranks, rids a global
+permutation block-partitioned by output position -- through the multi-GPU
+path (owner partition, NCCL all-to-alls, local DPG, reply scatter); job time
+= max over ranks of the CUDA-event time.
 
-The JSON line adds: roofline of the dominant kernel (k_probe_gather) from its
+The JSON line adds: roofline of the dominant kernel (k_dpg_fused) from its
 own CUDA-event time inside the same timed steps, the naive direct-gather
 comparison timed the same way, the end-to-end number through the host-buffer
 C-ABI entry, the oracle's CPU throughput (cpu_baseline) and the SM clocks
@@ -23,6 +25,8 @@ sampled during the timed region.
 from __future__ import annotations
 
 import argparse
+
+import numpy as np
 import json
 import os
 import sys
@@ -39,14 +43,20 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dpg", choices=["dpg", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3a", "c3b", "c4"])
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c5"],
+                    help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
+    ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
+    ap.add_argument("--c5-round-rows", type=int, default=1 << 26)
     ap.add_argument("--rec", type=int, default=None, help="record bytes for c3a/c3b")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config is None:
+        a.config = "c5" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "c2"
+    return a
 
 
 def dist_env():
@@ -61,7 +71,9 @@ def workload_name(cfg: str, rec: int | None) -> str:
             "c2": "c2: Datamation sort phase 3, 1,048,576 x 100 B, rids = stable argsort of 10-B keys",
             "c3a": f"c3a: 16,777,216 x {rec} B, uniform random permutation",
             "c3b": f"c3b: 16,777,216 x {rec} B, uniform rids with replacement",
-            "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)"}[cfg]
+            "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)",
+            "c5": "c5 sample for the host oracle: 2^22 x 100 B of the c5 source stream, "
+                  "rids = c5 Feistel permutation of [0, 2^22)"}[cfg]
 
 
 def make_inputs(cfg: str, rec: int | None):
@@ -119,7 +131,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.ok:
@@ -200,7 +212,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = args.config
-    w = make_inputs(cfg, args.rec)
+    if cfg == "c5":
+        # bounded sample of the c5 workload for the host oracle: 2^22 records
+        # of the c5 source stream, rids = the c5 Feistel permutation of [0, 2^22)
+        import datagen
+        n = 1 << 22
+        w = {"src": datagen.records(n, 100, datagen.STREAMS[("c5", "src")]),
+             "rids": datagen.feistel(n, 0, n, datagen.STREAMS[("c5", "rids")]).astype(np.uint32)}
+        cfg = "c2"     # same shape of work (100-byte records, 4-byte rids) for units()
+    else:
+        w = make_inputs(cfg, args.rec)
     import oracle
     n_out, rec, alg_bytes, _ = units(cfg, w)
     fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg == "c4" else \
@@ -221,7 +242,7 @@ def run_reference(args):
         "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (datagen, seed 0)",
-        "config": {"workload": workload_name(cfg, args.rec), "n_out": n_out, "rec_bytes": rec},
+        "config": {"workload": workload_name(args.config, args.rec), "n_out": n_out, "rec_bytes": rec},
         "records_per_s": n_out / t,
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                          "sample": f"full {cfg} workload, {len(times)} steps",
@@ -229,6 +250,86 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_c5(args, rank, world):
+    """BASELINE.json config 5: 2^30 x 100-byte records range-partitioned over the
+    ranks, rids = a Feistel permutation of [0, 2^30) block-partitioned by output
+    position; the multi-GPU path (paper_cs_0308004_b200/dist.py): owner
+    partition, NCCL all-to-alls, local DPG, reply scatter.  Inputs are
+    generated on each GPU by the counter-based generators (datagen)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    from paper_cs_0308004_b200.dist import owned_range, retrieve_dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rec = 100
+    n_total = 1 << args.c5_log2
+    lo, hi = owned_range(rank, world, n_total)
+    src = torch.empty((hi - lo, rec), dtype=torch.uint8, device=dev)
+    datagen.random_bytes_cuda(src.view(-1), datagen.STREAMS[("c5", "src")], offset=lo * rec)
+    b0, b1 = rank * n_total // world, (rank + 1) * n_total // world
+    rids = datagen.feistel_cuda(n_total, b0, b1 - b0, datagen.STREAMS[("c5", "rids")])
+    torch.cuda.synchronize()
+
+    def step():
+        return retrieve_dist(src, rids, n_total, max_rows_per_round=args.c5_round_rows)
+
+    out = None
+    for _ in range(max(1, min(args.warmup, 3))):
+        out = step()
+    torch.cuda.synchronize()
+    # sampled parity against the host generators (the definition, pointwise)
+    idx = np.random.default_rng(rank).integers(0, b1 - b0, 256)
+    got = out[torch.from_numpy(idx).to(dev)].cpu().numpy()
+    want_r = datagen.feistel(n_total, b0, b1 - b0, datagen.STREAMS[("c5", "rids")])[idx] \
+        if b1 - b0 <= (1 << 26) else np.array(
+            [datagen.feistel(n_total, b0 + int(j), 1, datagen.STREAMS[("c5", "rids")])[0] for j in idx])
+    want = np.stack([datagen.random_bytes(rec, datagen.STREAMS[("c5", "src")], offset=int(r) * rec)
+                     for r in want_r])
+    parity_ok = bool(np.array_equal(got, want))
+    del out
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            out = step()
+            del out
+        ev1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = torch.tensor([1 if parity_ok else 0], dtype=torch.int64, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    alg = n_total * (2 * rec + 8)
+    value = alg / (ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    nvl = (world - 1) / world * (n_total / world) * (rec + 4) / 900e9 * 1e3 if world > 1 else 0.0
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (datagen on device, seed 0)",
+            "config": {"workload": f"c5: 2^{args.c5_log2} x 100 B range-partitioned, rids = Feistel "
+                                   "permutation (uint64) block-partitioned", "n_total": n_total,
+                       "rec_bytes": rec, "rid_bytes": 8, "parallelism": f"ep{world} (owner exchange)",
+                       "round_rows": args.c5_round_rows, "l2": "inputs >> L2"},
+            "records_per_s": n_total / (ms * 1e-3),
+            "frac_of_hbm_peak_aggregate": value / (world * peak),
+            "nvlink_roofline_ms": nvl, "frac_of_nvlink_roofline": (nvl / ms) if nvl else None,
+            "parity_sampled_ok": bool(ok.item()),
+            "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev)}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
     return 0
 
 
@@ -248,6 +349,8 @@ def main():
     import paper_cs_0308004_b200 as dpg
 
     cfg = args.config
+    if cfg == "c5":
+        return run_c5(args, rank, world)
     w = make_inputs(cfg, args.rec)
     n_out, rec, alg_bytes, rid_bytes = units(cfg, w)
     dev = torch.device("cuda", torch.cuda.current_device())

@@ -49,13 +49,59 @@ STREAMS = {
 C3_RECS = (8, 16, 32, 64, 128, 256)
 
 
+_CU_SRC = os.path.join(_HERE, "gen_cuda.cu")
+_CU_LIB = os.path.join(_HERE, "libdpggen_cuda.so")
+_culib = None
+
+
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O3", "-std=c11", "-fopenmp", "-shared", "-fPIC",
                                _SRC, "-o", tmp])
         os.replace(tmp, _LIB)
+    if force or not os.path.exists(_CU_LIB) or os.path.getmtime(_CU_LIB) < os.path.getmtime(_CU_SRC):
+        tmp = _CU_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-O3", "-std=c++17", "-shared",
+                               "-Xcompiler", "-fPIC", "-cudart", "static",
+                               "-gencode", "arch=compute_100a,code=sm_100a", _CU_SRC, "-o", tmp])
+        os.replace(tmp, _CU_LIB)
     return _LIB
+
+
+def _load_cuda():
+    global _culib
+    if _culib is None:
+        build()
+        lib = ctypes.CDLL(_CU_LIB)
+        U, P = ctypes.c_uint64, ctypes.c_void_p
+        lib.gen_bytes_cuda.argtypes = [U, U, U, U, P, P]
+        lib.gen_feistel_cuda.argtypes = [U, U, ctypes.c_uint, ctypes.c_uint, U, U, U, P, P]
+        _culib = lib
+    return _culib
+
+
+def random_bytes_cuda(t, sid: int, seed: int = SEED, offset: int = 0):
+    """Fill the CUDA uint8 tensor t with bytes [offset, offset + t.numel()) of
+    stream sid (same values as random_bytes; offset and size multiples of 8)."""
+    import torch
+    s = torch.cuda.current_stream().cuda_stream
+    if _load_cuda().gen_bytes_cuda(seed, sid, offset, t.numel(), t.data_ptr(), s):
+        raise RuntimeError("gen_bytes_cuda failed")
+    return t
+
+
+def feistel_cuda(n: int, first: int, count: int, sid: int, seed: int = SEED, rounds: int = 6):
+    """Elements [first, first+count) of the Feistel permutation of [0, n) as a
+    CUDA int64 tensor (same values as feistel)."""
+    import torch
+    bits = max(2, (n - 1).bit_length())
+    bits += bits & 1
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    if _load_cuda().gen_feistel_cuda(seed, sid, bits, rounds, n, first, count, out.data_ptr(), s):
+        raise RuntimeError("gen_feistel_cuda failed")
+    return out
 
 
 def _load():
