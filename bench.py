@@ -340,8 +340,10 @@ def main():
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.config == "c5":
         torch.cuda.set_device(local)
+        if "MASTER_ADDR" not in os.environ:        # single process without torchrun
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
