@@ -435,10 +435,11 @@ def main():
     peak, peak_src = hbm_peak()
     dist_ms, probe_ms, calls = ph
     pg_ms = probe_ms / max(1, calls)
-    plan = dpg.dpg_plan(rec if cfg != "c4" else w["dim"].shape[1], n_src, n_out,
-                        16 if cfg == "c4" else 0, torch.cuda.get_device_properties(dev).multi_processor_count)
+    # (the join runs a DPG retrieval of dim rows -- no payload -- then a zip pass)
+    plan = dpg.dpg_plan(rec if cfg != "c4" else w["dim"].shape[1], n_src, n_out, 0,
+                        torch.cuda.get_device_properties(dev).multi_processor_count)
     src_rec = w["dim"].shape[1] if cfg == "c4" else rec
-    pay = 16 if cfg == "c4" else 0
+    pay = 0
     if plan["path"] == 1:
         # one persistent kernel runs the whole path: its algorithmic bytes are
         # the path's, N * (2 * rec + rid_bytes)

@@ -2,6 +2,7 @@
 // planning of the run length L, stream-ordered workspace, and the
 // kernel sequence  distribute (Phase I) -> fused probe+gather (Phases II+III).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -139,7 +140,11 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   auto fits = [&](uint32_t s, dpg_plan_t* q) -> bool {
     const uint64_t L = 1ull << s;
     const uint64_t K = (n_src + L - 1) >> s;
-    const uint64_t cap = align_up(L + L / 4 + 32, 8);
+    // expected entries per run: L * n_out / n_src (exactly L for a
+    // permutation); capacity = expectation + L/4 (+ 4 sigma when rids repeat)
+    const double expect = (double)L * (double)n_out / (double)std::max<uint64_t>(n_src, 1);
+    const uint64_t cap = align_up((uint64_t)(expect + (double)(L / 4) +
+                                             (n_out > n_src ? 4.0 * std::sqrt(expect) : 0.0)) + 32, 8);
     if (K * cap >= (1ull << 32)) return false;
     const uint32_t pb = gather == 2 ? (s <= 16 && !force8 ? 2u : 4u)
                                     : ((!force8 && s + pos_bits <= 32) ? 4u : 8u);
@@ -609,8 +614,48 @@ dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact
                             const uint32_t* fk_col, const void* dim, size_t rec_bytes,
                             uint64_t n_dim, void* out, dpg_stream_t stream,
                             const dpg_options_t* opt) {
-  return run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, fact, fact_bytes, out,
-                 (cudaStream_t)stream, opt);
+  // DPG-Move join: with the join triples in rid_R order, "move the
+  // records of F into a temporary file according to the ordering of the
+  // records of R" -- a DPG retrieval of dim by fk_col -- then "join the
+  // temporary file with the remaining relation", one sequential
+  // pass writing out row i = fact[i] ++ temp[i].  (opt->path == 2 with a
+  // payload instead carries the fact row through the distribute kernels.)
+  t_launches = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (fact_bytes == 0 || (opt && opt->path == 2))
+    return run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, fact, fact_bytes, out, st, opt);
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n_fact == 0) return DPG_OK;
+  if (!fact || !fk_col || !dim || !out || n_dim == 0) return DPG_ERR_INVALID_ARG;
+  uint64_t row, out_bytes, tmp_bytes, fact_total, dim_total;
+  if (__builtin_add_overflow((uint64_t)fact_bytes, (uint64_t)rec_bytes, &row) ||
+      __builtin_mul_overflow(n_fact, row, &out_bytes) ||
+      __builtin_mul_overflow(n_fact, (uint64_t)rec_bytes, &tmp_bytes) ||
+      __builtin_mul_overflow(n_fact, (uint64_t)fact_bytes, &fact_total) ||
+      __builtin_mul_overflow(n_dim, (uint64_t)rec_bytes, &dim_total))
+    return DPG_ERR_INVALID_ARG;
+  if (row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  if (overlaps(out, out_bytes, fact, fact_total) || overlaps(out, out_bytes, dim, dim_total) ||
+      overlaps(out, out_bytes, fk_col, n_fact * 4))
+    return DPG_ERR_INVALID_ARG;
+  void* tmp = nullptr;
+  if (cudaMallocAsync(&tmp, tmp_bytes + 256, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  dpg_status_t s = run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, nullptr, 0, tmp, st, opt);
+  uint32_t nl = t_launches;
+  if (s == DPG_OK) {
+    const uint32_t W = pow2_divisor(fact_bytes | rec_bytes | (uintptr_t)fact | (uintptr_t)tmp |
+                                    (uintptr_t)out);
+    cudaError_t e = launch_zip_rows((const uint8_t*)fact, (uint32_t)fact_bytes,
+                                    (const uint8_t*)tmp, (uint32_t)rec_bytes, n_fact,
+                                    (uint8_t*)out, W, current_sm_count(), st, &nl);
+    s = cuda_status(e);
+  }
+  cudaFreeAsync(tmp, st);
+  t_launches = nl;
+  return s;
 }
 
 dpg_status_t dpg_fk_join(const void* fact, size_t fact_bytes, uint64_t n_fact,
