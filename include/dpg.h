@@ -218,6 +218,11 @@ void dpg_phase_timing(int enable);
  * Phase I count done, barrier 1, scatter done, barrier 2, end).  NULL turns
  * it off. */
 void dpg_debug_phase_stamps(void *device_buf);
+
+/* Tuning experiments only: code-generation variants of the fused kernel that
+ * do not change any result (store cache policies, reservation order).  0 is
+ * the default and what every other caller gets. */
+void dpg_debug_flags(uint32_t flags);
 dpg_status_t dpg_phase_times(double *distribute_ms, double *probe_gather_ms, uint32_t *calls);
 
 int dpg_version(void);

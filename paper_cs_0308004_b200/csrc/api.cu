@@ -18,7 +18,8 @@ constexpr uint32_t kBarBytes = 128;
 constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives in smem
 
 thread_local uint32_t t_launches = 0;
-unsigned long long* g_debug_ts = nullptr;  // profiling: per-CTA phase stamps of the fused kernel
+unsigned long long* g_debug_ts = nullptr;
+uint32_t g_debug_flags = 0;            // tuning experiments only (dpg_debug_flags)  // profiling: per-CTA phase stamps of the fused kernel
 
 // ---- optional phase timing (events on the call's stream) --------------------
 std::mutex g_timing_mu;
@@ -467,6 +468,16 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.max_own = (uint32_t)((p.num_runs + p.grid_probe - 1) / p.grid_probe);
     f.status = status;
     f.ts = g_debug_ts;
+    f.dbg = g_debug_flags;
+    {
+      // Phase II: about 3/4 of the runs statically (c + t*G), the rest claimed
+      // dynamically by the CTAs that finish first
+      const uint64_t G = p.grid_probe, K = p.num_runs;
+      const uint64_t frac16 = (f.dbg >> 8) & 31 ? (f.dbg >> 8) & 31 : 12;
+      uint64_t ns = frac16 >= 16 ? (K + G - 1) / G : K * frac16 / (16 * G);
+      ns = std::max<uint64_t>(ns, p.npre);
+      f.n_static = (uint32_t)std::min<uint64_t>(ns, (K + G - 1) / G);
+    }
     uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst |
                               (f.mode == 1 ? (uintptr_t)f.internal : 0));
     uint32_t nl = 0;
@@ -556,6 +567,7 @@ int dpg_version(void) { return 1; }
 uint32_t dpg_last_launch_count(void) { return t_launches; }
 
 void dpg_debug_phase_stamps(void* device_buf) { g_debug_ts = (unsigned long long*)device_buf; }
+void dpg_debug_flags(uint32_t flags) { g_debug_flags = flags; }
 
 void dpg_phase_timing(int enable) {
   std::lock_guard<std::mutex> lk(g_timing_mu);

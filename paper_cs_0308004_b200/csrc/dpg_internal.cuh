@@ -155,8 +155,9 @@ struct FusedArgs {
   uint64_t n_out;
   uint64_t chunk;        // rids per CTA in the distribute phases
   uint32_t* total;       // [K] run totals; zero on entry, restored to zero on exit
-  uint32_t* gbar;        // [4] grid barrier (count, generation), overflow count, done
-                         //     counter; persistent, zero-restored by the kernel
+  uint32_t* gbar;        // [5] grid barrier (count, generation), overflow count, done
+                         //     counter, dynamic run counter; persistent, zero-restored
+                         //     by the kernel
   void* pairs;           // [n_out] pairs (+ slack for 16-byte bulk copies)
   uint32_t pair_bytes;
   uint8_t* dst;
@@ -178,6 +179,11 @@ struct FusedArgs {
   uint32_t mode;         // 0: probe writes rows straight to dst; 1: probe -> INTERNAL -> gather
   uint8_t* internal;     // [n_out * rec] INTERNAL file (mode 1)
   uint32_t* inv;         // [n_out] INTERNAL slot of output row i (mode 1)
+  uint32_t n_static;     // Phase II: static runs per CTA (c + t*grid, t < n_static); the
+                         // rest are claimed dynamically (gbar[4])
+  uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 plain row stores (no
+                         // evict_last hint), bit1 staggered run reservations,
+                         // bits 8-12 static share of Phase II runs in 16ths
 };
 
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion

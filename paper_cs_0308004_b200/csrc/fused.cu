@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
+  uint32_t* stage_run = reinterpret_cast<uint32_t*>(smem + 128);   // [kMaxStages] run in stage
+  uint32_t* stage_n = reinterpret_cast<uint32_t*>(smem + 160);     // [kMaxStages] its entries
   uint64_t* ridbar = reinterpret_cast<uint64_t*>(smem + 384);
   uint32_t* own_cnt = reinterpret_cast<uint32_t*>(smem + kHdr);   // entries of run c + t*G
   const uint32_t own_bytes = (a.max_own * 4 + 127) & ~127u;
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   // behind them.
   auto prefetch_runs = [&]() {
     if (warp == 0) {
-      for (uint32_t t = 0; t < a.npre; ++t) {
+      for (uint32_t t = 0; t < a.npre && t < a.n_static; ++t) {
         const uint32_t b = c + t * G;
         if (b < a.K) issue_region(a, b, stages + (size_t)t * a.stage_bytes, &full[t], lane, pol_first);
       }
@@ -226,17 +228,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
     if (tile_no == 0) DPG_STAMP(6);
     {
       constexpr int BPT = 8;    // a thread's reservations are all in flight together
+      const uint32_t rot = (a.dbg & 2) ? (uint32_t)(((uint64_t)c * a.K) / G) : 0u;
       for (uint32_t b0 = tid; b0 < a.K; b0 += BPT * blockDim.x) {
         uint32_t base[BPT];
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
-          const uint32_t b = b0 + q * blockDim.x;
+          uint32_t b = b0 + q * blockDim.x;
+          if (rot && b < a.K) b = b + rot < a.K ? b + rot : b + rot - a.K;
           const uint32_t n = b < a.K ? hc[b] : 0u;
           base[q] = n ? atomicAdd(&a.total[b], n) : 0u;
         }
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
-          const uint32_t b = b0 + q * blockDim.x;
+          uint32_t b = b0 + q * blockDim.x;
+          if (rot && b < a.K) b = b + rot < a.K ? b + rot : b + rot - a.K;
           if (b < a.K) hc[b] = base[q];
         }
       }
@@ -283,8 +288,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   grid_barrier(a.gbar, G);
   DPG_STAMP(3);
 
-  // entries of this CTA's runs; restore the zero invariant of the cursors
-  for (uint32_t t = tid; c + (uint64_t)t * G < a.K; t += blockDim.x) {
+  // entries of this CTA's static runs; restore the zero invariant of the cursors
+  for (uint32_t t = tid; t < a.n_static && c + (uint64_t)t * G < a.K; t += blockDim.x) {
     const uint32_t b = c + t * G;
     own_cnt[t] = min(__ldcg(a.total + b), a.cap);
     a.total[b] = 0;
@@ -292,17 +297,49 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
   __syncthreads();
 
   // ---- Phase II (+ III in mode 0) --------------------------------------------------
-  const uint32_t n_items = c < a.K ? (a.K - c + G - 1) / G : 0;
+  // Run schedule: the CTA's static runs c + t*G (t < n_static; the first npre
+  // of them were prefetched before Phase I), then runs claimed dynamically
+  // from the pool [n_static*G, K) through a global counter, so that CTAs that
+  // finish early take the remaining runs (the SMs' write rates differ by
+  // +-15% under this scattered-store load).  The producer publishes each
+  // stage's run and entry count in shared memory before its arrivals; a
+  // sentinel run ends the consumers' loop.
+  constexpr uint32_t kNoRun = 0xFFFFFFFFu;
+  const uint32_t n_stat = c < a.K ? min(a.n_static, (a.K - c + G - 1) / G) : 0;
+  const uint32_t dyn0 = a.n_static * G;
   if (warp == 0) {
     // producer
     fence_proxy_async_global();  // the entries were written by generic stores in Phase I
-    for (uint32_t t = 0; t < n_items; ++t) {
-      const uint32_t b = c + t * G;
+    for (uint32_t t = 0;; ++t) {
+      uint32_t b, n;
+      if (t < n_stat) {
+        b = c + t * G;
+        n = own_cnt[t];
+      } else {
+        uint32_t idx = 0;
+        if (lane == 0) idx = dyn0 < a.K ? atomicAdd(a.gbar + 4, 1u) : 0xFFFFFFFFu;
+        idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+        b = (idx < a.K - min(dyn0, a.K)) ? dyn0 + idx : kNoRun;
+        n = 0;
+        if (b != kNoRun && lane == 0) {
+          n = min(__ldcg(a.total + b), a.cap);
+          a.total[b] = 0;
+        }
+        n = __shfl_sync(0xFFFFFFFFu, n, 0);
+      }
       const uint32_t st = t % S;
       uint8_t* stage = stages + (size_t)st * a.stage_bytes;
       if (t >= S) mbar_wait(&empty[st], ((t / S) & 1) ^ 1);
-      const uint64_t p0 = (uint64_t)b * a.cap, p1 = p0 + own_cnt[t];
-      if (t >= a.npre) {
+      if (lane == 0) {
+        stage_run[st] = b;
+        stage_n[st] = n;
+      }
+      if (b == kNoRun) {
+        if (lane == 0) { mbar_arrive(&full[st]); mbar_arrive(&full[st]); }
+        break;
+      }
+      const uint64_t p0 = (uint64_t)b * a.cap, p1 = p0 + n;
+      if (t >= a.npre || t >= n_stat) {
         if (p1 > p0) issue_region(a, b, stage, &full[st], lane, pol_first);
         else if (lane == 0) mbar_arrive(&full[st]);
       }
@@ -318,14 +355,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
     const bool lane_on = R <= 32 ? (uint32_t)lane < RPI * R : true;
     const uint64_t pol_last = policy_evict_last();
     uint32_t q0 = 0;
-    for (uint32_t t = 0; t < n_items; ++t) {
-      const uint32_t b = c + t * G;
+    for (uint32_t t = 0;; ++t) {
       const uint32_t st = t % S;
       const uint8_t* stage = stages + (size_t)st * a.stage_bytes;
-      const uint64_t p0 = (uint64_t)b * a.cap;
-      const uint32_t n = own_cnt[t];
-      const uint32_t ng = (n + 31) / 32;
       mbar_wait(&full[st], (t / S) & 1);
+      const uint32_t b = stage_run[st];
+      if (b == kNoRun) break;
+      const uint32_t n = stage_n[st];
+      const uint64_t p0 = (uint64_t)b * a.cap;
+      const uint32_t ng = (n + 31) / 32;
       const uint8_t* r0 = a.src + ((uint64_t)b << a.s) * a.rec;
       const uint8_t* region = stage + (r0 - adn(r0));
       const uint8_t* pb = reinterpret_cast<const uint8_t*>(a.pairs) + p0 * a.pair_bytes;
@@ -357,7 +395,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
               const uint32_t rr = k0 + u * RPI + lr;
               if (lane_on && rr < cnt) {
                 uint8_t* d = obase + (uint64_t)ps[u] * a.row_bytes + lw * W;
-                if (MODE == 1) HintIO<W>::st(d, v[u], pol_last);
+                // rows with L2 evict_last: a row's partially written sectors stay
+                // in L2 until the neighbouring rows complete them (measured: -15%)
+                if (!(a.dbg & 1)) HintIO<W>::st(d, v[u], pol_last);
                 else *reinterpret_cast<T*>(d) = v[u];
               }
             }
@@ -371,7 +411,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
 #pragma unroll 4
             for (uint32_t w = lane; w < R; w += 32) {
               const T v = *reinterpret_cast<const T*>(srow + w * W);
-              if (MODE == 1) HintIO<W>::st(drow + w * W, v, pol_last);
+              if (!(a.dbg & 1)) HintIO<W>::st(drow + w * W, v, pol_last);
               else *reinterpret_cast<T*>(drow + w * W) = v;
             }
           }
@@ -381,6 +421,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+    if (a.ts && tid == 32) a.ts[(size_t)c * 16 + 9] = globaltimer();
   }
   DPG_STAMP(4);
 
@@ -404,6 +445,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
       __threadfence();
       if (atomicAdd(a.gbar + 3, 1u) == G - 1) {
         atomicExch(a.gbar + 2, 0u);
+        atomicExch(a.gbar + 4, 0u);
         atomicExch(a.gbar + 3, 0u);
       }
     }
