@@ -78,7 +78,11 @@ typedef struct {
     uint32_t hist_in_smem;  /* 1: per-CTA run histogram in shared memory        */
     uint32_t pay_bytes;     /* payload bytes carried per pair (join: fact row)  */
     uint32_t path;          /* 1 = one persistent cooperative kernel (fused.cu)
-                               2 = distribute kernels + probe-gather kernel     */
+                               2 = distribute kernels + probe-gather kernel
+                               3 = one L2-resident run (l2run.cu): the source
+                                   fits the L2 budget, K = 1; Phase II loads it
+                                   into L2, Phase III probes it in rid order
+                                   writing dst sequentially                    */
     uint32_t nstages;       /* shared-memory stages of the probe-gather pipeline */
     uint32_t stage_bytes;   /* bytes per stage                                  */
     uint32_t gather;        /* 1 = probe writes rows straight to dst (rows are
@@ -98,7 +102,8 @@ typedef struct {
     uint32_t grid_probe;
     uint32_t pair_bytes;    /* force 8-byte pairs                               */
     uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
-    uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel */
+    uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel,
+                               3 force the L2-run kernel (any source size)      */
     uint32_t gather;        /* 0 auto, 1 force direct-to-dst, 2 force INTERNAL  */
     uint32_t reserved;
 } dpg_options_t;

@@ -3,6 +3,7 @@
 // kernel sequence  distribute (Phase I) -> fused probe+gather (Phases II+III).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -48,6 +49,20 @@ int current_sm_count() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
       n = 148;
     cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+// L2 capacity of the current device (bytes); 126 MB when no device is present.
+uint64_t current_l2_bytes() {
+  static uint64_t cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 126ull << 20;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrL2CacheSize, dev) != cudaSuccess || n <= 0)
+      n = 126 << 20;
+    cache[dev] = (uint64_t)n;
   }
   return cache[dev];
 }
@@ -221,6 +236,39 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   return true;
 }
 
+// Plan for the L2-run kernel (l2run.cu): one run -- the whole source -- when
+// it fits the L2 budget (the paper's run-length rule, with the L2
+// as the cache), and each CTA's rid chunk fits its shared-memory buffer.
+constexpr uint64_t kL2RunMaxChunk = 16384;   // rids per CTA (64 KB of shared memory)
+
+uint64_t l2_budget(uint64_t l2_bytes) {
+  static uint64_t env = [] {
+    const char* e = getenv("DPG_L2_BUDGET_MB");
+    return e ? (uint64_t)atoll(e) << 20 : 0ull;
+  }();
+  return env ? env : l2_bytes / 8 * 7;
+}
+
+bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool forced, int sm,
+                uint64_t l2_bytes, dpg_plan_t* p) {
+  if (pay || n_out == 0) return false;
+  if (!forced && n_src * rec > l2_budget(l2_bytes)) return false;
+  const uint64_t chunk = align_up((n_out + sm - 1) / sm, 4);
+  if (chunk > kL2RunMaxChunk) return false;
+  std::memset(p, 0, sizeof(*p));
+  p->path = 3;
+  p->log2_run = bit_length(std::max<uint64_t>(n_src, 1) - 1);
+  p->run_len = 1ull << p->log2_run;
+  p->num_runs = 1;
+  p->word_bytes = pow2_divisor(rec);
+  p->grid_probe = (uint32_t)sm;
+  p->grid_distribute = (uint32_t)sm;
+  p->tile = (uint32_t)chunk;
+  p->smem_bytes = l2run_smem_bytes(chunk);
+  p->nstages = 4;
+  return true;
+}
+
 dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                        const dpg_options_t* opt, int sm, dpg_plan_t* p) {
   if (rec == 0 || !p) return DPG_ERR_INVALID_ARG;
@@ -228,6 +276,13 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   std::memset(p, 0, sizeof(*p));
   if (sm <= 0) sm = 148;
   const uint32_t want_path = opt ? opt->path : 0;
+  const bool overrides = opt && (opt->log2_run || opt->grid_distribute || opt->grid_probe ||
+                                 opt->hist_mode || opt->gather || opt->pair_bytes);
+  if (want_path == 3 || (want_path == 0 && !overrides)) {
+    if (plan_l2run(rec, n_src, n_out, pay, want_path == 3, sm, current_l2_bytes(), p))
+      return DPG_OK;
+    if (want_path == 3) return DPG_ERR_UNSUPPORTED;
+  }
   if (want_path != 2 && !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
       plan_fused(rec, n_src, n_out, pay, opt, sm, p))
     return DPG_OK;
@@ -418,6 +473,38 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (ps != DPG_OK) return ps;
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
+
+  if (p.path == 3) {
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* pairs = nullptr;
+    dpg_status_t ws = persist_ws(st, 1, 64, &gbar, &total, &pairs);
+    if (ws != DPG_OK) return ws;
+    L2RunArgs l;
+    std::memset(&l, 0, sizeof(l));
+    l.src = (const uint8_t*)src;
+    l.n_src = n_src;
+    l.rec = (uint32_t)rec;
+    l.rids = rids;
+    l.n_out = n_out;
+    l.chunk = p.tile;
+    l.dst = (uint8_t*)dst;
+    l.gbar = gbar;
+    l.status = status;
+    l.ts = g_debug_ts;
+    l.dbg = g_debug_flags;
+    l.stage = (l.dbg & 4) ? 0 : 1;
+    if (rec % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec / 4 - 1) / (rec / 4));
+    if (l.dbg >> 16) l.stage_bytes = (uint64_t)(l.dbg >> 16) << 20;   // tuning: MB staged
+    const uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
+    uint32_t nl = 0;
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    if (timed) cudaEventRecord(pe.e1, st);   // Phase I is empty (one run)
+    cudaError_t e = launch_l2run(l, W, p.grid_probe, st, &nl);
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_launches = nl;
+    return cuda_status(e);
+  }
 
   if (p.path == 1) {
     FusedArgs f;

@@ -75,6 +75,25 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   return v;
 }
 
+// Grid-wide barrier of a cooperative launch: gbar[0] arrival count, gbar[1]
+// generation (both persistent; the count returns to zero).
+__device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = ld_acquire_gpu(gbar + 1);
+    __threadfence();
+    if (atomicAdd(gbar, 1u) == G - 1) {
+      atomicExch(gbar, 0u);
+      __threadfence();
+      atomicAdd(gbar + 1, 1u);
+    } else {
+      while (ld_acquire_gpu(gbar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -186,6 +205,25 @@ struct FusedArgs {
                          // bits 8-12 static share of Phase II runs in 16ths
 };
 
+// DPG with one L2-resident run (l2run.cu).
+struct L2RunArgs {
+  const uint8_t* src;
+  uint64_t n_src;
+  uint32_t rec;
+  const uint32_t* rids;
+  uint64_t n_out;
+  uint64_t chunk;        // output rows (and rids) per CTA
+  uint8_t* dst;
+  uint32_t* gbar;        // [2] grid barrier (persistent, zero-restored)
+  unsigned long long* status;
+  unsigned long long* ts;  // optional [grid * 16] %globaltimer stamps, or null
+  uint64_t stage_bytes;  // bytes of the source staged into L2 by Phase II (0: all)
+  uint32_t stage;        // 1: Phase II stages the source into L2 (then a grid barrier)
+  uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
+  uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
+                         // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first
+};
+
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
 // signal); src and bytes 16-byte aligned / multiples of 16.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
@@ -251,6 +289,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_fused(const FusedArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                          cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStream_t st,
+                         uint32_t* nlaunch);
+uint32_t l2run_smem_bytes(uint64_t chunk_rids);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                                 cudaStream_t st, uint32_t* nlaunch);

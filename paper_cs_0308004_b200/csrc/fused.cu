@@ -38,23 +38,6 @@ static constexpr int kConsumers = kWarps - 1;
 static constexpr uint32_t kHdr = 512;
 static constexpr int kMaxStages = 8;
 
-__device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t G) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acquire_gpu(gbar + 1);
-    __threadfence();
-    if (atomicAdd(gbar, 1u) == G - 1) {
-      atomicExch(gbar, 0u);
-      __threadfence();
-      atomicAdd(gbar + 1, 1u);
-    } else {
-      while (ld_acquire_gpu(gbar + 1) == gen) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ const uint8_t* adn(const uint8_t* p) {
   return reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15));
 }

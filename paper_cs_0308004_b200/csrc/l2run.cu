@@ -1,0 +1,386 @@
+// l2run.cu -- DPG with the run sized to the L2 cache.
+//
+// The paper sizes a run so that "one data run plus a rid-run buffer fit in
+// cache" (section 2.1, constraints P:247-255; Fig. 1 `L <- CACHE_SIZE/2`,
+// P:396), and on its IBM p690 the cache that mattered was the 128 MB L3
+// (P:796-799, 846-847).  B200 has a 126 MB L2 in front of HBM.  When the
+// whole source fits the L2 budget there is one run (K = 1), and the three
+// phases become:
+//   Phase I   Distribute: with one run, RID_RUN[0] is the rid list itself
+//             (Fig. 1 P:406-411 appends every rid to run 0); nothing to do.
+//   Phase II  Probe: "load the i-th INPUT run entirely into cache"
+//             (P:299-302, 415-416): every CTA streams its slice of the source
+//             through TMA bulk copies (L2 evict_last), so the run is read from
+//             HBM once, sequentially, and stays resident in L2; a grid
+//             barrier ends the load.  The CTA's chunk of the rid list is bulk-
+//             copied into shared memory at the same time (the rid-run buffer).
+//   Phase III Gather, fused with the probe's copy: in
+//             rid order, each record is read from the L2-resident run and
+//             written to the next output row, so the output is one sequential
+//             write stream (stores L2 evict_first: the stream must not evict
+//             the run).
+// Every HBM access of the path is then sequential: the source once, the rids
+// once, the output once (2*rec + 4 bytes per record).
+//
+// Lane layout of the gather: a warp owns 32 consecutive output rows, i.e. one
+// contiguous span of 32*rec bytes of dst, viewed as 32*R words of W bytes
+// (R = rec/W).  Lane l moves words l, l+32, l+64, ...: every store
+// instruction writes 32 consecutive words (coalesced), and the word's row
+// (w / R) selects the source record through a shuffle of the row's rid.
+#include "dpg_internal.cuh"
+
+namespace dpg {
+
+static constexpr int kL2Threads = 768;
+static constexpr int kL2Warps = kL2Threads / 32;
+static constexpr uint32_t kL2Slots = 4;            // ring of Phase II bulk-copy slots
+static constexpr uint32_t kL2Chunk = 32u << 10;    // bytes per bulk copy
+static constexpr uint32_t kL2Region = kL2Slots * kL2Chunk;   // ring, then the gather tiles
+static constexpr uint32_t kL2WarpTile = 4096;                   // tile bytes per warp
+static_assert(kL2WarpTile * kL2Warps <= kL2Region, "gather tiles exceed the ring");
+
+// 16-byte global load under a predicate (no branch; zero when off).
+__device__ __forceinline__ uint4 ld16_pred(const void* p, uint32_t on, uint64_t pol) {
+  uint4 v = make_uint4(0, 0, 0, 0);
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+      "@q ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%5], %6;\n\t}"
+      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+      : "r"(on), "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ uintptr_t al_dn(uintptr_t p) { return p & ~uintptr_t(15); }
+__device__ __forceinline__ uintptr_t al_up(uintptr_t p) { return (p + 15) & ~uintptr_t(15); }
+
+// Bulk store shared -> global (TMA), tracked by the issuing thread's bulk group.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// REALIGN 0: rows are whole W-byte words (W = 16 when rec, src and dst allow):
+//            flat word loop, loads and stores straight between L2 and dst.
+// REALIGN 1: rows of any 4-byte multiple (e.g. the 100-byte records): each row
+//            is read as the 16-byte words of its enclosing aligned window (a
+//            16-byte load moves 4x the bytes of a 4-byte one per LSU
+//            instruction -- measured 88 vs 34 Grow/s for L2-resident 100-byte
+//            rows, profiles/r01_micro3_l2_rows.txt), realigned into the warp's
+//            output tile in shared memory, and the tile (32 consecutive
+//            output rows) leaves by one TMA bulk store.
+// REALIGN 2: as 1 with byte granularity (rec or src not 4-byte aligned).
+template <int W, int REALIGN>
+__global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
+  using T = typename Word<W>::T;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [kL2Slots] + rid barrier
+  uint8_t* ring = smem + 128;                                    // Phase II ring / Phase III tiles
+  // rcache[k] = rids[lo + k]; placed so that rcache and &rids[lo] agree mod 16
+  // (the bulk copy of the 16-byte interior then lands 16-byte aligned)
+  uint32_t* rcache = reinterpret_cast<uint32_t*>(
+      ring + kL2Region +
+      (reinterpret_cast<uintptr_t>(a.rids + min_u64(a.n_out, (uint64_t)blockIdx.x * a.chunk)) & 15));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t c = blockIdx.x, G = gridDim.x;
+  if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 0] = globaltimer();
+
+  // this CTA's output rows (and rids): [lo, hi)
+  const uint64_t lo = min_u64(a.n_out, (uint64_t)c * a.chunk);
+  const uint64_t hi = min_u64(a.n_out, lo + a.chunk);
+  if (tid == 0) {
+    for (uint32_t k = 0; k <= kL2Slots; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ---- Phase II: load the run (the whole source) into L2 ----------------------
+  if (tid == 0) {
+    const uint64_t pol_last = policy_evict_last();
+    const uint64_t pol_first = policy_evict_first();
+    // the rid-run buffer: this CTA's rids, one bulk copy (16-byte interior)
+    const uintptr_t r0 = reinterpret_cast<uintptr_t>(a.rids + lo);
+    const uintptr_t r1 = reinterpret_cast<uintptr_t>(a.rids + hi);
+    const uintptr_t ra0 = al_up(r0), ra1 = al_dn(r1);
+    const uint32_t rbytes = ra1 > ra0 ? (uint32_t)(ra1 - ra0) : 0u;
+    mbar_arrive_expect_tx(&bar[kL2Slots], rbytes);
+    if (rbytes)
+      bulk_g2s(reinterpret_cast<uint8_t*>(rcache) + (ra0 - r0), reinterpret_cast<const void*>(ra0),
+               rbytes, &bar[kL2Slots], pol_first);
+    // the CTA's slice of the source bytes, enclosing 16-byte blocks (a block
+    // holding at least one source byte is mapped, so this never faults)
+    const uintptr_t s0 = al_dn(reinterpret_cast<uintptr_t>(a.src));
+    const uintptr_t s1 = al_up(reinterpret_cast<uintptr_t>(a.src) + a.n_src * (uint64_t)a.rec);
+    const uint64_t total = a.stage_bytes ? min_u64(s1 - s0, a.stage_bytes) : s1 - s0;
+    const uint64_t slice = ((total + G - 1) / G + 15) & ~uint64_t(15);
+    const uint64_t b0 = min_u64(total, (uint64_t)c * slice), b1 = min_u64(total, b0 + slice);
+    // first the whole slice as L2 prefetches (fire-and-forget: every DRAM read
+    // of the slice is in flight at once), then the same bytes through the
+    // bulk-copy ring, whose completions say that the slice is resident
+    if (a.stage && (a.dbg & 8))
+    for (uint64_t off = b0; off < b1; off += kL2Chunk)
+      bulk_prefetch_l2(reinterpret_cast<const void*>(s0 + off), (uint32_t)min_u64(kL2Chunk, b1 - off),
+                       pol_last);
+    uint32_t j = 0;
+    if (a.stage)
+    for (uint64_t off = b0; off < b1; off += kL2Chunk, ++j) {
+      const uint32_t slot = j % kL2Slots;
+      if (j >= kL2Slots) mbar_wait(&bar[slot], ((j / kL2Slots) - 1) & 1);
+      const uint32_t bytes = (uint32_t)min_u64(kL2Chunk, b1 - off);
+      mbar_arrive_expect_tx(&bar[slot], bytes);
+      bulk_g2s(ring + (size_t)slot * kL2Chunk, reinterpret_cast<const void*>(s0 + off), bytes,
+               &bar[slot], pol_last);
+    }
+    // drain: the last min(j, kL2Slots) copies
+    for (uint32_t q = (j > kL2Slots ? j - kL2Slots : 0); q < j; ++q)
+      mbar_wait(&bar[q % kL2Slots], (q / kL2Slots) & 1);
+  }
+  // unaligned head/tail of the rid chunk, plain loads
+  {
+    const uintptr_t r0 = reinterpret_cast<uintptr_t>(a.rids + lo);
+    const uintptr_t r1 = reinterpret_cast<uintptr_t>(a.rids + hi);
+    const uint64_t nh = min_u64(hi - lo, (al_up(r0) - r0) / 4);
+    const uint64_t nt0 = al_dn(r1) > r0 ? max_u64(nh, (al_dn(r1) - r0) / 4) : nh;
+    for (uint64_t k = tid; k < nh; k += blockDim.x) rcache[k] = a.rids[lo + k];
+    for (uint64_t k = nt0 + tid; k < hi - lo; k += blockDim.x) rcache[k] = a.rids[lo + k];
+  }
+  if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 1] = globaltimer();
+  if (a.stage) grid_barrier(a.gbar, G);
+  else __syncthreads();
+  mbar_wait(&bar[kL2Slots], 0);
+  if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 2] = globaltimer();
+
+  // ---- Phase II probe + Phase III gather, in rid order ---------------------------
+  const uint64_t pol_last = policy_evict_last();
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t ngroups = (hi - lo + 31) / 32;
+  // loads: evict_last when the run was staged in L2 (Phase II), else evict_first
+  const uint64_t pol_load = a.stage ? pol_last : pol_first;
+  if (REALIGN == 0) {
+    const uint32_t R = a.rec / W;
+    const uint32_t q32 = 32 / R, r32 = 32 % R;     // advance of (row, word) per 32 words
+    constexpr int U = W >= 16 ? 4 : 8;
+    for (uint64_t g = warp; g < ngroups; g += kL2Warps) {
+      const uint64_t g0 = lo + g * 32;
+      const uint32_t cnt = (uint32_t)min_u64(32, hi - g0);
+      uint32_t my_r = 0, ok = 0;
+      if ((uint32_t)lane < cnt) {
+        my_r = rcache[g0 - lo + lane];
+        if (my_r < a.n_src) ok = 1;
+        else report_bad(a.status, g0 + lane);
+      }
+      const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+      const uint64_t nw = (uint64_t)cnt * R;          // words of this group
+      uint8_t* gdst = a.dst + g0 * a.rec;
+      uint32_t row = lane / R, off = lane % R;        // of word w = lane + 32*j
+      for (uint64_t w0 = 0; w0 < nw; w0 += 32 * U) {
+        T v[U];
+        uint32_t rw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t w = w0 + 32 * u + lane;
+          const uint32_t rrow = row < 32 ? row : 31;
+          const uint32_t r = __shfl_sync(0xffffffffu, my_r, rrow);
+          rw[u] = row;
+          if (w < nw && ((okm >> rrow) & 1)) {
+            const uint8_t* p = a.src + (uint64_t)r * a.rec + (uint64_t)off * W;
+            v[u] = HintIO<W>::ld(p, pol_load);
+          }
+          row += q32;
+          off += r32;
+          if (off >= R) { off -= R; ++row; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t w = w0 + 32 * u + lane;
+          if (w < nw && ((okm >> (rw[u] < 32 ? rw[u] : 31)) & 1))
+            HintIO<W>::st(gdst + w * W, v[u], pol_first);
+        }
+      }
+    }
+  } else {
+    const uint32_t rec = a.rec;
+    const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)
+    const uint32_t RPI = 32 / NW;                   // rows per load instruction
+    const uint32_t lr = lane / NW, lw = lane % NW;
+    const uint32_t nbuf = rec <= 64 ? 2 : 1;
+    const uint32_t tile_bytes = 32 * rec;
+    uint8_t* tiles = ring + (size_t)warp * kL2WarpTile;
+    constexpr int U = 8;
+    // fast path (whole groups of valid rows, rec % 4 == 0, rec <= 116): the
+    // 16-byte windows go to a window-layout tile (row pitch 128 B, one
+    // conflict-free 16-byte store each); each output 16-byte word is then
+    // assembled from the 4 dwords it needs and stored straight to dst.
+    const uintptr_t src_u = reinterpret_cast<uintptr_t>(a.src);
+    const bool fast_ok = REALIGN == 1 && rec <= 116 && rec >= 8;
+    const uint32_t FNW = (rec + 12 + 15) / 16;       // window words a row can need
+    const uint32_t FRPI = 32 / FNW, flr = lane / FNW, flw = lane % FNW;
+    const uint32_t RD = rec / 4;                       // dwords per row
+    uint32_t* wt = reinterpret_cast<uint32_t*>(tiles);
+    uint32_t gi = 0;
+    for (uint64_t g = warp; g < ngroups; g += kL2Warps, ++gi) {
+      const uint64_t g0 = lo + g * 32;
+      const uint32_t cnt = (uint32_t)min_u64(32, hi - g0);
+      uint32_t my_r = 0, ok = 0;
+      if ((uint32_t)lane < cnt) {
+        my_r = rcache[g0 - lo + lane];
+        if (my_r < a.n_src) ok = 1;
+        else report_bad(a.status, g0 + lane);
+      }
+      const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+      if (fast_ok && okm == 0xffffffffu &&
+          ((reinterpret_cast<uintptr_t>(a.dst) + g0 * rec) & 15) == 0) {
+        if (lane == 0) bulk_wait_read<0>();          // a slow-path tile store may read here
+        __syncwarp();
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t jj = (u * FRPI + flr) & 31;
+          const uint32_t r = __shfl_sync(0xffffffffu, my_r, jj);
+          const uintptr_t ra = src_u + (uint64_t)r * rec;
+          const uint32_t on = (flr < FRPI && u * FRPI + flr < 32 && 16 * flw < (uint32_t)(ra & 15) + rec);
+          v[u] = ld16_pred(reinterpret_cast<const void*>((ra & ~uintptr_t(15)) + 16 * flw), on, pol_load);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t jj = u * FRPI + flr;
+          if (flr < FRPI && jj < 32) *reinterpret_cast<uint4*>(wt + jj * 32 + 4 * flw) = v[u];
+        }
+        // dword shift of row 'lane' inside its window
+        const uint32_t sh = (uint32_t)(((src_u + (uint64_t)my_r * rec) >> 2) & 3);
+        __syncwarp();
+        uint8_t* gdst = a.dst + g0 * rec;
+        const uint32_t nwo = 2 * rec;                 // 16-byte words of 32 rows
+        for (uint32_t m0 = 0; m0 < nwo; m0 += 32) {
+          const uint32_t m = m0 + lane;
+          const uint32_t d0 = 4 * m;
+          const uint32_t j0 = min(__umulhi(d0, a.rd_magic), 31u);   // d0 / RD
+          const uint32_t q0 = d0 - j0 * RD;
+          const uint32_t s0 = __shfl_sync(0xffffffffu, sh, j0);
+          const uint32_t s1 = __shfl_sync(0xffffffffu, sh, min(j0 + 1, 31u));
+          const uint32_t b0 = j0 * 32 + s0 + q0, b1 = (j0 + 1) * 32 + s1 + q0 - RD;
+          uint4 x;
+          x.x = wt[q0 + 0 < RD ? b0 + 0 : b1 + 0];
+          x.y = wt[q0 + 1 < RD ? b0 + 1 : b1 + 1];
+          x.z = wt[q0 + 2 < RD ? b0 + 2 : b1 + 2];
+          x.w = wt[q0 + 3 < RD ? b0 + 3 : b1 + 3];
+          if (m < nwo) HintIO<16>::st(gdst + 16 * (uint64_t)m, x, pol_first);
+        }
+        __syncwarp();
+        continue;
+      }
+      uint8_t* tile = tiles + (size_t)(gi % nbuf) * ((tile_bytes + 127) & ~127u);
+      if (nbuf == 2) { if (lane == 0) bulk_wait_read<1>(); }
+      else { if (lane == 0) bulk_wait_read<0>(); }
+      __syncwarp();
+      for (uint32_t j0 = 0; j0 < cnt; j0 += RPI * U) {
+        uint4 v[U];
+        uint32_t o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = j0 + u * RPI + lr;
+          const uint32_t jj = j < 32 ? j : 31;
+          const uint32_t r = __shfl_sync(0xffffffffu, my_r, jj);
+          const uintptr_t ra = reinterpret_cast<uintptr_t>(a.src) + (uint64_t)r * rec;
+          o[u] = (uint32_t)(ra & 15);
+          v[u] = make_uint4(0, 0, 0, 0);
+          if (lr < RPI && j < cnt && ((okm >> jj) & 1) && 16 * lw < o[u] + rec)
+            v[u] = HintIO<16>::ld(reinterpret_cast<const void*>(al_dn(ra) + 16 * lw), pol_load);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = j0 + u * RPI + lr;
+          if (!(lr < RPI && j < cnt)) continue;
+          const int base = (int)(16 * lw) - (int)o[u];     // row byte of the word's first byte
+          uint8_t* trow = tile + j * rec;
+          if (REALIGN == 1) {
+            const uint32_t vw[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int sb = base + 4 * k;
+              if (sb >= 0 && sb < (int)rec) *reinterpret_cast<uint32_t*>(trow + sb) = vw[k];
+            }
+          } else {
+            const uint32_t vw[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int sb = base + k;
+              if (sb >= 0 && sb < (int)rec) trow[sb] = (uint8_t)(vw[k >> 2] >> (8 * (k & 3)));
+            }
+          }
+        }
+      }
+      // the tile (cnt consecutive output rows) to dst
+      uint8_t* gdst = a.dst + g0 * rec;
+      const uint32_t bytes = cnt * rec;
+      if (a.dbg & 2) {
+        __syncwarp();
+      } else if ((a.dbg & 1) && okm == (cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u)) &&
+          (reinterpret_cast<uintptr_t>(gdst) & 15) == 0 && (bytes & 15) == 0) {
+        __syncwarp();
+        for (uint32_t b = lane * 16; b < bytes; b += 512)
+          HintIO<16>::st(gdst + b, *reinterpret_cast<const uint4*>(tile + b), pol_first);
+        __syncwarp();
+      } else if (okm == (cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u)) &&
+          (reinterpret_cast<uintptr_t>(gdst) & 15) == 0 && (bytes & 15) == 0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_s2g(gdst, tile, bytes, pol_first);
+      } else {
+        __syncwarp();
+        // rows with a bad rid stay unwritten
+        for (uint32_t b = lane; b < bytes; b += 32) {
+          const uint32_t j = b / rec;
+          if ((okm >> j) & 1) gdst[b] = tile[b];
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  if (a.ts) {
+    __syncthreads();
+    if (tid == 0) a.ts[(size_t)c * 16 + 3] = globaltimer();
+  }
+}
+
+template <int W, int REALIGN>
+static cudaError_t launch_l2_w(const L2RunArgs& a, uint32_t grid, uint32_t smem, cudaStream_t st) {
+  auto fn = k_dpg_l2run<W, REALIGN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  L2RunArgs arg = a;
+  void* params[] = {&arg};
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kL2Threads), params, smem,
+                                     st);
+}
+
+uint32_t l2run_smem_bytes(uint64_t chunk_rids) {
+  return (uint32_t)(128 + kL2Region + ((chunk_rids * 4 + 16 + 127) & ~uint64_t(127)));
+}
+
+cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStream_t st,
+                         uint32_t* nl) {
+  ++*nl;
+  const uint32_t smem = l2run_smem_bytes(a.chunk);
+  if (W == 16) return launch_l2_w<16, 0>(a, grid, smem, st);
+  if (a.rec <= 128) {
+    const bool word4 = a.rec % 4 == 0 && reinterpret_cast<uintptr_t>(a.src) % 4 == 0;
+    return word4 ? launch_l2_w<16, 1>(a, grid, smem, st) : launch_l2_w<16, 2>(a, grid, smem, st);
+  }
+  switch (W) {
+    case 8: return launch_l2_w<8, 0>(a, grid, smem, st);
+    case 4: return launch_l2_w<4, 0>(a, grid, smem, st);
+    case 2: return launch_l2_w<2, 0>(a, grid, smem, st);
+    default: return launch_l2_w<1, 0>(a, grid, smem, st);
+  }
+}
+
+}  // namespace dpg

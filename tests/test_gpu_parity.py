@@ -123,11 +123,12 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
 
 
 @pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
-@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0)])
+@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0)])
 def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path, gather):
     """Every execution path on the same cases: the fused cooperative kernel
     writing rows straight to dst (gather 1) or through INTERNAL (gather 2),
-    and distribute kernels + probe-gather kernel (path 2).  A path is skipped
+    distribute kernels + probe-gather kernel (path 2), and the L2-run kernel
+    (path 3: one run, the whole source, staged in L2).  A path is skipped
     where its planner refuses with DPG_ERR_UNSUPPORTED."""
     src, rids = _case(k, n_src, rec, n_out, kind)
     try:
@@ -141,6 +142,53 @@ def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, p
                                 gather=gather))
     assert np.array_equal(got, oracle.retrieve(src, rids))
     dpg.dpg_sync_status()
+
+
+@pytest.mark.parametrize("rec", [100, 4, 12, 36, 64, 128, 96, 256, 3, 260, 4096])
+@pytest.mark.parametrize("soff,doff", [(0, 0), (4, 0), (0, 4), (1, 3)])
+def test_l2run_shapes_and_alignment(dpg, rec, soff, doff):
+    """The L2-run kernel (path 3) on every lane layout: 16-byte flat words,
+    16-byte windows realigned by dwords or by bytes in shared memory, narrow
+    flat words; many CTAs and groups, a ragged tail, unaligned pointers,
+    canaries around dst."""
+    n_src = max(1, min(40000, (6 << 20) // rec))
+    n_out = 3 * n_src // 2 + 7
+    src, rids = _case(rec * 7 + soff * 3 + doff, n_src, rec, n_out, "repl")
+    big_src = torch.zeros(n_src * rec + 64, dtype=torch.uint8, device="cuda")
+    big_src[soff:soff + n_src * rec] = dev(src.reshape(-1))
+    s = big_src[soff:soff + n_src * rec].view(n_src, rec)
+    canary = 0x5A
+    big_dst = torch.full((n_out * rec + 64,), canary, dtype=torch.uint8, device="cuda")
+    d = big_dst[doff:doff + n_out * rec].view(n_out, rec)
+    assert dpg.dpg_plan(rec, n_src, n_out, path=3)["path"] == 3
+    dpg.dpg_retrieve(s, dev(rids), dst=d, path=3)
+    out = host(big_dst)
+    assert np.all(out[:doff] == canary) and np.all(out[doff + n_out * rec:] == canary)
+    assert np.array_equal(out[doff:doff + n_out * rec].reshape(n_out, rec), oracle.retrieve(src, rids))
+    dpg.dpg_sync_status()
+
+
+def test_l2run_invalid_rids_leave_rows_unwritten(dpg):
+    src, rids = _case(11, 5000, 100, 9000, "repl")
+    bad = [0, 31, 32, 4001, 8999]
+    for b in bad:
+        rids[b] = 5000 + b
+    d = torch.zeros((9000, 100), dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=d, path=3)
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 0
+    out = host(d)
+    ok = np.ones(9000, bool)
+    ok[bad] = False
+    assert np.array_equal(out[ok], src[rids[ok].astype(np.int64)])
+    assert np.all(out[~ok] == 0)
+
+
+def test_plan_picks_l2run_when_the_source_fits_l2(dpg):
+    p = dpg.dpg_plan(100, 1 << 20, 1 << 20)
+    assert p["path"] == 3 and p["num_runs"] == 1
+    assert dpg.dpg_plan(100, 1 << 24, 1 << 24)["path"] != 3
 
 
 @pytest.mark.parametrize("hist_mode", [1, 2])
