@@ -8,7 +8,8 @@ One step = one pass of the whole hot path (plan,
 distribute, fused probe+gather) over one batch of synthetic input already
 resident in HBM: dpg_retrieve on BASELINE.json configs[1] (Datamation-shaped
 sort phase 3, 1,048,576 x 100-byte records, rids = stable argsort of the
-10-byte keys).  L2 is flushed (a 512 MiB write) before every timed step and
+10-byte keys).  L2 is flushed (a 512 MiB write, then a 512 MiB read, so no
+dirty flush line is left for the step to write back) before every timed step and
 each step is timed alone with CUDA events on the launching stream; flush time
 is excluded.  Multi-process (torchrun, N > 1): BASELINE.json config 5 --
 2^30 x 100-byte records range-partitioned over the ranks, rids a global
@@ -367,16 +368,24 @@ def main():
         fact, fk, dim = to_dev(w["fact"]), to_dev(w["fk"]), to_dev(w["dim"])
         out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
         step = lambda: dpg.dpg_fk_join(fact, fk, dim, out=out)
-        naive = None
+        naive = windowed = None
         n_src = dim.shape[0]
     else:
         src, rids = to_dev(w["src"]), to_dev(w["rids"])
         out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
         step = lambda: dpg.dpg_retrieve(src, rids, dst=out)
         naive = lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)
+        windowed = lambda: dpg.dpg_retrieve_direct_ex(src, rids, dst=out, hint=3)
         n_src = src.shape[0]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+
+    def flush_l2():
+        # evict L2: write a buffer > 126 MB, then read another one, so that no
+        # dirty line of the flush itself is left for the timed step to write back
+        flush.fill_(1)
+        flush_rd.view(torch.int32).max()
 
     def timed(fn, steps, phase=False):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -386,7 +395,7 @@ def main():
             dpg.dpg_phase_timing(True)
         launches = 0
         for e0, e1 in evs:
-            flush.fill_(1)                      # evict L2 (write > 126 MB)
+            flush_l2()
             e0.record(stream)
             fn()
             e1.record(stream)
@@ -404,6 +413,8 @@ def main():
         step()
         if naive:
             naive()
+        if windowed:
+            windowed()
     torch.cuda.synchronize()
     dpg.dpg_sync_status()
 
@@ -431,6 +442,15 @@ def main():
         nt = sum(nms) / len(nms)
         naive_res = {"value": alg_bytes / (nt * 1e-3) / 1e9, "unit": "GB/s",
                      "ms_per_step": nt, "kernel": "k_direct", "launches_per_step": nl / args.steps}
+    # the same direct retrieval on the best gather engine written here (the
+    # L2-run kernel's 16-byte-window gather, no staging): the strongest
+    # non-DPG comparison
+    windowed_res = None
+    if windowed is not None:
+        wms, wl, _ = timed(windowed, args.steps)
+        wt = sum(wms) / len(wms)
+        windowed_res = {"value": alg_bytes / (wt * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": wt,
+                        "kernel": "k_dpg_l2run (stage=0)", "launches_per_step": wl / args.steps}
 
     peak, peak_src = hbm_peak()
     dist_ms, probe_ms, calls = ph
@@ -440,7 +460,12 @@ def main():
                         torch.cuda.get_device_properties(dev).multi_processor_count)
     src_rec = w["dim"].shape[1] if cfg == "c4" else rec
     pay = 0
-    if plan["path"] == 1:
+    if plan["path"] == 3:
+        # one run (the whole source) staged in L2, probed in rid order: one
+        # kernel for the whole path, N * (2 * rec + rid_bytes)
+        kernel = "k_dpg_l2run"
+        pg_bytes = alg_bytes
+    elif plan["path"] == 1:
         # one persistent kernel runs the whole path: its algorithmic bytes are
         # the path's, N * (2 * rec + rid_bytes)
         kernel = "k_dpg_fused" + (" + k_direct(INTERNAL)" if plan["gather"] == 2 else "")
@@ -497,14 +522,16 @@ def main():
             "dtype": "u8", "data": "synthetic (datagen, seed 0)",
             "config": {"workload": workload_name(cfg, args.rec), "n_src": n_src, "n_out": n_out,
                        "rec_bytes": rec, "rid_bytes": rid_bytes,
-                       "alg_bytes_per_step": alg_bytes, "l2": "flushed before every step",
+                       "alg_bytes_per_step": alg_bytes,
+                       "l2": "flushed before every step (512 MiB write, then 512 MiB read)",
                        "parallelism": "replicas" if world > 1 else "single",
                        "run_len": plan["run_len"], "num_runs": plan["num_runs"],
-                       "pair_bytes": plan["pair_bytes"]},
+                       "pair_bytes": plan["pair_bytes"], "plan_path": plan["path"]},
             "records_per_s": world * n_out / (ms_per_step * 1e-3),
             "frac_of_hbm_peak": value / world / peak,
             "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
-            "roofline": roofline, "naive": naive_res, "e2e": e2e, "cpu_baseline": cpu,
+            "roofline": roofline, "naive": naive_res, "direct_windowed": windowed_res,
+            "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(), "gpu_launches": launches,
             "gpu": torch.cuda.get_device_name(dev),
         }

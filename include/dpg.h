@@ -135,7 +135,9 @@ dpg_status_t dpg_retrieve_direct(const void *src, size_t rec_bytes, uint64_t n_s
 
 /* dpg_retrieve_direct with L2 eviction hints: hint 0 plain, 1 loads and
  * stores evict_first, 2 loads evict_last + stores evict_first (source staged
- * in L2 beforehand, e.g. by dpg_l2_prefetch). */
+ * in L2 beforehand, e.g. by dpg_l2_prefetch); hint 3 the same direct
+ * retrieval on the L2-run kernel's gather (16-byte window loads realigned in
+ * shared memory, coalesced 16-byte output stores; path 3 without staging). */
 dpg_status_t dpg_retrieve_direct_ex(const void *src, size_t rec_bytes, uint64_t n_src,
                                     const uint32_t *rids, uint64_t n_out, void *dst,
                                     dpg_stream_t stream, int hint);

@@ -239,13 +239,19 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
 // Plan for the L2-run kernel (l2run.cu): one run -- the whole source -- when
 // it fits the L2 budget (the paper's run-length rule, with the L2
 // as the cache), and each CTA's rid chunk fits its shared-memory buffer.
-constexpr uint64_t kL2RunMaxChunk = 16384;   // rids per CTA (64 KB of shared memory)
 
 uint64_t l2_budget(uint64_t l2_bytes) {
   static uint64_t env = [] {
     const char* e = getenv("DPG_L2_BUDGET_MB");
     return e ? (uint64_t)atoll(e) << 20 : 0ull;
   }();
+  // The paper's constraint (1): one data run plus a rid-run buffer fit in the
+  // cache.  Budget 7/8 of the L2.  Measured on B200
+  // (profiles/r01_l2_retention_ncu.txt): a 52 MB run staged by TMA stays in
+  // L2 for the probe, of a 79 MB run only ~60% does (each die's half of the
+  // 126 MB L2 serves its own SMs); the probe's misses then go to HBM, and the
+  // single staged run still beats the shared-memory runs for 100-byte records
+  // up to the budget (profiles/r01_l2run_probe.txt).
   return env ? env : l2_bytes / 8 * 7;
 }
 
@@ -253,8 +259,7 @@ bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool
                 uint64_t l2_bytes, dpg_plan_t* p) {
   if (pay || n_out == 0) return false;
   if (!forced && n_src * rec > l2_budget(l2_bytes)) return false;
-  const uint64_t chunk = align_up((n_out + sm - 1) / sm, 4);
-  if (chunk > kL2RunMaxChunk) return false;
+  const uint64_t chunk = align_up((n_out + sm - 1) / sm, 32);
   std::memset(p, 0, sizeof(*p));
   p->path = 3;
   p->log2_run = bit_length(std::max<uint64_t>(n_src, 1) - 1);
@@ -492,9 +497,11 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     l.status = status;
     l.ts = g_debug_ts;
     l.dbg = g_debug_flags;
-    l.stage = (l.dbg & 4) ? 0 : 1;
+    l.stage = (l.dbg & 4) ? 0 : 1;   // tuning flag: probe without staging
     if (rec % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec / 4 - 1) / (rec / 4));
-    if (l.dbg >> 16) l.stage_bytes = (uint64_t)(l.dbg >> 16) << 20;   // tuning: MB staged
+    if (l.dbg >> 24) l.stage_bytes = (uint64_t)(l.dbg >> 24) << 20;   // tuning: MB staged
+    if ((l.dbg >> 8) & 15) l.ring_chunk = 1024u << ((l.dbg >> 8) & 15);   // tuning: 2^k KB
+    if ((l.dbg >> 12) & 15) l.ring_slots = (l.dbg >> 12) & 15;
     const uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
     uint32_t nl = 0;
     PhaseEvents pe;
@@ -799,6 +806,31 @@ dpg_status_t dpg_retrieve_direct_ex(const void* src, size_t rec_bytes, uint64_t 
   if (!status) return DPG_ERR_CUDA;
   uint32_t W = pow2_divisor(rec_bytes | (uintptr_t)src | (uintptr_t)dst);
   uint32_t nl = 0;
+  if (hint == 3) {
+    // the direct retrieval on the L2-run kernel's gather (16-byte windows,
+    // realigned in shared memory, coalesced 16-byte row stores), no staging
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* pairs = nullptr;
+    dpg_status_t ws = persist_ws((cudaStream_t)stream, 1, 64, &gbar, &total, &pairs);
+    if (ws != DPG_OK) return ws;
+    const int sm = current_sm_count();
+    L2RunArgs l;
+    std::memset(&l, 0, sizeof(l));
+    l.src = (const uint8_t*)src;
+    l.n_src = n_src;
+    l.rec = (uint32_t)rec_bytes;
+    l.rids = rids;
+    l.n_out = n_out;
+    l.chunk = align_up((n_out + sm - 1) / sm, 32);
+    l.dst = (uint8_t*)dst;
+    l.gbar = gbar;
+    l.status = status;
+    l.stage = 0;
+    if (rec_bytes % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec_bytes / 4 - 1) / (rec_bytes / 4));
+    cudaError_t e = launch_l2run(l, W, (uint32_t)sm, (cudaStream_t)stream, &nl);
+    t_launches = nl;
+    return cuda_status(e);
+  }
   cudaError_t e = launch_direct((const uint8_t*)src, n_src, (uint32_t)rec_bytes, rids, n_out,
                                 (uint8_t*)dst, W, current_sm_count(), status,
                                 (cudaStream_t)stream, &nl, hint);

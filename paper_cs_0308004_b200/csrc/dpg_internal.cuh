@@ -219,6 +219,8 @@ struct L2RunArgs {
   unsigned long long* ts;  // optional [grid * 16] %globaltimer stamps, or null
   uint64_t stage_bytes;  // bytes of the source staged into L2 by Phase II (0: all)
   uint32_t stage;        // 1: Phase II stages the source into L2 (then a grid barrier)
+  uint32_t ring_chunk;   // Phase II bulk-copy bytes per slot (0: 32 KB)
+  uint32_t ring_slots;   // Phase II ring slots (0: 6)
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
                          // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first

@@ -31,25 +31,36 @@
 
 namespace dpg {
 
-static constexpr int kL2Threads = 768;
+static constexpr int kL2Threads = 512;
 static constexpr int kL2Warps = kL2Threads / 32;
-static constexpr uint32_t kL2Slots = 4;            // ring of Phase II bulk-copy slots
-static constexpr uint32_t kL2Chunk = 32u << 10;    // bytes per bulk copy
-static constexpr uint32_t kL2Region = kL2Slots * kL2Chunk;   // ring, then the gather tiles
+static constexpr uint32_t kL2Slots = 16;           // max ring slots of Phase II bulk copies
+static constexpr uint32_t kL2Region = 192u << 10;  // Phase II ring, then the gather tiles
 static constexpr uint32_t kL2WarpTile = 4096;                   // tile bytes per warp
 static_assert(kL2WarpTile * kL2Warps <= kL2Region, "gather tiles exceed the ring");
+static_assert(128 >= 8 * kL2Slots, "barrier area");
 
-// 16-byte global load under a predicate (no branch; zero when off).
-__device__ __forceinline__ uint4 ld16_pred(const void* p, uint32_t on, uint64_t pol) {
-  uint4 v = make_uint4(0, 0, 0, 0);
+
+// 16-byte global load under a predicate (no branch; the registers keep their
+// value when off), read-only path, no L1 allocation.
+__device__ __forceinline__ void ld16_pred(uint4& v, const void* p, bool on) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-      "@q ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%5], %6;\n\t}"
+      "@q ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%5];\n\t}"
       : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "r"(on), "l"(p), "l"(pol));
-  return v;
+      : "r"((uint32_t)on), "l"(p));
 }
+// 4-byte shared store under a predicate.
+__device__ __forceinline__ void sts32_pred(uint32_t saddr, uint32_t v, bool on) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q st.shared.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v), "r"((uint32_t)on) : "memory");
+}
+// Streaming 16-byte global store (evict-first).
+__device__ __forceinline__ void st16_cs(void* p, uint4 v) { __stcs(reinterpret_cast<uint4*>(p), v); }
 
+__device__ __forceinline__ uint32_t ldg_first(const uint32_t* p) {
+  return __ldcs(p);   // streaming: read once
+}
 __device__ __forceinline__ uintptr_t al_dn(uintptr_t p) { return p & ~uintptr_t(15); }
 __device__ __forceinline__ uintptr_t al_up(uintptr_t p) { return (p + 15) & ~uintptr_t(15); }
 
@@ -83,11 +94,6 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [kL2Slots] + rid barrier
   uint8_t* ring = smem + 128;                                    // Phase II ring / Phase III tiles
-  // rcache[k] = rids[lo + k]; placed so that rcache and &rids[lo] agree mod 16
-  // (the bulk copy of the 16-byte interior then lands 16-byte aligned)
-  uint32_t* rcache = reinterpret_cast<uint32_t*>(
-      ring + kL2Region +
-      (reinterpret_cast<uintptr_t>(a.rids + min_u64(a.n_out, (uint64_t)blockIdx.x * a.chunk)) & 15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 0] = globaltimer();
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
   const uint64_t lo = min_u64(a.n_out, (uint64_t)c * a.chunk);
   const uint64_t hi = min_u64(a.n_out, lo + a.chunk);
   if (tid == 0) {
-    for (uint32_t k = 0; k <= kL2Slots; ++k) mbar_init(&bar[k], 1);
+    for (uint32_t k = 0; k < kL2Slots; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -105,15 +111,6 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
   if (tid == 0) {
     const uint64_t pol_last = policy_evict_last();
     const uint64_t pol_first = policy_evict_first();
-    // the rid-run buffer: this CTA's rids, one bulk copy (16-byte interior)
-    const uintptr_t r0 = reinterpret_cast<uintptr_t>(a.rids + lo);
-    const uintptr_t r1 = reinterpret_cast<uintptr_t>(a.rids + hi);
-    const uintptr_t ra0 = al_up(r0), ra1 = al_dn(r1);
-    const uint32_t rbytes = ra1 > ra0 ? (uint32_t)(ra1 - ra0) : 0u;
-    mbar_arrive_expect_tx(&bar[kL2Slots], rbytes);
-    if (rbytes)
-      bulk_g2s(reinterpret_cast<uint8_t*>(rcache) + (ra0 - r0), reinterpret_cast<const void*>(ra0),
-               rbytes, &bar[kL2Slots], pol_first);
     // the CTA's slice of the source bytes, enclosing 16-byte blocks (a block
     // holding at least one source byte is mapped, so this never faults)
     const uintptr_t s0 = al_dn(reinterpret_cast<uintptr_t>(a.src));
@@ -125,54 +122,56 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
     // of the slice is in flight at once), then the same bytes through the
     // bulk-copy ring, whose completions say that the slice is resident
     if (a.stage && (a.dbg & 8))
-    for (uint64_t off = b0; off < b1; off += kL2Chunk)
-      bulk_prefetch_l2(reinterpret_cast<const void*>(s0 + off), (uint32_t)min_u64(kL2Chunk, b1 - off),
+    for (uint64_t off = b0; off < b1; off += 32768)
+      bulk_prefetch_l2(reinterpret_cast<const void*>(s0 + off), (uint32_t)min_u64(32768, b1 - off),
                        pol_last);
+    // ring geometry (tunable): NS slots of CH bytes, NS * CH <= kL2Region
+    const uint32_t CH = a.ring_chunk ? a.ring_chunk : (32u << 10);
+    const uint32_t NS = a.ring_slots ? a.ring_slots : 6;
     uint32_t j = 0;
     if (a.stage)
-    for (uint64_t off = b0; off < b1; off += kL2Chunk, ++j) {
-      const uint32_t slot = j % kL2Slots;
-      if (j >= kL2Slots) mbar_wait(&bar[slot], ((j / kL2Slots) - 1) & 1);
-      const uint32_t bytes = (uint32_t)min_u64(kL2Chunk, b1 - off);
+    for (uint64_t off = b0; off < b1; off += CH, ++j) {
+      const uint32_t slot = j % NS;
+      if (j >= NS) mbar_wait(&bar[slot], ((j / NS) - 1) & 1);
+      const uint32_t bytes = (uint32_t)min_u64(CH, b1 - off);
       mbar_arrive_expect_tx(&bar[slot], bytes);
-      bulk_g2s(ring + (size_t)slot * kL2Chunk, reinterpret_cast<const void*>(s0 + off), bytes,
+      bulk_g2s(ring + (size_t)slot * CH, reinterpret_cast<const void*>(s0 + off), bytes,
                &bar[slot], pol_last);
     }
-    // drain: the last min(j, kL2Slots) copies
-    for (uint32_t q = (j > kL2Slots ? j - kL2Slots : 0); q < j; ++q)
-      mbar_wait(&bar[q % kL2Slots], (q / kL2Slots) & 1);
-  }
-  // unaligned head/tail of the rid chunk, plain loads
-  {
-    const uintptr_t r0 = reinterpret_cast<uintptr_t>(a.rids + lo);
-    const uintptr_t r1 = reinterpret_cast<uintptr_t>(a.rids + hi);
-    const uint64_t nh = min_u64(hi - lo, (al_up(r0) - r0) / 4);
-    const uint64_t nt0 = al_dn(r1) > r0 ? max_u64(nh, (al_dn(r1) - r0) / 4) : nh;
-    for (uint64_t k = tid; k < nh; k += blockDim.x) rcache[k] = a.rids[lo + k];
-    for (uint64_t k = nt0 + tid; k < hi - lo; k += blockDim.x) rcache[k] = a.rids[lo + k];
+    // drain: the last min(j, NS) copies
+    for (uint32_t q = (j > NS ? j - NS : 0); q < j; ++q)
+      mbar_wait(&bar[q % NS], (q / NS) & 1);
   }
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 1] = globaltimer();
   if (a.stage) grid_barrier(a.gbar, G);
-  else __syncthreads();
-  mbar_wait(&bar[kL2Slots], 0);
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 2] = globaltimer();
+
+  // The rid run (this CTA's chunk of the rid list) is read group by group,
+  // one coalesced 128-byte load per 32 rows, issued one group ahead.
+  const uint64_t ngroups = (hi - lo + 31) / 32;
+  auto rid_of = [&](uint64_t g) -> uint32_t {
+    const uint64_t i = lo + g * 32 + lane;
+    return (g < ngroups && i < hi) ? ldg_first(a.rids + i) : 0xFFFFFFFFu;
+  };
 
   // ---- Phase II probe + Phase III gather, in rid order ---------------------------
   const uint64_t pol_last = policy_evict_last();
   const uint64_t pol_first = policy_evict_first();
-  const uint64_t ngroups = (hi - lo + 31) / 32;
   // loads: evict_last when the run was staged in L2 (Phase II), else evict_first
   const uint64_t pol_load = a.stage ? pol_last : pol_first;
   if (REALIGN == 0) {
     const uint32_t R = a.rec / W;
     const uint32_t q32 = 32 / R, r32 = 32 % R;     // advance of (row, word) per 32 words
     constexpr int U = W >= 16 ? 4 : 8;
+    uint32_t nxt = rid_of(warp);
     for (uint64_t g = warp; g < ngroups; g += kL2Warps) {
       const uint64_t g0 = lo + g * 32;
       const uint32_t cnt = (uint32_t)min_u64(32, hi - g0);
+      const uint32_t cur = nxt;
+      nxt = rid_of(g + kL2Warps);
       uint32_t my_r = 0, ok = 0;
       if ((uint32_t)lane < cnt) {
-        my_r = rcache[g0 - lo + lane];
+        my_r = cur;
         if (my_r < a.n_src) ok = 1;
         else report_bad(a.status, g0 + lane);
       }
@@ -214,23 +213,30 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
     const uint32_t tile_bytes = 32 * rec;
     uint8_t* tiles = ring + (size_t)warp * kL2WarpTile;
     constexpr int U = 8;
-    // fast path (whole groups of valid rows, rec % 4 == 0, rec <= 116): the
-    // 16-byte windows go to a window-layout tile (row pitch 128 B, one
-    // conflict-free 16-byte store each); each output 16-byte word is then
-    // assembled from the 4 dwords it needs and stored straight to dst.
+    // fast path (whole groups of valid rows, rec % 4 == 0, rec <= 116): each
+    // 16-byte window word is stored by dwords straight into the output layout
+    // of the warp's tile (row jj at byte jj*rec; the dwords outside the row
+    // are dropped), then the tile leaves as aligned 16-byte words.
     const uintptr_t src_u = reinterpret_cast<uintptr_t>(a.src);
     const bool fast_ok = REALIGN == 1 && rec <= 116 && rec >= 8;
     const uint32_t FNW = (rec + 12 + 15) / 16;       // window words a row can need
     const uint32_t FRPI = 32 / FNW, flr = lane / FNW, flw = lane % FNW;
-    const uint32_t RD = rec / 4;                       // dwords per row
-    uint32_t* wt = reinterpret_cast<uint32_t*>(tiles);
+    uint32_t* ot = reinterpret_cast<uint32_t*>(tiles);
+    const uint32_t ot_s = smem_u32(ot);
+    const uint32_t RD = rec >> 2;                     // dwords per row
+    uint32_t on_mask = 0;                             // bit u: lane holds a row in load u
+#pragma unroll
+    for (int u = 0; u < 8; ++u) on_mask |= (uint32_t)(flr < FRPI && u * FRPI + flr < 32) << u;
     uint32_t gi = 0;
+    uint32_t nxt = rid_of(warp);
     for (uint64_t g = warp; g < ngroups; g += kL2Warps, ++gi) {
       const uint64_t g0 = lo + g * 32;
       const uint32_t cnt = (uint32_t)min_u64(32, hi - g0);
+      const uint32_t cur = nxt;
+      nxt = rid_of(g + kL2Warps);
       uint32_t my_r = 0, ok = 0;
       if ((uint32_t)lane < cnt) {
-        my_r = rcache[g0 - lo + lane];
+        my_r = cur;
         if (my_r < a.n_src) ok = 1;
         else report_bad(a.status, g0 + lane);
       }
@@ -240,39 +246,35 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
         if (lane == 0) bulk_wait_read<0>();          // a slow-path tile store may read here
         __syncwarp();
         uint4 v[8];
+        uint32_t o4p = 0;                               // 2-bit dword offsets, load u at bit 2u
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t jj = (u * FRPI + flr) & 31;
           const uint32_t r = __shfl_sync(0xffffffffu, my_r, jj);
           const uintptr_t ra = src_u + (uint64_t)r * rec;
-          const uint32_t on = (flr < FRPI && u * FRPI + flr < 32 && 16 * flw < (uint32_t)(ra & 15) + rec);
-          v[u] = ld16_pred(reinterpret_cast<const void*>((ra & ~uintptr_t(15)) + 16 * flw), on, pol_load);
+          const uint32_t o4 = (uint32_t)(ra >> 2) & 3;
+          o4p |= o4 << (2 * u);
+          ld16_pred(v[u], reinterpret_cast<const void*>((ra & ~uintptr_t(15)) + 16 * flw),
+                    ((on_mask >> u) & 1) && 4 * flw < o4 + RD);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t jj = u * FRPI + flr;
-          if (flr < FRPI && jj < 32) *reinterpret_cast<uint4*>(wt + jj * 32 + 4 * flw) = v[u];
+          // dword k of this window word is row dword 4*flw + k - o4 (kept when
+          // inside [0, RD)); row jj at dword jj*RD of the tile
+          const uint32_t jj = (u * FRPI + flr) & 31;
+          const uint32_t d0 = 4 * flw - ((o4p >> (2 * u)) & 3);   // may wrap below 0 (then > RD)
+          const uint32_t sa = ot_s + 4 * (jj * RD + d0);
+          const bool on = (on_mask >> u) & 1;
+          sts32_pred(sa + 0, v[u].x, on && d0 + 0 < RD);
+          sts32_pred(sa + 4, v[u].y, on && d0 + 1 < RD);
+          sts32_pred(sa + 8, v[u].z, on && d0 + 2 < RD);
+          sts32_pred(sa + 12, v[u].w, on && d0 + 3 < RD);
         }
-        // dword shift of row 'lane' inside its window
-        const uint32_t sh = (uint32_t)(((src_u + (uint64_t)my_r * rec) >> 2) & 3);
         __syncwarp();
         uint8_t* gdst = a.dst + g0 * rec;
         const uint32_t nwo = 2 * rec;                 // 16-byte words of 32 rows
-        for (uint32_t m0 = 0; m0 < nwo; m0 += 32) {
-          const uint32_t m = m0 + lane;
-          const uint32_t d0 = 4 * m;
-          const uint32_t j0 = min(__umulhi(d0, a.rd_magic), 31u);   // d0 / RD
-          const uint32_t q0 = d0 - j0 * RD;
-          const uint32_t s0 = __shfl_sync(0xffffffffu, sh, j0);
-          const uint32_t s1 = __shfl_sync(0xffffffffu, sh, min(j0 + 1, 31u));
-          const uint32_t b0 = j0 * 32 + s0 + q0, b1 = (j0 + 1) * 32 + s1 + q0 - RD;
-          uint4 x;
-          x.x = wt[q0 + 0 < RD ? b0 + 0 : b1 + 0];
-          x.y = wt[q0 + 1 < RD ? b0 + 1 : b1 + 1];
-          x.z = wt[q0 + 2 < RD ? b0 + 2 : b1 + 2];
-          x.w = wt[q0 + 3 < RD ? b0 + 3 : b1 + 3];
-          if (m < nwo) HintIO<16>::st(gdst + 16 * (uint64_t)m, x, pol_first);
-        }
+        for (uint32_t m = lane; m < nwo; m += 32)
+          st16_cs(gdst + 16 * (uint64_t)m, reinterpret_cast<const uint4*>(ot)[m]);
         __syncwarp();
         continue;
       }
@@ -362,15 +364,14 @@ static cudaError_t launch_l2_w(const L2RunArgs& a, uint32_t grid, uint32_t smem,
                                      st);
 }
 
-uint32_t l2run_smem_bytes(uint64_t chunk_rids) {
-  return (uint32_t)(128 + kL2Region + ((chunk_rids * 4 + 16 + 127) & ~uint64_t(127)));
-}
+uint32_t l2run_smem_bytes(uint64_t) { return 128 + kL2Region; }
 
 cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStream_t st,
                          uint32_t* nl) {
   ++*nl;
   const uint32_t smem = l2run_smem_bytes(a.chunk);
   if (W == 16) return launch_l2_w<16, 0>(a, grid, smem, st);
+  if (W == 8) return launch_l2_w<8, 0>(a, grid, smem, st);
   if (a.rec <= 128) {
     const bool word4 = a.rec % 4 == 0 && reinterpret_cast<uintptr_t>(a.src) % 4 == 0;
     return word4 ? launch_l2_w<16, 1>(a, grid, smem, st) : launch_l2_w<16, 2>(a, grid, smem, st);

@@ -90,7 +90,9 @@ def test_argument_validation_before_any_cuda_call(dpg):
     (256, 16777216, 256, 65536, 2),   # too many runs for the fused kernel
 ])
 def test_plan_run_length(dpg, rec, n, L, K, path):
-    p = dpg.dpg_plan(rec, n, n, 0, 148)
+    """Shared-memory runs (paths 1 and 2): the plan when the source exceeds the
+    L2 budget, or on request."""
+    p = dpg.dpg_plan(rec, n, n, 0, 148, path=path)
     assert p["run_len"] == L and p["num_runs"] == K and p["path"] == path
     assert p["run_len"] & (p["run_len"] - 1) == 0            # power of two (P:262-264)
     assert p["smem_bytes"] <= 232448                          # two stages fit one SM
@@ -100,12 +102,30 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
     assert m["path"] == 2 and m["nstages"] == 2
 
 
+@pytest.mark.parametrize("rec,n,auto_path", [
+    (100, 65536, 3),                  # config 1: 6.6 MB source, one L2 run
+    (100, 1048576, 3),                # config 2: 105 MB source <= 7/8 of the 126 MB L2
+    (64, 16777216, 1),                # config 3 at rec 64: 1.07 GB, shared-memory runs
+    (8, 1 << 24, 1),                  # 134 MB source > budget: shared-memory runs
+])
+def test_plan_l2_run_rule(dpg, rec, n, auto_path):
+    """The run is sized to the cache: one run (path 3) when the
+    whole source fits the L2 budget (7/8 of 126 MB with no device), else
+    shared-memory runs."""
+    budget = (126 << 20) // 8 * 7
+    p = dpg.dpg_plan(rec, n, n, 0, 148)
+    assert p["path"] == auto_path
+    assert (p["path"] == 3) == (rec * n <= budget)
+    if p["path"] == 3:
+        assert p["num_runs"] == 1 and p["run_len"] >= n
+
+
 def test_plan_pair_packing_and_overrides(dpg):
-    c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20)
+    c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20, path=1)
     assert c2["gather"] == 1 and c2["pair_bytes"] == 4                # 9 + 20 bits packed
     assert c2["slot_pairs"] == 672                                    # CAP = L + L/4 + 32
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, gather=2)["pair_bytes"] == 2   # u16 locals
-    assert dpg.dpg_plan(128, 1 << 20, 1 << 20)["gather"] == 1         # whole sectors
+    assert dpg.dpg_plan(128, 1 << 20, 1 << 20, path=1)["gather"] == 1  # whole sectors
     assert dpg.dpg_plan(64, 1 << 24, 1 << 26)["pair_bytes"] == 8      # 10 + 26 bits
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8, gather=1)["pair_bytes"] == 8
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, pair_bytes=8, gather=2)["pair_bytes"] == 4

@@ -186,7 +186,7 @@ def test_l2run_invalid_rids_leave_rows_unwritten(dpg):
 
 
 def test_plan_picks_l2run_when_the_source_fits_l2(dpg):
-    p = dpg.dpg_plan(100, 1 << 20, 1 << 20)
+    p = dpg.dpg_plan(100, 1 << 18, 1 << 18)
     assert p["path"] == 3 and p["num_runs"] == 1
     assert dpg.dpg_plan(100, 1 << 24, 1 << 24)["path"] != 3
 
