@@ -3,6 +3,7 @@
 // kernel sequence  distribute (Phase I) -> fused probe+gather (Phases II+III).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -255,6 +256,48 @@ uint64_t l2_budget(uint64_t l2_bytes) {
   return env ? env : l2_bytes / 8 * 7;
 }
 
+// Budget of one L2 run staged from all SMs and probed from all SMs: measured
+// retention ~60 MB of the 126 MB L2 (profiles/r01_l2_retention_ncu.txt).
+uint64_t l2_run_budget(uint64_t l2_bytes) {
+  static uint64_t env = [] {
+    const char* e = getenv("DPG_L2_RUN_MB");
+    return e ? (uint64_t)atoll(e) << 20 : 0ull;
+  }();
+  return env ? env : l2_bytes / 16 * 7;
+}
+
+// Two L2 runs (l2pair.cu): the source is more than one run and at most two;
+// rows of 4-byte words up to 116 bytes; each CTA's RID_RUN[0] buffer fits
+// shared memory.
+bool plan_l2pair(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool forced, int sm,
+                 uint64_t l2_bytes, dpg_plan_t* p) {
+  if (pay || n_out == 0 || rec % 4 || rec < 8 || rec > 116 || n_src < 2) return false;
+  const uint64_t B1 = l2_run_budget(l2_bytes);
+  uint32_t s = 0;
+  while ((2ull << s) * rec <= B1 && (2ull << s) < n_src) ++s;   // largest 2^s with 2^s*rec <= B1
+  const uint64_t L = 1ull << s;
+  if (forced) {
+    // any source: run 0 = the lower half (power of two)
+    s = bit_length(n_src - 1) - 1;
+  } else if (!(n_src * rec > B1 && n_src <= 2 * L)) {
+    return false;
+  }
+  const uint64_t chunk = align_up((n_out + sm - 1) / sm, 32);
+  if (l2pair_smem_bytes(chunk) > kSmemLimit) return false;
+  std::memset(p, 0, sizeof(*p));
+  p->path = 4;
+  p->log2_run = s;
+  p->run_len = 1ull << s;
+  p->num_runs = (n_src + p->run_len - 1) >> s;
+  p->word_bytes = 16;
+  p->grid_probe = (uint32_t)sm;
+  p->grid_distribute = (uint32_t)sm;
+  p->tile = (uint32_t)chunk;
+  p->smem_bytes = l2pair_smem_bytes(chunk);
+  p->nstages = 6;
+  return true;
+}
+
 bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool forced, int sm,
                 uint64_t l2_bytes, dpg_plan_t* p) {
   if (pay || n_out == 0) return false;
@@ -283,6 +326,14 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   const uint32_t want_path = opt ? opt->path : 0;
   const bool overrides = opt && (opt->log2_run || opt->grid_distribute || opt->grid_probe ||
                                  opt->hist_mode || opt->gather || opt->pair_bytes);
+  if (want_path == 4) {
+    // two L2 runs (Fig. 1 literally at the L2 level, INTERNAL run 0): on
+    // request only -- measured slower than one staged run for config 2
+    // (profiles/r01_l2pair_probe.txt: 76 vs 70 us; the INTERNAL round trip
+    // costs what the single run's L2 misses cost)
+    if (plan_l2pair(rec, n_src, n_out, pay, true, sm, current_l2_bytes(), p)) return DPG_OK;
+    return DPG_ERR_UNSUPPORTED;
+  }
   if (want_path == 3 || (want_path == 0 && !overrides)) {
     if (plan_l2run(rec, n_src, n_out, pay, want_path == 3, sm, current_l2_bytes(), p))
       return DPG_OK;
@@ -479,6 +530,43 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
 
+  if (p.path == 4 && ((uintptr_t)src % 16 || (uintptr_t)dst % 16)) {
+    // the two-run kernels move 16-byte words: unaligned buffers take one run
+    dpg_options_t o = opt ? *opt : dpg_options_t{};
+    o.path = 3;
+    if (make_plan(rec, n_src, n_out, pay, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
+  }
+  if (p.path == 4) {
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* internal = nullptr;
+    const uint64_t int_bytes = (uint64_t)p.grid_probe * p.tile * rec;
+    dpg_status_t ws = persist_ws(st, 1, int_bytes + 64, &gbar, &total, &internal);
+    if (ws != DPG_OK) return ws;
+    L2PairArgs l;
+    std::memset(&l, 0, sizeof(l));
+    l.src = (const uint8_t*)src;
+    l.n_src = n_src;
+    l.rec = (uint32_t)rec;
+    l.rids = rids;
+    l.n_out = n_out;
+    l.L = p.run_len;
+    l.chunk = p.tile;
+    l.max_groups = (uint32_t)((p.tile + 31) / 32);
+    l.internal = (uint8_t*)internal;
+    l.dst = (uint8_t*)dst;
+    l.gbar = gbar;
+    l.status = status;
+    l.ts = g_debug_ts;
+    l.dbg = g_debug_flags;
+    uint32_t nl = 0;
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    if (timed) cudaEventRecord(pe.e1, st);
+    cudaError_t e = launch_l2pair(l, p.grid_probe, st, &nl);
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_launches = nl;
+    return cuda_status(e);
+  }
   if (p.path == 3) {
     uint32_t *gbar = nullptr, *total = nullptr;
     void* pairs = nullptr;

@@ -80,16 +80,42 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t G) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    // arrival with acq_rel (cumulative over the CTA's writes, ordered by the
+    // bar.sync above); the last arriver resets the count and releases the
+    // next generation; the others acquire it
     const uint32_t gen = ld_acquire_gpu(gbar + 1);
-    __threadfence();
-    if (atomicAdd(gbar, 1u) == G - 1) {
-      atomicExch(gbar, 0u);
-      __threadfence();
-      atomicAdd(gbar + 1, 1u);
+    uint32_t old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(gbar) : "memory");
+    if (old == G - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(gbar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar + 1) : "memory");
     } else {
-      while (ld_acquire_gpu(gbar + 1) == gen) __nanosleep(32);
+      while (ld_acquire_gpu(gbar + 1) == gen) {
+      }
     }
-    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Grid barrier with one poller: every CTA adds 1 to a monotonic arrival
+// count (red.release, no return); CTA 0 waits for the count of this epoch and
+// publishes the next epoch; the others wait for the epoch word (a different
+// cache line from the count, so the waiters do not slow the arrivals).
+// w[0] = count, w[32] = epoch; both only grow (zero at allocation).  All
+// launches sharing w must use the same grid size G.
+__device__ __forceinline__ void grid_barrier_mono(uint32_t* w, uint32_t G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t epoch = ld_acquire_gpu(w + 32);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(w) : "memory");
+    if (blockIdx.x == 0) {
+      const uint32_t target = (epoch + 1) * G;
+      while ((int32_t)(ld_acquire_gpu(w) - target) < 0) {
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(w + 32), "r"(epoch + 1) : "memory");
+    } else {
+      while (ld_acquire_gpu(w + 32) == epoch) __nanosleep(64);
+    }
   }
   __syncthreads();
 }
@@ -221,9 +247,28 @@ struct L2RunArgs {
   uint32_t stage;        // 1: Phase II stages the source into L2 (then a grid barrier)
   uint32_t ring_chunk;   // Phase II bulk-copy bytes per slot (0: 32 KB)
   uint32_t ring_slots;   // Phase II ring slots (0: 6)
+  uint64_t persist_bytes;  // host side: bytes of src under a persisting L2 access window (0: none)
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
                          // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first
+};
+
+// DPG with two L2-resident runs (l2pair.cu).
+struct L2PairArgs {
+  const uint8_t* src;
+  uint64_t n_src;
+  uint32_t rec;
+  const uint32_t* rids;
+  uint64_t n_out;
+  uint64_t L;            // records of run 0 (a power of two); run 1 = [L, n_src)
+  uint64_t chunk;        // output rows per CTA (multiple of 32)
+  uint32_t max_groups;   // ceil(chunk / 32)
+  uint8_t* internal;     // INTERNAL run 0: the chunk of CTA c at internal + c*chunk*rec
+  uint8_t* dst;
+  uint32_t* gbar;        // [2] grid barrier (persistent, zero-restored)
+  unsigned long long* status;
+  unsigned long long* ts;
+  uint32_t dbg;          // tuning flags: bit0 skip Phase I (timing only), bit1 no grid barrier
 };
 
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
@@ -284,8 +329,77 @@ template <> struct HintIO<16> {
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
   return t;
+}
+
+// ---------------------------------------------------------------------------
+// Helpers of the L2-run kernels (l2run.cu, l2pair.cu).
+// ---------------------------------------------------------------------------
+// 16-byte global load under a predicate (no branch; the registers keep their
+// value when off), read-only path, no L1 allocation.
+__device__ __forceinline__ void ld16_pred(uint4& v, const void* p, bool on, uint64_t pol) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%5], %6;\n\t}"
+      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+      : "r"((uint32_t)on), "l"(p), "l"(pol));
+}
+// 4-byte shared store under a predicate.
+__device__ __forceinline__ void sts32_pred(uint32_t saddr, uint32_t v, bool on) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q st.shared.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v), "r"((uint32_t)on) : "memory");
+}
+// Streaming 16-byte global store (evict-first).
+__device__ __forceinline__ void st16_cs(void* p, uint4 v) { __stcs(reinterpret_cast<uint4*>(p), v); }
+
+__device__ __forceinline__ uint32_t ldg_first(const uint32_t* p) {
+  return __ldcs(p);   // streaming: read once
+}
+__device__ __forceinline__ uintptr_t al_dn(uintptr_t p) { return p & ~uintptr_t(15); }
+__device__ __forceinline__ uintptr_t al_up(uintptr_t p) { return (p + 15) & ~uintptr_t(15); }
+
+// Bulk store shared -> global (TMA), tracked by the issuing thread's bulk group.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+
+// Phase II staging of [base, base + bytes) into L2 by one thread of each CTA:
+// the CTA's slice (16-byte blocks) goes through a ring of NS bulk copies of CH
+// bytes into shared memory with L2 evict_last; returns once every copy of the
+// slice has landed (the slice is then resident in L2).  bar: NS mbarriers
+// initialised with count 1.
+__device__ __forceinline__ uint32_t l2_stage_slice(const uint8_t* base, uint64_t bytes, uint32_t c,
+                                                   uint32_t G, uint8_t* ring, uint64_t* bar,
+                                                   uint32_t CH, uint32_t NS, uint64_t pol,
+                                                   uint32_t jb = 0) {
+  // jb: copies issued into this ring before (the mbarrier phases continue)
+  const uintptr_t s0 = al_dn(reinterpret_cast<uintptr_t>(base));
+  const uintptr_t s1 = al_up(reinterpret_cast<uintptr_t>(base) + bytes);
+  const uint64_t total = s1 - s0;
+  const uint64_t slice = ((total + G - 1) / G + 15) & ~uint64_t(15);
+  const uint64_t b0 = min_u64(total, (uint64_t)c * slice), b1 = min_u64(total, b0 + slice);
+  uint32_t j = jb;
+  for (uint64_t off = b0; off < b1; off += CH, ++j) {
+    const uint32_t slot = j % NS;
+    if (j >= NS) mbar_wait(&bar[slot], ((j / NS) - 1) & 1);
+    const uint32_t nb = (uint32_t)min_u64(CH, b1 - off);
+    mbar_arrive_expect_tx(&bar[slot], nb);
+    bulk_g2s(ring + (size_t)slot * CH, reinterpret_cast<const void*>(s0 + off), nb, &bar[slot], pol);
+  }
+  for (uint32_t q = (j > jb + NS ? j - NS : jb); q < j; ++q) mbar_wait(&bar[q % NS], (q / NS) & 1);
+  return j;
 }
 
 // Launchers (return cudaError_t of the launch).
@@ -294,6 +408,8 @@ cudaError_t launch_fused(const FusedArgs& a, uint32_t W, uint32_t grid, uint32_t
 cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStream_t st,
                          uint32_t* nlaunch);
 uint32_t l2run_smem_bytes(uint64_t chunk_rids);
+cudaError_t launch_l2pair(const L2PairArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nlaunch);
+uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                                 cudaStream_t st, uint32_t* nlaunch);
@@ -314,4 +430,119 @@ cudaError_t launch_split_entries(const DistArgs& a, uint32_t* local_out, uint32_
 cudaError_t launch_unpack_pairs(const DistArgs& a, uint64_t* pairs_out, uint64_t* run_start_out,
                                 cudaStream_t st, uint32_t* nlaunch);
 
+}  // namespace dpg
+
+namespace dpg {
+
+// ---------------------------------------------------------------------------
+// Asynchronous window gather (l2pair.cu, l2run.cu): a warp moves groups of up
+// to 32 rows of rec bytes (rec % 4 == 0, rec <= 116) from arbitrary 4-byte
+// aligned source addresses to a contiguous output span.  Issue: each row's
+// enclosing 16-byte-aligned window (<= 8 words) is copied by cp.async (16 B
+// per lane, L2 only) into the group's tile in shared memory (row pitch
+// 128 B); several groups are in flight per warp without holding registers.
+// Consume: output dword d of the group is row d / RD, dword d % RD, read from
+// the tile at the row's dword shift, and stored with coalesced 4-byte
+// streaming stores (any 4-byte-aligned output).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kAgTile = 32 * 128;   // bytes of one group's window tile
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// lane j of the warp holds row j's source address (my_addr) and whether the
+// row is to be copied (my_on); rows >= cnt are off.
+__device__ __forceinline__ void ag_issue(uint32_t tile_s, uint64_t my_addr, bool my_on, uint32_t rec,
+                                         uint32_t lane) {
+  const uint32_t FNW = (rec + 27) / 16;
+  const uint32_t FRPI = 32 / FNW, flr = lane / FNW, flw = lane % FNW;
+  const uint32_t lim = rec - 16 * flw;     // word flw is needed iff (addr & 15) + rec > 16 flw
+  uint32_t jj = flr;
+  uint32_t so = tile_s + flr * 128 + 16 * flw;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t j = jj & 31;
+    const uint32_t lo32 = __shfl_sync(0xffffffffu, (uint32_t)my_addr, j);
+    const uint32_t hi32 = __shfl_sync(0xffffffffu, (uint32_t)(my_addr >> 32), j);
+    const uint32_t on_j = __shfl_sync(0xffffffffu, (uint32_t)my_on, j);
+    const bool on = on_j && flr < FRPI && jj < 32 && (int)(lo32 & 15) + (int)lim > 0;
+    if (on)   // the window words a row needs; the consume step reads no others
+      cp_async16(so, reinterpret_cast<const void*>(((((uint64_t)hi32 << 32) | lo32) & ~uint64_t(15)) +
+                                                  16 * flw), 16u);
+    jj += FRPI;
+    so += FRPI * 128;
+  }
+}
+
+// my_o4: row lane's dword shift inside its window ((addr >> 2) & 3);
+// okm: rows to store; out: 4-byte aligned.
+__device__ __forceinline__ void ag_consume(const uint32_t* tile, uint32_t my_o4, uint32_t okm,
+                                           uint32_t cnt, uint32_t rec, uint32_t* out,
+                                           uint32_t lane) {
+  const uint32_t RD = rec >> 2;
+  const uint32_t n = cnt * RD;
+  const uint32_t q32 = 32 / RD, r32 = 32 % RD;
+  uint32_t j = lane / RD, q = lane % RD;
+  for (uint32_t d0 = 0; d0 < n; d0 += 32) {
+    const uint32_t d = d0 + lane;
+    const uint32_t jj = j < 32 ? j : 31;
+    const uint32_t s = __shfl_sync(0xffffffffu, my_o4, jj);
+    if (d < n && ((okm >> jj) & 1)) __stcs(out + d, tile[jj * 32 + s + q]);
+    j += q32;
+    q += r32;
+    if (q >= RD) { q -= RD; ++j; }
+  }
+}
+
+}  // namespace dpg
+
+namespace dpg {
+// ag_consume with 16-byte output words (4x fewer global store instructions):
+// out 16-byte aligned and cnt * rec a multiple of 16.  The word -> (row,
+// dword) map of a full group is per-lane constant: AgMap holds it for the
+// lane's words m = lane + 32 i (i < 8, rec <= 116 gives <= 232 words).
+struct AgMap {
+  uint32_t b0[8];     // tile dword index of the word's first dword in row j0, before the shift
+  uint32_t b1[8];     // same for the next row (j0 + 1), minus RD
+  uint32_t jp[8];     // j0 | (j0 + 1) << 8 | split << 16 (dwords e < split are row j0's)
+};
+__device__ __forceinline__ void ag_map_init(AgMap& M, uint32_t rec, uint32_t lane) {
+  const uint32_t RD = rec >> 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t d0 = 4 * (lane + 32 * i);
+    const uint32_t j0 = min(d0 / RD, 31u);
+    const uint32_t q0 = d0 - j0 * RD;
+    const uint32_t j1 = min(j0 + 1, 31u);
+    M.b0[i] = j0 * 32 + q0;
+    M.b1[i] = j1 * 32 + q0 - RD;
+    M.jp[i] = j0 | (j1 << 8) | (min(RD - min(q0, RD), 4u) << 16);
+  }
+}
+__device__ __forceinline__ void ag_consume16(const uint32_t* tile, uint32_t my_o4, const AgMap& M,
+                                             uint32_t cnt, uint32_t rec, uint32_t* out,
+                                             uint32_t lane) {
+  const uint32_t nw = cnt * (rec >> 2) / 4;         // 16-byte output words
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (32 * i >= nw) break;                        // warp-uniform
+    const uint32_t m = lane + 32 * i;
+    const uint32_t jp = M.jp[i];
+    const uint32_t s0 = __shfl_sync(0xffffffffu, my_o4, jp & 31);
+    const uint32_t s1 = __shfl_sync(0xffffffffu, my_o4, (jp >> 8) & 31);
+    const uint32_t split = jp >> 16;
+    const uint32_t a0 = M.b0[i] + s0, a1 = M.b1[i] + s1;
+    uint4 v;
+    v.x = tile[a0];                                  // split >= 1
+    v.y = tile[1 < split ? a0 + 1 : a1 + 1];
+    v.z = tile[2 < split ? a0 + 2 : a1 + 2];
+    v.w = tile[3 < split ? a0 + 3 : a1 + 3];
+    if (m < nw) __stcs(reinterpret_cast<uint4*>(out) + m, v);
+  }
+}
 }  // namespace dpg

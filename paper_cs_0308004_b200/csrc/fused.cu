@@ -443,8 +443,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
 template <int W, typename PairT, int MODE>
 static cudaError_t launch_t(const FusedArgs& a, uint32_t grid, uint32_t smem, cudaStream_t st) {
   auto fn = k_dpg_fused<W, PairT, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // opt in to the dynamic shared memory once per device and size
+  static int set_dev = -1;
+  static uint32_t set_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev || set_smem < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set_dev = dev;
+    set_smem = smem;
+  }
   FusedArgs arg = a;
   void* params[] = {&arg};
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kFusedThreads), params,

@@ -40,44 +40,6 @@ static_assert(kL2WarpTile * kL2Warps <= kL2Region, "gather tiles exceed the ring
 static_assert(128 >= 8 * kL2Slots, "barrier area");
 
 
-// 16-byte global load under a predicate (no branch; the registers keep their
-// value when off), read-only path, no L1 allocation.
-__device__ __forceinline__ void ld16_pred(uint4& v, const void* p, bool on) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-      "@q ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%5];\n\t}"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "r"((uint32_t)on), "l"(p));
-}
-// 4-byte shared store under a predicate.
-__device__ __forceinline__ void sts32_pred(uint32_t saddr, uint32_t v, bool on) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-      "@q st.shared.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v), "r"((uint32_t)on) : "memory");
-}
-// Streaming 16-byte global store (evict-first).
-__device__ __forceinline__ void st16_cs(void* p, uint4 v) { __stcs(reinterpret_cast<uint4*>(p), v); }
-
-__device__ __forceinline__ uint32_t ldg_first(const uint32_t* p) {
-  return __ldcs(p);   // streaming: read once
-}
-__device__ __forceinline__ uintptr_t al_dn(uintptr_t p) { return p & ~uintptr_t(15); }
-__device__ __forceinline__ uintptr_t al_up(uintptr_t p) { return (p + 15) & ~uintptr_t(15); }
-
-// Bulk store shared -> global (TMA), tracked by the issuing thread's bulk group.
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
-               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol) : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 // REALIGN 0: rows are whole W-byte words (W = 16 when rec, src and dst allow):
 //            flat word loop, loads and stores straight between L2 and dst.
 // REALIGN 1: rows of any 4-byte multiple (e.g. the 100-byte records): each row
@@ -108,7 +70,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
   __syncthreads();
 
   // ---- Phase II: load the run (the whole source) into L2 ----------------------
-  if (tid == 0) {
+  // (one lane of warp 0 issues; the warp reconverges before any CTA barrier)
+  if (warp == 0) {
+  if (lane == 0) {
     const uint64_t pol_last = policy_evict_last();
     const uint64_t pol_first = policy_evict_first();
     // the CTA's slice of the source bytes, enclosing 16-byte blocks (a block
@@ -142,6 +106,8 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
     for (uint32_t q = (j > NS ? j - NS : 0); q < j; ++q)
       mbar_wait(&bar[q % NS], (q / NS) & 1);
   }
+  __syncwarp();
+  }
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 1] = globaltimer();
   if (a.stage) grid_barrier(a.gbar, G);
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 2] = globaltimer();
@@ -159,6 +125,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
   const uint64_t pol_first = policy_evict_first();
   // loads: evict_last when the run was staged in L2 (Phase II), else evict_first
   const uint64_t pol_load = a.stage ? pol_last : pol_first;
+  // the window gather: hits leave the staged lines' priority alone; a miss's
+  // fill is evict_first so it does not displace the staged run (tunable)
+  const uint64_t pol_gather = (a.dbg & 64) ? pol_last : pol_first;
   if (REALIGN == 0) {
     const uint32_t R = a.rec / W;
     const uint32_t q32 = 32 / R, r32 = 32 % R;     // advance of (row, word) per 32 words
@@ -255,7 +224,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
           const uint32_t o4 = (uint32_t)(ra >> 2) & 3;
           o4p |= o4 << (2 * u);
           ld16_pred(v[u], reinterpret_cast<const void*>((ra & ~uintptr_t(15)) + 16 * flw),
-                    ((on_mask >> u) & 1) && 4 * flw < o4 + RD);
+                    ((on_mask >> u) & 1) && 4 * flw < o4 + RD, pol_gather);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -356,12 +325,40 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
 template <int W, int REALIGN>
 static cudaError_t launch_l2_w(const L2RunArgs& a, uint32_t grid, uint32_t smem, cudaStream_t st) {
   auto fn = k_dpg_l2run<W, REALIGN>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  L2RunArgs arg = a;
-  void* params[] = {&arg};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kL2Threads), params, smem,
-                                     st);
+  // opt in to the dynamic shared memory once per device and size
+  static int set_dev = -1;
+  static uint32_t set_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev || set_smem < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set_dev = dev;
+    set_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kL2Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeCooperative;   // the grid barrier ends Phase II
+  at[na].val.cooperative = a.stage ? 1 : 0;
+  ++na;
+  if (a.persist_bytes) {
+    // L2 set-aside for the staged run: the source window is marked persisting
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(a.src);
+    at[na].val.accessPolicyWindow.num_bytes = a.persist_bytes;
+    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
 uint32_t l2run_smem_bytes(uint64_t) { return 128 + kL2Region; }

@@ -104,7 +104,7 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
 
 @pytest.mark.parametrize("rec,n,auto_path", [
     (100, 65536, 3),                  # config 1: 6.6 MB source, one L2 run
-    (100, 1048576, 3),                # config 2: 105 MB source <= 7/8 of the 126 MB L2
+    (100, 1048576, 3),                # config 2: 105 MB source <= 7/8 of the L2, one staged run
     (64, 16777216, 1),                # config 3 at rec 64: 1.07 GB, shared-memory runs
     (8, 1 << 24, 1),                  # 134 MB source > budget: shared-memory runs
 ])
@@ -112,12 +112,17 @@ def test_plan_l2_run_rule(dpg, rec, n, auto_path):
     """The run is sized to the cache: one run (path 3) when the
     whole source fits the L2 budget (7/8 of 126 MB with no device), else
     shared-memory runs."""
-    budget = (126 << 20) // 8 * 7
+    run_budget = (126 << 20) // 16 * 7                 # one L2 run (measured retention)
     p = dpg.dpg_plan(rec, n, n, 0, 148)
     assert p["path"] == auto_path
-    assert (p["path"] == 3) == (rec * n <= budget)
+    q = dpg.dpg_plan(rec, n, n, 0, 148, path=4) if rec % 4 == 0 and rec <= 116 and n <= 1 << 20 else None
+    if q is not None:                                  # two L2 runs on request
+        assert q["num_runs"] == 2 and 2 * q["run_len"] >= n
     if p["path"] == 3:
         assert p["num_runs"] == 1 and p["run_len"] >= n
+    if p["path"] == 4:
+        assert p["num_runs"] == 2 and p["run_len"] * rec <= run_budget < n * rec
+        assert p["run_len"] & (p["run_len"] - 1) == 0 and 2 * p["run_len"] >= n
 
 
 def test_plan_pair_packing_and_overrides(dpg):

@@ -123,7 +123,7 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
 
 
 @pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
-@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0)])
+@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0), (4, 0)])
 def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path, gather):
     """Every execution path on the same cases: the fused cooperative kernel
     writing rows straight to dst (gather 1) or through INTERNAL (gather 2),
@@ -168,6 +168,55 @@ def test_l2run_shapes_and_alignment(dpg, rec, soff, doff):
     dpg.dpg_sync_status()
 
 
+@pytest.mark.parametrize("rec", [8, 12, 36, 64, 100, 116])
+@pytest.mark.parametrize("kind", ["perm", "repl", "equal", "sorted"])
+def test_l2pair_two_runs(dpg, rec, kind):
+    """The two-L2-run kernels (path 4): Phase I + probe of run 0 into INTERNAL,
+    then run 1 fused with Phase III; ragged CTA chunks and group tails."""
+    n_src = 30011 + rec
+    n_out = n_src if kind == "perm" else 2 * n_src + 13
+    src, rids = _case(rec * 31 + len(kind), n_src, rec, n_out, kind)
+    p = dpg.dpg_plan(rec, n_src, n_out, path=4)
+    assert p["path"] == 4 and p["num_runs"] == 2
+    got = host(dpg.dpg_retrieve(dev(src), dev(rids), path=4))
+    assert np.array_equal(got, oracle.retrieve(src, rids))
+    dpg.dpg_sync_status()
+
+
+def test_l2pair_large_chunks(dpg):
+    """CTA chunks of more than one Phase I register batch (> 7680 rows)."""
+    n_src, n_out = 1 << 18, 148 * 8448 - 77
+    src, rids = _case(77, n_src, 8, n_out, "repl")
+    got = host(dpg.dpg_retrieve(dev(src), dev(rids), path=4))
+    assert np.array_equal(got, oracle.retrieve(src, rids))
+
+
+def test_l2pair_invalid_and_unaligned(dpg):
+    src, rids = _case(12, 20000, 100, 33333, "repl")
+    bad = [0, 5, 31, 32, 20000, 33332]
+    for b in bad:
+        rids[b] = 20000 + b
+    d = torch.zeros((33333, 100), dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=d, path=4)
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 0
+    out = host(d)
+    ok = np.ones(33333, bool)
+    ok[bad] = False
+    assert np.array_equal(out[ok], src[rids[ok].astype(np.int64)])
+    assert np.all(out[~ok] == 0)
+    # unaligned buffers fall back to one run; canaries around dst
+    big = torch.full((33333 * 100 + 64,), 0xEE, dtype=torch.uint8, device="cuda")
+    d2 = big[4:4 + 33333 * 100].view(33333, 100)
+    good = rids.copy()
+    good[bad] = 7
+    dpg.dpg_retrieve(dev(src), dev(good), dst=d2, path=4)
+    o = host(big)
+    assert np.all(o[:4] == 0xEE) and np.all(o[4 + 33333 * 100:] == 0xEE)
+    assert np.array_equal(o[4:4 + 33333 * 100].reshape(33333, 100), oracle.retrieve(src, good))
+
+
 def test_l2run_invalid_rids_leave_rows_unwritten(dpg):
     src, rids = _case(11, 5000, 100, 9000, "repl")
     bad = [0, 31, 32, 4001, 8999]
@@ -188,7 +237,11 @@ def test_l2run_invalid_rids_leave_rows_unwritten(dpg):
 def test_plan_picks_l2run_when_the_source_fits_l2(dpg):
     p = dpg.dpg_plan(100, 1 << 18, 1 << 18)
     assert p["path"] == 3 and p["num_runs"] == 1
-    assert dpg.dpg_plan(100, 1 << 24, 1 << 24)["path"] != 3
+    p = dpg.dpg_plan(100, 1 << 20, 1 << 20)                 # config 2: one staged run
+    assert p["path"] == 3 and p["num_runs"] == 1
+    p = dpg.dpg_plan(100, 1 << 20, 1 << 20, path=4)         # two L2 runs on request
+    assert p["path"] == 4 and p["num_runs"] == 2
+    assert dpg.dpg_plan(100, 1 << 24, 1 << 24)["path"] in (1, 2)
 
 
 @pytest.mark.parametrize("hist_mode", [1, 2])
