@@ -546,3 +546,50 @@ __device__ __forceinline__ void ag_consume16(const uint32_t* tile, uint32_t my_o
   }
 }
 }  // namespace dpg
+
+namespace dpg {
+// One group of the asynchronous window gather: lane j's row j.
+struct AgGroup {
+  uint64_t addr;      // source address of the lane's row
+  uint32_t cnt;       // rows in the group (<= 32)
+  uint32_t okm;       // rows to store (a bad rid leaves its row unwritten)
+  uint32_t o4;        // the lane's row: dword shift inside its window
+  uint32_t* out;      // the group's output span (cnt * rec bytes, 4-byte aligned)
+  bool on;            // the lane's row is copied
+};
+
+// Run the window gather over a warp's groups t = 0 .. nt-1 (group(t) builds
+// the descriptor of group t, called in order): groups t+1 and t+2 are in
+// flight (cp.async into three tiles of tile_bytes) while t is consumed; the
+// descriptors rotate through registers.
+template <typename F>
+__device__ __forceinline__ void ag_pipeline(uint32_t nt, F group, uint8_t* wtiles, uint32_t wt_s,
+                                            uint32_t tile_bytes, const AgMap& amap, uint32_t rec,
+                                            uint32_t lane) {
+  AgGroup q0{}, q1{}, q2{};
+  if (0 < nt) { q0 = group(0); ag_issue(wt_s, q0.addr, q0.on, rec, lane); }
+  cp_async_commit();
+  if (1 < nt) { q1 = group(1); ag_issue(wt_s + tile_bytes, q1.addr, q1.on, rec, lane); }
+  cp_async_commit();
+  uint32_t slot = 0;
+  for (uint32_t t = 0; t < nt; ++t) {
+    const uint32_t slot2 = slot == 0 ? 2 : slot - 1;
+    if (t + 2 < nt) { q2 = group(t + 2); ag_issue(wt_s + slot2 * tile_bytes, q2.addr, q2.on, rec, lane); }
+    cp_async_commit();
+    cp_async_wait<2>();
+    __syncwarp();
+    const uint32_t* wt = reinterpret_cast<const uint32_t*>(wtiles + slot * tile_bytes);
+    const uint32_t full = q0.cnt == 32 ? 0xffffffffu : ((1u << q0.cnt) - 1u);
+    if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * rec)) & 15) == 0)
+      ag_consume16(wt, q0.o4, amap, q0.cnt, rec, q0.out, lane);
+    else
+      ag_consume(wt, q0.o4, q0.okm, q0.cnt, rec, q0.out, lane);
+    __syncwarp();
+    q0 = q1;
+    q1 = q2;
+    slot = slot == 2 ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+}
+}  // namespace dpg
+

@@ -157,35 +157,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_dpg_l2pair(L2PairArgs a) {
   const uintptr_t seg_u = reinterpret_cast<uintptr_t>(seg);
   AgMap amap;
   ag_map_init(amap, a.rec, lane);
-  struct Grp { uint64_t addr; uint32_t cnt, okm, o4; uint32_t* out; bool on; };
-  // Run the pipeline over this warp's groups t = 0..nt-1 (group(t) describes
-  // group t): groups t+1 and t+2 are in flight while t is consumed; the
-  // descriptors rotate through registers.
   auto pipeline = [&](uint32_t nt, auto group) {
-    Grp q0{}, q1{}, q2{};
-    if (0 < nt) { q0 = group(0); ag_issue(wt_s, q0.addr, q0.on, a.rec, lane); }
-    cp_async_commit();
-    if (1 < nt) { q1 = group(1); ag_issue(wt_s + kPTile, q1.addr, q1.on, a.rec, lane); }
-    cp_async_commit();
-    uint32_t slot = 0;
-    for (uint32_t t = 0; t < nt; ++t) {
-      const uint32_t slot2 = slot == 0 ? 2 : slot - 1;
-      if (t + 2 < nt) { q2 = group(t + 2); ag_issue(wt_s + slot2 * kPTile, q2.addr, q2.on, a.rec, lane); }
-      cp_async_commit();
-      cp_async_wait<2>();
-      __syncwarp();
-      const uint32_t* wt = reinterpret_cast<const uint32_t*>(wtiles + slot * kPTile);
-      const uint32_t full = q0.cnt == 32 ? 0xffffffffu : ((1u << q0.cnt) - 1u);
-      if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * a.rec)) & 15) == 0)
-        ag_consume16(wt, q0.o4, amap, q0.cnt, a.rec, q0.out, lane);
-      else
-        ag_consume(wt, q0.o4, q0.okm, q0.cnt, a.rec, q0.out, lane);
-      __syncwarp();
-      q0 = q1;
-      q1 = q2;
-      slot = slot == 2 ? 0 : slot + 1;
-    }
-    cp_async_wait<0>();
+    ag_pipeline(nt, group, wtiles, wt_s, kPTile, amap, a.rec, lane);
   };
 
   // ---- Phase II (run 0), second step, the probe:
@@ -194,8 +167,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_dpg_l2pair(L2PairArgs a) {
     const uint32_t n0 = gcnt[ngroups];
     const uint32_t ng = (n0 + 31) / 32;
     const uint32_t nt = ng > (uint32_t)warp ? (ng - warp + kPWarps - 1) / kPWarps : 0;
-    pipeline(nt, [&](uint32_t t) -> Grp {
-      Grp q;
+    pipeline(nt, [&](uint32_t t) -> AgGroup {
+      AgGroup q;
       const uint32_t k0 = 32 * (warp + t * kPWarps);
       q.cnt = min(32u, n0 - k0);
       q.on = (uint32_t)lane < q.cnt;
@@ -233,7 +206,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_dpg_l2pair(L2PairArgs a) {
     };
     uint32_t rq0 = rid_load(0), rq1 = rid_load(1), rq2 = rid_load(2), rq3 = rid_load(3);
     uint32_t next_t = 0;
-    pipeline(nt, [&](uint32_t t) -> Grp {
+    pipeline(nt, [&](uint32_t t) -> AgGroup {
       // groups are requested in order t = 0, 1, 2, ...: rotate the rid registers
       (void)next_t;
       const uint32_t r = rq0;
@@ -241,7 +214,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_dpg_l2pair(L2PairArgs a) {
       rq1 = rq2;
       rq2 = rq3;
       rq3 = rid_load(t + 4);
-      Grp q;
+      AgGroup q;
       const uint32_t g = warp + t * kPWarps;
       const uint64_t g0 = lo + 32 * (uint64_t)g;
       q.cnt = (uint32_t)min_u64(32, hi - g0);

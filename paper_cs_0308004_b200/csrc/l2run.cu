@@ -82,13 +82,6 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
     const uint64_t total = a.stage_bytes ? min_u64(s1 - s0, a.stage_bytes) : s1 - s0;
     const uint64_t slice = ((total + G - 1) / G + 15) & ~uint64_t(15);
     const uint64_t b0 = min_u64(total, (uint64_t)c * slice), b1 = min_u64(total, b0 + slice);
-    // first the whole slice as L2 prefetches (fire-and-forget: every DRAM read
-    // of the slice is in flight at once), then the same bytes through the
-    // bulk-copy ring, whose completions say that the slice is resident
-    if (a.stage && (a.dbg & 8))
-    for (uint64_t off = b0; off < b1; off += 32768)
-      bulk_prefetch_l2(reinterpret_cast<const void*>(s0 + off), (uint32_t)min_u64(32768, b1 - off),
-                       pol_last);
     // ring geometry (tunable): NS slots of CH bytes, NS * CH <= kL2Region
     const uint32_t CH = a.ring_chunk ? a.ring_chunk : (32u << 10);
     const uint32_t NS = a.ring_slots ? a.ring_slots : 6;
@@ -173,6 +166,40 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
         }
       }
     }
+  } else if (REALIGN == 1 && a.rec >= 8 && a.rec <= 116 &&
+             (reinterpret_cast<uintptr_t>(a.dst) & 3) == 0) {
+    // the asynchronous window gather (dpg_internal.cuh): three groups of 32
+    // rows per warp in flight through cp.async, rids loaded four groups ahead
+    static_assert(3 * kAgTile * kL2Warps <= kL2Region, "window tiles exceed the region");
+    uint8_t* wtiles = ring + (size_t)warp * 3 * kAgTile;
+    const uint32_t wt_s = smem_u32(wtiles);
+    const uintptr_t src_u = reinterpret_cast<uintptr_t>(a.src);
+    AgMap amap;
+    ag_map_init(amap, a.rec, lane);
+    const uint32_t ng = (uint32_t)ngroups;
+    const uint32_t nt = ng > (uint32_t)warp ? (ng - warp + kL2Warps - 1) / kL2Warps : 0;
+    auto rid_load = [&](uint32_t t) -> uint32_t {
+      const uint64_t i = lo + 32 * (uint64_t)(warp + t * kL2Warps) + lane;
+      return (t < nt && i < hi) ? ldg_first(a.rids + i) : 0xFFFFFFFFu;
+    };
+    uint32_t rq0 = rid_load(0), rq1 = rid_load(1), rq2 = rid_load(2), rq3 = rid_load(3);
+    ag_pipeline(nt, [&](uint32_t t) -> AgGroup {
+      const uint32_t r = rq0;
+      rq0 = rq1;
+      rq1 = rq2;
+      rq2 = rq3;
+      rq3 = rid_load(t + 4);
+      AgGroup q;
+      const uint64_t g0 = lo + 32 * (uint64_t)(warp + t * kL2Warps);
+      q.cnt = (uint32_t)min_u64(32, hi - g0);
+      q.on = r < a.n_src;
+      if ((uint32_t)lane < q.cnt && !q.on) report_bad(a.status, g0 + lane);
+      q.addr = q.on ? src_u + (uint64_t)r * a.rec : src_u;
+      q.okm = __ballot_sync(0xffffffffu, q.on);
+      q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
+      q.o4 = (uint32_t)(q.addr >> 2) & 3;
+      return q;
+    }, wtiles, wt_s, kAgTile, amap, a.rec, lane);
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)
