@@ -463,7 +463,12 @@ def main():
                         torch.cuda.get_device_properties(dev).multi_processor_count)
     src_rec = w["dim"].shape[1] if cfg == "c4" else rec
     pay = 0
-    if plan["path"] == 3:
+    if plan["path"] == 5:
+        # K staged L2 runs probed into INTERNAL + the Phase III gather: the
+        # L2-run kernel launches between the distribute and the end of the call
+        kernel = "k_dpg_l2run (K runs + Phase III)"
+        pg_bytes = alg_bytes
+    elif plan["path"] == 3:
         # one run (the whole source) staged in L2, probed in rid order: one
         # kernel for the whole path, N * (2 * rec + rid_bytes)
         kernel = "k_dpg_l2run"

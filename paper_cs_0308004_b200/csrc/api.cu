@@ -298,6 +298,50 @@ bool plan_l2pair(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, boo
   return true;
 }
 
+// Record sizes for which the K-run L2 plan is the automatic choice over the
+// shared-memory runs for sources beyond the L2 (measured).
+bool l2k_auto(uint64_t rec) {
+  static int env = [] {
+    const char* e = getenv("DPG_L2K_AUTO");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return env != 0;
+  // measured on 16 M records (profiles/r01_sweep_c3_l2k.txt): slower than the
+  // shared-memory runs at every record size (K launches of stage + probe at
+  // ~36 G rows/s, then a full Phase III gather), so only on request
+  (void)rec;
+  return false;
+}
+
+// K L2 runs (l2k.cu): runs of L = 2^s records sized to one L2 run budget; the
+// source is larger than the single-run budget.  s may be forced (tests).
+bool plan_l2k(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool forced,
+              uint32_t force_s, int sm, uint64_t l2_bytes, dpg_plan_t* p) {
+  if (pay || n_out == 0 || n_src < 2) return false;
+  if (!forced && n_src * rec <= l2_budget(l2_bytes)) return false;
+  const uint64_t B1 = l2_run_budget(l2_bytes);
+  uint32_t s = 0;
+  if (force_s) {
+    s = force_s;
+  } else {
+    while ((2ull << s) * rec <= B1 && (2ull << s) < n_src) ++s;
+  }
+  const uint64_t K = (n_src + (1ull << s) - 1) >> s;
+  if (K < 2 || K > 512) return false;
+  if (n_out >= (1ull << 32) - 1) return false;
+  std::memset(p, 0, sizeof(*p));
+  p->path = 5;
+  p->log2_run = s;
+  p->run_len = 1ull << s;
+  p->num_runs = K;
+  p->word_bytes = pow2_divisor(rec);
+  p->grid_probe = (uint32_t)sm;
+  p->grid_distribute = (uint32_t)sm;
+  p->tile = (uint32_t)std::min<uint64_t>(UINT32_MAX, align_up((n_out + sm - 1) / sm, 32));
+  p->smem_bytes = l2k_smem_bytes((uint32_t)K);
+  return true;
+}
+
 bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool forced, int sm,
                 uint64_t l2_bytes, dpg_plan_t* p) {
   if (pay || n_out == 0) return false;
@@ -338,6 +382,12 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
     if (plan_l2run(rec, n_src, n_out, pay, want_path == 3, sm, current_l2_bytes(), p))
       return DPG_OK;
     if (want_path == 3) return DPG_ERR_UNSUPPORTED;
+  }
+  if (want_path == 5 || (want_path == 0 && !overrides && l2k_auto(rec))) {
+    if (plan_l2k(rec, n_src, n_out, pay, want_path == 5, opt ? opt->log2_run : 0, sm,
+                 current_l2_bytes(), p))
+      return DPG_OK;
+    if (want_path == 5) return DPG_ERR_UNSUPPORTED;
   }
   if (want_path != 2 && !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
       plan_fused(rec, n_src, n_out, pay, opt, sm, p))
@@ -530,6 +580,81 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
 
+  if (p.path == 5) {
+    const uint32_t G = p.grid_probe, K = (uint32_t)p.num_runs;
+    const uint64_t L = p.run_len;
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* ws = nullptr;
+    const uint64_t off_counts = 0;
+    const uint64_t off_rs = align_up(off_counts + (uint64_t)K * G * 4, 256);
+    const uint64_t off_local = align_up(off_rs + (K + 1) * 4, 256);
+    const uint64_t off_inv = align_up(off_local + n_out * 4 + 16, 256);
+    const uint64_t off_int = align_up(off_inv + n_out * 4 + 16, 256);
+    const uint64_t bytes = off_int + n_out * rec + 64;
+    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+    if (wst != DPG_OK) return wst;
+    uint8_t* wb = (uint8_t*)ws;
+    L2KArgs d;
+    std::memset(&d, 0, sizeof(d));
+    d.rids = rids;
+    d.n_out = n_out;
+    d.n_src = n_src;
+    d.s = p.log2_run;
+    d.K = K;
+    d.chunk = p.tile;
+    d.counts = (uint32_t*)(wb + off_counts);
+    d.run_start = (uint32_t*)(wb + off_rs);
+    d.local = (uint32_t*)(wb + off_local);
+    d.inv = (uint32_t*)(wb + off_inv);
+    d.gbar = gbar + 16;
+    d.status = status;
+    uint8_t* internal = wb + off_int;
+    uint32_t nl = 0;
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    cudaError_t e = launch_l2k_distribute(d, G, st, &nl);
+    if (timed) cudaEventRecord(pe.e1, st);
+    for (uint32_t b = 0; b < K && e == cudaSuccess; ++b) {
+      // Phase II of run b: stage it into L2, probe its RID_RUN into INTERNAL
+      L2RunArgs l;
+      std::memset(&l, 0, sizeof(l));
+      l.src = (const uint8_t*)src + (uint64_t)b * L * rec;
+      l.n_src = std::min<uint64_t>(L, n_src - (uint64_t)b * L);
+      l.rec = (uint32_t)rec;
+      l.rids = d.local;
+      l.n_out = n_out;                       // replaced on the device by the run's range
+      l.chunk = p.tile;
+      l.dev_range = d.run_start + b;
+      l.dst = internal;
+      l.gbar = gbar;
+      l.stage = 1;
+      l.dbg = g_debug_flags & ~4u;
+      l.ts = nullptr;
+      if (rec % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec / 4 - 1) / (rec / 4));
+      const uint32_t W = pow2_divisor(rec | (uintptr_t)l.src | (uintptr_t)internal);
+      e = launch_l2run(l, W, G, st, &nl);
+    }
+    if (e == cudaSuccess) {
+      // Phase III: dst[i] = INTERNAL[inv[i]] in output order
+      L2RunArgs l;
+      std::memset(&l, 0, sizeof(l));
+      l.src = internal;
+      l.n_src = n_out;
+      l.rec = (uint32_t)rec;
+      l.rids = d.inv;
+      l.n_out = n_out;
+      l.chunk = p.tile;
+      l.dst = (uint8_t*)dst;
+      l.gbar = gbar;
+      l.stage = 0;
+      if (rec % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec / 4 - 1) / (rec / 4));
+      const uint32_t W = pow2_divisor(rec | (uintptr_t)internal | (uintptr_t)dst);
+      e = launch_l2run(l, W, G, st, &nl);
+    }
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_launches = nl;
+    return cuda_status(e);
+  }
   if (p.path == 4 && ((uintptr_t)src % 16 || (uintptr_t)dst % 16)) {
     // the two-run kernels move 16-byte words: unaligned buffers take one run
     dpg_options_t o = opt ? *opt : dpg_options_t{};

@@ -248,6 +248,7 @@ struct L2RunArgs {
   uint32_t ring_chunk;   // Phase II bulk-copy bytes per slot (0: 32 KB)
   uint32_t ring_slots;   // Phase II ring slots (0: 6)
   uint64_t persist_bytes;  // host side: bytes of src under a persisting L2 access window (0: none)
+  const uint32_t* dev_range;  // optional [2] on the device: rows [r0, r1) (rids, dst offset by r0)
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
                          // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first
@@ -269,6 +270,22 @@ struct L2PairArgs {
   unsigned long long* status;
   unsigned long long* ts;
   uint32_t dbg;          // tuning flags: bit0 skip Phase I (timing only), bit1 no grid barrier
+};
+
+// Phase I of the K-run L2 plan (l2k.cu).
+struct L2KArgs {
+  const uint32_t* rids;
+  uint64_t n_out;
+  uint64_t n_src;
+  uint32_t s;            // log2 of the run length L (records)
+  uint32_t K;            // runs
+  uint64_t chunk;        // output rows per CTA (multiple of 32; the gather's geometry)
+  uint32_t* counts;      // [K * grid] rows per (run, CTA)
+  uint32_t* run_start;   // [K + 1] first slot of each run; [K] = valid rows
+  uint32_t* local;       // [n_out] r - b*L, run-major
+  uint32_t* inv;         // [n_out] slot of output row i (0xFFFFFFFF: bad rid)
+  uint32_t* gbar;        // monotonic grid barrier words (w[0], w[32])
+  unsigned long long* status;
 };
 
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
@@ -409,6 +426,8 @@ cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStre
                          uint32_t* nlaunch);
 uint32_t l2run_smem_bytes(uint64_t chunk_rids);
 cudaError_t launch_l2pair(const L2PairArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nlaunch);
+cudaError_t launch_l2k_distribute(const L2KArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nlaunch);
+uint32_t l2k_smem_bytes(uint32_t K);
 uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,

@@ -51,7 +51,17 @@ static_assert(128 >= 8 * kL2Slots, "barrier area");
 //            output rows) leaves by one TMA bulk store.
 // REALIGN 2: as 1 with byte granularity (rec or src not 4-byte aligned).
 template <int W, int REALIGN>
-__global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a) {
+__global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
+  L2RunArgs a = a0;
+  if (a.dev_range) {
+    // the rows [range[0], range[1]) of rids/dst, known on the device only (the
+    // run of a K-run plan, l2k.cu): rids and dst are offset by range[0]
+    const uint32_t r0 = __ldg(a.dev_range), r1 = __ldg(a.dev_range + 1);
+    a.rids += r0;
+    a.dst += (uint64_t)r0 * a.rec;
+    a.n_out = r1 - r0;
+    a.chunk = ((a.n_out + gridDim.x - 1) / gridDim.x + 31) & ~uint64_t(31);
+  }
   using T = typename Word<W>::T;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [kL2Slots] + rid barrier

@@ -123,7 +123,7 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
 
 
 @pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
-@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0), (4, 0)])
+@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0), (4, 0), (5, 0)])
 def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path, gather):
     """Every execution path on the same cases: the fused cooperative kernel
     writing rows straight to dst (gather 1) or through INTERNAL (gather 2),
@@ -215,6 +215,31 @@ def test_l2pair_invalid_and_unaligned(dpg):
     o = host(big)
     assert np.all(o[:4] == 0xEE) and np.all(o[4 + 33333 * 100:] == 0xEE)
     assert np.array_equal(o[4:4 + 33333 * 100].reshape(33333, 100), oracle.retrieve(src, good))
+
+
+@pytest.mark.parametrize("rec", [4, 8, 12, 36, 100, 128, 3, 256])
+@pytest.mark.parametrize("log2_run", [6, 11])
+def test_l2k_many_runs(dpg, rec, log2_run):
+    """The K-run L2 plan (path 5): Phase I distribute into K runs, K staged
+    probes into INTERNAL, Phase III gather; duplicates, ragged chunks, bad rids."""
+    n_src = 20000 + rec
+    n_out = 31111
+    src, rids = _case(rec * 5 + log2_run, n_src, rec, n_out, "repl")
+    bad = [0, 17, 4096, n_out - 1]
+    for b in bad:
+        rids[b] = n_src + b
+    p = dpg.dpg_plan(rec, n_src, n_out, path=5, log2_run=log2_run)
+    assert p["path"] == 5 and p["num_runs"] == (n_src + (1 << log2_run) - 1) >> log2_run
+    d = torch.zeros((n_out, rec), dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=d, path=5, log2_run=log2_run)
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 0
+    out = host(d)
+    ok = np.ones(n_out, bool)
+    ok[bad] = False
+    assert np.array_equal(out[ok], src[rids[ok].astype(np.int64)])
+    assert np.all(out[~ok] == 0)
 
 
 def test_l2run_invalid_rids_leave_rows_unwritten(dpg):
