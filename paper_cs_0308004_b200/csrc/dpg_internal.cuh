@@ -611,4 +611,3 @@ __device__ __forceinline__ void ag_pipeline(uint32_t nt, F group, uint8_t* wtile
   cp_async_wait<0>();
 }
 }  // namespace dpg
-

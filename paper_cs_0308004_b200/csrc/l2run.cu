@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       return (t < nt && i < hi) ? ldg_first(a.rids + i) : 0xFFFFFFFFu;
     };
     uint32_t rq0 = rid_load(0), rq1 = rid_load(1), rq2 = rid_load(2), rq3 = rid_load(3);
-    ag_pipeline(nt, [&](uint32_t t) -> AgGroup {
+    auto grp = [&](uint32_t t) -> AgGroup {
       const uint32_t r = rq0;
       rq0 = rq1;
       rq1 = rq2;
@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
       q.o4 = (uint32_t)(q.addr >> 2) & 3;
       return q;
-    }, wtiles, wt_s, kAgTile, amap, a.rec, lane);
+    };
+    ag_pipeline(nt, grp, wtiles, wt_s, kAgTile, amap, a.rec, lane);
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)
