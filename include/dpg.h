@@ -82,7 +82,13 @@ typedef struct {
                                3 = one L2-resident run (l2run.cu): the source
                                    fits the L2 budget, K = 1; Phase II loads it
                                    into L2, Phase III probes it in rid order
-                                   writing dst sequentially                    */
+                                   writing dst sequentially
+                               4 = two L2 runs (l2pair.cu): Phase I compaction,
+                                   run 0 probed into INTERNAL, run 1 fused with
+                                   Phase III (one cooperative kernel)
+                               5 = K L2 runs (l2k.cu): Phase I distribute
+                                   kernel, K staged probes into INTERNAL,
+                                   Phase III gather                            */
     uint32_t nstages;       /* shared-memory stages of the probe-gather pipeline */
     uint32_t stage_bytes;   /* bytes per stage                                  */
     uint32_t gather;        /* 1 = probe writes rows straight to dst (rows are
@@ -103,7 +109,10 @@ typedef struct {
     uint32_t pair_bytes;    /* force 8-byte pairs                               */
     uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
     uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel,
-                               3 force the L2-run kernel (any source size)      */
+                               3 force the L2-run kernel (any source size),
+                               4 two L2 runs (rec % 4 == 0, 8..116 bytes),
+                               5 K L2 runs (log2_run, if set, fixes the run
+                                 length)                                        */
     uint32_t gather;        /* 0 auto, 1 force direct-to-dst, 2 force INTERNAL  */
     uint32_t reserved;
 } dpg_options_t;

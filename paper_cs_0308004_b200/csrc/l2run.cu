@@ -93,6 +93,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
     const uint64_t slice = ((total + G - 1) / G + 15) & ~uint64_t(15);
     const uint64_t b0 = min_u64(total, (uint64_t)c * slice), b1 = min_u64(total, b0 + slice);
     // ring geometry (tunable): NS slots of CH bytes, NS * CH <= kL2Region
+    // (evict_normal or a 0.5 evict_last fraction kept less of the run:
+    // profiles/r01_l2_stage_policy.txt)
+    const uint64_t pol_stage = pol_last;
     const uint32_t CH = a.ring_chunk ? a.ring_chunk : (32u << 10);
     const uint32_t NS = a.ring_slots ? a.ring_slots : 6;
     uint32_t j = 0;
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       const uint32_t bytes = (uint32_t)min_u64(CH, b1 - off);
       mbar_arrive_expect_tx(&bar[slot], bytes);
       bulk_g2s(ring + (size_t)slot * CH, reinterpret_cast<const void*>(s0 + off), bytes,
-               &bar[slot], pol_last);
+               &bar[slot], pol_stage);
     }
     // drain: the last min(j, NS) copies
     for (uint32_t q = (j > NS ? j - NS : 0); q < j; ++q)
