@@ -97,6 +97,16 @@ __device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t G) {
   __syncthreads();
 }
 
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+// Named barrier over n threads (a multiple of 32) of the CTA.
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // Grid barrier with one poller: every CTA adds 1 to a monotonic arrival
 // count (red.release, no return); CTA 0 waits for the count of this epoch and
 // publishes the next epoch; the others wait for the epoch word (a different
@@ -247,7 +257,6 @@ struct L2RunArgs {
   uint32_t stage;        // 1: Phase II stages the source into L2 (then a grid barrier)
   uint32_t ring_chunk;   // Phase II bulk-copy bytes per slot (0: 32 KB)
   uint32_t ring_slots;   // Phase II ring slots (0: 6)
-  uint64_t persist_bytes;  // host side: bytes of src under a persisting L2 access window (0: none)
   const uint32_t* dev_range;  // optional [2] on the device: rows [r0, r1) (rids, dst offset by r0)
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,

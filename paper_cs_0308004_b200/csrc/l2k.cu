@@ -29,12 +29,6 @@ namespace dpg {
 static constexpr int kKThreads = 512;
 static constexpr int kKWarps = kKThreads / 32;
 
-__device__ __forceinline__ uint32_t lanemask_lt_k() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* wrun = sm;                                  // [kKWarps][K] counts, then cursors
@@ -66,7 +60,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (i < hi && !valid) report_bad(a.status, i);
       const uint32_t b = valid ? r[u] >> a.s : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, b);
-      if (valid && (peers & lanemask_lt_k()) == 0) my[b] += __popc(peers);
+      if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
     }
   }
   __syncthreads();
@@ -149,9 +143,9 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint32_t b = valid ? r[u] >> a.s : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, b);
       uint32_t slot = 0;
-      if (valid) slot = my[b] + __popc(peers & lanemask_lt_k());
+      if (valid) slot = my[b] + __popc(peers & lanemask_lt());
       __syncwarp();
-      if (valid && (peers & lanemask_lt_k()) == 0) my[b] += __popc(peers);
+      if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
       if (i < hi) {
         a.inv[i] = valid ? slot : 0xFFFFFFFFu;
         if (valid) a.local[slot] = r[u] & lmask;

@@ -47,15 +47,6 @@ static constexpr uint32_t kPSlots = 6;
 static constexpr uint32_t kPChunk = 32u << 10;
 static_assert(kPNB * kPTile * kPWarps <= kPRegion, "tiles exceed the region");
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 // One cooperative kernel for the whole path (two grid barriers).
 __global__ void __launch_bounds__(kPThreads, 1) k_dpg_l2pair(L2PairArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];

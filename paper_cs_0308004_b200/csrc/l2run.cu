@@ -382,21 +382,11 @@ static cudaError_t launch_l2_w(const L2RunArgs& a, uint32_t grid, uint32_t smem,
   cfg.blockDim = dim3(kL2Threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   int na = 0;
   at[na].id = cudaLaunchAttributeCooperative;   // the grid barrier ends Phase II
   at[na].val.cooperative = a.stage ? 1 : 0;
   ++na;
-  if (a.persist_bytes) {
-    // L2 set-aside for the staged run: the source window is marked persisting
-    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[na].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(a.src);
-    at[na].val.accessPolicyWindow.num_bytes = a.persist_bytes;
-    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    ++na;
-  }
   cfg.attrs = at;
   cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, fn, a);
