@@ -392,12 +392,45 @@ def test_fk_join_shapes(dpg, fb, rec):
 # --------------------------------------------------------------------------
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
 def test_configs_1_2_full(dpg, cfg):
+    """Configs 1 and 2 in full, every plan: the planner's (one L2 run), the
+    shared-memory runs (both gather modes), two L2 runs, K L2 runs, and both
+    direct retrievals."""
     w = datagen.make(cfg)
     want = oracle.retrieve(w["src"], w["rids"])
     s, r = dev(w["src"]), dev(w["rids"])
     assert np.array_equal(host(dpg.dpg_retrieve(s, r)), want)
+    for opts in ({"path": 1, "gather": 1}, {"path": 1, "gather": 2}, {"path": 2}, {"path": 4},
+                 {"path": 5, "log2_run": 14}):
+        assert np.array_equal(host(dpg.dpg_retrieve(s, r, **opts)), want), opts
     assert np.array_equal(host(dpg.dpg_retrieve_direct(s, r)), want)
+    assert np.array_equal(host(dpg.dpg_retrieve_direct_ex(s, r, hint=3)), want)
     dpg.dpg_sync_status()
+
+
+@pytest.mark.parametrize("rec", [1, 3, 4, 12, 100, 128, 260])
+@pytest.mark.parametrize("soff,doff", [(0, 0), (4, 4), (1, 3)])
+def test_direct_windowed_shapes(dpg, rec, soff, doff):
+    """The direct retrieval on the window-gather kernel (hint 3): every lane
+    layout, unaligned pointers, canaries, bad rids left unwritten."""
+    n_src, n_out = 9000, 12345
+    src, rids = _case(rec + soff * 7 + doff, n_src, rec, n_out, "repl")
+    rids[[3, 4000]] = [n_src, 0xFFFFFFFF]
+    big_src = torch.zeros(n_src * rec + 64, dtype=torch.uint8, device="cuda")
+    big_src[soff:soff + n_src * rec] = dev(src.reshape(-1))
+    sv = big_src[soff:soff + n_src * rec].view(n_src, rec)
+    big_dst = torch.full((n_out * rec + 64,), 0x3C, dtype=torch.uint8, device="cuda")
+    d = big_dst[doff:doff + n_out * rec].view(n_out, rec)
+    dpg.dpg_retrieve_direct_ex(sv, dev(rids), dst=d, hint=3)
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 3
+    out = host(big_dst)
+    assert np.all(out[:doff] == 0x3C) and np.all(out[doff + n_out * rec:] == 0x3C)
+    body = out[doff:doff + n_out * rec].reshape(n_out, rec)
+    ok = np.ones(n_out, bool)
+    ok[[3, 4000]] = False
+    assert np.array_equal(body[ok], src[rids[ok].astype(np.int64)])
+    assert np.all(body[~ok] == 0x3C)
 
 
 def _sampled(n, k=200000, seed=0):
@@ -420,6 +453,11 @@ def test_config_3_full_size_sampled(dpg, variant, rec):
     del out
     out = dpg.dpg_retrieve_direct(s, r)
     assert np.array_equal(host(out[ti]), want)
+    del out
+    if rec in (32, 128):                     # K L2 runs at full size
+        out = dpg.dpg_retrieve(s, r, path=5)
+        assert np.array_equal(host(out[ti]), want)
+        del out
     dpg.dpg_sync_status()
 
 
