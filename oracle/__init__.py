@@ -12,6 +12,9 @@ Each wrapper cites the passage the C function follows:
 * :func:`dpg_fig1`    -- the three phases of Fig. 1, INTERNAL materialised
 * :func:`fk_join`     -- DPG-Move join rows ``fact[i] ++ dim[fk[i]]``
 * :func:`retrieve_at` -- the definition evaluated at sampled output positions
+* :func:`sort_rids`   -- phases 1-2 of three-phase key-pointer sorting:
+  the rids in stable key order
+* :func:`sort`        -- the whole three-phase sort: sort_rids then retrieve
 
 Errors (reading A6 in DESIGN.md): a rid >= n_src raises :class:`RidRangeError`
 carrying the smallest offending position.
@@ -56,8 +59,9 @@ def _load():
         lib.oracle_dpg_fig1.argtypes = [P, U, U, P, U, U, P, P, P, P, P, P]
         lib.oracle_fk_join.argtypes = [P, U, U, P, P, U, U, P, P]
         lib.oracle_retrieve_at.argtypes = [P, U, U, P, P, U, P]
+        lib.oracle_sort_rids.argtypes = [P, U, U, U, U, P]
         for f in (lib.oracle_retrieve, lib.oracle_retrieve_u64, lib.oracle_dpg_fig1,
-                  lib.oracle_fk_join, lib.oracle_retrieve_at):
+                  lib.oracle_fk_join, lib.oracle_retrieve_at, lib.oracle_sort_rids):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -146,3 +150,20 @@ def fk_join(fact: np.ndarray, fk: np.ndarray, dim: np.ndarray) -> np.ndarray:
     _check(_load().oracle_fk_join(_ptr(fact), fact_bytes, n_fact, _ptr(fk), _ptr(dim), rec,
                                   n_dim, _ptr(out), ctypes.byref(bad)), bad)
     return out
+
+
+def sort_rids(src: np.ndarray, key_off: int, key_bytes: int) -> np.ndarray:
+    """Phases 1-2 of three-phase sorting: the rids of the records
+    in stable order of their key (key_bytes unsigned bytes at key_off)."""
+    src = _records(src)
+    n, rec = src.shape
+    out = np.zeros(n, dtype=np.uint32)
+    if _load().oracle_sort_rids(_ptr(src), rec, n, key_off, key_bytes, _ptr(out)):
+        raise ValueError("invalid argument")
+    return out
+
+
+def sort(src: np.ndarray, key_off: int, key_bytes: int) -> np.ndarray:
+    """The three-phase key-pointer sort: sorted records."""
+    return retrieve(src, sort_rids(src, key_off, key_bytes))
+

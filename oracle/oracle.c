@@ -198,3 +198,52 @@ int oracle_retrieve_at(const uint8_t *src, uint64_t rec, uint64_t n_src,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ *
+ * (4) Three-phase key-pointer sorting (section 3): "extract the  *
+ *     key-pointer pairs, sort the pairs by key, then retrieve the records   *
+ *     in the sorted order" -- the last step is record retrieval (1).        *
+ *     Keys: key_bytes bytes at key_off inside each record, compared as      *
+ *     unsigned bytes, lexicographically (the Datamation key;     *
+ *     reading A10); the sort is stable, so equal keys keep ascending rids.  *
+ *     Phase 2 here is a plain bottom-up merge sort of the rids (stable by   *
+ *     construction).  out_rids[n] receives the sorted rid sequence.         *
+ * ------------------------------------------------------------------------ */
+static int key_less_eq(const uint8_t *src, uint64_t rec, uint64_t key_off, uint64_t key_bytes,
+                       uint32_t a, uint32_t b)
+{
+    /* a's key <= b's key */
+    return memcmp(src + (uint64_t)a * rec + key_off, src + (uint64_t)b * rec + key_off,
+                  key_bytes) <= 0;
+}
+
+int oracle_sort_rids(const uint8_t *src, uint64_t rec, uint64_t n, uint64_t key_off,
+                     uint64_t key_bytes, uint32_t *out_rids)
+{
+    if (rec == 0 || key_off + key_bytes > rec || n >= (1ull << 32)) return -1;
+    uint32_t *a = malloc((n ? n : 1) * sizeof(uint32_t));
+    uint32_t *b = malloc((n ? n : 1) * sizeof(uint32_t));
+    if (!a || !b) { free(a); free(b); return -1; }
+    /* Phase 1: the key-pointer pairs (the key stays in the record; the
+     * pointer is the rid, i.e. the record's position). */
+    for (uint64_t i = 0; i < n; ++i) a[i] = (uint32_t)i;
+    /* Phase 2: stable merge sort of the pointers by key. */
+    for (uint64_t w = 1; w < n; w *= 2) {
+        for (uint64_t lo = 0; lo < n; lo += 2 * w) {
+            uint64_t mid = lo + w < n ? lo + w : n;
+            uint64_t hi = lo + 2 * w < n ? lo + 2 * w : n;
+            uint64_t i = lo, j = mid, k = lo;
+            while (i < mid && j < hi) {
+                /* left element first when keys are equal: stability */
+                if (key_less_eq(src, rec, key_off, key_bytes, a[i], a[j])) b[k++] = a[i++];
+                else b[k++] = a[j++];
+            }
+            while (i < mid) b[k++] = a[i++];
+            while (j < hi) b[k++] = a[j++];
+        }
+        uint32_t *t = a; a = b; b = t;
+    }
+    memcpy(out_rids, a, n * sizeof(uint32_t));
+    free(a); free(b);
+    return 0;
+}

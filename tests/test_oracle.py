@@ -249,3 +249,45 @@ def test_generators():
     assert np.array_equal(np.sort(f), np.arange(1000, dtype=np.uint64))
     f2 = datagen.feistel(1000, 300, 50, 11)
     assert np.array_equal(f2, f[300:350])
+
+
+# --------------------------------------------------------------------------
+# Three-phase key-pointer sorting (section 3): the sort oracle.
+# --------------------------------------------------------------------------
+def test_sort_oracle_brute_force_tiny():
+    """Every tiny input against Python's sorted() on (key bytes, rid) -- an
+    independent stable ordering -- with alphabets small enough to force ties."""
+    rng = np.random.default_rng(5)
+    for n in range(0, 8):
+        for trial in range(40):
+            rec = int(rng.integers(1, 6))
+            key_off = int(rng.integers(0, rec))
+            key_bytes = int(rng.integers(1, rec - key_off + 1))
+            src = rng.integers(0, 3, (n, rec), dtype=np.uint8)
+            want = sorted(range(n), key=lambda i: (bytes(src[i, key_off:key_off + key_bytes]), i))
+            got = oracle.sort_rids(src, key_off, key_bytes)
+            assert got.tolist() == want
+            assert np.array_equal(oracle.sort(src, key_off, key_bytes),
+                                  src[np.array(want, dtype=np.int64)] if n else src[:0])
+
+
+def test_sort_oracle_against_lexsort_and_invariants():
+    rng = np.random.default_rng(6)
+    for n, rec, off, kb, alpha in [(5000, 100, 0, 10, 256), (3000, 24, 7, 9, 4), (4096, 16, 2, 3, 2)]:
+        src = rng.integers(0, alpha, (n, rec), dtype=np.uint8)
+        got = oracle.sort_rids(src, off, kb)
+        # library routine: numpy's stable lexsort (last key = primary)
+        cols = [src[:, off + j] for j in reversed(range(kb))]
+        assert np.array_equal(got, np.lexsort(cols).astype(np.uint32))
+        # invariants: a permutation, keys non-decreasing, ties by ascending rid
+        assert np.array_equal(np.sort(got), np.arange(n, dtype=np.uint32))
+        keys = [bytes(src[r, off:off + kb]) for r in got]
+        for a, b, ra, rb in zip(keys, keys[1:], got, got[1:]):
+            assert a < b or (a == b and ra < rb)
+
+
+def test_sort_oracle_matches_datamation_generator():
+    """Config 2's rids (the generator's own stable argsort of the 10-byte keys)
+    are the oracle's sorted rids."""
+    w = datagen.make("c2", scale=16)
+    assert np.array_equal(oracle.sort_rids(w["src"], 0, 10), w["rids"])
