@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--rec", type=int, default=None, help="record bytes for c3a/c3b")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sort", action="store_true", help="skip the end-to-end DPG sort timing (c2)")
     a = ap.parse_args()
     if a.config is None:
         a.config = "c5" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "c2"
@@ -455,6 +456,24 @@ def main():
         windowed_res = {"value": alg_bytes / (wt * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": wt,
                         "kernel": "k_dpg_l2run (stage=0)", "launches_per_step": wl / args.steps}
 
+    # the paper's application of the path (section 3): the whole Datamation
+    # sort on the GPU -- key extraction + stable radix sort of the key-pointer
+    # pairs (phases 1-2) + DPG retrieval (phase 3), timed the same way
+    sort_res = None
+    if cfg == "c2" and not args.no_sort:
+        srids = torch.empty(n_out, dtype=torch.int32, device=dev)
+        for _ in range(2):
+            dpg.dpg_sort(src, 0, 10, dst=out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out[:1000].cpu().numpy(), w["src"][w["rids"][:1000].astype(np.int64)])
+        sms, sl, _ = timed(lambda: dpg.dpg_sort(src, 0, 10, dst=out), args.steps)
+        rms, _, _ = timed(lambda: dpg.dpg_sort_rids(src, 0, 10, rids=srids), args.steps)
+        st_ = sum(sms) / len(sms)
+        sort_res = {"records_per_s": n_out / (st_ * 1e-3), "ms_per_sort": st_,
+                    "ms_phases_1_2": sum(rms) / len(rms), "ms_phase_3": ms_per_step,
+                    "launches_per_sort": sl / args.steps,
+                    "what": "dpg_sort: 10-byte keys at offset 0, stable LSD radix sort "
+                            "(10 passes) + dpg_retrieve"}
     peak, peak_src = hbm_peak()
     dist_ms, probe_ms, calls = ph
     pg_ms = probe_ms / max(1, calls)
@@ -539,6 +558,7 @@ def main():
             "frac_of_hbm_peak": value / world / peak,
             "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
             "roofline": roofline, "naive": naive_res, "direct_windowed": windowed_res,
+            "dpg_sort": sort_res,
             "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(), "gpu_launches": launches,
             "gpu": torch.cuda.get_device_name(dev),

@@ -215,6 +215,23 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* Three-phase key-pointer sorting with DPG as the record-copy phase
+ * (section 3; DPG sort).  Keys: key_bytes
+ * (1..12) unsigned bytes at key_off inside each record, compared
+ * lexicographically (the Datamation key: 10 bytes at offset 0);
+ * the sort is stable (equal keys keep ascending rid, reading A10).
+ * dpg_sort_rids: phases 1-2 only -- rids_out[n] (device) receives the rids in
+ *   sorted order (key extraction + a stable LSD radix sort, one key byte per
+ *   pass).  rids_out must not overlap src.
+ * dpg_sort: phases 1-3 -- dst[n*rec] (device, not overlapping src) receives
+ *   the records in sorted order (phase 3 = dpg_retrieve).
+ * Errors: DPG_ERR_INVALID_ARG for a bad key range, NULL pointers with n > 0
+ * or overlap; DPG_ERR_UNSUPPORTED for n >= 2^32.  Asynchronous on `stream`. */
+dpg_status_t dpg_sort_rids(const void *src, size_t rec_bytes, uint64_t n, size_t key_off,
+                           size_t key_bytes, uint32_t *rids_out, dpg_stream_t stream);
+dpg_status_t dpg_sort(const void *src, size_t rec_bytes, uint64_t n, size_t key_off,
+                      size_t key_bytes, void *dst, dpg_stream_t stream);
+
 dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t *first_bad_index);
 
 const char *dpg_status_string(dpg_status_t status);

@@ -9,6 +9,7 @@ been built (``python -m paper_cs_0308004_b200.build``).
 Functions carry the C ABI's names:
 
 * :func:`dpg_retrieve`        ``dst[i] = src[rids[i]]`` by distribute-probe-gather (Fig. 1)
+* :func:`dpg_sort`            three-phase key-pointer sort with DPG as phase 3
 * :func:`dpg_retrieve_direct` the standard direct retrieval, the measured comparison
 * :func:`dpg_fk_join`         DPG-Move join rows ``fact[i] ++ dim[fk[i]]``
 * :func:`dpg_distribute`      Phase I alone, for tests
@@ -89,6 +90,8 @@ _sigs = {
     "dpg_l2_prefetch": [_P, _U, _P],
     "dpg_partition": [_P, ctypes.c_uint32, _U, _U, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _P,
                       _P],
+    "dpg_sort_rids": [_P, _S, _U, _S, _S, _P, _P],
+    "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -315,6 +318,32 @@ def dpg_retrieve_host(src, rids, dst, stream=None):
     n_src, rec = src.shape
     _check(_lib.dpg_retrieve_host(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
                                   dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_host")
+    return dst
+
+
+def dpg_sort_rids(src, key_off: int, key_bytes: int, rids=None, stream=None):
+    """Phases 1-2 of three-phase sorting: the rids of src's
+    records in stable order of their key (key_bytes bytes at key_off)."""
+    torch = _torch()
+    src = _records(src, "src")
+    n, rec = src.shape
+    if rids is None:
+        rids = torch.empty(n, dtype=torch.int32, device=src.device)
+    _check(_lib.dpg_sort_rids(src.data_ptr(), rec, n, key_off, key_bytes, rids.data_ptr(),
+                              _stream_ptr(stream)), "dpg_sort_rids")
+    return rids
+
+
+def dpg_sort(src, key_off: int, key_bytes: int, dst=None, stream=None):
+    """The DPG sort: src's records sorted by key, with
+    DPG record retrieval as the record-copy phase."""
+    torch = _torch()
+    src = _records(src, "src")
+    n, rec = src.shape
+    if dst is None:
+        dst = torch.empty((n, rec), dtype=torch.uint8, device=src.device)
+    _check(_lib.dpg_sort(src.data_ptr(), rec, n, key_off, key_bytes, dst.data_ptr(),
+                         _stream_ptr(stream)), "dpg_sort")
     return dst
 
 

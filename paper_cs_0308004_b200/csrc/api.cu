@@ -1175,6 +1175,60 @@ dpg_status_t dpg_scatter_rows(const void* rows, size_t rec_bytes, const uint32_t
   return cuda_status(e);
 }
 
+dpg_status_t dpg_sort_rids(const void* src, size_t rec_bytes, uint64_t n, size_t key_off,
+                           size_t key_bytes, uint32_t* rids_out, dpg_stream_t stream) {
+  // Phases 1-2 of three-phase sorting: stable rid order by key.
+  t_launches = 0;
+  if (rec_bytes == 0 || key_bytes == 0 || key_bytes > 12 || key_off + key_bytes > rec_bytes)
+    return DPG_ERR_INVALID_ARG;
+  if (n == 0) return DPG_OK;
+  if (!src || !rids_out) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32) || rec_bytes > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  uint64_t src_bytes;
+  if (__builtin_mul_overflow(n, (uint64_t)rec_bytes, &src_bytes)) return DPG_ERR_INVALID_ARG;
+  if (overlaps(rids_out, n * 4, src, src_bytes)) return DPG_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = current_sm_count();
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  dpg_status_t w = persist_ws(st, 1, sort_ws_bytes(n, sm), &gbar, &total, &ws);
+  if (w != DPG_OK) return w;
+  uint32_t nl = 0;
+  cudaError_t e = launch_sort_rids((const uint8_t*)src, (uint32_t)rec_bytes, n, (uint32_t)key_off,
+                                   (uint32_t)key_bytes, (uint8_t*)ws, rids_out, gbar + 16, sm, st,
+                                   &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_sort(const void* src, size_t rec_bytes, uint64_t n, size_t key_off,
+                      size_t key_bytes, void* dst, dpg_stream_t stream) {
+  // The whole three-phase sort: phases 1-2 (dpg_sort_rids), then phase 3 =
+  // DPG record retrieval of the records in sorted rid order.
+  t_launches = 0;
+  if (n == 0) return (rec_bytes && key_bytes && key_off + key_bytes <= rec_bytes) ? DPG_OK
+                                                                                 : DPG_ERR_INVALID_ARG;
+  if (!dst) return DPG_ERR_INVALID_ARG;
+  uint64_t bytes;
+  if (__builtin_mul_overflow(n, (uint64_t)rec_bytes, &bytes)) return DPG_ERR_INVALID_ARG;
+  if (overlaps(dst, bytes, src, bytes)) return DPG_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* rids = nullptr;
+  if (cudaMallocAsync(&rids, n * 4 + 64, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  dpg_status_t s = dpg_sort_rids(src, rec_bytes, n, key_off, key_bytes, (uint32_t*)rids, stream);
+  uint32_t nl = t_launches;
+  if (s == DPG_OK) {
+    s = run_dpg(src, rec_bytes, n, (const uint32_t*)rids, n, nullptr, 0, dst, st, nullptr);
+    nl += t_launches;
+  }
+  cudaFreeAsync(rids, st);
+  t_launches = nl;
+  return s;
+}
+
 dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_status(e);

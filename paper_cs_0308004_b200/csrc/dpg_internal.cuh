@@ -437,6 +437,10 @@ uint32_t l2run_smem_bytes(uint64_t chunk_rids);
 cudaError_t launch_l2pair(const L2PairArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_l2k_distribute(const L2KArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nlaunch);
 uint32_t l2k_smem_bytes(uint32_t K);
+cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
+                             uint32_t key_bytes, uint8_t* ws, uint32_t* rids_out, uint32_t* gbar,
+                             int sm, cudaStream_t st, uint32_t* nlaunch);
+uint64_t sort_ws_bytes(uint64_t n, int sm);
 uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,

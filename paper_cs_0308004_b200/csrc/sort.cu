@@ -1,0 +1,291 @@
+// sort.cu -- three-phase key-pointer sorting with DPG as phase 3 (section 3,
+// P:481-490; "DPG acts as an accelerator for ... main memory sorting
+// algorithms"; the Datamation shape).
+//
+//   phase 1  k_sort_extract: the key-pointer pairs -- each record's key
+//            (key_bytes <= 12 unsigned bytes at key_off) as a big-endian
+//            (hi: bytes 0..7, lo: bytes 8..11) pair and its rid.
+//   phase 2  k_sort_pass x key_bytes: a stable LSD radix sort, one byte of the
+//            key per pass from the last to the first (a counting sort per
+//            byte: "count the number of elements destined for each bucket,
+//            set bucket boundaries, distribute").  One cooperative
+//            kernel per pass: per-CTA digit counts, a grid barrier, every CTA
+//            derives its bucket bases, then the CTA's chunk is distributed
+//            in order, 512 elements (one row) at a time: a rank inside the
+//            warp (match_any), the warps' counts before it, the CTA's
+//            running count of the digit -- so equal digits keep their order
+//            (stable), which makes the LSD sort correct.
+//   phase 3  dpg_retrieve of the records in the sorted rid order (api.cu).
+#include "dpg_internal.cuh"
+
+namespace dpg {
+
+static constexpr int kSThreads = 512;
+static constexpr int kSWarps = kSThreads / 32;
+
+__global__ void k_sort_extract(const uint8_t* __restrict__ src, uint32_t rec, uint64_t n,
+                               uint32_t key_off, uint32_t key_bytes, uint64_t* __restrict__ khi,
+                               uint32_t* __restrict__ klo, uint32_t* __restrict__ rid) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t* k = src + i * rec + key_off;
+    uint64_t hi = 0;
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t b = 0; b < 8; ++b) hi = (hi << 8) | (b < key_bytes ? k[b] : 0u);
+#pragma unroll
+    for (uint32_t b = 8; b < 12; ++b) lo = (lo << 8) | (b < key_bytes ? k[b] : 0u);
+    khi[i] = hi;
+    if (key_bytes > 8) klo[i] = lo;
+    rid[i] = (uint32_t)i;
+  }
+}
+
+struct SortPassArgs {
+  const uint64_t* khi_in;
+  const uint32_t* klo_in;
+  const uint32_t* rid_in;
+  uint64_t* khi_out;
+  uint32_t* klo_out;
+  uint32_t* rid_out;
+  uint64_t n;
+  uint64_t chunk;        // elements per CTA (multiple of kSThreads)
+  uint32_t byte;         // key byte of this pass (0 = most significant)
+  uint32_t with_lo;      // key_bytes > 8: carry the low word
+  uint32_t* counts;      // [256 * grid]
+  uint32_t* gbar;        // monotonic grid barrier words
+  uint32_t cache;        // 1: the CTA's chunk is kept in shared memory between the passes
+};
+
+__device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, uint32_t byte) {
+  return byte < 8 ? (uint32_t)(hi >> (8 * (7 - byte))) & 255u : (lo >> (8 * (11 - byte))) & 255u;
+}
+
+__global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
+  // with a.cache: [chunk] khi, [chunk] klo, [chunk] rid of the chunk in bucket
+  // order (staged, then written out as one contiguous run per bucket)
+  extern __shared__ __align__(16) uint8_t sdyn[];
+  __shared__ uint32_t hist[256];       // CTA counts
+  __shared__ uint32_t gbase[256];      // first global slot of this CTA's block of digit d
+  __shared__ uint32_t lbase[256];      // first staged slot of digit d (exclusive scan of hist)
+  __shared__ uint32_t run[256];        // elements of digit d placed so far (this CTA)
+  __shared__ uint32_t wcnt[kSWarps][256];   // (row tag << 16 | count) per warp and digit
+  __shared__ uint32_t wsum[kSWarps], wsum2[kSWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t c = blockIdx.x, G = gridDim.x;
+  const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
+  const uint64_t hi = min_u64(a.n, lo + a.chunk);
+  for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
+  for (uint32_t k = tid; k < kSWarps * 256; k += kSThreads) (&wcnt[0][0])[k] = 0xFFFF0000u;
+  __syncthreads();
+  // ---- count ----
+  for (uint64_t i0 = lo + tid; i0 < hi; i0 += 4 * kSThreads) {
+    uint64_t kh[4];
+    uint32_t kl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = i0 + u * kSThreads;
+      kh[u] = 0; kl[u] = 0;
+      if (i < hi) {
+        kh[u] = __ldcg(a.khi_in + i);
+        if (a.with_lo) kl[u] = __ldcg(a.klo_in + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * kSThreads < hi) atomicAdd(&hist[digit_of(kh[u], kl[u], a.byte)], 1u);
+  }
+  __syncthreads();
+  for (uint32_t d = tid; d < 256; d += kSThreads) a.counts[c * 256 + d] = hist[d];
+  grid_barrier_mono(a.gbar, G);
+  // ---- bases: global (smaller digits, then earlier CTAs) and local; the
+  // CTA rows of counts are read coalesced, 8 independent loads in flight ----
+  if (tid < 256) {
+    uint32_t tot = 0, pre = 0;
+    uint32_t q = 0;
+    for (; q + 8 <= G; q += 8) {
+      uint32_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(a.counts + (q + u) * 256 + tid);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        tot += x[u];
+        if (q + u < c) pre += x[u];
+      }
+    }
+    for (; q < G; ++q) {
+      const uint32_t x = __ldcg(a.counts + q * 256 + tid);
+      tot += x;
+      if (q < c) pre += x;
+    }
+    const uint32_t mine = hist[tid];
+    uint32_t y = tot, z = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
+      const uint32_t t2 = __shfl_up_sync(0xffffffffu, z, d);
+      if (lane >= d) { y += t; z += t2; }
+    }
+    if (lane == 31) { wsum[warp] = y; wsum2[warp] = z; }
+    gbase[tid] = y - tot + pre;
+    lbase[tid] = z - mine;
+  }
+  __syncthreads();
+  if (tid < 256) {
+    uint32_t off = 0, off2 = 0;
+    for (int w = 0; w < warp; ++w) { off += wsum[w]; off2 += wsum2[w]; }
+    gbase[tid] += off;
+    lbase[tid] += off2;
+  }
+  __syncthreads();
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);
+  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * a.chunk);
+  uint32_t* sr = sl + a.chunk;
+  // ---- distribute, 512 elements per row, rows in order (stable) ----
+  uint32_t tag = 0;
+  // the next two rows' elements are loaded while a row is distributed
+  auto load_row = [&](uint64_t r0, uint64_t& kh, uint32_t& kl, uint32_t& rd) {
+    const uint64_t i = r0 + tid;
+    kh = 0; kl = 0; rd = 0;
+    if (r0 < hi && i < hi) {
+      kh = __ldcs(a.khi_in + i);
+      if (a.with_lo) kl = __ldcs(a.klo_in + i);
+      rd = __ldcs(a.rid_in + i);
+    }
+  };
+  uint64_t nh0, nh1;
+  uint32_t nl0, nl1, nr0, nr1;
+  load_row(lo, nh0, nl0, nr0);
+  load_row(lo + kSThreads, nh1, nl1, nr1);
+  for (uint64_t r0 = lo; r0 < hi; r0 += kSThreads, ++tag) {
+    const uint64_t i = r0 + tid;
+    const bool on = i < hi;
+    const uint64_t kh = nh0;
+    const uint32_t kl = nl0, rd = nr0;
+    nh0 = nh1; nl0 = nl1; nr0 = nr1;
+    load_row(r0 + 2 * kSThreads, nh1, nl1, nr1);
+    const uint32_t d = on ? digit_of(kh, kl, a.byte) : 256u + lane;   // off lanes: unique dummies
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    const uint32_t t16 = (tag & 0xFFFFu) << 16;
+    if (on && rank == 0) wcnt[warp][d] = t16 | __popc(peers);
+    __syncthreads();
+    if (on) {
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) {
+        const uint32_t x = wcnt[w][d];
+        before += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
+      }
+      const uint32_t k = run[d] + before + rank;     // stable rank of the element in its digit
+      if (a.cache) {
+        const uint32_t p = lbase[d] + k;
+        sk[p] = kh;
+        sl[p] = kl;
+        sr[p] = rd;
+      } else {
+        const uint32_t slot = gbase[d] + k;
+        a.khi_out[slot] = kh;
+        if (a.with_lo) a.klo_out[slot] = kl;
+        a.rid_out[slot] = rd;
+      }
+    }
+    __syncthreads();
+    if (tid < 256) {
+      uint32_t add = 0;
+      for (int w = 0; w < kSWarps; ++w) {
+        const uint32_t x = wcnt[w][tid];
+        add += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
+      }
+      run[tid] += add;
+    }
+    __syncthreads();
+  }
+  if (a.cache) {
+    // ---- write out: staged slot p of digit d goes to gbase[d] + p - lbase[d]:
+    // consecutive threads, consecutive slots of one bucket run ----
+    const uint32_t cnt = (uint32_t)(hi - lo);
+    for (uint32_t p = tid; p < cnt; p += kSThreads) {
+      const uint64_t kh = sk[p];
+      const uint32_t kl = sl[p];
+      const uint32_t d = digit_of(kh, kl, a.byte);
+      const uint32_t slot = gbase[d] + (p - lbase[d]);
+      a.khi_out[slot] = kh;
+      if (a.with_lo) a.klo_out[slot] = kl;
+      a.rid_out[slot] = sr[p];
+    }
+  }
+}
+
+cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
+                             uint32_t key_bytes, uint8_t* ws, uint32_t* rids_out, uint32_t* gbar,
+                             int sm, cudaStream_t st, uint32_t* nl) {
+  // ws: [khi 0 | khi 1 | klo 0 | klo 1 | rid 0 | counts], 256-byte aligned pieces
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  uint64_t* khi[2] = {reinterpret_cast<uint64_t*>(ws), reinterpret_cast<uint64_t*>(ws + al(8 * n))};
+  uint8_t* p = ws + 2 * al(8 * n);
+  uint32_t* klo[2] = {reinterpret_cast<uint32_t*>(p), reinterpret_cast<uint32_t*>(p + al(4 * n))};
+  p += 2 * al(4 * n);
+  uint32_t* rid0 = reinterpret_cast<uint32_t*>(p);
+  p += al(4 * n);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+  uint32_t* rid[2] = {rid0, rids_out};
+  // the passes alternate buffers; start so that the last pass lands in rids_out
+  if (key_bytes % 2 == 0) {
+    uint32_t* t = rid[0];
+    rid[0] = rid[1];
+    rid[1] = t;
+  }
+  ++*nl;
+  const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 255) / 256, (uint64_t)sm * 8));
+  k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0]);
+  cudaError_t e = cudaGetLastError();
+  const uint64_t chunk = ((n + sm - 1) / sm + kSThreads - 1) / kSThreads * kSThreads;
+  // shared-memory copy of the chunk (16 B per element) when it fits beside
+  // the 17 KB of static counters
+  uint32_t dyn = 16 * chunk <= 200u * 1024 ? (uint32_t)(16 * chunk) : 0u;
+  if (dyn) {
+    static int set_dev = -1;
+    static uint32_t set_smem = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (set_dev != dev || set_smem < dyn) {
+      if (cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        dyn = 0;
+      } else {
+        set_dev = dev;
+        set_smem = dyn;
+      }
+    }
+  }
+  uint32_t in = 0;
+  for (int byte = (int)key_bytes - 1; byte >= 0 && e == cudaSuccess; --byte, in ^= 1) {
+    SortPassArgs s;
+    s.khi_in = khi[in];
+    s.klo_in = klo[in];
+    s.rid_in = rid[in];
+    s.khi_out = khi[in ^ 1];
+    s.klo_out = klo[in ^ 1];
+    s.rid_out = rid[in ^ 1];
+    s.n = n;
+    s.chunk = chunk;
+    s.byte = (uint32_t)byte;
+    s.with_lo = key_bytes > 8;
+    s.counts = counts;
+    s.gbar = gbar;
+    s.cache = dyn ? 1 : 0;
+    void* params[] = {&s};
+    ++*nl;
+    e = cudaLaunchCooperativeKernel((const void*)k_sort_pass, dim3(sm), dim3(kSThreads), params, dyn,
+                                    st);
+  }
+  return e;
+}
+
+uint64_t sort_ws_bytes(uint64_t n, int sm) {
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  return 2 * al(8 * n) + 2 * al(4 * n) + al(4 * n) + al(256ull * 4 * sm) + 256;
+}
+
+}  // namespace dpg
