@@ -197,6 +197,25 @@ dpg_status_t dpg_partition(const void *rids, uint32_t rid_bytes, uint64_t n, uin
                            uint32_t log2_span, uint32_t parts, uint32_t *local_out,
                            uint32_t *pos_out, uint64_t *counts_out, dpg_stream_t stream);
 
+/* Multi-GPU Phase I with Phase III's map: rids
+ * (uint32 or uint64 by rid_bytes, n of them, device) are grouped by owner =
+ * rid >> log2_span (parts owners, <= 512); local_out[m] (device, n entries)
+ * receives the owner-local offsets (rid - owner << log2_span), owner by
+ * owner, each row's in output order within its CTA block; inv_out[i]
+ * (device, n) the position of row i's request in local_out (0xFFFFFFFF for a
+ * rid >= n_src_total, which is also reported to dpg_sync_status);
+ * counts_out[parts] (device, uint64) the requests per owner.  Asynchronous. */
+dpg_status_t dpg_partition_inv(const void *rids, uint32_t rid_bytes, uint64_t n,
+                               uint64_t n_src_total, uint32_t log2_span, uint32_t parts,
+                               uint32_t *local_out, uint32_t *inv_out, uint64_t *counts_out,
+                               dpg_stream_t stream);
+
+/* Phase III over the replies: dst[i] = rows[inv[i]] for inv[i] < n_rows (rows
+ * of rec_bytes, device; dst n rows, device; other rows left unwritten).
+ * Output rows written in order (sequential stores).  Asynchronous. */
+dpg_status_t dpg_gather_rows(const void *rows, size_t rec_bytes, uint64_t n_rows,
+                             const uint32_t *inv, uint64_t n, void *dst, dpg_stream_t stream);
+
 /* Owner-side helper of the multi-GPU path: dst[pos[k]] = rows[k] for k in
  * [0, n) (Phase III against received replies).  pos must be distinct. */
 dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t *pos,

@@ -91,6 +91,9 @@ _sigs = {
     "dpg_partition": [_P, ctypes.c_uint32, _U, _U, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _P,
                       _P],
     "dpg_sort_rids": [_P, _S, _U, _S, _S, _P, _P],
+    "dpg_partition_inv": [_P, ctypes.c_uint32, _U, _U, ctypes.c_uint32, ctypes.c_uint32, _P, _P,
+                          _P, _P],
+    "dpg_gather_rows": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
 }
 for _name, _args in _sigs.items():
@@ -296,6 +299,38 @@ def dpg_partition(rids, n_src_total: int, log2_span: int, parts: int, stream=Non
                               local.data_ptr(), pos.data_ptr(), counts.data_ptr(),
                               _stream_ptr(stream)), "dpg_partition")
     return local, pos, counts
+
+
+def dpg_partition_inv(rids, n_src_total: int, log2_span: int, parts: int, stream=None):
+    """Group rids (CUDA, 32/64-bit) by owner rid >> log2_span.  Returns (local
+    int32 [n], inv int32 [n], counts int64 [parts]): the owner-local offsets
+    owner by owner (the first sum(counts) entries), and for every row the
+    position of its request (-1 for a rid out of range)."""
+    torch = _torch()
+    if not rids.is_cuda or not rids.is_contiguous():
+        raise ValueError("rids must be a contiguous CUDA tensor (no CPU fallback)")
+    rb = rids.element_size()
+    if rb not in (4, 8):
+        raise ValueError("rids must be 32- or 64-bit")
+    n = rids.numel()
+    local = torch.empty(max(n, 1), dtype=torch.int32, device=rids.device)
+    inv = torch.empty(max(n, 1), dtype=torch.int32, device=rids.device)
+    counts = torch.empty(parts, dtype=torch.int64, device=rids.device)
+    _check(_lib.dpg_partition_inv(rids.data_ptr(), rb, n, n_src_total, log2_span, parts,
+                                  local.data_ptr(), inv.data_ptr(), counts.data_ptr(),
+                                  _stream_ptr(stream)), "dpg_partition_inv")
+    return local, inv[:n], counts
+
+
+def dpg_gather_rows(rows, inv, dst, stream=None):
+    """dst[i] = rows[inv[i]] for inv[i] in range (other rows left unwritten)."""
+    rows = _records(rows, "rows")
+    inv = _rid_tensor(inv, "inv")
+    dst = _records(dst, "dst")
+    n_rows, rec = rows.shape
+    _check(_lib.dpg_gather_rows(rows.data_ptr(), rec, n_rows, inv.data_ptr(), inv.numel(),
+                                dst.data_ptr(), _stream_ptr(stream)), "dpg_gather_rows")
+    return dst
 
 
 def dpg_scatter_rows(rows, pos, dst, stream=None):

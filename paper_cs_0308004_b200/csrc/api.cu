@@ -597,6 +597,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     L2KArgs d;
     std::memset(&d, 0, sizeof(d));
     d.rids = rids;
+    d.rid_bytes = 4;
     d.n_out = n_out;
     d.n_src = n_src;
     d.s = p.log2_run;
@@ -1155,6 +1156,86 @@ dpg_status_t dpg_partition(const void* rids, uint32_t rid_bytes, uint64_t n, uin
   cudaError_t e = launch_distribute(d, rid_bytes == 8, st, &nl);
   if (e == cudaSuccess) e = launch_split_entries(d, local_out, pos_out, counts_out, st, &nl);
   cudaFreeAsync(w.base, st);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_partition_inv(const void* rids, uint32_t rid_bytes, uint64_t n,
+                               uint64_t n_src_total, uint32_t log2_span, uint32_t parts,
+                               uint32_t* local_out, uint32_t* inv_out, uint64_t* counts_out,
+                               dpg_stream_t stream) {
+  // Phase I of the multi-GPU path with Phase III's map: requests grouped by
+  // owner (owner = rid >> log2_span), and for every row the slot of its request
+  // (the replies come back in request order, so dst[i] = reply[inv[i]]).
+  t_launches = 0;
+  if ((rid_bytes != 4 && rid_bytes != 8) || parts == 0 || parts > 512 || log2_span > 32 ||
+      !counts_out)
+    return DPG_ERR_INVALID_ARG;
+  if (n && (!rids || !local_out || !inv_out)) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32) - 1) return DPG_ERR_UNSUPPORTED;
+  if (n_src_total == 0 || (((n_src_total - 1) >> log2_span) >= parts)) return DPG_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  if (n == 0) return cuda_status(cudaMemsetAsync(counts_out, 0, parts * sizeof(uint64_t), st));
+  const int sm = current_sm_count();
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  const uint64_t cbytes = align_up((uint64_t)parts * sm * 4, 256) + align_up((parts + 1) * 4, 256);
+  dpg_status_t w = persist_ws(st, 1, cbytes, &gbar, &total, &ws);
+  if (w != DPG_OK) return w;
+  L2KArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = rids;
+  d.rid_bytes = rid_bytes;
+  d.counts64 = counts_out;
+  d.n_out = n;
+  d.n_src = n_src_total;
+  d.s = log2_span;
+  d.K = parts;
+  d.chunk = align_up((n + sm - 1) / sm, 32);
+  d.counts = (uint32_t*)ws;
+  d.run_start = (uint32_t*)((uint8_t*)ws + align_up((uint64_t)parts * sm * 4, 256));
+  d.local = local_out;
+  d.inv = inv_out;
+  d.gbar = gbar + 16;
+  d.status = status;
+  uint32_t nl = 0;
+  cudaError_t e = launch_l2k_distribute(d, (uint32_t)sm, st, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_gather_rows(const void* rows, size_t rec_bytes, uint64_t n_rows, const uint32_t* inv,
+                             uint64_t n, void* dst, dpg_stream_t stream) {
+  // dst[i] = rows[inv[i]] (rows with inv[i] >= n_rows stay unwritten): the
+  // multi-GPU path's Phase III over the replies, in output order.
+  t_launches = 0;
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n == 0) return DPG_OK;
+  if (!inv || !dst || (n_rows && !rows)) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32) || n_rows > (1ull << 32) || rec_bytes > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  dpg_status_t w = persist_ws(st, 1, 64, &gbar, &total, &ws);
+  if (w != DPG_OK) return w;
+  const int sm = current_sm_count();
+  L2RunArgs l;
+  std::memset(&l, 0, sizeof(l));
+  l.src = (const uint8_t*)rows;
+  l.n_src = n_rows;
+  l.rec = (uint32_t)rec_bytes;
+  l.rids = inv;
+  l.n_out = n;
+  l.chunk = align_up((n + sm - 1) / sm, 32);
+  l.dst = (uint8_t*)dst;
+  l.gbar = gbar;
+  l.stage = 0;
+  if (rec_bytes % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec_bytes / 4 - 1) / (rec_bytes / 4));
+  const uint32_t W = pow2_divisor(rec_bytes | (uintptr_t)rows | (uintptr_t)dst);
+  uint32_t nl = 0;
+  cudaError_t e = launch_l2run(l, W, (uint32_t)sm, st, &nl);
   t_launches = nl;
   return cuda_status(e);
 }

@@ -283,7 +283,9 @@ struct L2PairArgs {
 
 // Phase I of the K-run L2 plan (l2k.cu).
 struct L2KArgs {
-  const uint32_t* rids;
+  const void* rids;      // uint32 or uint64 (rid_bytes)
+  uint32_t rid_bytes;
+  uint64_t* counts64;    // optional [K]: rows per run (CTA 0 writes)
   uint64_t n_out;
   uint64_t n_src;
   uint32_t s;            // log2 of the run length L (records)

@@ -29,7 +29,9 @@ namespace dpg {
 static constexpr int kKThreads = 512;
 static constexpr int kKWarps = kKThreads / 32;
 
+template <typename RidT>
 __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
+  const RidT* rids = reinterpret_cast<const RidT*>(a.rids);
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* wrun = sm;                                  // [kKWarps][K] counts, then cursors
   uint32_t* base = sm + kKWarps * a.K;                  // [K] start of this CTA's block of run b
@@ -44,12 +46,12 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
 
   // ---- pass 1: rows per (warp, run) ----
   for (uint32_t g0 = warp; g0 < ngroups; g0 += 8 * kKWarps) {
-    uint32_t r[8];
+    RidT r[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t g = g0 + u * kKWarps;
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
-      r[u] = (g < ngroups && i < hi) ? __ldcg(a.rids + i) : 0xFFFFFFFFu;
+      r[u] = (g < ngroups && i < hi) ? __ldcg(rids + i) : ~RidT(0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       const bool valid = r[u] < a.n_src;
       if (i < hi && !valid) report_bad(a.status, i);
-      const uint32_t b = valid ? r[u] >> a.s : 0xFFFFFFFFu;
+      const uint32_t b = valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, b);
       if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
     }
@@ -107,7 +109,10 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint32_t start = woff + y - tot;
       if (b < K) {
         base[b] = start + pre;
-        if (c == 0) a.run_start[b] = start;
+        if (c == 0) {
+          a.run_start[b] = start;
+          if (a.counts64) a.counts64[b] = tot;
+        }
       }
       __syncthreads();
       if (tid == 0) {
@@ -125,14 +130,14 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
   __syncthreads();
 
   // ---- pass 2: append (the same groups, the same order) ----
-  const uint32_t lmask = (1u << a.s) - 1u;
+  const RidT lmask = (RidT)((1ull << a.s) - 1ull);
   for (uint32_t g0 = warp; g0 < ngroups; g0 += 8 * kKWarps) {
-    uint32_t r[8];
+    RidT r[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t g = g0 + u * kKWarps;
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
-      r[u] = (g < ngroups && i < hi) ? __ldcs(a.rids + i) : 0xFFFFFFFFu;
+      r[u] = (g < ngroups && i < hi) ? __ldcs(rids + i) : ~RidT(0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (g >= ngroups) break;
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       const bool valid = r[u] < a.n_src;
-      const uint32_t b = valid ? r[u] >> a.s : 0xFFFFFFFFu;
+      const uint32_t b = valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, b);
       uint32_t slot = 0;
       if (valid) slot = my[b] + __popc(peers & lanemask_lt());
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
       if (i < hi) {
         a.inv[i] = valid ? slot : 0xFFFFFFFFu;
-        if (valid) a.local[slot] = r[u] & lmask;
+        if (valid) a.local[slot] = (uint32_t)(r[u] & lmask);
       }
     }
   }
@@ -159,17 +164,9 @@ uint32_t l2k_smem_bytes(uint32_t K) { return (kKWarps + 1) * K * 4 + 64; }
 cudaError_t launch_l2k_distribute(const L2KArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nl) {
   ++*nl;
   const uint32_t smem = l2k_smem_bytes(a.K);
-  auto fn = k_l2k_distribute;
-  static int set_dev = -1;
-  static uint32_t set_smem = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (set_dev != dev || set_smem < smem) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set_dev = dev;
-    set_smem = smem;
-  }
+  auto fn = a.rid_bytes == 8 ? k_l2k_distribute<uint64_t> : k_l2k_distribute<uint32_t>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   L2KArgs arg = a;
   void* params[] = {&arg};
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kKThreads), params, smem, st);

@@ -9,15 +9,16 @@ problem (reading A14).
 
 The paper's three phases map onto the cluster:
 
-* Phase I, distribute by owner -- ``dpg_partition``: the distribute kernels
-  with one run per owner (runs of ``S`` records), producing owner-local
-  offsets (requests) and the output position of each request;
+* Phase I, distribute by owner -- ``dpg_partition_inv``: one run per owner
+  (runs of ``S`` records), producing owner-local offsets (requests, owner by
+  owner) and, for every output row, the position of its request;
 * exchange 1 -- ``all_to_all_single`` of the per-owner counts, then of the
   requests (NCCL over NVLink / NVSwitch);
 * Phase II+III on the owner -- the local DPG (``dpg_retrieve``) of the
   requests it received, rows written in request order;
 * exchange 2 -- ``all_to_all_single`` of the rows back to the requesters;
-* the reply scatter ``dst[pos[k]] = rows[k]`` (``dpg_scatter_rows``).
+* Phase III: ``dst[i] = reply[inv[i]]`` in output order (``dpg_gather_rows``;
+  sequential output writes, the replies read as one stream per owner).
 
 Every step on the data runs in libdpg.so kernels (``CudaOps``); this module
 only sizes buffers and drives ``torch.distributed``.  The local-step object is
@@ -53,10 +54,10 @@ class CudaOps:
         self.dpg = dpg
 
     def partition(self, rids, n_src_total, log2_span, parts):
-        local, pos, counts = self.dpg.dpg_partition(rids, n_src_total, log2_span, parts)
+        local, inv, counts = self.dpg.dpg_partition_inv(rids, n_src_total, log2_span, parts)
         counts = [int(c) for c in counts.cpu().tolist()]
         m = sum(counts)
-        return local[:m], pos[:m], counts
+        return local[:m], inv, counts
 
     def empty_u32(self, n, like):
         return torch.empty(n, dtype=torch.int32, device=like.device)
@@ -67,9 +68,9 @@ class CudaOps:
     def retrieve(self, src_shard, requests):
         return self.dpg.dpg_retrieve(src_shard, requests)
 
-    def scatter(self, rows, pos, dst):
-        if rows.shape[0]:
-            self.dpg.dpg_scatter_rows(rows, pos, dst)
+    def gather(self, replies, inv, dst):
+        if inv.numel():
+            self.dpg.dpg_gather_rows(replies, inv, dst)
 
     def counts_tensor(self, counts, like):
         return torch.tensor(counts, dtype=torch.int64, device=like.device)
@@ -97,7 +98,7 @@ def retrieve_dist(src_shard, rids, n_src_total: int, group=None, ops=None,
         lo = min(n, k * step)
         hi = min(n, lo + step)
         chunk = rids[lo:hi]
-        local, pos, counts = ops.partition(chunk, n_src_total, log2_span, world)
+        local, inv, counts = ops.partition(chunk, n_src_total, log2_span, world)
         send_c = ops.counts_tensor(counts, src_shard)
         recv_c = torch.empty_like(send_c)
         dist.all_to_all_single(recv_c, send_c, group=group)
@@ -111,5 +112,5 @@ def retrieve_dist(src_shard, rids, n_src_total: int, group=None, ops=None,
         dist.all_to_all_single(back.view(-1), rows.reshape(-1),
                                output_split_sizes=[c * rec for c in counts],
                                input_split_sizes=[c * rec for c in rcounts], group=group)
-        ops.scatter(back, pos, dst[lo:hi])
+        ops.gather(back, inv, dst[lo:hi])
     return dst

@@ -1,6 +1,6 @@
 """Multi-process tests of the multi-GPU exchange logic (paper_cs_0308004_b200
 /dist.py) on CPU with the gloo backend, world size 2 (and 1).  The local steps
-(owner partition, local retrieval, reply scatter) are numpy stand-ins here --
+(owner partition, local retrieval, reply gather) are numpy stand-ins here --
 test scaffolding for the host logic; on GPUs the same function runs the
 libdpg.so kernels (CudaOps).  The result is checked against the oracle of the
 global problem."""
@@ -18,6 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 class NumpyOps:
+    """Plain stand-ins of the GPU steps: a stable partition by owner with the
+    request position of every row, retrieval, and the gather by position."""
+
     def partition(self, rids, n_src_total, log2_span, parts):
         r = rids.numpy().astype(np.int64)
         ok = (r >= 0) & (r < n_src_total)
@@ -27,7 +30,9 @@ class NumpyOps:
         idx = idx[order]
         local = (r[idx] - (owner[order] << log2_span)).astype(np.int32)
         counts = np.bincount(owner, minlength=parts).tolist()
-        return torch.from_numpy(local), torch.from_numpy(idx.astype(np.int32)), counts
+        inv = np.full(r.size, -1, dtype=np.int64)
+        inv[idx] = np.arange(idx.size)
+        return torch.from_numpy(local), torch.from_numpy(inv.astype(np.int32)), counts
 
     def empty_u32(self, n, like):
         return torch.empty(n, dtype=torch.int32)
@@ -38,9 +43,10 @@ class NumpyOps:
     def retrieve(self, src_shard, requests):
         return src_shard[requests.long()].contiguous()
 
-    def scatter(self, rows, pos, dst):
-        if rows.shape[0]:
-            dst[pos.long()] = rows
+    def gather(self, replies, inv, dst):
+        i = inv.long()
+        ok = i >= 0
+        dst[ok] = replies[i[ok]]
 
     def counts_tensor(self, counts, like):
         return torch.tensor(counts, dtype=torch.int64)

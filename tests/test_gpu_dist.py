@@ -42,6 +42,39 @@ def test_partition_groups_by_owner(dpg, dtype, parts, log2_span, n_total):
         assert np.array_equal(seg_loc + (o << log2_span), rids[seg_pos].astype(np.int64))
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("parts,log2_span,n_total", [(4, 10, 4096), (8, 7, 1000), (1, 12, 3000),
+                                                     (300, 4, 4800)])
+def test_partition_inv(dpg, dtype, parts, log2_span, n_total):
+    """Requests owner by owner (stable within each owner), inv = each row's
+    request position; the reply gather restores output order."""
+    rng = np.random.default_rng(parts * 10 + log2_span)
+    rids = rng.integers(0, n_total, 7777).astype(dtype)
+    rids[[5, 600]] = n_total + 3                       # out of range: no request
+    local, inv, counts = dpg.dpg_partition_inv(torch.from_numpy(rids).cuda(), n_total, log2_span,
+                                               parts)
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_sync_status()
+    counts = counts.cpu().numpy()
+    inv = inv.cpu().numpy().astype(np.int64)
+    local = local.cpu().numpy().astype(np.int64)
+    ok = rids.astype(np.int64) < n_total
+    owner = rids.astype(np.int64) >> log2_span
+    assert np.array_equal(counts, np.bincount(owner[ok], minlength=parts))
+    assert np.all(inv[~ok] == -1)
+    assert np.array_equal(np.sort(inv[ok]), np.arange(ok.sum()))
+    assert np.array_equal(local[inv[ok]] + (owner[ok] << log2_span), rids[ok].astype(np.int64))
+    start = np.concatenate([[0], np.cumsum(counts)])
+    assert np.all((inv[ok] >= start[owner[ok]]) & (inv[ok] < start[owner[ok] + 1]))
+    # the reply gather: rows of the requests in request order -> output order
+    rows = torch.from_numpy(rng.integers(0, 256, (int(ok.sum()), 36), dtype=np.uint8)).cuda()
+    dst = torch.zeros((rids.size, 36), dtype=torch.uint8, device="cuda")
+    dpg.dpg_gather_rows(rows, torch.from_numpy(inv.astype(np.int32)).cuda(), dst)
+    d = dst.cpu().numpy()
+    assert np.array_equal(d[ok], rows.cpu().numpy()[inv[ok]])
+    assert np.all(d[~ok] == 0)
+
+
 def test_retrieve_dist_single_rank_nccl(dpg):
     import torch.distributed as dist
     from paper_cs_0308004_b200.dist import retrieve_dist
