@@ -54,7 +54,8 @@ struct SortPassArgs {
   uint32_t with_lo;      // key_bytes > 8: carry the low word
   uint32_t* counts;      // [256 * grid]
   uint32_t* gbar;        // monotonic grid barrier words
-  uint32_t cache;        // 1: the CTA's chunk is kept in shared memory between the passes
+  uint32_t cache;        // 1: each tile is staged in shared memory, written out as bucket runs
+  uint32_t tile;         // elements per tile (staging capacity)
 };
 
 __device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, uint32_t byte) {
@@ -67,10 +68,9 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   extern __shared__ __align__(16) uint8_t sdyn[];
   __shared__ uint32_t hist[256];       // CTA counts
   __shared__ uint32_t gbase[256];      // first global slot of this CTA's block of digit d
-  __shared__ uint32_t lbase[256];      // first staged slot of digit d (exclusive scan of hist)
   __shared__ uint32_t run[256];        // elements of digit d placed so far (this CTA)
   __shared__ uint32_t wcnt[kSWarps][256];   // (row tag << 16 | count) per warp and digit
-  __shared__ uint32_t wsum[kSWarps], wsum2[kSWarps];
+  __shared__ uint32_t wsum[kSWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
   const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
@@ -118,101 +118,136 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
       tot += x;
       if (q < c) pre += x;
     }
-    const uint32_t mine = hist[tid];
-    uint32_t y = tot, z = mine;
+    uint32_t y = tot;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
-      const uint32_t t2 = __shfl_up_sync(0xffffffffu, z, d);
-      if (lane >= d) { y += t; z += t2; }
+      if (lane >= d) y += t;
     }
-    if (lane == 31) { wsum[warp] = y; wsum2[warp] = z; }
+    if (lane == 31) wsum[warp] = y;
     gbase[tid] = y - tot + pre;
-    lbase[tid] = z - mine;
   }
   __syncthreads();
   if (tid < 256) {
-    uint32_t off = 0, off2 = 0;
-    for (int w = 0; w < warp; ++w) { off += wsum[w]; off2 += wsum2[w]; }
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
     gbase[tid] += off;
-    lbase[tid] += off2;
   }
   __syncthreads();
   uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);
-  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * a.chunk);
-  uint32_t* sr = sl + a.chunk;
-  // ---- distribute, 512 elements per row, rows in order (stable) ----
+  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * a.tile);
+  uint32_t* sr = sl + a.tile;
+  __shared__ uint32_t th[256];         // digit counts of the current tile
+  __shared__ uint32_t tl[256];         // their exclusive scan (tile staging bases)
   uint32_t tag = 0;
-  // the next two rows' elements are loaded while a row is distributed
-  auto load_row = [&](uint64_t r0, uint64_t& kh, uint32_t& kl, uint32_t& rd) {
-    const uint64_t i = r0 + tid;
-    kh = 0; kl = 0; rd = 0;
-    if (r0 < hi && i < hi) {
-      kh = __ldcs(a.khi_in + i);
-      if (a.with_lo) kl = __ldcs(a.klo_in + i);
-      rd = __ldcs(a.rid_in + i);
-    }
-  };
-  uint64_t nh0, nh1;
-  uint32_t nl0, nl1, nr0, nr1;
-  load_row(lo, nh0, nl0, nr0);
-  load_row(lo + kSThreads, nh1, nl1, nr1);
-  for (uint64_t r0 = lo; r0 < hi; r0 += kSThreads, ++tag) {
-    const uint64_t i = r0 + tid;
-    const bool on = i < hi;
-    const uint64_t kh = nh0;
-    const uint32_t kl = nl0, rd = nr0;
-    nh0 = nh1; nl0 = nl1; nr0 = nr1;
-    load_row(r0 + 2 * kSThreads, nh1, nl1, nr1);
-    const uint32_t d = on ? digit_of(kh, kl, a.byte) : 256u + lane;   // off lanes: unique dummies
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t rank = __popc(peers & lanemask_lt());
-    const uint32_t t16 = (tag & 0xFFFFu) << 16;
-    if (on && rank == 0) wcnt[warp][d] = t16 | __popc(peers);
-    __syncthreads();
-    if (on) {
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) {
-        const uint32_t x = wcnt[w][d];
-        before += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
+  // the CTA's chunk in tiles of a.tile elements (staged in shared memory and
+  // written out as one contiguous run per digit); rows of 512 in order
+  for (uint64_t t0 = lo; t0 < hi; t0 += a.tile) {
+    const uint64_t t1 = min_u64(hi, t0 + a.tile);
+    if (a.cache) {
+      // tile histogram and its scan
+      for (uint32_t d = tid; d < 256; d += kSThreads) th[d] = 0;
+      __syncthreads();
+      for (uint64_t i = t0 + tid; i < t1; i += kSThreads)
+        atomicAdd(&th[digit_of(__ldcg(a.khi_in + i), a.with_lo ? __ldcg(a.klo_in + i) : 0u, a.byte)], 1u);
+      __syncthreads();
+      if (tid < 256) {
+        const uint32_t x = th[tid];
+        uint32_t y = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
+          if (lane >= d) y += t;
+        }
+        if (lane == 31) wsum[warp] = y;
+        tl[tid] = y - x;
       }
-      const uint32_t k = run[d] + before + rank;     // stable rank of the element in its digit
-      if (a.cache) {
-        const uint32_t p = lbase[d] + k;
-        sk[p] = kh;
-        sl[p] = kl;
-        sr[p] = rd;
-      } else {
-        const uint32_t slot = gbase[d] + k;
+      __syncthreads();
+      if (tid < 256) {
+        uint32_t off = 0;
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+        tl[tid] += off;
+      }
+      __syncthreads();
+    }
+    // elements of this tile placed so far, per digit (the CTA's running count
+    // run[] holds the tiles before)
+    __shared__ uint32_t trun[256];
+    for (uint32_t d = tid; d < 256; d += kSThreads) trun[d] = 0;
+    __syncthreads();
+    auto load_row = [&](uint64_t r0, uint64_t& kh, uint32_t& kl, uint32_t& rd) {
+      const uint64_t i = r0 + tid;
+      kh = 0; kl = 0; rd = 0;
+      if (r0 < t1 && i < t1) {
+        kh = __ldcs(a.khi_in + i);
+        if (a.with_lo) kl = __ldcs(a.klo_in + i);
+        rd = __ldcs(a.rid_in + i);
+      }
+    };
+    uint64_t nh0, nh1;
+    uint32_t nl0, nl1, nr0, nr1;
+    load_row(t0, nh0, nl0, nr0);
+    load_row(t0 + kSThreads, nh1, nl1, nr1);
+    for (uint64_t r0 = t0; r0 < t1; r0 += kSThreads, ++tag) {
+      const uint64_t i = r0 + tid;
+      const bool on = i < t1;
+      const uint64_t kh = nh0;
+      const uint32_t kl = nl0, rd = nr0;
+      nh0 = nh1; nl0 = nl1; nr0 = nr1;
+      load_row(r0 + 2 * kSThreads, nh1, nl1, nr1);
+      const uint32_t d = on ? digit_of(kh, kl, a.byte) : 256u + lane;   // off lanes: unique dummies
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t rank = __popc(peers & lanemask_lt());
+      const uint32_t t16 = (tag & 0xFFFFu) << 16;
+      if (on && rank == 0) wcnt[warp][d] = t16 | __popc(peers);
+      __syncthreads();
+      if (on) {
+        uint32_t before = 0;
+        for (int w = 0; w < warp; ++w) {
+          const uint32_t x = wcnt[w][d];
+          before += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
+        }
+        const uint32_t k = trun[d] + before + rank;   // stable rank of the element in the tile
+        if (a.cache) {
+          const uint32_t p = tl[d] + k;
+          sk[p] = kh;
+          sl[p] = kl;
+          sr[p] = rd;
+        } else {
+          const uint32_t slot = gbase[d] + run[d] + k;
+          a.khi_out[slot] = kh;
+          if (a.with_lo) a.klo_out[slot] = kl;
+          a.rid_out[slot] = rd;
+        }
+      }
+      __syncthreads();
+      if (tid < 256) {
+        uint32_t add = 0;
+        for (int w = 0; w < kSWarps; ++w) {
+          const uint32_t x = wcnt[w][tid];
+          add += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
+        }
+        trun[tid] += add;
+      }
+      __syncthreads();
+    }
+    if (a.cache) {
+      // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
+      // p - tl[d]: consecutive threads, consecutive slots of one bucket run ----
+      const uint32_t cnt = (uint32_t)(t1 - t0);
+      for (uint32_t p = tid; p < cnt; p += kSThreads) {
+        const uint64_t kh = sk[p];
+        const uint32_t kl = sl[p];
+        const uint32_t d = digit_of(kh, kl, a.byte);
+        const uint32_t slot = gbase[d] + run[d] + (p - tl[d]);
         a.khi_out[slot] = kh;
         if (a.with_lo) a.klo_out[slot] = kl;
-        a.rid_out[slot] = rd;
+        a.rid_out[slot] = sr[p];
       }
+      __syncthreads();
     }
+    for (uint32_t d = tid; d < 256; d += kSThreads) run[d] += trun[d];
     __syncthreads();
-    if (tid < 256) {
-      uint32_t add = 0;
-      for (int w = 0; w < kSWarps; ++w) {
-        const uint32_t x = wcnt[w][tid];
-        add += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
-      }
-      run[tid] += add;
-    }
-    __syncthreads();
-  }
-  if (a.cache) {
-    // ---- write out: staged slot p of digit d goes to gbase[d] + p - lbase[d]:
-    // consecutive threads, consecutive slots of one bucket run ----
-    const uint32_t cnt = (uint32_t)(hi - lo);
-    for (uint32_t p = tid; p < cnt; p += kSThreads) {
-      const uint64_t kh = sk[p];
-      const uint32_t kl = sl[p];
-      const uint32_t d = digit_of(kh, kl, a.byte);
-      const uint32_t slot = gbase[d] + (p - lbase[d]);
-      a.khi_out[slot] = kh;
-      if (a.with_lo) a.klo_out[slot] = kl;
-      a.rid_out[slot] = sr[p];
-    }
   }
 }
 
@@ -240,22 +275,20 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0]);
   cudaError_t e = cudaGetLastError();
   const uint64_t chunk = ((n + sm - 1) / sm + kSThreads - 1) / kSThreads * kSThreads;
-  // shared-memory copy of the chunk (16 B per element) when it fits beside
-  // the 17 KB of static counters
-  uint32_t dyn = 16 * chunk <= 200u * 1024 ? (uint32_t)(16 * chunk) : 0u;
-  if (dyn) {
+  // staging of one tile (16 B per element): 8192 elements = 128 KB
+  const uint32_t tile = 8192;
+  uint32_t dyn = 16 * tile;
+  {
     static int set_dev = -1;
-    static uint32_t set_smem = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (set_dev != dev || set_smem < dyn) {
+    if (set_dev != dev) {
       if (cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
           cudaSuccess) {
         cudaGetLastError();
         dyn = 0;
       } else {
         set_dev = dev;
-        set_smem = dyn;
       }
     }
   }
@@ -275,6 +308,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     s.counts = counts;
     s.gbar = gbar;
     s.cache = dyn ? 1 : 0;
+    s.tile = dyn ? tile : kSThreads;
     void* params[] = {&s};
     ++*nl;
     e = cudaLaunchCooperativeKernel((const void*)k_sort_pass, dim3(sm), dim3(kSThreads), params, dyn,

@@ -523,3 +523,13 @@ def test_dpg_sort_rejects_bad_keys(dpg):
     for off, kb in ((0, 0), (0, 13), (5, 4)):
         with pytest.raises(dpg.DPGError):
             dpg.dpg_sort(s, off, kb)
+
+
+def test_dpg_sort_many_tiles(dpg):
+    """Chunks of several staging tiles per CTA (n > 148 x 8192)."""
+    rng = np.random.default_rng(99)
+    n = 148 * 8192 * 2 + 12345
+    src = rng.integers(0, 256, (n, 8), dtype=np.uint8)
+    src[:, 3:6] = rng.integers(0, 3, (n, 3), dtype=np.uint8)     # many ties
+    want = oracle.sort_rids(src, 2, 5)
+    assert np.array_equal(host(dpg.dpg_sort_rids(dev(src), 2, 5)).view(np.uint32), want)
