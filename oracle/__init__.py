@@ -15,6 +15,8 @@ Each wrapper cites the passage the C function follows:
 * :func:`sort_rids`   -- phases 1-2 of three-phase key-pointer sorting:
   the rids in stable key order
 * :func:`sort`        -- the whole three-phase sort: sort_rids then retrieve
+* :func:`fk_join_sort` -- DPG-Sort join rows ``fact[rid_R] ++ dim[rid_F]`` in rid_F order
+  (P:595-598, 610-615)
 
 Errors (reading A6 in DESIGN.md): a rid >= n_src raises :class:`RidRangeError`
 carrying the smallest offending position.
@@ -60,6 +62,8 @@ def _load():
         lib.oracle_fk_join.argtypes = [P, U, U, P, P, U, U, P, P]
         lib.oracle_retrieve_at.argtypes = [P, U, U, P, P, U, P]
         lib.oracle_sort_rids.argtypes = [P, U, U, U, U, P]
+        lib.oracle_fk_join_sort.argtypes = [P, U, U, P, P, U, U, P, P]
+        lib.oracle_fk_join_sort.restype = ctypes.c_int
         for f in (lib.oracle_retrieve, lib.oracle_retrieve_u64, lib.oracle_dpg_fig1,
                   lib.oracle_fk_join, lib.oracle_retrieve_at, lib.oracle_sort_rids):
             f.restype = ctypes.c_int
@@ -166,4 +170,20 @@ def sort_rids(src: np.ndarray, key_off: int, key_bytes: int) -> np.ndarray:
 def sort(src: np.ndarray, key_off: int, key_bytes: int) -> np.ndarray:
     """The three-phase key-pointer sort: sorted records."""
     return retrieve(src, sort_rids(src, key_off, key_bytes))
+
+
+def fk_join_sort(fact: np.ndarray, fk: np.ndarray, dim: np.ndarray) -> np.ndarray:
+    """DPG-Sort join rows ``fact[rid_R] ++ dim[rid_F]`` with the pairs in stable
+    rid_F (= fk) order (reading A11)."""
+    fact = _records(fact)
+    dim = _records(dim)
+    n_fact, fact_bytes = fact.shape
+    n_dim, rec = dim.shape
+    fk = np.ascontiguousarray(fk, dtype=np.uint32)
+    assert fk.size == n_fact
+    out = np.zeros((n_fact, fact_bytes + rec), dtype=np.uint8)
+    bad = ctypes.c_uint64(0)
+    _check(_load().oracle_fk_join_sort(_ptr(fact), fact_bytes, n_fact, _ptr(fk), _ptr(dim), rec,
+                                       n_dim, _ptr(out), ctypes.byref(bad)), bad)
+    return out
 

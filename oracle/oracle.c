@@ -247,3 +247,47 @@ int oracle_sort_rids(const uint8_t *src, uint64_t rec, uint64_t n, uint64_t key_
     free(a); free(b);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ *
+ * (5) DPG-Sort join: "sort the rid pairs (rid_R,      *
+ *     rid_F) according to the order of rid_F", then "move the records of R *
+ *     according to the ordering of rid_F in the sorted sequence"; joined   *
+ *     with F read in rid_F order.  With the dense key of reading A11,       *
+ *     rid_R = i and rid_F = fk[i].  Output row j = fact[rid_R_j] (fact      *
+ *     bytes) ++ dim[rid_F_j] (rec bytes), the pairs in stable rid_F order   *
+ *     (ties keep ascending rid_R).  Phase "sort" is a plain bottom-up merge *
+ *     sort; an fk >= n_dim is an error at the smallest fact position.       *
+ * ------------------------------------------------------------------------ */
+int oracle_fk_join_sort(const uint8_t *fact, uint64_t fact_bytes, uint64_t n_fact,
+                        const uint32_t *fk, const uint8_t *dim, uint64_t rec,
+                        uint64_t n_dim, uint8_t *out, uint64_t *bad_index)
+{
+    if (rec == 0 || n_fact >= (1ull << 32)) return -1;
+    for (uint64_t i = 0; i < n_fact; ++i)
+        if (fk[i] >= n_dim) { if (bad_index) *bad_index = i; return 1; }
+    uint32_t *a = malloc((n_fact ? n_fact : 1) * sizeof(uint32_t));
+    uint32_t *b = malloc((n_fact ? n_fact : 1) * sizeof(uint32_t));
+    if (!a || !b) { free(a); free(b); return -1; }
+    for (uint64_t i = 0; i < n_fact; ++i) a[i] = (uint32_t)i;       /* the pairs (i, fk[i]) */
+    for (uint64_t w = 1; w < n_fact; w *= 2) {                      /* stable sort by rid_F */
+        for (uint64_t lo = 0; lo < n_fact; lo += 2 * w) {
+            uint64_t mid = lo + w < n_fact ? lo + w : n_fact;
+            uint64_t hi = lo + 2 * w < n_fact ? lo + 2 * w : n_fact;
+            uint64_t i = lo, j = mid, k = lo;
+            while (i < mid && j < hi) {
+                if (fk[a[i]] <= fk[a[j]]) b[k++] = a[i++];
+                else b[k++] = a[j++];
+            }
+            while (i < mid) b[k++] = a[i++];
+            while (j < hi) b[k++] = a[j++];
+        }
+        uint32_t *t = a; a = b; b = t;
+    }
+    uint64_t row = fact_bytes + rec;
+    for (uint64_t j = 0; j < n_fact; ++j) {                         /* move R, join with F */
+        memcpy(out + j * row, fact + (uint64_t)a[j] * fact_bytes, fact_bytes);
+        memcpy(out + j * row + fact_bytes, dim + (uint64_t)fk[a[j]] * rec, rec);
+    }
+    free(a); free(b);
+    return 0;
+}

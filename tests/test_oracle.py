@@ -291,3 +291,19 @@ def test_sort_oracle_matches_datamation_generator():
     are the oracle's sorted rids."""
     w = datagen.make("c2", scale=16)
     assert np.array_equal(oracle.sort_rids(w["src"], 0, 10), w["rids"])
+
+
+def test_fk_join_sort_oracle_is_the_move_join_in_fk_order():
+    """DPG-Sort join: the same rows as the DPG-Move join, permuted
+    into stable fk order (numpy's stable argsort, an independent ordering)."""
+    rng = np.random.default_rng(8)
+    for n_fact, n_dim, fb, rec in [(0, 3, 4, 8), (1, 1, 2, 3), (500, 40, 16, 64), (3000, 7, 5, 11)]:
+        dim = rng.integers(0, 256, (n_dim, rec), dtype=np.uint8)
+        fact = rng.integers(0, 256, (n_fact, fb), dtype=np.uint8)
+        fk = rng.integers(0, n_dim, n_fact).astype(np.uint32)
+        move = oracle.fk_join(fact, fk, dim)
+        order = np.argsort(fk, kind="stable")
+        assert np.array_equal(oracle.fk_join_sort(fact, fk, dim), move[order])
+    fk[17 % max(1, fk.size)] = n_dim
+    with pytest.raises(oracle.RidRangeError):
+        oracle.fk_join_sort(fact, fk, dim)
