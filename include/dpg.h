@@ -234,6 +234,18 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* DPG-Sort join: the join pairs (rid_R = i, rid_F =
+ * fk_col[i]) sorted by rid_F (stable), the fact rows (R) moved into a
+ * temporary file in that order by DPG retrieval, then joined with dim (F)
+ * read in rid_F order.  out (device, n_fact rows of fact_bytes + rec_bytes):
+ * row j = fact[rid_R_j] ++ dim[rid_F_j], pairs in stable fk order -- the same
+ * rows as dpg_fk_join, in fk order instead of fact order.  An fk >= n_dim
+ * leaves its row unwritten and is reported at its fact position
+ * (dpg_sync_status).  Same argument rules as dpg_fk_join.  Asynchronous. */
+dpg_status_t dpg_fk_join_sort(const void *fact, size_t fact_bytes, uint64_t n_fact,
+                              const uint32_t *fk_col, const void *dim, size_t rec_bytes,
+                              uint64_t n_dim, void *out, dpg_stream_t stream);
+
 /* Three-phase key-pointer sorting with DPG as the record-copy phase
  * (section 3; DPG sort).  Keys: key_bytes
  * (1..12) unsigned bytes at key_off inside each record, compared

@@ -95,6 +95,7 @@ _sigs = {
                           _P, _P],
     "dpg_gather_rows": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
+    "dpg_fk_join_sort": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -354,6 +355,24 @@ def dpg_retrieve_host(src, rids, dst, stream=None):
     _check(_lib.dpg_retrieve_host(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
                                   dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_host")
     return dst
+
+
+def dpg_fk_join_sort(fact, fk_col, dim, out=None, stream=None):
+    """DPG-Sort join: rows fact[rid_R] ++ dim[fk] in stable fk order."""
+    torch = _torch()
+    fact = _records(fact, "fact")
+    dim = _records(dim, "dim")
+    fk_col = _rid_tensor(fk_col, "fk_col")
+    n_fact, fact_bytes = fact.shape
+    n_dim, rec = dim.shape
+    if fk_col.numel() != n_fact:
+        raise ValueError("fk_col must have one entry per fact row")
+    if out is None:
+        out = torch.empty((n_fact, fact_bytes + rec), dtype=torch.uint8, device=dim.device)
+    _check(_lib.dpg_fk_join_sort(fact.data_ptr(), fact_bytes, n_fact, fk_col.data_ptr(),
+                                 dim.data_ptr(), rec, n_dim, out.data_ptr(), _stream_ptr(stream)),
+           "dpg_fk_join_sort")
+    return out
 
 
 def dpg_sort_rids(src, key_off: int, key_bytes: int, rids=None, stream=None):

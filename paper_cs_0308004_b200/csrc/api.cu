@@ -1310,6 +1310,68 @@ dpg_status_t dpg_sort(const void* src, size_t rec_bytes, uint64_t n, size_t key_
   return s;
 }
 
+dpg_status_t dpg_fk_join_sort(const void* fact, size_t fact_bytes, uint64_t n_fact,
+                              const uint32_t* fk_col, const void* dim, size_t rec_bytes,
+                              uint64_t n_dim, void* out, dpg_stream_t stream) {
+  // DPG-Sort join: sort the pairs (rid_R = i, rid_F =
+  // fk[i]) by rid_F (stable radix sort, sort.cu), move the records of R (the
+  // fact rows) into a temporary file in that order by DPG retrieval, then join
+  // the temporary file with F read in rid_F order.  out row j = fact[rid_R_j]
+  // ++ dim[rid_F_j]; rows with fk >= n_dim stay unwritten and are reported.
+  t_launches = 0;
+  if (rec_bytes == 0 || fact_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n_fact == 0) return DPG_OK;
+  if (!fact || !fk_col || !dim || !out || n_dim == 0) return DPG_ERR_INVALID_ARG;
+  if (n_fact >= (1ull << 32) || n_dim > (1ull << 32)) return DPG_ERR_UNSUPPORTED;
+  uint64_t row, out_bytes, fact_total, dim_total;
+  if (__builtin_add_overflow((uint64_t)fact_bytes, (uint64_t)rec_bytes, &row) ||
+      __builtin_mul_overflow(n_fact, row, &out_bytes) ||
+      __builtin_mul_overflow(n_fact, (uint64_t)fact_bytes, &fact_total) ||
+      __builtin_mul_overflow(n_dim, (uint64_t)rec_bytes, &dim_total))
+    return DPG_ERR_INVALID_ARG;
+  if (row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  if (overlaps(out, out_bytes, fact, fact_total) || overlaps(out, out_bytes, dim, dim_total) ||
+      overlaps(out, out_bytes, fk_col, n_fact * 4))
+    return DPG_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  const int sm = current_sm_count();
+  // [rid_R | rid_F sorted | temporary file of fact rows]
+  const uint64_t o_fk = align_up(n_fact * 4 + 16, 256);
+  const uint64_t o_tmp = o_fk + align_up(n_fact * 4 + 16, 256);
+  void* buf = nullptr;
+  if (cudaMallocAsync(&buf, o_tmp + n_fact * fact_bytes + 64, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  uint32_t* rid_r = (uint32_t*)buf;
+  uint32_t* fks = (uint32_t*)((uint8_t*)buf + o_fk);
+  uint8_t* tmp = (uint8_t*)buf + o_tmp;
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  uint32_t nl = 0;
+  dpg_status_t s = persist_ws(st, 1, sort_ws_bytes(n_fact, sm), &gbar, &total, &ws);
+  cudaError_t e = cudaSuccess;
+  if (s == DPG_OK)
+    e = launch_sort_rids(nullptr, 4, n_fact, 0, 4, (uint8_t*)ws, rid_r, gbar + 16, sm, st, &nl,
+                         fk_col, fks, n_dim, status);
+  if (s == DPG_OK && e == cudaSuccess) {
+    // the fact rows in rid_F order: DPG retrieval (all rid_R are valid)
+    s = run_dpg(fact, fact_bytes, n_fact, rid_r, n_fact, nullptr, 0, tmp, st, nullptr);
+    nl += t_launches;
+  }
+  if (s == DPG_OK && e == cudaSuccess) {
+    const uint32_t W = pow2_divisor(fact_bytes | rec_bytes | (uintptr_t)tmp | (uintptr_t)dim |
+                                    (uintptr_t)out);
+    e = launch_zip_gather(tmp, (uint32_t)fact_bytes, (const uint8_t*)dim, (uint32_t)rec_bytes, n_dim,
+                          fks, n_fact, (uint8_t*)out, W, sm, st, &nl);
+  }
+  cudaFreeAsync(buf, st);
+  t_launches = nl;
+  return s != DPG_OK ? s : cuda_status(e);
+}
+
 dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_status(e);

@@ -441,7 +441,12 @@ cudaError_t launch_l2k_distribute(const L2KArgs& a, uint32_t grid, cudaStream_t 
 uint32_t l2k_smem_bytes(uint32_t K);
 cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
                              uint32_t key_bytes, uint8_t* ws, uint32_t* rids_out, uint32_t* gbar,
-                             int sm, cudaStream_t st, uint32_t* nlaunch);
+                             int sm, cudaStream_t st, uint32_t* nlaunch,
+                             const uint32_t* keys_u32 = nullptr, uint32_t* keys_out = nullptr,
+                             uint64_t key_limit = ~0ull, unsigned long long* status = nullptr);
+cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
+                              uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
+                              int sm, cudaStream_t st, uint32_t* nlaunch);
 uint64_t sort_ws_bytes(uint64_t n, int sm);
 uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);

@@ -25,9 +25,20 @@ static constexpr int kSWarps = kSThreads / 32;
 
 __global__ void k_sort_extract(const uint8_t* __restrict__ src, uint32_t rec, uint64_t n,
                                uint32_t key_off, uint32_t key_bytes, uint64_t* __restrict__ khi,
-                               uint32_t* __restrict__ klo, uint32_t* __restrict__ rid) {
+                               uint32_t* __restrict__ klo, uint32_t* __restrict__ rid,
+                               const uint32_t* __restrict__ keys_u32, uint64_t key_limit,
+                               unsigned long long* status) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
+    if (keys_u32) {
+      // numeric 32-bit keys: the value's bytes, most significant first (a key
+      // >= key_limit is reported at its position: referential integrity)
+      const uint32_t kv = __ldcs(keys_u32 + i);
+      if (kv >= key_limit) report_bad(status, i);
+      khi[i] = (uint64_t)kv << 32;
+      rid[i] = (uint32_t)i;
+      continue;
+    }
     const uint8_t* k = src + i * rec + key_off;
     uint64_t hi = 0;
     uint32_t lo = 0;
@@ -251,9 +262,16 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   }
 }
 
+__global__ void k_keys_u32(const uint64_t* __restrict__ khi, uint64_t n, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)(__ldcs(khi + i) >> 32);
+}
+
 cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
                              uint32_t key_bytes, uint8_t* ws, uint32_t* rids_out, uint32_t* gbar,
-                             int sm, cudaStream_t st, uint32_t* nl) {
+                             int sm, cudaStream_t st, uint32_t* nl, const uint32_t* keys_u32,
+                             uint32_t* keys_out, uint64_t key_limit, unsigned long long* status) {
   // ws: [khi 0 | khi 1 | klo 0 | klo 1 | rid 0 | counts], 256-byte aligned pieces
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
   uint64_t* khi[2] = {reinterpret_cast<uint64_t*>(ws), reinterpret_cast<uint64_t*>(ws + al(8 * n))};
@@ -272,7 +290,8 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   }
   ++*nl;
   const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 255) / 256, (uint64_t)sm * 8));
-  k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0]);
+  k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0],
+                                    keys_u32, key_limit, status);
   cudaError_t e = cudaGetLastError();
   const uint64_t chunk = ((n + sm - 1) / sm + kSThreads - 1) / kSThreads * kSThreads;
   // staging of one tile (16 B per element): 8192 elements = 128 KB
@@ -314,12 +333,58 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     e = cudaLaunchCooperativeKernel((const void*)k_sort_pass, dim3(sm), dim3(kSThreads), params, dyn,
                                     st);
   }
+  if (e == cudaSuccess && keys_out) {
+    // the sorted keys (numeric mode): the last pass's key buffer
+    ++*nl;
+    k_keys_u32<<<g, 256, 0, st>>>(khi[key_bytes % 2], n, keys_out);
+    e = cudaGetLastError();
+  }
   return e;
 }
 
 uint64_t sort_ws_bytes(uint64_t n, int sm) {
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
   return 2 * al(8 * n) + 2 * al(4 * n) + al(4 * n) + al(256ull * 4 * sm) + 256;
+}
+
+// DPG-Sort join, last step: out row j = a[j] (a_bytes, the moved
+// R records, sequential) ++ b[idx[j]] (b_bytes, F read in rid_F order:
+// non-decreasing idx, so F streams through once).  W-byte words, flat over
+// the output (coalesced stores); rows with idx >= n_b stay unwritten.
+template <int W>
+__global__ void __launch_bounds__(256) k_zip_gather(const uint8_t* __restrict__ a, uint32_t a_bytes,
+                                                    const uint8_t* __restrict__ b, uint32_t b_bytes,
+                                                    uint64_t n_b, const uint32_t* __restrict__ idx,
+                                                    uint64_t n, uint8_t* __restrict__ out) {
+  using T = typename Word<W>::T;
+  const uint32_t AW = a_bytes / W, R = (a_bytes + b_bytes) / W;
+  const uint64_t words = n * R;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < words; k += stride) {
+    const uint64_t row = k / R;
+    const uint32_t w = (uint32_t)(k - row * R);
+    const uint32_t f = __ldg(idx + row);
+    if (f >= n_b) continue;
+    const T v = w < AW ? __ldcs(reinterpret_cast<const T*>(a + row * a_bytes) + w)
+                       : __ldg(reinterpret_cast<const T*>(b + (uint64_t)f * b_bytes) + (w - AW));
+    __stcs(reinterpret_cast<T*>(out) + k, v);
+  }
+}
+
+cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
+                              uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
+                              int sm, cudaStream_t st, uint32_t* nl) {
+  const uint64_t words = n * ((a_bytes + b_bytes) / W);
+  const uint32_t grid = (uint32_t)max_u64(1, min_u64((words + 255) / 256, (uint64_t)sm * 8));
+  ++*nl;
+  switch (W) {
+    case 16: k_zip_gather<16><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+    case 8: k_zip_gather<8><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+    case 4: k_zip_gather<4><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+    case 2: k_zip_gather<2><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+    default: k_zip_gather<1><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace dpg

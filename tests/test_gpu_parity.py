@@ -533,3 +533,30 @@ def test_dpg_sort_many_tiles(dpg):
     src[:, 3:6] = rng.integers(0, 3, (n, 3), dtype=np.uint8)     # many ties
     want = oracle.sort_rids(src, 2, 5)
     assert np.array_equal(host(dpg.dpg_sort_rids(dev(src), 2, 5)).view(np.uint32), want)
+
+
+# --------------------------------------------------------------------------
+# DPG-Sort join.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n_fact,n_dim,fb,rec", [(1, 1, 16, 64), (7000, 3000, 16, 64),
+                                                 (50000, 77, 4, 12), (20000, 20000, 12, 100),
+                                                 (4099, 5000, 3, 5)])
+def test_fk_join_sort_matches_oracle(dpg, n_fact, n_dim, fb, rec):
+    rng = np.random.default_rng(n_fact + rec)
+    dim = rng.integers(0, 256, (n_dim, rec), dtype=np.uint8)
+    fact = rng.integers(0, 256, (n_fact, fb), dtype=np.uint8)
+    fk = rng.integers(0, n_dim, n_fact).astype(np.uint32)
+    got = host(dpg.dpg_fk_join_sort(dev(fact), dev(fk), dev(dim)))
+    assert np.array_equal(got, oracle.fk_join_sort(fact, fk, dim))
+
+
+def test_fk_join_sort_config_4_scaled_and_integrity(dpg):
+    w = datagen.make("c4", scale=16)
+    got = host(dpg.dpg_fk_join_sort(dev(w["fact"]), dev(w["fk"]), dev(w["dim"])))
+    assert np.array_equal(got, oracle.fk_join_sort(w["fact"], w["fk"], w["dim"]))
+    fk = w["fk"].copy()
+    fk[[123, 4567]] = w["dim"].shape[0] + 5
+    dpg.dpg_fk_join_sort(dev(w["fact"]), dev(fk), dev(w["dim"]))
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 123
