@@ -474,6 +474,21 @@ def main():
                     "launches_per_sort": sl / args.steps,
                     "what": "dpg_sort: 10-byte keys at offset 0, stable LSD radix sort "
                             "(10 passes) + dpg_retrieve"}
+    # the paper's DPG-Sort join: the same join in fk order
+    join_sort_res = None
+    if cfg == "c4" and not args.no_sort:
+        js = lambda: dpg.dpg_fk_join_sort(fact, fk, dim, out=out)
+        for _ in range(2):
+            js()
+        torch.cuda.synchronize()
+        dpg.dpg_sync_status()
+        jms, jl, _ = timed(js, args.steps)
+        jt = sum(jms) / len(jms)
+        join_sort_res = {"value": alg_bytes / (jt * 1e-3) / 1e9, "unit": "GB/s",
+                         "ms_per_step": jt, "launches_per_step": jl / args.steps,
+                         "what": "dpg_fk_join_sort: stable radix sort of (rid_R, fk) pairs by "
+                                 "fk + DPG retrieval of fact rows into a temporary file + "
+                                 "zip with dim rows read in fk order"}
     peak, peak_src = hbm_peak()
     dist_ms, probe_ms, calls = ph
     pg_ms = probe_ms / max(1, calls)
@@ -558,6 +573,7 @@ def main():
             "frac_of_hbm_peak": value / world / peak,
             "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
             "roofline": roofline, "naive": naive_res, "direct_windowed": windowed_res,
+            "dpg_join_sort": join_sort_res,
             "dpg_sort": sort_res,
             "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(), "gpu_launches": launches,

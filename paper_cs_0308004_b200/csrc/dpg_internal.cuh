@@ -631,3 +631,151 @@ __device__ __forceinline__ void ag_pipeline(uint32_t nt, F group, uint8_t* wtile
   cp_async_wait<0>();
 }
 }  // namespace dpg
+
+namespace dpg {
+// ---------------------------------------------------------------------------
+// Row-index window gather (l2run.cu): the same asynchronous window gather
+// with one source base for the whole warp.  A group is described by each
+// lane's 32-bit row index (~0u: row not copied) instead of a 64-bit address,
+// so issuing a window word costs one shuffle and, when the source spans less
+// than 4 GB (OFF32), 32-bit offset arithmetic; the lane constants of issue
+// and consume are computed once per warp (byte addresses inside the tile),
+// and the consume step reads the dword shifts of rows j and j + 1 with one
+// shuffle of a packed value.
+// ---------------------------------------------------------------------------
+struct AgrLane {
+  uintptr_t wbase;    // (base & ~15) + the lane's window word offset
+  uint32_t bl;        // base & 15
+  uint32_t frpi;      // rows per issue instruction (32 / window words)
+  uint32_t flr;       // the lane's row inside an instruction (>= frpi: idle lane)
+  int32_t lim;        // word flw is needed iff (addr & 15) + lim > 0
+  uint32_t so0;       // the lane's byte offset inside a tile
+};
+__device__ __forceinline__ AgrLane agr_lane(uintptr_t base, uint32_t rec, uint32_t lane) {
+  AgrLane L;
+  const uint32_t fnw = (rec + 27) / 16;
+  L.frpi = 32 / fnw;
+  L.flr = lane / fnw;
+  const uint32_t flw = lane - L.flr * fnw;
+  L.wbase = (base & ~uintptr_t(15)) + 16 * flw;
+  L.bl = (uint32_t)base & 15u;
+  L.lim = (int32_t)rec - (int32_t)(16 * flw);
+  L.so0 = L.flr * 128 + 16 * flw;
+  return L;
+}
+template <bool OFF32>
+__device__ __forceinline__ void agr_issue(uint32_t tile_s, uint32_t rec, uint32_t my_r, const AgrLane& L) {
+  uint32_t j = L.flr;
+  uint32_t so = tile_s + L.so0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    if ((uint32_t)u * L.frpi >= 32) break;            // warp-uniform
+    const uint32_t r = __shfl_sync(0xffffffffu, my_r, j & 31);
+    if (OFF32) {
+      const uint32_t x = L.bl + r * rec;               // offset from base & ~15
+      if (j < 32 && (int32_t)(x & 15u) + L.lim > 0)
+        cp_async16(so, reinterpret_cast<const void*>(L.wbase + (x & ~15u)), 16u);
+    } else {
+      const uint64_t x = L.bl + (uint64_t)r * rec;
+      if (j < 32 && (int32_t)((uint32_t)x & 15u) + L.lim > 0)
+        cp_async16(so, reinterpret_cast<const void*>(L.wbase + (x & ~uint64_t(15))), 16u);
+    }
+    j += L.frpi;
+    so += L.frpi * 128;
+  }
+}
+// Consume map of a full group, per lane: output word m = lane + 32 i reads
+// dwords of row j0 (byte b0 in the tile before the row's shift) and, from
+// dword `split` on, of row j0 + 1 (b1, minus the row length).
+struct AgrMap {
+  uint32_t b0[8];
+  uint32_t b1[8];
+  uint32_t jp[8];     // j0 | split << 8
+};
+__device__ __forceinline__ void agr_map_init(AgrMap& M, uint32_t rec, uint32_t lane) {
+  const uint32_t RD = rec >> 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t d0 = 4 * (lane + 32 * i);
+    const uint32_t j0 = min(d0 / RD, 31u);
+    const uint32_t q0 = d0 - j0 * RD;
+    const uint32_t j1 = min(j0 + 1, 31u);
+    const bool in = d0 < 32 * RD;                   // words past a full group read the tile start
+    M.b0[i] = in ? 4 * (j0 * 32 + q0) : 0u;
+    M.b1[i] = in ? 4 * (j1 * 32 + q0 - RD) : 0u;
+    M.jp[i] = in ? j0 | (min(RD - q0, 4u) << 8) : 4u << 8;
+  }
+}
+// packed (lane j): bits 0-15 = 4 x dword shift of row j, bits 16-31 = of row j + 1.
+// The loads of a batch of four output words are written before its stores:
+// the streaming store is a compiler memory barrier, so this order is what
+// lets the shuffles and shared loads of a batch overlap.  Every map entry
+// addresses the tile, so the batch needs no guard; the stores are predicated.
+__device__ __forceinline__ void agr_consume16(const uint8_t* tile, uint32_t packed, const AgrMap& M,
+                                              uint32_t cnt, uint32_t rec, uint32_t* out,
+                                              uint32_t lane) {
+  const uint32_t nw = cnt * (rec >> 2) / 4;         // 16-byte output words
+  uint4* o = reinterpret_cast<uint4*>(out) + lane;
+#pragma unroll
+  for (int h = 0; h < 8; h += 4) {
+    if (32 * h >= nw) break;                        // warp-uniform
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t jp = M.jp[h + k];
+      const uint32_t s = __shfl_sync(0xffffffffu, packed, jp & 31);
+      const uint32_t split = jp >> 8;
+      const uint8_t* r0 = tile + M.b0[h + k] + (s & 0xffffu);
+      const uint8_t* r1 = tile + M.b1[h + k] + (s >> 16);
+      v[k].x = *reinterpret_cast<const uint32_t*>(r0);
+      v[k].y = *reinterpret_cast<const uint32_t*>((1 < split ? r0 : r1) + 4);
+      v[k].z = *reinterpret_cast<const uint32_t*>((2 < split ? r0 : r1) + 8);
+      v[k].w = *reinterpret_cast<const uint32_t*>((3 < split ? r0 : r1) + 12);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (lane + 32 * (h + k) < nw) __stcs(o + 32 * (h + k), v[k]);
+  }
+}
+struct AgrGroup {
+  uint32_t r;         // the lane's row index (a row not stored reads row 0)
+  uint32_t cnt;       // rows in the group (<= 32)
+  uint32_t okm;       // rows to store
+  uint32_t* out;      // the group's output span
+};
+// Three groups per warp in flight, as ag_pipeline.  OFF32: every row offset
+// (base & 15) + r * rec of the source fits in 32 bits.
+template <bool OFF32, typename F>
+__device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, uint8_t* wtiles, uint32_t wt_s,
+                                             uint32_t tile_bytes, const AgrMap& amap, uintptr_t base,
+                                             uint32_t rec, uint32_t lane) {
+  const AgrLane L = agr_lane(base, rec, lane);
+  AgrGroup q0{}, q1{}, q2{};
+  if (0 < nt) { q0 = group(0); agr_issue<OFF32>(wt_s, rec, q0.r, L); }
+  cp_async_commit();
+  if (1 < nt) { q1 = group(1); agr_issue<OFF32>(wt_s + tile_bytes, rec, q1.r, L); }
+  cp_async_commit();
+  uint32_t slot = 0;
+  for (uint32_t t = 0; t < nt; ++t) {
+    const uint32_t slot2 = slot == 0 ? 2 : slot - 1;
+    if (t + 2 < nt) { q2 = group(t + 2); agr_issue<OFF32>(wt_s + slot2 * tile_bytes, rec, q2.r, L); }
+    cp_async_commit();
+    const uint32_t o4 = (L.bl + q0.r * rec) >> 2 & 3u;   // (base + r*rec) >> 2 & 3
+    const uint32_t nx = __shfl_down_sync(0xffffffffu, o4, 1);
+    cp_async_wait<2>();
+    __syncwarp();
+    const uint8_t* ts = wtiles + slot * tile_bytes;
+    const uint32_t full = q0.cnt == 32 ? 0xffffffffu : ((1u << q0.cnt) - 1u);
+    if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * rec)) & 15) == 0)
+      agr_consume16(ts, (o4 << 2) | (nx << 18), amap, q0.cnt, rec, q0.out, lane);
+    else
+      ag_consume(reinterpret_cast<const uint32_t*>(wtiles + slot * tile_bytes), o4, q0.okm, q0.cnt,
+                 rec, q0.out, lane);
+    __syncwarp();
+    q0 = q1;
+    q1 = q2;
+    slot = slot == 2 ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+}
+}  // namespace dpg

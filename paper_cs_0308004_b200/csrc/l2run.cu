@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
     uint8_t* wtiles = ring + (size_t)warp * 3 * kAgTile;
     const uint32_t wt_s = smem_u32(wtiles);
     const uintptr_t src_u = reinterpret_cast<uintptr_t>(a.src);
-    AgMap amap;
-    ag_map_init(amap, a.rec, lane);
+    AgrMap amap;
+    agr_map_init(amap, a.rec, lane);
     const uint32_t ng = (uint32_t)ngroups;
     const uint32_t nt = ng > (uint32_t)warp ? (ng - warp + kL2Warps - 1) / kL2Warps : 0;
     auto rid_load = [&](uint32_t t) -> uint32_t {
@@ -196,24 +196,26 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       return (t < nt && i < hi) ? ldg_first(a.rids + i) : 0xFFFFFFFFu;
     };
     uint32_t rq0 = rid_load(0), rq1 = rid_load(1), rq2 = rid_load(2), rq3 = rid_load(3);
-    auto grp = [&](uint32_t t) -> AgGroup {
+    auto grp = [&](uint32_t t) -> AgrGroup {
       const uint32_t r = rq0;
       rq0 = rq1;
       rq1 = rq2;
       rq2 = rq3;
       rq3 = rid_load(t + 4);
-      AgGroup q;
+      AgrGroup q;
       const uint64_t g0 = lo + 32 * (uint64_t)(warp + t * kL2Warps);
       q.cnt = (uint32_t)min_u64(32, hi - g0);
-      q.on = r < a.n_src;
-      if ((uint32_t)lane < q.cnt && !q.on) report_bad(a.status, g0 + lane);
-      q.addr = q.on ? src_u + (uint64_t)r * a.rec : src_u;
-      q.okm = __ballot_sync(0xffffffffu, q.on);
+      const bool on = r < a.n_src;
+      if ((uint32_t)lane < q.cnt && !on) report_bad(a.status, g0 + lane);
+      q.r = on ? r : 0u;          // (row 0 is read, not stored)
+      q.okm = __ballot_sync(0xffffffffu, on);
       q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
-      q.o4 = (uint32_t)(q.addr >> 2) & 3;
       return q;
     };
-    ag_pipeline(nt, grp, wtiles, wt_s, kAgTile, amap, a.rec, lane);
+    if (a.n_src * a.rec + 16 <= 0xFFFFFFFFull)
+      agr_pipeline<true>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane);
+    else
+      agr_pipeline<false>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane);
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)

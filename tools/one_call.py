@@ -19,6 +19,7 @@ ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--flags", type=lambda x: int(x, 0), default=0)
 ap.add_argument("--direct", action="store_true")
 ap.add_argument("--calls", type=int, default=2)
+ap.add_argument("--noflush", action="store_true", help="keep the L2 warm between calls")
 a = ap.parse_args()
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
@@ -31,7 +32,8 @@ lib.dpg_debug_flags.restype = None
 lib.dpg_debug_flags(a.flags)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.calls):
-    flush.fill_(1)
+    if not a.noflush:
+        flush.fill_(1)
     if a.direct:
         dpg.dpg_retrieve_direct(src, rids, dst=out)
     else:
