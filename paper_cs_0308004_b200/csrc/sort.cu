@@ -35,8 +35,7 @@ __global__ void k_sort_extract(const uint8_t* __restrict__ src, uint32_t rec, ui
       // >= key_limit is reported at its position: referential integrity)
       const uint32_t kv = __ldcs(keys_u32 + i);
       if (kv >= key_limit) report_bad(status, i);
-      khi[i] = (uint64_t)kv << 32;
-      rid[i] = (uint32_t)i;
+      khi[i] = (uint64_t)kv << 32 | (uint32_t)i;      // the rid rides in the low half
       continue;
     }
     const uint8_t* k = src + i * rec + key_off;
@@ -60,57 +59,84 @@ struct SortPassArgs {
   uint32_t* klo_out;
   uint32_t* rid_out;
   uint64_t n;
-  uint64_t chunk;        // elements per CTA (multiple of kSThreads)
+  uint64_t chunk;        // elements per CTA (multiple of the tile)
   uint32_t byte;         // key byte of this pass (0 = most significant)
-  uint32_t with_lo;      // key_bytes > 8: carry the low word
-  uint32_t* counts;      // [256 * grid]
+  uint32_t* counts;      // [grid * 256]
   uint32_t* gbar;        // monotonic grid barrier words
-  uint32_t cache;        // 1: each tile is staged in shared memory, written out as bucket runs
-  uint32_t tile;         // elements per tile (staging capacity)
 };
+
+static constexpr int kSKpt = 16;                         // elements per lane in a tile
+static constexpr uint32_t kSTile = kSThreads * kSKpt;    // 8192 elements per tile
 
 __device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, uint32_t byte) {
   return byte < 8 ? (uint32_t)(hi >> (8 * (7 - byte))) & 255u : (lo >> (8 * (11 - byte))) & 255u;
 }
 
+// The lanes of `on` (a warp ballot) whose digit d (< 256) equals this
+// lane's: eight ballots (cheaper than match.any, whose issue rate is low).
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
+  uint32_t m = on;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bit = (d >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+    m &= ~(v ^ (0u - bit));                // v if the bit is set, ~v if not
+  }
+  return m;
+}
+
+// One counting-sort pass over key byte a.byte.  LO: the key has a
+// low word (key bytes 8..11); RID: the rid travels in its own array (else it
+// is packed in the low half of the key word, numeric keys <= 4 bytes).
+//   count   the CTA's digit counts, a grid barrier, every CTA derives its
+//           bucket bases (smaller digits first, then earlier CTAs);
+//   place   the chunk in tiles of 8192: warp w takes the tile's elements
+//           [512 w, 512 w + 512) into registers (16 per lane, index order =
+//           (k, lane)), counts them per digit (warp-private counters), the
+//           16 x 256 counters become per-warp offsets into a
+//           shared-memory staging area in digit order, and every element goes
+//           to its stable position there (rank among equal digits of the same
+//           32 elements from ballots); the staged tile then leaves as one
+//           contiguous run per digit.  Four CTA barriers per tile.
+template <bool LO, bool RID>
 __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
-  // with a.cache: [chunk] khi, [chunk] klo, [chunk] rid of the chunk in bucket
-  // order (staged, then written out as one contiguous run per bucket)
   extern __shared__ __align__(16) uint8_t sdyn[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kSTile]
+  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * kSTile);   // [kSTile] (LO)
+  uint32_t* sr = sl + (LO ? kSTile : 0);                           // [kSTile] (RID)
   __shared__ uint32_t hist[256];       // CTA counts
   __shared__ uint32_t gbase[256];      // first global slot of this CTA's block of digit d
-  __shared__ uint32_t run[256];        // elements of digit d placed so far (this CTA)
-  __shared__ uint32_t wcnt[kSWarps][256];   // (row tag << 16 | count) per warp and digit
+  __shared__ uint32_t run[256];        // elements of digit d written so far (this CTA)
+  __shared__ uint32_t woff[kSWarps][256];   // per warp: counts, then staging offsets
+  __shared__ uint32_t tl[256];         // staging base of digit d in the current tile
+  __shared__ uint32_t tt[256];         // elements of digit d in the current tile
+  __shared__ uint32_t delta[256];      // gbase + run - tl: staged position -> global slot
   __shared__ uint32_t wsum[kSWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
   const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
   const uint64_t hi = min_u64(a.n, lo + a.chunk);
+  const uint32_t byte = a.byte;
   for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
-  for (uint32_t k = tid; k < kSWarps * 256; k += kSThreads) (&wcnt[0][0])[k] = 0xFFFF0000u;
   __syncthreads();
-  // ---- count ----
-  for (uint64_t i0 = lo + tid; i0 < hi; i0 += 4 * kSThreads) {
-    uint64_t kh[4];
-    uint32_t kl[4];
+  // ---- count (only the key word that holds the digit is read) ----
+  for (uint64_t i0 = lo + tid; i0 < hi; i0 += 16 * kSThreads) {
+    uint32_t dg[16];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const uint64_t i = i0 + u * kSThreads;
-      kh[u] = 0; kl[u] = 0;
-      if (i < hi) {
-        kh[u] = __ldcg(a.khi_in + i);
-        if (a.with_lo) kl[u] = __ldcg(a.klo_in + i);
-      }
+      dg[u] = 256;
+      if (i < hi) dg[u] = (!LO || byte < 8) ? digit_of(__ldcg(a.khi_in + i), 0u, byte)
+                                            : digit_of(0ull, __ldcg(a.klo_in + i), byte);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i0 + u * kSThreads < hi) atomicAdd(&hist[digit_of(kh[u], kl[u], a.byte)], 1u);
+    for (int u = 0; u < 16; ++u)
+      if (dg[u] < 256) atomicAdd(&hist[dg[u]], 1u);
   }
   __syncthreads();
   for (uint32_t d = tid; d < 256; d += kSThreads) a.counts[c * 256 + d] = hist[d];
   grid_barrier_mono(a.gbar, G);
-  // ---- bases: global (smaller digits, then earlier CTAs) and local; the
-  // CTA rows of counts are read coalesced, 8 independent loads in flight ----
+  // ---- bases: the CTA rows of counts read coalesced, 8 loads in flight ----
   if (tid < 256) {
     uint32_t tot = 0, pre = 0;
     uint32_t q = 0;
@@ -145,120 +171,99 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     gbase[tid] += off;
   }
   __syncthreads();
-  uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);
-  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * a.tile);
-  uint32_t* sr = sl + a.tile;
-  __shared__ uint32_t th[256];         // digit counts of the current tile
-  __shared__ uint32_t tl[256];         // their exclusive scan (tile staging bases)
-  uint32_t tag = 0;
-  // the CTA's chunk in tiles of a.tile elements (staged in shared memory and
-  // written out as one contiguous run per digit); rows of 512 in order
-  for (uint64_t t0 = lo; t0 < hi; t0 += a.tile) {
-    const uint64_t t1 = min_u64(hi, t0 + a.tile);
-    if (a.cache) {
-      // tile histogram and its scan
-      for (uint32_t d = tid; d < 256; d += kSThreads) th[d] = 0;
-      __syncthreads();
-      for (uint64_t i = t0 + tid; i < t1; i += kSThreads)
-        atomicAdd(&th[digit_of(__ldcg(a.khi_in + i), a.with_lo ? __ldcg(a.klo_in + i) : 0u, a.byte)], 1u);
-      __syncthreads();
-      if (tid < 256) {
-        const uint32_t x = th[tid];
-        uint32_t y = x;
+
+  const uint32_t wb = warp * 512;
+  uint64_t kh[kSKpt];
+  uint32_t kl[kSKpt], rd[kSKpt];
+  // the warp's 512 elements of the tile at t0 into registers (index order =
+  // (k, lane)); issued for the next tile before the current one is written out
+  auto load_tile = [&](uint64_t t0) {
+    const uint32_t cnt = (uint32_t)min_u64(kSTile, hi > t0 ? hi - t0 : 0);
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
-          if (lane >= d) y += t;
-        }
-        if (lane == 31) wsum[warp] = y;
-        tl[tid] = y - x;
+    for (int k = 0; k < kSKpt; ++k) {
+      const uint32_t e = wb + k * 32 + lane;
+      kh[k] = 0;
+      kl[k] = 0;
+      rd[k] = 0;
+      if (e < cnt) {
+        kh[k] = __ldcs(a.khi_in + t0 + e);
+        if (LO) kl[k] = __ldcs(a.klo_in + t0 + e);
+        if (RID) rd[k] = __ldcs(a.rid_in + t0 + e);
       }
-      __syncthreads();
-      if (tid < 256) {
-        uint32_t off = 0;
-        for (int w = 0; w < warp; ++w) off += wsum[w];
-        tl[tid] += off;
-      }
-      __syncthreads();
     }
-    // elements of this tile placed so far, per digit (the CTA's running count
-    // run[] holds the tiles before)
-    __shared__ uint32_t trun[256];
-    for (uint32_t d = tid; d < 256; d += kSThreads) trun[d] = 0;
+  };
+  load_tile(lo);
+  for (uint64_t t0 = lo; t0 < hi; t0 += kSTile) {
+    const uint32_t cnt = (uint32_t)min_u64(kSTile, hi - t0);
+    // ---- count the warp's elements per digit ----
+    uint32_t* wo = woff[warp];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wo[k * 32 + lane] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kSKpt; ++k)
+      if (wb + k * 32 + lane < cnt) atomicAdd(&wo[digit_of(kh[k], kl[k], byte)], 1u);
     __syncthreads();
-    auto load_row = [&](uint64_t r0, uint64_t& kh, uint32_t& kl, uint32_t& rd) {
-      const uint64_t i = r0 + tid;
-      kh = 0; kl = 0; rd = 0;
-      if (r0 < t1 && i < t1) {
-        kh = __ldcs(a.khi_in + i);
-        if (a.with_lo) kl = __ldcs(a.klo_in + i);
-        rd = __ldcs(a.rid_in + i);
+    // ---- per-digit tile totals, their scan (staging bases), per-warp offsets ----
+    if (tid < 256) {
+      uint32_t s2 = 0;
+#pragma unroll
+      for (int w = 0; w < kSWarps; ++w) {
+        const uint32_t x = woff[w][tid];
+        woff[w][tid] = s2;
+        s2 += x;
       }
-    };
-    uint64_t nh0, nh1;
-    uint32_t nl0, nl1, nr0, nr1;
-    load_row(t0, nh0, nl0, nr0);
-    load_row(t0 + kSThreads, nh1, nl1, nr1);
-    for (uint64_t r0 = t0; r0 < t1; r0 += kSThreads, ++tag) {
-      const uint64_t i = r0 + tid;
-      const bool on = i < t1;
-      const uint64_t kh = nh0;
-      const uint32_t kl = nl0, rd = nr0;
-      nh0 = nh1; nl0 = nl1; nr0 = nr1;
-      load_row(r0 + 2 * kSThreads, nh1, nl1, nr1);
-      const uint32_t d = on ? digit_of(kh, kl, a.byte) : 256u + lane;   // off lanes: unique dummies
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t rank = __popc(peers & lanemask_lt());
-      const uint32_t t16 = (tag & 0xFFFFu) << 16;
-      if (on && rank == 0) wcnt[warp][d] = t16 | __popc(peers);
-      __syncthreads();
+      tt[tid] = s2;
+      uint32_t y = s2;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
+        if (lane >= d) y += t;
+      }
+      if (lane == 31) wsum[warp] = y;
+      tl[tid] = y - s2;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      uint32_t off = 0;
+      for (int w = 0; w < warp; ++w) off += wsum[w];
+      tl[tid] += off;
+      delta[tid] = gbase[tid] + run[tid] - tl[tid];
+    }
+    __syncthreads();
+    // ---- place every element at its stable staging position ----
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kSKpt; ++k) {
+      const bool on = wb + k * 32 + lane < cnt;
+      const uint32_t d = digit_of(kh[k], kl[k], byte);
+      const uint32_t pm = match_digit(d, __ballot_sync(0xffffffffu, on));
       if (on) {
-        uint32_t before = 0;
-        for (int w = 0; w < warp; ++w) {
-          const uint32_t x = wcnt[w][d];
-          before += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
-        }
-        const uint32_t k = trun[d] + before + rank;   // stable rank of the element in the tile
-        if (a.cache) {
-          const uint32_t p = tl[d] + k;
-          sk[p] = kh;
-          sl[p] = kl;
-          sr[p] = rd;
-        } else {
-          const uint32_t slot = gbase[d] + run[d] + k;
-          a.khi_out[slot] = kh;
-          if (a.with_lo) a.klo_out[slot] = kl;
-          a.rid_out[slot] = rd;
-        }
+        const uint32_t pos = tl[d] + wo[d] + __popc(pm & lt);
+        sk[pos] = kh[k];
+        if (LO) sl[pos] = kl[k];
+        if (RID) sr[pos] = rd[k];
       }
-      __syncthreads();
-      if (tid < 256) {
-        uint32_t add = 0;
-        for (int w = 0; w < kSWarps; ++w) {
-          const uint32_t x = wcnt[w][tid];
-          add += (x & 0xFFFF0000u) == t16 ? (x & 0xFFFFu) : 0u;
-        }
-        trun[tid] += add;
-      }
-      __syncthreads();
+      __syncwarp();
+      if (on && (pm & lt) == 0) wo[d] += __popc(pm);
+      __syncwarp();
     }
-    if (a.cache) {
-      // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
-      // p - tl[d]: consecutive threads, consecutive slots of one bucket run ----
-      const uint32_t cnt = (uint32_t)(t1 - t0);
-      for (uint32_t p = tid; p < cnt; p += kSThreads) {
-        const uint64_t kh = sk[p];
-        const uint32_t kl = sl[p];
-        const uint32_t d = digit_of(kh, kl, a.byte);
-        const uint32_t slot = gbase[d] + run[d] + (p - tl[d]);
-        a.khi_out[slot] = kh;
-        if (a.with_lo) a.klo_out[slot] = kl;
-        a.rid_out[slot] = sr[p];
-      }
-      __syncthreads();
-    }
-    for (uint32_t d = tid; d < 256; d += kSThreads) run[d] += trun[d];
+    load_tile(t0 + kSTile);     // in flight during the write-out
     __syncthreads();
+    // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
+    // p - tl[d]: consecutive threads, consecutive slots of one digit run ----
+    for (uint32_t p = tid; p < cnt; p += kSThreads) {
+      const uint64_t k = sk[p];
+      const uint32_t l = LO ? sl[p] : 0u;
+      const uint32_t d = digit_of(k, l, byte);
+      const uint32_t slot = delta[d] + p;
+      __stcg(a.khi_out + slot, k);
+      if (LO) __stcg(a.klo_out + slot, l);
+      if (RID) __stcg(a.rid_out + slot, sr[p]);
+    }
+    __syncthreads();
+    if (tid < 256) run[tid] += tt[tid];
+    // (the next tile's first barrier orders this update before the next write-out)
   }
 }
 
@@ -266,6 +271,29 @@ __global__ void k_keys_u32(const uint64_t* __restrict__ khi, uint64_t n, uint32_
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = (uint32_t)(__ldcs(khi + i) >> 32);
+}
+
+__global__ void k_unpack(const uint64_t* __restrict__ khi, uint64_t n, uint32_t* __restrict__ rids,
+                         uint32_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = __ldcs(khi + i);
+    rids[i] = (uint32_t)x;
+    if (keys) keys[i] = (uint32_t)(x >> 32);
+  }
+}
+
+template <bool LO, bool RID>
+static cudaError_t set_pass_smem() {
+  static int set_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev == dev) return cudaSuccess;
+  const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSTile;
+  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (e == cudaSuccess) set_dev = dev;
+  return e;
 }
 
 cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
@@ -281,9 +309,19 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   uint32_t* rid0 = reinterpret_cast<uint32_t*>(p);
   p += al(4 * n);
   uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+  // numeric keys (<= 4 bytes): the rid rides in the low half of the key word;
+  // only the key bytes a key below key_limit can have nonzero are sorted on
+  const bool packed = keys_u32 != nullptr;
+  uint32_t first = 0;
+  if (packed && key_limit != ~0ull) {
+    uint32_t kb = 0;
+    for (uint64_t m = key_limit > 0 ? key_limit - 1 : 0; m; m >>= 8) ++kb;
+    first = 4 - max(kb, 1u);
+  }
+  const uint32_t passes = key_bytes - first;
   uint32_t* rid[2] = {rid0, rids_out};
   // the passes alternate buffers; start so that the last pass lands in rids_out
-  if (key_bytes % 2 == 0) {
+  if (passes % 2 == 0) {
     uint32_t* t = rid[0];
     rid[0] = rid[1];
     rid[1] = t;
@@ -293,26 +331,15 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0],
                                     keys_u32, key_limit, status);
   cudaError_t e = cudaGetLastError();
-  const uint64_t chunk = ((n + sm - 1) / sm + kSThreads - 1) / kSThreads * kSThreads;
-  // staging of one tile (16 B per element): 8192 elements = 128 KB
-  const uint32_t tile = 8192;
-  uint32_t dyn = 16 * tile;
-  {
-    static int set_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (set_dev != dev) {
-      if (cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
-          cudaSuccess) {
-        cudaGetLastError();
-        dyn = 0;
-      } else {
-        set_dev = dev;
-      }
-    }
-  }
+  const bool lo_w = key_bytes > 8;
+  if (e == cudaSuccess)
+    e = packed ? set_pass_smem<false, false>() : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
+  const uint64_t chunk = ((n + sm - 1) / sm + kSTile - 1) / kSTile * kSTile;
+  const uint32_t dyn = (8 + (lo_w ? 4 : 0) + (packed ? 0 : 4)) * kSTile;
+  const void* fn = packed ? (const void*)k_sort_pass<false, false>
+                          : lo_w ? (const void*)k_sort_pass<true, true> : (const void*)k_sort_pass<false, true>;
   uint32_t in = 0;
-  for (int byte = (int)key_bytes - 1; byte >= 0 && e == cudaSuccess; --byte, in ^= 1) {
+  for (int byte = (int)key_bytes - 1; byte >= (int)first && e == cudaSuccess; --byte, in ^= 1) {
     SortPassArgs s;
     s.khi_in = khi[in];
     s.klo_in = klo[in];
@@ -323,20 +350,20 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     s.n = n;
     s.chunk = chunk;
     s.byte = (uint32_t)byte;
-    s.with_lo = key_bytes > 8;
     s.counts = counts;
     s.gbar = gbar;
-    s.cache = dyn ? 1 : 0;
-    s.tile = dyn ? tile : kSThreads;
     void* params[] = {&s};
     ++*nl;
-    e = cudaLaunchCooperativeKernel((const void*)k_sort_pass, dim3(sm), dim3(kSThreads), params, dyn,
-                                    st);
+    e = cudaLaunchCooperativeKernel(fn, dim3(sm), dim3(kSThreads), params, dyn, st);
   }
-  if (e == cudaSuccess && keys_out) {
-    // the sorted keys (numeric mode): the last pass's key buffer
+  if (e == cudaSuccess && packed) {
+    // the sorted (key, rid) words of the last pass: rids (and keys) out
     ++*nl;
-    k_keys_u32<<<g, 256, 0, st>>>(khi[key_bytes % 2], n, keys_out);
+    k_unpack<<<g, 256, 0, st>>>(khi[passes % 2], n, rids_out, keys_out);
+    e = cudaGetLastError();
+  } else if (e == cudaSuccess && keys_out) {
+    ++*nl;
+    k_keys_u32<<<g, 256, 0, st>>>(khi[passes % 2], n, keys_out);
     e = cudaGetLastError();
   }
   return e;
