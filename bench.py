@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dpg", choices=["dpg", "reference"])
-    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c5"],
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c4x", "c5"],
                     help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
     ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
     ap.add_argument("--c5-round-rows", type=int, default=1 << 26)
@@ -74,6 +74,7 @@ def workload_name(cfg: str, rec: int | None) -> str:
             "c3a": f"c3a: 16,777,216 x {rec} B, uniform random permutation",
             "c3b": f"c3b: 16,777,216 x {rec} B, uniform rids with replacement",
             "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)",
+            "c4x": "c4x: config 4 with the paper's exponential join keys (P:890-892)",
             "c5": "c5 sample for the host oracle: 2^22 x 100 B of the c5 source stream, "
                   "rids = c5 Feistel permutation of [0, 2^22)"}[cfg]
 
@@ -88,7 +89,7 @@ def make_inputs(cfg: str, rec: int | None):
 def units(cfg, w):
     """(n_out, rec, algorithmic bytes per step, rid bytes) per SURVEY 8(d):
     B = N * (2 * rec + rid_bytes)."""
-    if cfg == "c4":
+    if cfg in ("c4", "c4x"):
         n_out = w["fk"].size
         rec = w["dim"].shape[1] + w["fact"].shape[1]          # 80-byte output rows
         # join rows: read fk (4) + fact payload (16) + dim record (64), write 80
@@ -180,7 +181,7 @@ def cpu_baseline(cfg, w, budget_s=10.0):
     host, repeated over the full workload until ~budget_s of CPU work."""
     import oracle
     n_out, rec, alg_bytes, _ = units(cfg, w)
-    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg == "c4" else \
+    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg in ("c4", "c4x") else \
         (lambda: oracle.retrieve(w["src"], w["rids"]))
     fn()  # warm (page in)
     reps, t0 = 0, time.perf_counter()
@@ -226,7 +227,7 @@ def run_reference(args):
         w = make_inputs(cfg, args.rec)
     import oracle
     n_out, rec, alg_bytes, _ = units(cfg, w)
-    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg == "c4" else \
+    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg in ("c4", "c4x") else \
         (lambda: oracle.retrieve(w["src"], w["rids"]))
     for _ in range(max(0, min(args.warmup, 3))):
         fn()
@@ -365,7 +366,7 @@ def main():
             a = a.view(np.int32)
         return torch.from_numpy(a).to(dev)
 
-    if cfg == "c4":
+    if cfg in ("c4", "c4x"):
         fact, fk, dim = to_dev(w["fact"]), to_dev(w["fk"]), to_dev(w["dim"])
         out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
         step = lambda: dpg.dpg_fk_join(fact, fk, dim, out=out)
@@ -476,7 +477,7 @@ def main():
                             "(10 passes) + dpg_retrieve"}
     # the paper's DPG-Sort join: the same join in fk order
     join_sort_res = None
-    if cfg == "c4" and not args.no_sort:
+    if cfg in ("c4", "c4x") and not args.no_sort:
         js = lambda: dpg.dpg_fk_join_sort(fact, fk, dim, out=out)
         for _ in range(2):
             js()
@@ -493,9 +494,9 @@ def main():
     dist_ms, probe_ms, calls = ph
     pg_ms = probe_ms / max(1, calls)
     # (the join runs a DPG retrieval of dim rows -- no payload -- then a zip pass)
-    plan = dpg.dpg_plan(rec if cfg != "c4" else w["dim"].shape[1], n_src, n_out, 0,
+    plan = dpg.dpg_plan(rec if cfg not in ("c4", "c4x") else w["dim"].shape[1], n_src, n_out, 0,
                         torch.cuda.get_device_properties(dev).multi_processor_count)
-    src_rec = w["dim"].shape[1] if cfg == "c4" else rec
+    src_rec = w["dim"].shape[1] if cfg in ("c4", "c4x") else rec
     pay = 0
     if plan["path"] == 5:
         # K staged L2 runs probed into INTERNAL + the Phase III gather: the
@@ -529,7 +530,7 @@ def main():
 
     # end to end through the host-buffer C-ABI entry
     e2e = None
-    if not args.no_e2e and cfg != "c4":
+    if not args.no_e2e and cfg not in ("c4", "c4x"):
         hs = torch.from_numpy(w["src"]).pin_memory()
         hr = torch.from_numpy(w["rids"].view(np.int32)).pin_memory()
         hd = torch.empty((n_out, rec), dtype=torch.uint8).pin_memory()

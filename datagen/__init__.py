@@ -16,6 +16,9 @@ Workloads (BASELINE.json ``configs``):
 * ``c3b`` same, rids iid uniform with replacement
 * ``c4``  dimension 16,777,216 x 64 B; fact 67,108,864 x (uint32 fk uniform in
   [0, 2^24) ++ 16-byte payload) -- the DPG-Move join
+* ``c4x`` config 4 with the paper's non-uniform foreign keys:
+  fk = min(n_dim - 1, floor(n_dim * exp(c * (r >> 10)))), r a uniform 31-bit
+  draw (the range of UNIX random()), c = -1e-7 (reading A18 in DESIGN.md)
 * ``c5``  2^30 x 100 B, rids = Feistel permutation (uint64), evaluated pointwise
 
 These synthetic inputs stand in for the paper's workloads (Datamation
@@ -41,7 +44,7 @@ STREAMS = {
     ("c1", "src"): 0x101, ("c1", "rids"): 0x102,
     ("c2", "src"): 0x201,
     ("c3", "src"): 0x301, ("c3a", "rids"): 0x302, ("c3b", "rids"): 0x303,
-    ("c4", "dim"): 0x401, ("c4", "fact"): 0x402, ("c4", "fk"): 0x403,
+    ("c4", "dim"): 0x401, ("c4", "fact"): 0x402, ("c4", "fk"): 0x403, ("c4x", "fk"): 0x404,
     ("c5", "src"): 0x501, ("c5", "rids"): 0x502,
     ("test", "src"): 0x901, ("test", "rids"): 0x902,
 }
@@ -167,6 +170,16 @@ def feistel(n: int, first: int, count: int, sid: int, seed: int = SEED,
     return out
 
 
+def exp_fk(n: int, n_dim: int, sid: int, seed: int = SEED, c: float = -1e-7) -> np.ndarray:
+    """The paper's exponential join keys, exp(c * (random() >> 10))
+    with random() a uniform 31-bit draw, scaled to the key domain [0, n_dim)
+    (reading A18): uint32, concentrated in the top ~19% of the domain with
+    density proportional to 1/key."""
+    r = uniform(n, 2 ** 31, sid, seed).astype(np.int64)
+    y = np.exp(c * (r >> 10).astype(np.float64))
+    return np.minimum(n_dim - 1, np.floor(n_dim * y)).astype(np.uint32)
+
+
 def stable_key_argsort(recs: np.ndarray, key_len: int = 10) -> np.ndarray:
     """Stable argsort of the records' key bytes (offset 0, unsigned
     lexicographic), ties by ascending rid (reading A10).  Part of the input
@@ -199,10 +212,11 @@ def make(config: str, rec: int | None = None, scale: int = 1) -> dict:
         else:
             rids = uniform(n, n, STREAMS[("c3b", "rids")])
         return {"src": src, "rids": rids}
-    if config == "c4":
+    if config in ("c4", "c4x"):
         n_dim = 16777216 // scale
         n_fact = 67108864 // scale
+        fk = uniform(n_fact, n_dim, STREAMS[("c4", "fk")]) if config == "c4" else \
+            exp_fk(n_fact, n_dim, STREAMS[("c4x", "fk")])
         return {"dim": records(n_dim, 64, STREAMS[("c4", "dim")]),
-                "fact": records(n_fact, 16, STREAMS[("c4", "fact")]),
-                "fk": uniform(n_fact, n_dim, STREAMS[("c4", "fk")])}
+                "fact": records(n_fact, 16, STREAMS[("c4", "fact")]), "fk": fk}
     raise KeyError(config)

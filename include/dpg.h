@@ -270,6 +270,15 @@ const char *dpg_status_string(dpg_status_t status);
 /* Number of kernel launches the most recent call on this host thread enqueued. */
 uint32_t dpg_last_launch_count(void);
 
+/* Plan path (dpg_plan_t.path) the most recent dpg_retrieve / dpg_fk_join on
+ * this host thread ran.  With the automatic plan, an input of >= 4 Mi rids
+ * planned on shared-memory runs (path 1) is first sampled for data skew
+ * (section 2.3: 65,536 rids at evenly spaced positions, counted
+ * per group of runs; one stream synchronisation); when the estimated rids
+ * beyond the runs' fixed capacity exceed 2% of the input, the call runs the
+ * count-based L2 runs (path 5) instead, whose run sizes are exact. */
+uint32_t dpg_last_path(void);
+
 /* Phase timing (bench.py's roofline): while enabled, every dpg_retrieve /
  * dpg_fk_join call records CUDA events on its own stream around Phase I
  * (distribute) and the fused probe-gather kernel.  dpg_phase_times

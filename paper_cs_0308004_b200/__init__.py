@@ -41,7 +41,7 @@ EXPORTED = (
     "dpg_fk_join_ex", "dpg_distribute", "dpg_scatter_rows", "dpg_retrieve_host",
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
-    "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition",
+    "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
 )
 
 
@@ -104,6 +104,7 @@ for _name, _args in _sigs.items():
 _lib.dpg_status_string.argtypes = [_st]
 _lib.dpg_status_string.restype = ctypes.c_char_p
 _lib.dpg_last_launch_count.restype = ctypes.c_uint32
+_lib.dpg_last_path.restype = ctypes.c_uint32
 _lib.dpg_version.restype = ctypes.c_int
 _lib.dpg_release_cache.restype = None
 _lib.dpg_phase_timing.argtypes = [ctypes.c_int]
@@ -142,6 +143,12 @@ def dpg_plan(rec_bytes: int, n_src: int, n_out: int, pay_bytes: int = 0, sm_coun
 
 def last_launch_count() -> int:
     return int(_lib.dpg_last_launch_count())
+
+
+def last_path() -> int:
+    """Plan path the last dpg_retrieve / dpg_fk_join on this thread ran (after
+    the data skew check)."""
+    return int(_lib.dpg_last_path())
 
 
 def dpg_phase_timing(enable: bool = True):

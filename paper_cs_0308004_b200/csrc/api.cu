@@ -20,6 +20,7 @@ constexpr uint32_t kBarBytes = 128;
 constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives in smem
 
 thread_local uint32_t t_launches = 0;
+thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
 unsigned long long* g_debug_ts = nullptr;
 uint32_t g_debug_flags = 0;            // tuning experiments only (dpg_debug_flags)  // profiling: per-CTA phase stamps of the fused kernel
 
@@ -547,6 +548,43 @@ dpg_status_t cuda_status(cudaError_t e) {
 }
 
 // Shared body of dpg_retrieve and dpg_fk_join: rows of (pay ++ rec) bytes.
+constexpr uint64_t kSkewMinRids = 1ull << 22;   // sample inputs from 4 Mi rids on
+constexpr uint32_t kSkewSamples = 65536;
+
+// Estimated rids beyond the fixed run capacity of plan p (skew.cu): S sampled
+// rids counted per group of runs on the device, the estimate read back (one
+// stream synchronisation).
+dpg_status_t skew_excess(const uint32_t* rids, uint64_t n_out, uint64_t n_src, const dpg_plan_t& p,
+                         cudaStream_t st, uint64_t* excess, uint32_t* nl) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, uint8_t*>> bufs;     // per device: [result | hist]
+  static unsigned long long* host = nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DPG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  uint8_t* b = nullptr;
+  for (auto& kv : bufs)
+    if (kv.first == dev) b = kv.second;
+  const uint64_t words = kSkewSamples / 64 + 2;           // groups of >= 64 expected samples
+  if (!b) {
+    if (cudaMalloc(&b, 256 + words * 4) != cudaSuccess) { cudaGetLastError(); return DPG_ERR_OOM; }
+    if (cudaMemset(b, 0, 256 + words * 4) != cudaSuccess) return DPG_ERR_CUDA;
+    bufs.push_back({dev, b});
+  }
+  if (!host && cudaMallocHost(&host, sizeof(*host)) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  cudaError_t e = launch_skew_check(rids, n_out, n_src, p.log2_run, (uint32_t)p.num_runs,
+                                    p.slot_pairs, kSkewSamples, (uint32_t*)(b + 256),
+                                    (unsigned long long*)b, st, nl);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host, b, sizeof(*host), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  *excess = *host;
+  return DPG_OK;
+}
+
 dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32_t* rids,
                      uint64_t n_out, const void* pay_src, uint64_t pay, void* dst,
                      cudaStream_t st, const dpg_options_t* opt) {
@@ -579,6 +617,25 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (ps != DPG_OK) return ps;
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
+  uint32_t nl_skew = 0;
+  {
+    // Data skew (section 2.3): a large input planned on fixed
+    // shared-memory runs is sampled first; a rid list that would overflow the
+    // runs' capacity takes the count-based L2 runs (exact run sizes) instead.
+    const bool auto_plan = !opt || (opt->path == 0 && !opt->log2_run && !opt->grid_distribute &&
+                                    !opt->grid_probe && !opt->hist_mode && !opt->gather &&
+                                    !opt->pair_bytes);
+    if (auto_plan && p.path == 1 && pay == 0 && n_out >= kSkewMinRids && !(g_debug_flags & 64)) {
+      uint64_t excess = 0;
+      dpg_status_t ks = skew_excess(rids, n_out, n_src, p, st, &excess, &nl_skew);
+      if (ks != DPG_OK) return ks;
+      dpg_plan_t q;
+      if (excess > n_out / 50 &&
+          plan_l2k(rec, n_src, n_out, 0, false, 0, sm, current_l2_bytes(), &q))
+        p = q;
+    }
+  }
+  t_path = p.path;
 
   if (p.path == 5) {
     const uint32_t G = p.grid_probe, K = (uint32_t)p.num_runs;
@@ -653,7 +710,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       e = launch_l2run(l, W, G, st, &nl);
     }
     if (timed) cudaEventRecord(pe.e2, st);
-    t_launches = nl;
+    t_launches = nl + nl_skew;
     return cuda_status(e);
   }
   if (p.path == 4 && ((uintptr_t)src % 16 || (uintptr_t)dst % 16)) {
@@ -690,7 +747,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     if (timed) cudaEventRecord(pe.e1, st);
     cudaError_t e = launch_l2pair(l, p.grid_probe, st, &nl);
     if (timed) cudaEventRecord(pe.e2, st);
-    t_launches = nl;
+    t_launches = nl + nl_skew;
     return cuda_status(e);
   }
   if (p.path == 3) {
@@ -723,7 +780,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     if (timed) cudaEventRecord(pe.e1, st);   // Phase I is empty (one run)
     cudaError_t e = launch_l2run(l, W, p.grid_probe, st, &nl);
     if (timed) cudaEventRecord(pe.e2, st);
-    t_launches = nl;
+    t_launches = nl + nl_skew;
     return cuda_status(e);
   }
 
@@ -804,7 +861,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
                         st, &nl, /*hint=*/1);
     }
     if (timed) cudaEventRecord(pe.e2, st);
-    t_launches = nl;
+    t_launches = nl + nl_skew;
     return cuda_status(e);
   }
 
@@ -862,7 +919,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   }
   if (timed) cudaEventRecord(pe.e2, st);
   cudaFreeAsync(w.base, st);
-  t_launches = nl;
+  t_launches = nl + nl_skew;
   return cuda_status(e);
 }
 
@@ -871,6 +928,8 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
 extern "C" {
 
 int dpg_version(void) { return 1; }
+
+uint32_t dpg_last_path(void) { return t_path; }
 
 uint32_t dpg_last_launch_count(void) { return t_launches; }
 

@@ -444,6 +444,11 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
                              int sm, cudaStream_t st, uint32_t* nlaunch,
                              const uint32_t* keys_u32 = nullptr, uint32_t* keys_out = nullptr,
                              uint64_t key_limit = ~0ull, unsigned long long* status = nullptr);
+// Data skew check (skew.cu): estimated rids beyond the fixed run
+// capacity from S evenly spaced samples; hist: ceil(K / group) zeroed words.
+cudaError_t launch_skew_check(const uint32_t* rids, uint64_t n_out, uint64_t n_src, uint32_t s,
+                              uint32_t K, uint32_t cap, uint32_t S, uint32_t* hist,
+                              unsigned long long* out, cudaStream_t st, uint32_t* nl);
 cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                               uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
                               int sm, cudaStream_t st, uint32_t* nlaunch);

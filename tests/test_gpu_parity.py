@@ -560,3 +560,36 @@ def test_fk_join_sort_config_4_scaled_and_integrity(dpg):
     with pytest.raises(dpg.DPGError) as e:
         dpg.dpg_sync_status()
     assert e.value.index == 123
+
+
+# --------------------------------------------------------------------------
+# The paper's non-uniform join keys (reading A18): both joins on
+# every plan the join can take.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("opts", [{}, {"path": 1, "gather": 1}, {"path": 1, "gather": 2},
+                                  {"path": 2}, {"path": 5, "log2_run": 14}])
+def test_fk_join_exponential_keys(dpg, opts):
+    w = datagen.make("c4x", scale=16)
+    want = oracle.fk_join(w["fact"], w["fk"], w["dim"])
+    got = host(dpg.dpg_fk_join(dev(w["fact"]), dev(w["fk"]), dev(w["dim"]), **opts))
+    assert np.array_equal(got, want), opts
+
+
+def test_fk_join_sort_exponential_keys(dpg):
+    w = datagen.make("c4x", scale=16)
+    got = host(dpg.dpg_fk_join_sort(dev(w["fact"]), dev(w["fk"]), dev(w["dim"])))
+    assert np.array_equal(got, oracle.fk_join_sort(w["fact"], w["fk"], w["dim"]))
+
+
+def test_skew_check_switches_plan(dpg):
+    """Section 2.3: a large rid list that would overflow the fixed
+    shared-memory runs (the exponential join keys) is detected by sampling and
+    runs on the count-based L2 runs; a uniform list keeps the fixed runs."""
+    for cfg, want in (("c4x", 5), ("c4", 1)):
+        w = datagen.make(cfg, scale=4)
+        d = dpg.dpg_fk_join(dev(w["fact"]), dev(w["fk"]), dev(w["dim"]))
+        assert dpg.last_path() == want, cfg
+        got = host(d)
+        i = np.random.default_rng(1).integers(0, w["fk"].size, 20000)
+        assert np.array_equal(got[i, :16], w["fact"][i])
+        assert np.array_equal(got[i, 16:], w["dim"][w["fk"][i].astype(np.int64)])

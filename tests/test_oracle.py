@@ -307,3 +307,15 @@ def test_fk_join_sort_oracle_is_the_move_join_in_fk_order():
     fk[17 % max(1, fk.size)] = n_dim
     with pytest.raises(oracle.RidRangeError):
         oracle.fk_join_sort(fact, fk, dim)
+
+
+def test_exponential_fk_generator_shape():
+    """Reading A18: exp(c * (r >> 10)) with r < 2^31 and c = -1e-7
+    lies in (e^{-0.2097152}, 1], so the keys fill [0.8108 n_dim, n_dim) with a
+    density falling as 1/key."""
+    n_dim = 1 << 16
+    fk = datagen.exp_fk(200000, n_dim, datagen.STREAMS[("c4x", "fk")])
+    assert fk.dtype == np.uint32 and fk.max() < n_dim
+    assert fk.min() >= int(np.floor(n_dim * np.exp(-1e-7 * ((2 ** 31 - 1) >> 10))))
+    h = np.histogram(fk, bins=4, range=(int(0.8109 * n_dim), n_dim))[0]
+    assert np.all(np.diff(h) < 0)
