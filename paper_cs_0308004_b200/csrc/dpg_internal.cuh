@@ -753,17 +753,23 @@ struct AgrGroup {
 template <bool OFF32, typename F>
 __device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, uint8_t* wtiles, uint32_t wt_s,
                                              uint32_t tile_bytes, const AgrMap& amap, uintptr_t base,
-                                             uint32_t rec, uint32_t lane) {
+                                             uint32_t rec, uint32_t lane, uint32_t dbg = 0) {
+  // dbg (experiments, tools/engine_probe.py): bit 20 skips the consume step,
+  // bit 21 the issue step (the output is then wrong)
+  const bool no_consume = dbg & (1u << 20), no_issue = dbg & (1u << 21);
   const AgrLane L = agr_lane(base, rec, lane);
   AgrGroup q0{}, q1{}, q2{};
-  if (0 < nt) { q0 = group(0); agr_issue<OFF32>(wt_s, rec, q0.r, L); }
+  if (0 < nt) { q0 = group(0); if (!no_issue) agr_issue<OFF32>(wt_s, rec, q0.r, L); }
   cp_async_commit();
-  if (1 < nt) { q1 = group(1); agr_issue<OFF32>(wt_s + tile_bytes, rec, q1.r, L); }
+  if (1 < nt) { q1 = group(1); if (!no_issue) agr_issue<OFF32>(wt_s + tile_bytes, rec, q1.r, L); }
   cp_async_commit();
   uint32_t slot = 0;
   for (uint32_t t = 0; t < nt; ++t) {
     const uint32_t slot2 = slot == 0 ? 2 : slot - 1;
-    if (t + 2 < nt) { q2 = group(t + 2); agr_issue<OFF32>(wt_s + slot2 * tile_bytes, rec, q2.r, L); }
+    if (t + 2 < nt) {
+      q2 = group(t + 2);
+      if (!no_issue) agr_issue<OFF32>(wt_s + slot2 * tile_bytes, rec, q2.r, L);
+    }
     cp_async_commit();
     const uint32_t o4 = (L.bl + q0.r * rec) >> 2 & 3u;   // (base + r*rec) >> 2 & 3
     const uint32_t nx = __shfl_down_sync(0xffffffffu, o4, 1);
@@ -771,7 +777,8 @@ __device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, uint8_t* wtil
     __syncwarp();
     const uint8_t* ts = wtiles + slot * tile_bytes;
     const uint32_t full = q0.cnt == 32 ? 0xffffffffu : ((1u << q0.cnt) - 1u);
-    if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * rec)) & 15) == 0)
+    if (no_consume) {
+    } else if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * rec)) & 15) == 0)
       agr_consume16(ts, (o4 << 2) | (nx << 18), amap, q0.cnt, rec, q0.out, lane);
     else
       ag_consume(reinterpret_cast<const uint32_t*>(wtiles + slot * tile_bytes), o4, q0.okm, q0.cnt,

@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       return q;
     };
     if (a.n_src * a.rec + 16 <= 0xFFFFFFFFull)
-      agr_pipeline<true>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane);
+      agr_pipeline<true>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
     else
-      agr_pipeline<false>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane);
+      agr_pipeline<false>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)
