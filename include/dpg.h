@@ -234,6 +234,26 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* Retrieval into output segments: D[k] = R[rids[k]] as dpg_retrieve, with
+ * output row k of segment q (rows seg_rows[0] + ... + seg_rows[q-1] up to the
+ * next boundary) written to seg_dst[q] + (k - first row of q) * rec_bytes.
+ * nseg in [1, 8]; seg_rows and seg_dst are HOST arrays of nseg entries (the
+ * row counts must sum to n_out); each seg_dst[q] is a device pointer, and it
+ * may be a peer GPU's memory mapped into this process (dpg_ipc_open): the
+ * multi-GPU exchange uses this to write an owner's replies straight into each
+ * requester's receive window over NVLink, with no reply buffer and no
+ * separate collective for the records (north_star config 5; SV 8(f) #1).
+ * The plan is dpg_retrieve's: shared-memory runs write each staged record to
+ * its segment row; the L2 run and the K-run L2 plan's last gather do the
+ * same per 32-row group (4-byte-multiple records of 8..116 bytes); other
+ * records use one direct gather per segment.  Errors as dpg_retrieve
+ * (DPG_ERR_INVALID_ARG also for counts that do not sum to n_out, a NULL
+ * segment with rows, or a segment overlapping src or rids).  Asynchronous. */
+dpg_status_t dpg_retrieve_segments(const void *src, size_t rec_bytes, uint64_t n_src,
+                                   const uint32_t *rids, uint64_t n_out, uint32_t nseg,
+                                   const uint64_t *seg_rows, void *const *seg_dst,
+                                   dpg_stream_t stream);
+
 /* DPG-Sort join: the join pairs (rid_R = i, rid_F =
  * fk_col[i]) sorted by rid_F (stable), the fact rows (R) moved into a
  * temporary file in that order by DPG retrieval, then joined with dim (F)

@@ -96,6 +96,7 @@ _sigs = {
     "dpg_gather_rows": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
     "dpg_fk_join_sort": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
+    "dpg_retrieve_segments": [_P, _S, _U, _P, _U, ctypes.c_uint32, _P, _P, _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -362,6 +363,25 @@ def dpg_retrieve_host(src, rids, dst, stream=None):
     _check(_lib.dpg_retrieve_host(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
                                   dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_host")
     return dst
+
+
+def dpg_retrieve_segments(src, rids, seg_rows, seg_dst, stream=None):
+    """D[k] = src[rids[k]] with the output split into segments: the rows of
+    segment q go to seg_dst[q] (a uint8 CUDA tensor, or an integer device
+    address such as a peer window from ipc_open) in order."""
+    src = _records(src, "src")
+    rids = _rid_tensor(rids, "rids")
+    n_src, rec = src.shape
+    nseg = len(seg_rows)
+    if nseg != len(seg_dst):
+        raise ValueError("seg_rows and seg_dst differ in length")
+    rows = (ctypes.c_uint64 * nseg)(*[int(x) for x in seg_rows])
+    ptrs = (ctypes.c_void_p * nseg)(*[int(d) if isinstance(d, int) else d.data_ptr()
+                                      for d in seg_dst])
+    _check(_lib.dpg_retrieve_segments(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
+                                      nseg, ctypes.cast(rows, ctypes.c_void_p),
+                                      ctypes.cast(ptrs, ctypes.c_void_p), _stream_ptr(stream)),
+           "dpg_retrieve_segments")
 
 
 def dpg_fk_join_sort(fact, fk_col, dim, out=None, stream=None):

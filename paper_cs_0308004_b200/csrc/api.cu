@@ -21,6 +21,8 @@ constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives 
 
 thread_local uint32_t t_launches = 0;
 thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
+thread_local const OutSegs* t_seg = nullptr;   // output segments of the current call (or none)
+thread_local bool g_seg_nostage = false;        // segmented call re-planned onto path 3 past the L2
 unsigned long long* g_debug_ts = nullptr;
 uint32_t g_debug_flags = 0;            // tuning experiments only (dpg_debug_flags)  // profiling: per-CTA phase stamps of the fused kernel
 
@@ -600,8 +602,9 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (__builtin_mul_overflow(n_out, row, &dst_bytes)) return DPG_ERR_INVALID_ARG;
   if (__builtin_mul_overflow(n_out, pay, &pay_bytes_total)) return DPG_ERR_INVALID_ARG;
   if (rec > UINT32_MAX / 2 || row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
-  if (overlaps(dst, dst_bytes, src, src_bytes) || overlaps(dst, dst_bytes, rids, n_out * 4) ||
-      (pay && overlaps(dst, dst_bytes, pay_src, pay_bytes_total)))
+  if (!t_seg &&   // (segmented output: each segment was checked by dpg_retrieve_segments)
+      (overlaps(dst, dst_bytes, src, src_bytes) || overlaps(dst, dst_bytes, rids, n_out * 4) ||
+       (pay && overlaps(dst, dst_bytes, pay_src, pay_bytes_total))))
     return DPG_ERR_INVALID_ARG;
 
   const int sm = current_sm_count();
@@ -633,6 +636,37 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       if (excess > n_out / 50 &&
           plan_l2k(rec, n_src, n_out, 0, false, 0, sm, current_l2_bytes(), &q))
         p = q;
+    }
+  }
+  if (t_seg) {
+    // output segments: the plans whose last writer is the fused probe (mode 0)
+    // or the window gather; others take the window gather without staging
+    const OutSegs& sg = *t_seg;
+    bool al4 = true;
+    for (uint32_t q = 0; q < sg.n; ++q) al4 = al4 && ((uintptr_t)sg.out[q] % 4 == 0);
+    const bool agr_ok = rec % 4 == 0 && rec >= 8 && rec <= 116 && al4 && (uintptr_t)src % 4 == 0;
+    if (p.path == 1 && pay == 0) {
+      p.gather = 1;
+    } else if (p.path == 5 && agr_ok) {
+    } else if (agr_ok && n_src * rec <= ((uint64_t)1 << 32)) {
+      dpg_options_t o{};
+      o.path = 3;
+      if (make_plan(rec, n_src, n_out, 0, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
+      if (p.path == 3 && n_src * rec > l2_budget(current_l2_bytes())) g_seg_nostage = true;
+    } else {
+      // any other record: the direct gather, one launch per segment
+      uint32_t nl = 0;
+      for (uint32_t q = 0; q < sg.n; ++q) {
+        const uint64_t k0 = sg.start[q], k1 = sg.start[q + 1];
+        if (k1 == k0) continue;
+        dpg_status_t ds = dpg_retrieve_direct(src, rec, n_src, rids + k0, k1 - k0, sg.out[q],
+                                              (dpg_stream_t)st);
+        nl += t_launches;
+        if (ds != DPG_OK) return ds;
+      }
+      t_path = 0;
+      t_launches = nl + nl_skew;
+      return DPG_OK;
     }
   }
   t_path = p.path;
@@ -705,8 +739,12 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       l.dst = (uint8_t*)dst;
       l.gbar = gbar;
       l.stage = 0;
+      if (t_seg) {
+        l.seg = *t_seg;
+        l.dst = t_seg->out[0];
+      }
       if (rec % 4 == 0) l.rd_magic = (uint32_t)(((1ull << 32) + rec / 4 - 1) / (rec / 4));
-      const uint32_t W = pow2_divisor(rec | (uintptr_t)internal | (uintptr_t)dst);
+      const uint32_t W = t_seg ? 4u : pow2_divisor(rec | (uintptr_t)internal | (uintptr_t)dst);
       e = launch_l2run(l, W, G, st, &nl);
     }
     if (timed) cudaEventRecord(pe.e2, st);
@@ -773,7 +811,15 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     if (l.dbg >> 24) l.stage_bytes = (uint64_t)(l.dbg >> 24) << 20;   // tuning: MB staged
     if ((l.dbg >> 8) & 15) l.ring_chunk = 1024u << ((l.dbg >> 8) & 15);   // tuning: 2^k KB
     if ((l.dbg >> 12) & 15) l.ring_slots = (l.dbg >> 12) & 15;
-    const uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
+    uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst);
+    if (t_seg) {
+      // segmented output: the window gather (REALIGN 1) with the segments
+      l.seg = *t_seg;
+      l.dst = t_seg->out[0];
+      W = 4;
+      if (g_seg_nostage) l.stage = 0;   // a source beyond the L2 budget: no Phase II
+      g_seg_nostage = false;
+    }
     uint32_t nl = 0;
     PhaseEvents pe;
     const bool timed = timing_begin(st, &pe);
@@ -819,6 +865,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.pairs = pairs;
     f.pair_bytes = p.pair_bytes;
     f.dst = (uint8_t*)dst;
+    if (t_seg) f.seg = *t_seg;   // mode 0 writes each row to its segment
     f.row_bytes = (uint32_t)row;
     f.slot_pairs = p.slot_pairs;
     f.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
@@ -843,7 +890,10 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       ns = std::max<uint64_t>(ns, p.npre);
       f.n_static = (uint32_t)std::min<uint64_t>(ns, (K + G - 1) / G);
     }
-    uint32_t W = pow2_divisor(rec | (uintptr_t)src | (uintptr_t)dst |
+    uintptr_t outs = (uintptr_t)dst;
+    if (t_seg)
+      for (uint32_t q = 0; q < t_seg->n; ++q) outs |= (uintptr_t)t_seg->out[q];
+    uint32_t W = pow2_divisor(rec | (uintptr_t)src | outs |
                               (f.mode == 1 ? (uintptr_t)f.internal : 0));
     uint32_t nl = 0;
     PhaseEvents pe;
@@ -987,6 +1037,43 @@ dpg_status_t dpg_retrieve_ex(const void* src, size_t rec_bytes, uint64_t n_src,
 dpg_status_t dpg_retrieve(const void* src, size_t rec_bytes, uint64_t n_src, const uint32_t* rids,
                           uint64_t n_out, void* dst, dpg_stream_t stream) {
   return dpg_retrieve_ex(src, rec_bytes, n_src, rids, n_out, dst, stream, nullptr);
+}
+
+dpg_status_t dpg_retrieve_segments(const void* src, size_t rec_bytes, uint64_t n_src,
+                                   const uint32_t* rids, uint64_t n_out, uint32_t nseg,
+                                   const uint64_t* seg_rows, void* const* seg_dst,
+                                   dpg_stream_t stream) {
+  t_launches = 0;
+  if (nseg == 0 || nseg > (uint32_t)kMaxSegs || !seg_rows || !seg_dst) return DPG_ERR_INVALID_ARG;
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  OutSegs sg;
+  std::memset(&sg, 0, sizeof(sg));
+  sg.n = nseg;
+  uint64_t k = 0;
+  for (uint32_t q = 0; q < nseg; ++q) {
+    sg.start[q] = (uint32_t)k;
+    sg.out[q] = (uint8_t*)seg_dst[q];
+    if (seg_rows[q] && !seg_dst[q]) return DPG_ERR_INVALID_ARG;
+    uint64_t bytes;
+    if (__builtin_mul_overflow(seg_rows[q], (uint64_t)rec_bytes, &bytes)) return DPG_ERR_INVALID_ARG;
+    if (seg_rows[q] && (overlaps(seg_dst[q], bytes, src, n_src * rec_bytes) ||
+                        overlaps(seg_dst[q], bytes, rids, n_out * 4)))
+      return DPG_ERR_INVALID_ARG;
+    if (!sg.out[0] && seg_rows[q]) sg.out[0] = sg.out[q];
+    k += seg_rows[q];
+    if (k > UINT32_MAX) return DPG_ERR_UNSUPPORTED;
+  }
+  if (k != n_out) return DPG_ERR_INVALID_ARG;
+  sg.start[nseg] = (uint32_t)k;
+  for (uint32_t q = 0; q < nseg; ++q)
+    if (!sg.out[q]) sg.out[q] = sg.out[0];          // empty segments: never written
+  if (n_out == 0) return DPG_OK;
+  t_seg = &sg;
+  // (dst is only a placeholder for the argument checks: every row goes to its segment)
+  const dpg_status_t s = run_dpg(src, rec_bytes, n_src, rids, n_out, nullptr, 0, sg.out[0],
+                                 (cudaStream_t)stream, nullptr);
+  t_seg = nullptr;
+  return s;
 }
 
 dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact,

@@ -198,6 +198,29 @@ struct ProbeArgs {
   uint32_t slot_bytes;         // total bytes per stage
 };
 
+// Output split into segments (dpg_retrieve_segments; the multi-GPU exchange
+// writes each requester's replies straight into its window over NVLink):
+// output row k of segment q (start[q] <= k < start[q+1]) goes to
+// out[q] + (k - start[q]) * row_bytes.  n = 0: one contiguous dst.
+constexpr int kMaxSegs = 8;
+struct OutSegs {
+  uint32_t n;
+  uint32_t start[kMaxSegs + 1];
+  uint8_t* out[kMaxSegs];
+};
+__device__ __forceinline__ uint32_t seg_of(const OutSegs& o, uint64_t k) {
+  uint32_t q = 0;
+#pragma unroll
+  for (int j = 1; j < kMaxSegs; ++j) q += (j < (int)o.n && k >= o.start[j]) ? 1u : 0u;
+  return q;
+}
+__device__ __forceinline__ uint8_t* seg_row(const OutSegs& o, uint8_t* dst, uint64_t k,
+                                            uint32_t row_bytes) {
+  if (!o.n) return dst + k * row_bytes;
+  const uint32_t q = seg_of(o, k);
+  return o.out[q] + (k - o.start[q]) * row_bytes;
+}
+
 // One persistent cooperative kernel for the whole path (fused.cu).
 struct FusedArgs {
   const uint8_t* src;
@@ -239,6 +262,7 @@ struct FusedArgs {
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 plain row stores (no
                          // evict_last hint), bit1 staggered run reservations,
                          // bits 8-12 static share of Phase II runs in 16ths
+  OutSegs seg;           // mode 0: output segments (seg.n = 0: dst)
 };
 
 // DPG with one L2-resident run (l2run.cu).
@@ -261,6 +285,7 @@ struct L2RunArgs {
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
                          // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first
+  OutSegs seg;           // output segments (seg.n = 0: dst); the window-gather path only
 };
 
 // DPG with two L2-resident runs (l2pair.cu).
@@ -746,12 +771,15 @@ struct AgrGroup {
   uint32_t r;         // the lane's row index (a row not stored reads row 0)
   uint32_t cnt;       // rows in the group (<= 32)
   uint32_t okm;       // rows to store
-  uint32_t* out;      // the group's output span
+  uint32_t* out;      // the group's output span (nullptr: rows go to several output segments)
+  uint64_t g0;        // the group's first output row (for split)
 };
 // Three groups per warp in flight, as ag_pipeline.  OFF32: every row offset
-// (base & 15) + r * rec of the source fits in 32 bits.
-template <bool OFF32, typename F>
-__device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, uint8_t* wtiles, uint32_t wt_s,
+// (base & 15) + r * rec of the source fits in 32 bits.  A group whose rows
+// belong to several output segments (out == nullptr) is stored by
+// split(group, tile, lane's dword shift).
+template <bool OFF32, typename F, typename S>
+__device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, S split, uint8_t* wtiles, uint32_t wt_s,
                                              uint32_t tile_bytes, const AgrMap& amap, uintptr_t base,
                                              uint32_t rec, uint32_t lane, uint32_t dbg = 0) {
   // dbg (experiments, tools/engine_probe.py): bit 20 skips the consume step,
@@ -778,6 +806,8 @@ __device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, uint8_t* wtil
     const uint8_t* ts = wtiles + slot * tile_bytes;
     const uint32_t full = q0.cnt == 32 ? 0xffffffffu : ((1u << q0.cnt) - 1u);
     if (no_consume) {
+    } else if (!q0.out) {
+      split(q0, reinterpret_cast<const uint32_t*>(ts), o4);
     } else if (q0.okm == full && ((reinterpret_cast<uintptr_t>(q0.out) | (q0.cnt * rec)) & 15) == 0)
       agr_consume16(ts, (o4 << 2) | (nx << 18), amap, q0.cnt, rec, q0.out, lane);
     else

@@ -209,13 +209,34 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       if ((uint32_t)lane < q.cnt && !on) report_bad(a.status, g0 + lane);
       q.r = on ? r : 0u;          // (row 0 is read, not stored)
       q.okm = __ballot_sync(0xffffffffu, on);
-      q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
+      q.g0 = g0;
+      if (!a.seg.n) {
+        q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
+      } else {
+        // output segments: the group's rows in one segment store as usual
+        const uint32_t qa = seg_of(a.seg, g0), qb = seg_of(a.seg, g0 + q.cnt - 1);
+        q.out = qa == qb ? reinterpret_cast<uint32_t*>(a.seg.out[qa] + (g0 - a.seg.start[qa]) * a.rec)
+                         : nullptr;
+      }
       return q;
     };
+    // a group across output segments: one masked dword store per segment, the
+    // span placed so that row j lands at its segment's row (g0 + j - start)
+    auto split = [&](const AgrGroup& q, const uint32_t* tile, uint32_t o4) {
+      const uint64_t g0 = q.g0;
+      const uint32_t qa = seg_of(a.seg, g0), qb = seg_of(a.seg, g0 + q.cnt - 1);
+      for (uint32_t sq = qa; sq <= qb; ++sq) {
+        const uint64_t s0 = a.seg.start[sq], s1 = a.seg.start[sq + 1];
+        const uint32_t j0 = (uint32_t)(max_u64(s0, g0) - g0), j1 = (uint32_t)min_u64(s1 - g0, 32);
+        const uint32_t m = (j1 >= 32 ? 0xffffffffu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
+        uint8_t* out = a.seg.out[sq] + (int64_t)(g0 - s0) * (int64_t)a.rec;
+        ag_consume(tile, o4, q.okm & m, q.cnt, a.rec, reinterpret_cast<uint32_t*>(out), lane);
+      }
+    };
     if (a.n_src * a.rec + 16 <= 0xFFFFFFFFull)
-      agr_pipeline<true>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
+      agr_pipeline<true>(nt, grp, split, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
     else
-      agr_pipeline<false>(nt, grp, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
+      agr_pipeline<false>(nt, grp, split, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)

@@ -593,3 +593,81 @@ def test_skew_check_switches_plan(dpg):
         i = np.random.default_rng(1).integers(0, w["fk"].size, 20000)
         assert np.array_equal(got[i, :16], w["fact"][i])
         assert np.array_equal(got[i, 16:], w["dim"][w["fk"][i].astype(np.int64)])
+
+
+# --------------------------------------------------------------------------
+# Output segments (dpg_retrieve_segments): the rows of segment q land in its
+# own buffer -- the owner side of the fused multi-GPU exchange.
+# --------------------------------------------------------------------------
+def _check_segments(dpg, src, rids, sizes, shift=0, rec_out=None):
+    want = oracle.retrieve(src, rids)
+    rec = src.shape[1]
+    bufs = [torch.full((max(n, 1) * rec + shift,), 0xA5, dtype=torch.uint8, device="cuda")
+            for n in sizes]
+    dsts = [b.data_ptr() + shift for b in bufs]
+    dpg.dpg_retrieve_segments(dev(src), dev(rids), sizes, dsts)
+    k = 0
+    for n, b in zip(sizes, bufs):
+        got = host(b)[shift:shift + n * rec].reshape(n, rec)
+        assert np.array_equal(got, want[k:k + n])
+        assert np.all(host(b)[shift + n * rec:] == 0xA5)       # nothing past the segment
+        k += n
+
+
+@pytest.mark.parametrize("rec", [100, 64, 12, 116])
+def test_segments_l2_run(dpg, rec):
+    rng = np.random.default_rng(rec)
+    src = rng.integers(0, 256, (50000, rec), dtype=np.uint8)
+    rids = rng.integers(0, 50000, 70000).astype(np.uint32)
+    _check_segments(dpg, src, rids, [0, 17, 20000, 31, 33, 49919])
+    assert dpg.last_path() == 3
+
+
+@pytest.mark.parametrize("rec,shift", [(6, 0), (128, 0), (100, 2), (256, 0)])
+def test_segments_direct_fallback(dpg, rec, shift):
+    rng = np.random.default_rng(rec + shift)
+    src = rng.integers(0, 256, (3000, rec), dtype=np.uint8)
+    rids = rng.integers(0, 3000, 9000).astype(np.uint32)
+    _check_segments(dpg, src, rids, [4000, 1, 0, 4999], shift=shift)
+
+
+def test_segments_shared_memory_runs(dpg):
+    """A source beyond the L2 budget: the fused probe writes each staged
+    record to its segment row."""
+    rng = np.random.default_rng(5)
+    n_src = 3 << 20
+    src = rng.integers(0, 256, (n_src, 100), dtype=np.uint8)
+    rids = rng.integers(0, n_src, 1 << 20).astype(np.uint32)
+    sizes = [300000, 5, 400000, (1 << 20) - 700005]
+    _check_segments(dpg, src, rids, sizes)
+    assert dpg.last_path() == 1
+
+
+def test_segments_skewed_k_runs(dpg):
+    """A skewed list (exponential keys) switches to the K-run L2 plan, whose
+    last gather writes the segments."""
+    w = datagen.make("c4x", scale=8)
+    rids = w["fk"][: (1 << 22) + 77]
+    sizes = [1 << 20, 12345, (1 << 21), len(rids) - (1 << 20) - 12345 - (1 << 21)]
+    want = oracle.retrieve(w["dim"], rids)
+    bufs = [torch.empty((n, 64), dtype=torch.uint8, device="cuda") for n in sizes]
+    dpg.dpg_retrieve_segments(dev(w["dim"]), dev(rids), sizes, bufs)
+    assert dpg.last_path() == 5
+    k = 0
+    for n, b in zip(sizes, bufs):
+        assert np.array_equal(host(b), want[k:k + n])
+        k += n
+
+
+def test_segments_errors(dpg):
+    src = dev(np.zeros((100, 8), np.uint8))
+    rids = dev(np.arange(10, dtype=np.uint32))
+    b = torch.empty((10, 8), dtype=torch.uint8, device="cuda")
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_retrieve_segments(src, rids, [5, 4], [b, b])          # counts != n_out
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_retrieve_segments(src, rids, [10], [0])                # NULL with rows
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_retrieve_segments(src, rids, [1] * 9 + [1], [b] * 10)  # more than 8
+    with pytest.raises(dpg.DPGError):
+        dpg.dpg_retrieve_segments(src, rids, [10], [src.data_ptr()])   # overlaps src
