@@ -51,6 +51,9 @@ def parse():
                     help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
     ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
     ap.add_argument("--c5-round-rows", type=int, default=1 << 26)
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="c5: replies written into the requesters' windows over NVLink "
+                         "(fused) or returned by an NCCL all-to-all")
     ap.add_argument("--rec", type=int, default=None, help="record bytes for c3a/c3b")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -267,7 +270,7 @@ def run_c5(args, rank, world):
     import torch.distributed as dist
 
     import datagen
-    from paper_cs_0308004_b200.dist import owned_range, retrieve_dist
+    from paper_cs_0308004_b200.dist import PeerWindows, owned_range, retrieve_dist
     dev = torch.device("cuda", torch.cuda.current_device())
     rec = 100
     n_total = 1 << args.c5_log2
@@ -278,8 +281,26 @@ def run_c5(args, rank, world):
     rids = datagen.feistel_cuda(n_total, b0, b1 - b0, datagen.STREAMS[("c5", "rids")])
     torch.cuda.synchronize()
 
+    # fused exchange: one receive window per rank, mapped into every peer (CUDA
+    # IPC); if any rank cannot map its peers, every rank uses the NCCL replies
+    exchange, win = args.exchange, None
+    if exchange == "fused":
+        ok = 1
+        try:
+            win = PeerWindows(min(args.c5_round_rows, b1 - b0) * rec)
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            print(f"fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int64, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item():
+            if win is not None:
+                win.close()
+            win, exchange = None, "nccl (fused windows unavailable)"
+
     def step():
-        return retrieve_dist(src, rids, n_total, max_rows_per_round=args.c5_round_rows)
+        return retrieve_dist(src, rids, n_total, max_rows_per_round=args.c5_round_rows,
+                             fused=win is not None, windows=win)
 
     out = None
     for _ in range(max(1, min(args.warmup, 3))):
@@ -325,13 +346,18 @@ def run_c5(args, rank, world):
             "config": {"workload": f"c5: 2^{args.c5_log2} x 100 B range-partitioned, rids = Feistel "
                                    "permutation (uint64) block-partitioned", "n_total": n_total,
                        "rec_bytes": rec, "rid_bytes": 8, "parallelism": f"ep{world} (owner exchange)",
-                       "round_rows": args.c5_round_rows, "l2": "inputs >> L2"},
+                       "round_rows": args.c5_round_rows, "l2": "inputs >> L2",
+                       "exchange": exchange},
             "records_per_s": n_total / (ms * 1e-3),
             "frac_of_hbm_peak_aggregate": value / (world * peak),
             "nvlink_roofline_ms": nvl, "frac_of_nvlink_roofline": (nvl / ms) if nvl else None,
             "parity_sampled_ok": bool(ok.item()),
             "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev)}), flush=True)
     dist.barrier()
+    if win is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        win.close()
     dist.destroy_process_group()
     return 0
 

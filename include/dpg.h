@@ -234,6 +234,20 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* Receive windows for the fused multi-GPU exchange (one process per GPU on
+ * one node).  dpg_ipc_alloc: a device buffer of `bytes` on the current device
+ * (library-owned until dpg_ipc_free) and its 64-byte CUDA IPC handle, to be
+ * sent to the peer processes.  dpg_ipc_open: maps a peer's buffer from its
+ * handle into this process (peer access over NVLink enabled lazily); the
+ * pointer is valid for kernels on this device until dpg_ipc_close.  A
+ * process cannot open its own handle.  Errors: DPG_ERR_INVALID_ARG (NULL
+ * arguments, zero bytes), DPG_ERR_OOM, DPG_ERR_CUDA (the driver's
+ * refusal, e.g. no peer access).  Synchronous. */
+dpg_status_t dpg_ipc_alloc(size_t bytes, void **ptr, uint8_t handle[64]);
+dpg_status_t dpg_ipc_open(const uint8_t handle[64], void **ptr);
+dpg_status_t dpg_ipc_close(void *ptr);
+dpg_status_t dpg_ipc_free(void *ptr);
+
 /* Retrieval into output segments: D[k] = R[rids[k]] as dpg_retrieve, with
  * output row k of segment q (rows seg_rows[0] + ... + seg_rows[q-1] up to the
  * next boundary) written to seg_dst[q] + (k - first row of q) * rec_bytes.

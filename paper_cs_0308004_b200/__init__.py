@@ -97,6 +97,10 @@ _sigs = {
     "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
     "dpg_fk_join_sort": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
     "dpg_retrieve_segments": [_P, _S, _U, _P, _U, ctypes.c_uint32, _P, _P, _P],
+    "dpg_ipc_alloc": [_S, _P, _P],
+    "dpg_ipc_open": [_P, _P],
+    "dpg_ipc_close": [_P],
+    "dpg_ipc_free": [_P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -331,13 +335,20 @@ def dpg_partition_inv(rids, n_src_total: int, log2_span: int, parts: int, stream
     return local, inv[:n], counts
 
 
-def dpg_gather_rows(rows, inv, dst, stream=None):
-    """dst[i] = rows[inv[i]] for inv[i] in range (other rows left unwritten)."""
-    rows = _records(rows, "rows")
+def dpg_gather_rows(rows, inv, dst, stream=None, n_rows=None):
+    """dst[i] = rows[inv[i]] for inv[i] in range (other rows left unwritten).
+    rows: a uint8 [n_rows, rec] CUDA tensor, or an integer device address of
+    n_rows rows of dst's row size (a receive window)."""
     inv = _rid_tensor(inv, "inv")
     dst = _records(dst, "dst")
-    n_rows, rec = rows.shape
-    _check(_lib.dpg_gather_rows(rows.data_ptr(), rec, n_rows, inv.data_ptr(), inv.numel(),
+    rec = dst.shape[1]
+    if isinstance(rows, int):
+        ptr = rows
+    else:
+        rows = _records(rows, "rows")
+        n_rows, rec = rows.shape
+        ptr = rows.data_ptr()
+    _check(_lib.dpg_gather_rows(ptr, rec, n_rows, inv.data_ptr(), inv.numel(),
                                 dst.data_ptr(), _stream_ptr(stream)), "dpg_gather_rows")
     return dst
 
@@ -382,6 +393,30 @@ def dpg_retrieve_segments(src, rids, seg_rows, seg_dst, stream=None):
                                       nseg, ctypes.cast(rows, ctypes.c_void_p),
                                       ctypes.cast(ptrs, ctypes.c_void_p), _stream_ptr(stream)),
            "dpg_retrieve_segments")
+
+
+def ipc_alloc(nbytes: int) -> tuple[int, bytes]:
+    """A device buffer (library-owned) and its 64-byte IPC handle."""
+    p = ctypes.c_void_p()
+    h = (ctypes.c_uint8 * 64)()
+    _check(_lib.dpg_ipc_alloc(nbytes, ctypes.byref(p), h), "dpg_ipc_alloc")
+    return int(p.value), bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    """A peer process's buffer mapped into this one (device address)."""
+    p = ctypes.c_void_p()
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    _check(_lib.dpg_ipc_open(h, ctypes.byref(p)), "dpg_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_lib.dpg_ipc_close(ctypes.c_void_p(ptr)), "dpg_ipc_close")
+
+
+def ipc_free(ptr: int) -> None:
+    _check(_lib.dpg_ipc_free(ctypes.c_void_p(ptr)), "dpg_ipc_free")
 
 
 def dpg_fk_join_sort(fact, fk_col, dim, out=None, stream=None):

@@ -1352,6 +1352,36 @@ dpg_status_t dpg_partition_inv(const void* rids, uint32_t rid_bytes, uint64_t n,
   return cuda_status(e);
 }
 
+dpg_status_t dpg_ipc_alloc(size_t bytes, void** ptr, uint8_t handle[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (!ptr || !handle || bytes == 0) return DPG_ERR_INVALID_ARG;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return DPG_ERR_OOM;
+  }
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_status(e);
+  }
+  std::memcpy(handle, &h, 64);
+  *ptr = p;
+  return DPG_OK;
+}
+
+dpg_status_t dpg_ipc_open(const uint8_t handle[64], void** ptr) {
+  if (!ptr || !handle) return DPG_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+dpg_status_t dpg_ipc_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr)); }
+
+dpg_status_t dpg_ipc_free(void* ptr) { return cuda_status(cudaFree(ptr)); }
+
 dpg_status_t dpg_gather_rows(const void* rows, size_t rec_bytes, uint64_t n_rows, const uint32_t* inv,
                              uint64_t n, void* dst, dpg_stream_t stream) {
   // dst[i] = rows[inv[i]] (rows with inv[i] >= n_rows stay unwritten): the

@@ -424,6 +424,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
           *reinterpret_cast<T*>(d + w * W) = *reinterpret_cast<const T*>(s + w * W);
       }
     }
+    // rows written into peer memory (output segments mapped from other GPUs)
+    // are made visible system-wide before the kernel ends
+    if (a.seg.n) __threadfence_system();
     // the last CTA through here resets the overflow count for the next call
     __syncthreads();
     if (tid == 0) {

@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       agr_pipeline<true>(nt, grp, split, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
     else
       agr_pipeline<false>(nt, grp, split, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
+    // rows written into peer memory (output segments mapped from other GPUs)
+    // are made visible system-wide before the kernel ends
+    if (a.seg.n) __threadfence_system();
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)

@@ -51,6 +51,49 @@ class NumpyOps:
     def counts_tensor(self, counts, like):
         return torch.tensor(counts, dtype=torch.int64)
 
+    # fused exchange: a window is a local byte tensor; the owner's writes into
+    # a peer's window are emulated by all-to-alls that carry the rows and the
+    # owner-computed row offset, which the receiver honours as given
+    def window_alloc(self, nbytes):
+        return torch.zeros(max(nbytes, 1), dtype=torch.uint8), b"emulated"
+
+    def window_open(self, handle):
+        return None
+
+    def window_close(self, ptr):
+        pass
+
+    def window_free(self, ptr):
+        pass
+
+    def push(self, src_shard, requests, rcounts, targets, win, group=None):
+        world = len(rcounts)
+        rec = src_shard.shape[1]
+        rows = src_shard[requests.long()].contiguous().view(-1)
+        send_n = torch.tensor(rcounts, dtype=torch.int64)
+        recv_n = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(recv_n, send_n, group=group)
+        send_off = torch.tensor([off for _, off in targets], dtype=torch.int64)
+        assert [q for q, _ in targets] == list(range(world))
+        recv_off = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(recv_off, send_off, group=group)
+        recv_n = recv_n.tolist()
+        got = torch.empty(sum(recv_n) * rec, dtype=torch.uint8)
+        dist.all_to_all_single(got, rows, output_split_sizes=[x * rec for x in recv_n],
+                               input_split_sizes=[x * rec for x in rcounts], group=group)
+        k = 0
+        for o in range(world):
+            off = int(recv_off[o])
+            win.local[off * rec:(off + recv_n[o]) * rec] = got[k:k + recv_n[o] * rec]
+            k += recv_n[o] * rec
+
+    def window_barrier(self, like, group=None):
+        dist.barrier(group=group)
+
+    def window_gather(self, win, n_rows, inv, dst):
+        rec = dst.shape[1]
+        self.gather(win.local[:n_rows * rec].view(n_rows, rec), inv, dst)
+
 
 def _free_port():
     s = socket.socket()
@@ -60,7 +103,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_total, rec, n_out, seed, round_rows, q):
+def _worker(rank, world, port, n_total, rec, n_out, seed, round_rows, q, fused=False):
     sys.path.insert(0, ROOT)
     from paper_cs_0308004_b200.dist import owned_range, retrieve_dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
@@ -74,12 +117,13 @@ def _worker(rank, world, port, n_total, rec, n_out, seed, round_rows, q):
         b0 = rank * n_out // world
         b1 = (rank + 1) * n_out // world
         out = retrieve_dist(torch.from_numpy(src[lo:hi].copy()), torch.from_numpy(rids[b0:b1].copy()),
-                            n_total, ops=NumpyOps(), max_rows_per_round=round_rows)
+                            n_total, ops=NumpyOps(), max_rows_per_round=round_rows, fused=fused)
         q.put((rank, b0, out.numpy()))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("world,n_total,rec,n_out,round_rows", [
     (2, 1000, 12, 1500, None),      # uneven ranges: rank 1 owns 488 records
     (2, 4096, 100, 4096, 700),      # permutation, several rounds
@@ -87,13 +131,14 @@ def _worker(rank, world, port, n_total, rec, n_out, seed, round_rows, q):
     (1, 300, 7, 450, None),
     (2, 1, 5, 9, None),             # rank 1 owns nothing
 ])
-def test_retrieve_dist_matches_oracle(world, n_total, rec, n_out, round_rows):
+def test_retrieve_dist_matches_oracle(world, n_total, rec, n_out, round_rows, fused):
     sys.path.insert(0, ROOT)
     import oracle
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n_total, rec, n_out, 7, round_rows, q))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, n_total, rec, n_out, 7, round_rows, q, fused))
              for r in range(world)]
     for p in procs:
         p.start()

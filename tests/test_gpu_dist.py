@@ -94,3 +94,77 @@ def test_retrieve_dist_single_rank_nccl(dpg):
         assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
     finally:
         dist.destroy_process_group()
+
+
+def test_retrieve_dist_fused_single_rank_nccl(dpg):
+    """The fused exchange at P = 1: the owner's retrieval writes into the
+    rank's own receive window (dpg_ipc_alloc), Phase III gathers from it."""
+    import torch.distributed as dist
+    from paper_cs_0308004_b200.dist import retrieve_dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(4)
+        src = rng.integers(0, 256, (50000, 100), dtype=np.uint8)
+        rids = rng.integers(0, 50000, 70000).astype(np.int64)
+        out = retrieve_dist(torch.from_numpy(src).cuda(), torch.from_numpy(rids).cuda(), 50000,
+                            max_rows_per_round=30000, fused=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _ipc_child(handle, n_rows, rec, seed, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch as t
+    import paper_cs_0308004_b200 as m
+    try:
+        rng = np.random.default_rng(seed)
+        src = rng.integers(0, 256, (5000, rec), dtype=np.uint8)
+        rids = rng.integers(0, 5000, n_rows).astype(np.uint32)
+        win = m.ipc_open(handle)
+        # two segments into the parent's window: rows [0, 1000) at row 3000 of
+        # the window, the rest at row 0 -- the owner side of the fused exchange
+        m.dpg_retrieve_segments(t.from_numpy(src).cuda(), t.from_numpy(rids.view(np.int32)).cuda(),
+                                [1000, n_rows - 1000], [win + 3000 * rec, win])
+        t.cuda.synchronize()
+        m.ipc_close(win)
+        q.put("ok")
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(repr(e))
+
+
+def test_ipc_window_written_by_another_process(dpg):
+    """A receive window allocated here and written by a second process that
+    maps it from its IPC handle (the same GPU stands in for the peer: the
+    mapping and the segment addressing are what is tested; no kernel waits on
+    another process)."""
+    import multiprocessing as mpp
+    rec, n_rows = 100, 3000
+    ptr, handle = dpg.ipc_alloc((n_rows + 1000) * rec)
+    try:
+        ctx = mpp.get_context("spawn")
+        q = ctx.Queue()
+        p = ctx.Process(target=_ipc_child, args=(handle, n_rows, rec, 9, q))
+        p.start()
+        msg = q.get(timeout=240)
+        p.join(60)
+        assert msg == "ok", msg
+        got = torch.empty((n_rows + 1000, rec), dtype=torch.uint8, device="cuda")
+        dpg.dpg_gather_rows(ptr, torch.arange(n_rows + 1000, dtype=torch.int32, device="cuda"), got,
+                            n_rows=n_rows + 1000)
+        got = got.cpu().numpy()
+        rng = np.random.default_rng(9)
+        src = rng.integers(0, 256, (5000, rec), dtype=np.uint8)
+        rids = rng.integers(0, 5000, n_rows).astype(np.uint32)
+        want = oracle.retrieve(src, rids)
+        assert np.array_equal(got[3000:4000], want[:1000])
+        assert np.array_equal(got[:n_rows - 1000], want[1000:])
+    finally:
+        dpg.ipc_free(ptr)
