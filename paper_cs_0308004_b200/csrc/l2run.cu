@@ -51,8 +51,9 @@ static_assert(128 >= 8 * kL2Slots, "barrier area");
 //            output rows) leaves by one TMA bulk store.
 // REALIGN 2: as 1 with byte granularity (rec or src not 4-byte aligned).
 template <int W, int REALIGN>
-__global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
+__global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(const __grid_constant__ L2RunArgs a0) {
   L2RunArgs a = a0;
+  const OutSegs& sg = a0.seg;   // (read in place: dynamic segment indices use the constant bank)
   if (a.dev_range) {
     // the rows [range[0], range[1]) of rids/dst, known on the device only (the
     // run of a K-run plan, l2k.cu): rids and dst are offset by range[0]
@@ -210,12 +211,12 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       q.r = on ? r : 0u;          // (row 0 is read, not stored)
       q.okm = __ballot_sync(0xffffffffu, on);
       q.g0 = g0;
-      if (!a.seg.n) {
+      if (!sg.n) {
         q.out = reinterpret_cast<uint32_t*>(a.dst + g0 * a.rec);
       } else {
         // output segments: the group's rows in one segment store as usual
-        const uint32_t qa = seg_of(a.seg, g0), qb = seg_of(a.seg, g0 + q.cnt - 1);
-        q.out = qa == qb ? reinterpret_cast<uint32_t*>(a.seg.out[qa] + (g0 - a.seg.start[qa]) * a.rec)
+        const uint32_t qa = seg_of(sg, g0), qb = seg_of(sg, g0 + q.cnt - 1);
+        q.out = qa == qb ? reinterpret_cast<uint32_t*>(sg.out[qa] + (g0 - sg.start[qa]) * a.rec)
                          : nullptr;
       }
       return q;
@@ -224,12 +225,12 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
     // span placed so that row j lands at its segment's row (g0 + j - start)
     auto split = [&](const AgrGroup& q, const uint32_t* tile, uint32_t o4) {
       const uint64_t g0 = q.g0;
-      const uint32_t qa = seg_of(a.seg, g0), qb = seg_of(a.seg, g0 + q.cnt - 1);
+      const uint32_t qa = seg_of(sg, g0), qb = seg_of(sg, g0 + q.cnt - 1);
       for (uint32_t sq = qa; sq <= qb; ++sq) {
-        const uint64_t s0 = a.seg.start[sq], s1 = a.seg.start[sq + 1];
+        const uint64_t s0 = sg.start[sq], s1 = sg.start[sq + 1];
         const uint32_t j0 = (uint32_t)(max_u64(s0, g0) - g0), j1 = (uint32_t)min_u64(s1 - g0, 32);
         const uint32_t m = (j1 >= 32 ? 0xffffffffu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
-        uint8_t* out = a.seg.out[sq] + (int64_t)(g0 - s0) * (int64_t)a.rec;
+        uint8_t* out = sg.out[sq] + (int64_t)(g0 - s0) * (int64_t)a.rec;
         ag_consume(tile, o4, q.okm & m, q.cnt, a.rec, reinterpret_cast<uint32_t*>(out), lane);
       }
     };
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(L2RunArgs a0) {
       agr_pipeline<false>(nt, grp, split, wtiles, wt_s, kAgTile, amap, src_u, a.rec, lane, a.dbg);
     // rows written into peer memory (output segments mapped from other GPUs)
     // are made visible system-wide before the kernel ends
-    if (a.seg.n) __threadfence_system();
+    if (sg.n) __threadfence_system();
   } else {
     const uint32_t rec = a.rec;
     const uint32_t NW = (rec + 30) / 16;            // 16-byte words of a row's window (max)
