@@ -234,6 +234,32 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* Multi-GPU retrieval (north_star config 5; not in the paper: reading A14,
+ * DESIGN.md section 8).  One process per GPU.  dpg_get_unique_id: an NCCL
+ * unique id (128 bytes) made on one rank and sent to the others by the
+ * caller.  dpg_comm_create: the communicator of `nranks` (<= 8) processes on
+ * the current device (blocking until all ranks join); dpg_comm_destroy frees
+ * it and its receive windows.  dpg_retrieve_dist: the global retrieval
+ * D[i] = R[rids[i]] over a source of n_src_total records range-partitioned
+ * by rank (rank r owns records [r*S, (r+1)*S), S = the smallest power of two
+ * with nranks * S >= n_src_total; src_shard holds this rank's records, device)
+ * and an output block-partitioned by the caller: this rank passes the rids
+ * (uint64, device) of its n_out_local output rows and receives their records
+ * in dst (device, n_out_local * rec_bytes).  Collective: every rank calls it
+ * (with its own block; 0 rows allowed).  Steps: owner partition, one NCCL
+ * all-gather of the count matrix, grouped send/recv of the requests, the
+ * owner's DPG writing each requester's rows straight into that requester's
+ * receive window (CUDA IPC, NVLink), a stream-ordered all-reduce, Phase III
+ * from the window.  NCCL is loaded at run time (DPG_ERR_NCCL if absent or on
+ * an NCCL failure).  Invalid rids as dpg_retrieve.  Synchronises `stream`
+ * once (the counts size the exchange). */
+dpg_status_t dpg_get_unique_id(uint8_t id[128]);
+dpg_status_t dpg_comm_create(const uint8_t id[128], int nranks, int rank, void **comm);
+dpg_status_t dpg_retrieve_dist(void *comm, const void *src_shard, size_t rec_bytes,
+                               uint64_t n_src_total, const uint64_t *rids, uint64_t n_out_local,
+                               void *dst, dpg_stream_t stream);
+dpg_status_t dpg_comm_destroy(void *comm);
+
 /* Receive windows for the fused multi-GPU exchange (one process per GPU on
  * one node).  dpg_ipc_alloc: a device buffer of `bytes` on the current device
  * (library-owned until dpg_ipc_free) and its 64-byte CUDA IPC handle, to be

@@ -98,6 +98,10 @@ _sigs = {
     "dpg_fk_join_sort": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
     "dpg_retrieve_segments": [_P, _S, _U, _P, _U, ctypes.c_uint32, _P, _P, _P],
     "dpg_ipc_alloc": [_S, _P, _P],
+    "dpg_get_unique_id": [_P],
+    "dpg_comm_create": [_P, ctypes.c_int, ctypes.c_int, _P],
+    "dpg_retrieve_dist": [_P, _P, _S, _U, _P, _U, _P, _P],
+    "dpg_comm_destroy": [_P],
     "dpg_ipc_open": [_P, _P],
     "dpg_ipc_close": [_P],
     "dpg_ipc_free": [_P],
@@ -393,6 +397,41 @@ def dpg_retrieve_segments(src, rids, seg_rows, seg_dst, stream=None):
                                       nseg, ctypes.cast(rows, ctypes.c_void_p),
                                       ctypes.cast(ptrs, ctypes.c_void_p), _stream_ptr(stream)),
            "dpg_retrieve_segments")
+
+
+def dpg_get_unique_id() -> bytes:
+    """An NCCL unique id for dpg_comm_create (make on one rank, send to all)."""
+    b = (ctypes.c_uint8 * 128)()
+    _check(_lib.dpg_get_unique_id(b), "dpg_get_unique_id")
+    return bytes(b)
+
+
+def dpg_comm_create(uid: bytes, nranks: int, rank: int) -> int:
+    """The library's own communicator on the current device (collective)."""
+    c = ctypes.c_void_p()
+    u = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(_lib.dpg_comm_create(u, nranks, rank, ctypes.byref(c)), "dpg_comm_create")
+    return int(c.value)
+
+
+def dpg_comm_destroy(comm: int) -> None:
+    _check(_lib.dpg_comm_destroy(ctypes.c_void_p(comm)), "dpg_comm_destroy")
+
+
+def dpg_retrieve_dist(comm: int, src_shard, n_src_total: int, rids, dst=None, stream=None):
+    """The multi-GPU retrieval behind the C ABI (collective over comm): rows
+    src_global[rids] for this rank's block; src_shard = this rank's records."""
+    torch = _torch()
+    src_shard = _records(src_shard, "src_shard")
+    rec = src_shard.shape[1]
+    if rids.dtype != torch.int64 or not rids.is_cuda or not rids.is_contiguous():
+        raise TypeError("rids must be a contiguous CUDA int64 tensor")
+    if dst is None:
+        dst = torch.empty((rids.numel(), rec), dtype=torch.uint8, device=rids.device)
+    _check(_lib.dpg_retrieve_dist(ctypes.c_void_p(comm), src_shard.data_ptr(), rec, n_src_total,
+                                  rids.data_ptr(), rids.numel(), dst.data_ptr(),
+                                  _stream_ptr(stream)), "dpg_retrieve_dist")
+    return dst
 
 
 def ipc_alloc(nbytes: int) -> tuple[int, bytes]:

@@ -26,6 +26,21 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_flags() -> list[str]:
+    """The NCCL headers and library of the nvidia-nccl wheel (comm.cu loads the
+    library at run time); without them the multi-GPU C entries report
+    DPG_ERR_NCCL."""
+    try:
+        import nvidia.nccl as m
+        base = list(m.__path__)[0]
+    except Exception:
+        base = None
+    if base and os.path.exists(os.path.join(base, "include", "nccl.h")):
+        lib = os.path.join(base, "lib", "libnccl.so.2")
+        return ["-I", os.path.join(base, "include"), f'-DDPG_NCCL_LIB="{lib}"']
+    return ["-DDPG_NO_NCCL"]
+
+
 def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -43,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp]
+    cmd = [NVCC, *NVCC_FLAGS, *nccl_flags(), "-I", os.path.join(ROOT, "include"), *sources(),
+           "-ldl", "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

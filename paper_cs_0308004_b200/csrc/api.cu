@@ -975,6 +975,11 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
 
 }  // namespace
 
+namespace dpg {
+uint32_t t_launches_get() { return t_launches; }
+void t_launches_set(uint32_t n) { t_launches = n; }
+}  // namespace dpg
+
 extern "C" {
 
 int dpg_version(void) { return 1; }

@@ -469,6 +469,10 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
                              int sm, cudaStream_t st, uint32_t* nlaunch,
                              const uint32_t* keys_u32 = nullptr, uint32_t* keys_out = nullptr,
                              uint64_t key_limit = ~0ull, unsigned long long* status = nullptr);
+// Launch count of the last call on this host thread (api.cu).
+uint32_t t_launches_get();
+void t_launches_set(uint32_t n);
+
 // Data skew check (skew.cu): estimated rids beyond the fixed run
 // capacity from S evenly spaced samples; hist: ceil(K / group) zeroed words.
 cudaError_t launch_skew_check(const uint32_t* rids, uint64_t n_out, uint64_t n_src, uint32_t s,

@@ -168,3 +168,30 @@ def test_ipc_window_written_by_another_process(dpg):
         assert np.array_equal(got[:n_rows - 1000], want[1000:])
     finally:
         dpg.ipc_free(ptr)
+
+
+def test_c_abi_retrieve_dist_single_rank(dpg):
+    """dpg_comm_create / dpg_retrieve_dist / dpg_comm_destroy at one rank:
+    the native exchange (NCCL loaded by the library, the rank's own window)
+    against the oracle, including a rank whose block is empty and an invalid
+    rid."""
+    comm = dpg.dpg_comm_create(dpg.dpg_get_unique_id(), 1, 0)
+    try:
+        rng = np.random.default_rng(11)
+        for n_total, rec, n_out in ((50000, 100, 70000), (1000, 12, 0), (3, 8, 500),
+                                    (4096, 64, 4096)):
+            src = rng.integers(0, 256, (n_total, rec), dtype=np.uint8)
+            rids = rng.integers(0, n_total, n_out).astype(np.int64)
+            out = dpg.dpg_retrieve_dist(comm, torch.from_numpy(src).cuda(), n_total,
+                                        torch.from_numpy(rids).cuda())
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+        rids = np.arange(100, dtype=np.int64)
+        rids[37] = 5000
+        dpg.dpg_retrieve_dist(comm, torch.zeros((100, 8), dtype=torch.uint8, device="cuda"), 100,
+                              torch.from_numpy(rids).cuda())
+        with pytest.raises(dpg.DPGError) as e:
+            dpg.dpg_sync_status()
+        assert e.value.index == 37
+    finally:
+        dpg.dpg_comm_destroy(comm)
