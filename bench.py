@@ -335,6 +335,24 @@ def run_c5(args, rank, world):
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     alg = n_total * (2 * rec + 8)
     value = alg / (ms * 1e-3) / 1e9
+    # NCCL all-to-all bus bandwidth on equal 256 MiB per-rank buffers (SV 8(e))
+    busbw = None
+    if world > 1:
+        a2a_in = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        a2a_out = torch.empty_like(a2a_in)
+        for _ in range(3):
+            dist.all_to_all_single(a2a_out, a2a_in)
+        torch.cuda.synchronize()
+        b0e, b1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0e.record()
+        for _ in range(10):
+            dist.all_to_all_single(a2a_out, a2a_in)
+        b1e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([b0e.elapsed_time(b1e) / 10], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        busbw = (256 << 20) * (world - 1) / world / (float(t.item()) * 1e-3) / 1e9
+        del a2a_in, a2a_out
     peak, peak_src = hbm_peak()
     nvl = (world - 1) / world * (n_total / world) * (rec + 4) / 900e9 * 1e3 if world > 1 else 0.0
     if rank == 0:
@@ -351,6 +369,7 @@ def run_c5(args, rank, world):
             "records_per_s": n_total / (ms * 1e-3),
             "frac_of_hbm_peak_aggregate": value / (world * peak),
             "nvlink_roofline_ms": nvl, "frac_of_nvlink_roofline": (nvl / ms) if nvl else None,
+            "nccl_alltoall_busbw_gbs": busbw,
             "parity_sampled_ok": bool(ok.item()),
             "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev)}), flush=True)
     dist.barrier()
