@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dpg", choices=["dpg", "reference"])
-    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c4x", "c5"],
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c4x", "c5", "h1"],
                     help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
     ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
     ap.add_argument("--c5-round-rows", type=int, default=1 << 26)
@@ -381,10 +381,76 @@ def run_c5(args, rank, world):
     return 0
 
 
+def run_h1(args):
+    """Batch lookup in a hash index (section 4): an index of 2^24
+    distinct keys (2^24 slots of 16 B + slot-ordered overflow, 268 MB) and
+    2^26 queries (5% absent).  DPG (distribute by partition, probe with the
+    partition L2-resident, gather) beside the direct lookup."""
+    import numpy as np
+    import torch
+
+    import datagen
+    import oracle
+    import paper_cs_0308004_b200 as dpg
+    torch.cuda.set_device(0)
+    w = datagen.hash_workload(1 << 24, 24, 1 << 26)
+    t = torch.from_numpy(w["table"].view(np.int32)).cuda()
+    p = torch.from_numpy(w["pool"].view(np.int32)).cuda()
+    q = torch.from_numpy(w["queries"].view(np.int32)).cuda()
+    out = torch.empty_like(q)
+    n = q.numel()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def timed(direct):
+        for _ in range(max(3, args.warmup)):
+            dpg.dpg_hash_lookup(t, p, q, out=out, direct=direct)
+        torch.cuda.synchronize()
+        idx = np.random.default_rng(0).integers(0, n, 4096)
+        ok = np.array_equal(out.cpu().numpy().view(np.uint32)[idx],
+                            oracle.batch_lookup(w["keys"], w["queries"][idx]))
+        ms = []
+        launches = 0
+        for _ in range(args.steps):
+            flush.fill_(1)
+            flush_rd.view(torch.int32).max()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dpg.dpg_hash_lookup(t, p, q, out=out, direct=direct)
+            e1.record()
+            launches += dpg.last_launch_count()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return sum(ms) / len(ms), ok, launches
+
+    with ClockSampler(0) as clk:
+        ms, ok, launches = timed(False)
+    dms, dok, _ = timed(True)
+    alg = n * (4 + 16 + 4)        # key in, the key's 16-byte slot, rid out
+    peak, peak_src = hbm_peak()
+    print(json.dumps({
+        "metric": "batch index lookups/s (hash index, DPG)", "value": n / (ms * 1e-3),
+        "unit": "lookups/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic (datagen.hash_workload, seed 0)",
+        "config": {"workload": "h1: hash index of 2^24 keys (2^24 slots x 16 B, overflow in slot "
+                               "order), 2^26 queries (5% absent)", "slots": 1 << 24,
+                   "pool_entries": int(w["pool"].shape[0]), "queries": n,
+                   "l2": "flushed before every step"},
+        "effective_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak,
+        "direct": {"value": n / (dms * 1e-3), "unit": "lookups/s", "ms_per_step": dms,
+                   "parity_sampled_ok": bool(dok)},
+        "parity_sampled_ok": bool(ok), "gpu_launches": launches, "clocks": clk.summary()}),
+        flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "h1":
+        return run_h1(args)
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()

@@ -47,6 +47,7 @@ STREAMS = {
     ("c4", "dim"): 0x401, ("c4", "fact"): 0x402, ("c4", "fk"): 0x403, ("c4x", "fk"): 0x404,
     ("c5", "src"): 0x501, ("c5", "rids"): 0x502,
     ("test", "src"): 0x901, ("test", "rids"): 0x902,
+    ("h1", "keys"): 0x601, ("h1", "queries"): 0x602, ("h1", "absent"): 0x603,
 }
 
 C3_RECS = (8, 16, 32, 64, 128, 256)
@@ -119,6 +120,8 @@ def _load():
         lib.gen_permutation_u32.argtypes = [U, U, U, P]
         lib.gen_uniform_u32.argtypes = [U, U, U, U, P]
         lib.gen_feistel_u64.argtypes = [U, U, ctypes.c_uint, ctypes.c_uint, U, U, U, P]
+        lib.gen_hash_index.argtypes = [P, U, ctypes.c_uint, P, P]
+        lib.gen_hash_index.restype = U
         _lib = lib
     return _lib
 
@@ -178,6 +181,30 @@ def exp_fk(n: int, n_dim: int, sid: int, seed: int = SEED, c: float = -1e-7) -> 
     r = uniform(n, 2 ** 31, sid, seed).astype(np.int64)
     y = np.exp(c * (r >> 10).astype(np.float64))
     return np.minimum(n_dim - 1, np.floor(n_dim * y)).astype(np.uint32)
+
+
+def hash_index(keys: np.ndarray, m_log2: int):
+    """The hash index of the batch lookup over (keys[j], rid j) (gen.c
+    gen_hash_index): (table uint32 [2^m_log2, 4], pool uint32 [P, 4])."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    table = np.empty((1 << m_log2, 4), dtype=np.uint32)
+    pool = np.empty((max(1, keys.size), 4), dtype=np.uint32)
+    n_pool = _load().gen_hash_index(_p(keys), keys.size, m_log2, _p(table), _p(pool))
+    return table, pool[:max(1, n_pool)].copy()
+
+
+def hash_workload(n_keys: int, m_log2: int, n_queries: int, absent_per_mille: int = 50):
+    """Batch lookup workload: distinct uint32 keys (a 32-bit
+    Feistel permutation), their index, and queries drawn uniformly from the
+    keys with ~absent_per_mille / 1000 of them replaced by absent keys."""
+    keys = feistel(1 << 32, 0, n_keys, STREAMS[("h1", "keys")]).astype(np.uint32)
+    table, pool = hash_index(keys, m_log2)
+    q = keys[uniform(n_queries, n_keys, STREAMS[("h1", "queries")]).astype(np.int64)]
+    n_abs = n_queries * absent_per_mille // 1000
+    if n_abs:
+        pos = uniform(n_abs, n_queries, STREAMS[("h1", "absent")]).astype(np.int64)
+        q[pos] = feistel(1 << 32, n_keys, n_abs, STREAMS[("h1", "keys")]).astype(np.uint32)
+    return {"keys": keys, "table": table, "pool": pool, "queries": q}
 
 
 def stable_key_argsort(recs: np.ndarray, key_len: int = 10) -> np.ndarray:

@@ -21,6 +21,7 @@
  * use a keyed balanced Feistel network on 2^bits with cycle walking.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define GOLDEN 0x9E3779B97F4A7C15ULL
@@ -146,4 +147,58 @@ void gen_feistel_u64(uint64_t seed, uint64_t sid, unsigned bits, unsigned rounds
         while (x >= n) x = feistel_once(key, half, rounds, x);
         out[j] = x;
     }
+}
+
+/* Hash index over (keys[j], rid j), j < n (the indexed relation F of the
+ * batch lookup): a primary array of 2^m_log2 slots and an overflow
+ * pool, 16-byte entries {key, rid, next, 0}; slot h(key) = (key * 0x9E3779B1)
+ * >> (32 - m_log2) holds the first key that hashes there, later colliding
+ * keys go to the pool, linked from the slot (newest first); rid 0xFFFFFFFF
+ * marks an empty slot, next 0xFFFFFFFF the end of a chain.  The pool is
+ * then laid out in slot order (reading A20: the overflow area is "a second
+ * hash array").  Returns the pool entries used. */
+uint64_t gen_hash_index(const uint32_t *keys, uint64_t n, unsigned m_log2, uint32_t *table,
+                        uint32_t *pool)
+{
+    const uint64_t M = 1ULL << m_log2;
+    for (uint64_t h = 0; h < M; ++h) {
+        table[4 * h] = 0; table[4 * h + 1] = 0xFFFFFFFFu;
+        table[4 * h + 2] = 0xFFFFFFFFu; table[4 * h + 3] = 0;
+    }
+    uint64_t np = 0;
+    for (uint64_t j = 0; j < n; ++j) {
+        const uint32_t k = keys[j];
+        const uint64_t h = (uint32_t)(k * 0x9E3779B1u) >> (32 - m_log2);
+        uint32_t *s = table + 4 * h;
+        if (s[1] == 0xFFFFFFFFu) {
+            s[0] = k; s[1] = (uint32_t)j;
+        } else {
+            uint32_t *p = pool + 4 * np;
+            p[0] = k; p[1] = (uint32_t)j; p[2] = s[2]; p[3] = 0;
+            s[2] = (uint32_t)np++;
+        }
+    }
+    /* the overflow pool in slot order ("a second hash array"):
+     * chain of slot 0 first, each chain's entries consecutive */
+    if (np) {
+        uint32_t *sorted = (uint32_t *)malloc(np * 16);
+        if (!sorted) return np;
+        uint64_t w = 0;
+        for (uint64_t h = 0; h < M; ++h) {
+            uint32_t nx = table[4 * h + 2];
+            if (nx == 0xFFFFFFFFu) continue;
+            table[4 * h + 2] = (uint32_t)w;
+            while (nx != 0xFFFFFFFFu) {
+                const uint32_t *p = pool + 4 * (uint64_t)nx;
+                uint32_t *d = sorted + 4 * w;
+                d[0] = p[0]; d[1] = p[1]; d[3] = 0;
+                nx = p[2];
+                d[2] = nx == 0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)(w + 1);
+                ++w;
+            }
+        }
+        memcpy(pool, sorted, np * 16);
+        free(sorted);
+    }
+    return np;
 }

@@ -234,6 +234,28 @@ void dpg_release_cache(void);
  * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
  * recorded since the last call, or DPG_OK.  The status word is per device,
  * shared by all streams. */
+/* Batch lookup of keys in a hash index (section 4).  The index
+ * (device, built by the caller): `table` = 2^m_log2 primary slots and `pool`
+ * = overflow entries, each 16 bytes {uint32 key, uint32 rid, uint32 next,
+ * uint32 0}; key k is in slot h(k) = (k * 0x9E3779B1 mod 2^32) >> (32 -
+ * m_log2) or in the chain of pool entries linked from that slot by `next`
+ * (0xFFFFFFFF ends a chain); rid 0xFFFFFFFF marks an empty slot (whose next
+ * is 0xFFFFFFFF).  Keys in the index are distinct.  out[i] (device, n) =
+ * the rid of keys[i] (device, n), 0xFFFFFFFF when absent.  m_log2 in
+ * [1, 31].
+ * dpg_hash_lookup: DPG -- the keys distributed into runs by
+ * partition of the hash array (partitions of at most the L2 run budget, or
+ * 2^log2_run slots when log2_run > 0; at most 512), each partition staged
+ * into the L2 and probed by its run's keys, the rids gathered back into query
+ * order.  dpg_hash_lookup_direct: one random slot read per key.
+ * Asynchronous; workspace library-owned. */
+dpg_status_t dpg_hash_lookup(const void *table, uint32_t m_log2, const void *pool,
+                             const uint32_t *keys, uint64_t n, uint32_t *out,
+                             dpg_stream_t stream, uint32_t log2_run);
+dpg_status_t dpg_hash_lookup_direct(const void *table, uint32_t m_log2, const void *pool,
+                                    const uint32_t *keys, uint64_t n, uint32_t *out,
+                                    dpg_stream_t stream);
+
 /* Multi-GPU retrieval (north_star config 5; not in the paper: reading A14,
  * DESIGN.md section 8).  One process per GPU.  dpg_get_unique_id: an NCCL
  * unique id (128 bytes) made on one rank and sent to the others by the

@@ -63,6 +63,8 @@ def _load():
         lib.oracle_retrieve_at.argtypes = [P, U, U, P, P, U, P]
         lib.oracle_sort_rids.argtypes = [P, U, U, U, U, P]
         lib.oracle_fk_join_sort.argtypes = [P, U, U, P, P, U, U, P, P]
+        lib.oracle_batch_lookup.argtypes = [P, U, P, U, P]
+        lib.oracle_batch_lookup.restype = ctypes.c_int
         lib.oracle_fk_join_sort.restype = ctypes.c_int
         for f in (lib.oracle_retrieve, lib.oracle_retrieve_u64, lib.oracle_dpg_fig1,
                   lib.oracle_fk_join, lib.oracle_retrieve_at, lib.oracle_sort_rids):
@@ -187,3 +189,17 @@ def fk_join_sort(fact: np.ndarray, fk: np.ndarray, dim: np.ndarray) -> np.ndarra
                                        n_dim, _ptr(out), ctypes.byref(bad)), bad)
     return out
 
+
+
+NOT_FOUND = 0xFFFFFFFF
+
+
+def batch_lookup(keys: np.ndarray, queries: np.ndarray) -> np.ndarray:
+    """Batch index lookup: out[i] = j with keys[j] == queries[i]
+    (keys distinct), NOT_FOUND if none -- sorted pairs and binary search."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    q = np.ascontiguousarray(queries, dtype=np.uint32)
+    out = np.empty(q.size, dtype=np.uint32)
+    if _load().oracle_batch_lookup(_ptr(keys), keys.size, _ptr(q), q.size, _ptr(out)) != 0:
+        raise ValueError("invalid argument")
+    return out

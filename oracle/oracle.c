@@ -291,3 +291,38 @@ int oracle_fk_join_sort(const uint8_t *fact, uint64_t fact_bytes, uint64_t n_fac
     free(a); free(b);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ *
+ * Batch index lookup (section 4): for each query key q[i], the    *
+ * rid of the indexed record with that key, or 0xFFFFFFFF when no record has *
+ * it.  The index maps keys[j] -> rid j (distinct keys).  The plain          *
+ * definition: the (key, rid) pairs sorted by key (library qsort), each       *
+ * query found by binary search -- no hash index involved, so the result does *
+ * not depend on any index layout.                                            *
+ * ------------------------------------------------------------------------ */
+static int cmp_pair(const void *a, const void *b)
+{
+    const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return x < y ? -1 : x > y;
+}
+
+int oracle_batch_lookup(const uint32_t *keys, uint64_t n_keys, const uint32_t *q, uint64_t n_q,
+                        uint32_t *out)
+{
+    if (n_keys >= (1ull << 32)) return -1;
+    uint64_t *pairs = malloc((n_keys ? n_keys : 1) * sizeof(uint64_t));
+    if (!pairs) return -1;
+    for (uint64_t j = 0; j < n_keys; ++j) pairs[j] = ((uint64_t)keys[j] << 32) | j;
+    qsort(pairs, n_keys, sizeof(uint64_t), cmp_pair);
+    for (uint64_t i = 0; i < n_q; ++i) {
+        uint64_t lo = 0, hi = n_keys;                /* first pair with key >= q[i] */
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if ((uint32_t)(pairs[mid] >> 32) < q[i]) lo = mid + 1; else hi = mid;
+        }
+        out[i] = (lo < n_keys && (uint32_t)(pairs[lo] >> 32) == q[i]) ? (uint32_t)pairs[lo]
+                                                                       : 0xFFFFFFFFu;
+    }
+    free(pairs);
+    return 0;
+}

@@ -99,6 +99,8 @@ _sigs = {
     "dpg_retrieve_segments": [_P, _S, _U, _P, _U, ctypes.c_uint32, _P, _P, _P],
     "dpg_ipc_alloc": [_S, _P, _P],
     "dpg_get_unique_id": [_P],
+    "dpg_hash_lookup": [_P, ctypes.c_uint32, _P, _P, _U, _P, _P, ctypes.c_uint32],
+    "dpg_hash_lookup_direct": [_P, ctypes.c_uint32, _P, _P, _U, _P, _P],
     "dpg_comm_create": [_P, ctypes.c_int, ctypes.c_int, _P],
     "dpg_retrieve_dist": [_P, _P, _S, _U, _P, _U, _P, _P],
     "dpg_comm_destroy": [_P],
@@ -397,6 +399,28 @@ def dpg_retrieve_segments(src, rids, seg_rows, seg_dst, stream=None):
                                       nseg, ctypes.cast(rows, ctypes.c_void_p),
                                       ctypes.cast(ptrs, ctypes.c_void_p), _stream_ptr(stream)),
            "dpg_retrieve_segments")
+
+
+def dpg_hash_lookup(table, pool, keys, out=None, stream=None, direct=False, log2_run=0):
+    """Batch lookup: out[i] = rid of keys[i] in the hash index
+    (table: uint32 [2^m, 4] CUDA tensor, pool: uint32 [P, 4]), 0xFFFFFFFF
+    if absent.  direct=True: one random slot read per key instead of DPG."""
+    torch = _torch()
+    m = int(table.shape[0]).bit_length() - 1
+    if table.shape[0] != 1 << m or table.shape[-1] != 4 or not table.is_cuda:
+        raise ValueError("table must be a CUDA [2^m, 4] uint32/int32 tensor")
+    keys = _rid_tensor(keys, "keys")
+    if out is None:
+        out = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+    if direct:
+        _check(_lib.dpg_hash_lookup_direct(table.data_ptr(), m, pool.data_ptr(), keys.data_ptr(),
+                                           keys.numel(), out.data_ptr(), _stream_ptr(stream)),
+               "dpg_hash_lookup_direct")
+    else:
+        _check(_lib.dpg_hash_lookup(table.data_ptr(), m, pool.data_ptr(), keys.data_ptr(),
+                                    keys.numel(), out.data_ptr(), _stream_ptr(stream), log2_run),
+               "dpg_hash_lookup")
+    return out
 
 
 def dpg_get_unique_id() -> bytes:

@@ -1357,6 +1357,82 @@ dpg_status_t dpg_partition_inv(const void* rids, uint32_t rid_bytes, uint64_t n,
   return cuda_status(e);
 }
 
+dpg_status_t dpg_hash_lookup_direct(const void* table, uint32_t m_log2, const void* pool,
+                                    const uint32_t* keys, uint64_t n, uint32_t* out,
+                                    dpg_stream_t stream) {
+  t_launches = 0;
+  if (m_log2 == 0 || m_log2 > 31) return DPG_ERR_INVALID_ARG;
+  if (n == 0) return DPG_OK;
+  if (!table || !keys || !out) return DPG_ERR_INVALID_ARG;
+  uint32_t nl = 0;
+  const cudaError_t e = launch_hash_direct(table, m_log2, pool, keys, n, out, current_sm_count(),
+                                           (cudaStream_t)stream, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_hash_lookup(const void* table, uint32_t m_log2, const void* pool,
+                             const uint32_t* keys, uint64_t n, uint32_t* out, dpg_stream_t stream,
+                             uint32_t log2_run) {
+  // DPG batch lookup: Phase I distributes the keys by partition
+  // of the hash array, Phase II probes partition by partition with the
+  // partition L2-resident, Phase III gathers the rids back into query order.
+  t_launches = 0;
+  if (m_log2 == 0 || m_log2 > 31) return DPG_ERR_INVALID_ARG;
+  if (n == 0) return DPG_OK;
+  if (!table || !keys || !out) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32) - 1) return DPG_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = current_sm_count();
+  // partitions of at most one L2 run budget of slots (16 bytes each), <= 512 runs
+  uint32_t s = m_log2;
+  if (log2_run) {
+    s = std::min<uint32_t>(log2_run, m_log2);
+  } else {
+    const uint64_t B1 = l2_run_budget(current_l2_bytes());
+    while (s > 0 && (1ull << s) * 16 > B1) --s;
+  }
+  const uint32_t K = 1u << (m_log2 - s);
+  if (K > 512) return DPG_ERR_UNSUPPORTED;
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  const uint64_t off_counts = 0;
+  const uint64_t off_rs = align_up((uint64_t)K * sm * 4, 256);
+  const uint64_t off_q = align_up(off_rs + (K + 1) * 4, 256);
+  const uint64_t off_inv = align_up(off_q + n * 4 + 16, 256);
+  const uint64_t off_tmp = align_up(off_inv + n * 4 + 16, 256);
+  const uint64_t bytes = off_tmp + n * 4 + 64;
+  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+  if (w != DPG_OK) return w;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  uint8_t* wb = (uint8_t*)ws;
+  L2KArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = keys;
+  d.rid_bytes = 4;
+  d.n_out = n;
+  d.n_src = 1ull << m_log2;
+  d.s = s;
+  d.K = K;
+  d.chunk = align_up((n + sm - 1) / sm, 32);
+  d.counts = (uint32_t*)(wb + off_counts);
+  d.run_start = (uint32_t*)(wb + off_rs);
+  d.local = (uint32_t*)(wb + off_q);
+  d.inv = (uint32_t*)(wb + off_inv);
+  d.gbar = gbar + 16;
+  d.status = status;
+  d.hash_m = m_log2;
+  uint32_t* tmp = (uint32_t*)(wb + off_tmp);
+  uint32_t nl = 0;
+  cudaError_t e = launch_l2k_distribute(d, (uint32_t)sm, st, &nl);
+  if (e == cudaSuccess)
+    e = launch_hash_probe(table, m_log2, s, K, pool, d.local, d.run_start, tmp, gbar, sm, st, &nl);
+  if (e == cudaSuccess) e = launch_gather_u32(tmp, d.inv, n, out, sm, st, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
 dpg_status_t dpg_ipc_alloc(size_t bytes, void** ptr, uint8_t handle[64]) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   if (!ptr || !handle || bytes == 0) return DPG_ERR_INVALID_ARG;

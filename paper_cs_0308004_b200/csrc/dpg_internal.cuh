@@ -322,6 +322,8 @@ struct L2KArgs {
   uint32_t* inv;         // [n_out] slot of output row i (0xFFFFFFFF: bad rid)
   uint32_t* gbar;        // monotonic grid barrier words (w[0], w[32])
   unsigned long long* status;
+  uint32_t hash_m;       // 0: rids; else the entries are uint32 keys, run of key k =
+                         // hash slot (k * 0x9E3779B1) >> (32 - hash_m) >> s, local = k
 };
 
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
@@ -469,6 +471,15 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
                              int sm, cudaStream_t st, uint32_t* nlaunch,
                              const uint32_t* keys_u32 = nullptr, uint32_t* keys_out = nullptr,
                              uint64_t key_limit = ~0ull, unsigned long long* status = nullptr);
+// Batch lookup in a hash index (hash.cu).
+cudaError_t launch_hash_direct(const void* table, uint32_t m, const void* pool, const uint32_t* keys,
+                               uint64_t n, uint32_t* out, int sm, cudaStream_t st, uint32_t* nl);
+cudaError_t launch_gather_u32(const uint32_t* tmp, const uint32_t* inv, uint64_t n, uint32_t* out,
+                              int sm, cudaStream_t st, uint32_t* nl);
+cudaError_t launch_hash_probe(const void* table, uint32_t m, uint32_t s, uint32_t K, const void* pool,
+                              const uint32_t* qkeys, const uint32_t* run_start, uint32_t* tmp,
+                              uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl);
+
 // Launch count of the last call on this host thread (api.cu).
 uint32_t t_launches_get();
 void t_launches_set(uint32_t n);

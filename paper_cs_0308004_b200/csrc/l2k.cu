@@ -29,7 +29,10 @@ namespace dpg {
 static constexpr int kKThreads = 512;
 static constexpr int kKWarps = kKThreads / 32;
 
-template <typename RidT>
+// HASH: the entries are query keys of the batch index lookup:
+// the "rid" is the key's hash slot, the run its partition of the hash array,
+// and the appended value is the key itself.
+template <typename RidT, bool HASH>
 __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
   const RidT* rids = reinterpret_cast<const RidT*>(a.rids);
   extern __shared__ __align__(16) uint32_t sm[];
@@ -52,6 +55,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint32_t g = g0 + u * kKWarps;
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       r[u] = (g < ngroups && i < hi) ? __ldcg(rids + i) : ~RidT(0);
+      if (HASH && g < ngroups && i < hi) r[u] = (uint32_t)(r[u] * 0x9E3779B1u) >> (32 - a.hash_m);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -59,7 +63,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (g >= ngroups) break;
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       const bool valid = r[u] < a.n_src;
-      if (i < hi && !valid) report_bad(a.status, i);
+      if (!HASH && i < hi && !valid) report_bad(a.status, i);
       const uint32_t b = valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, b);
       if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
@@ -139,6 +143,14 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       r[u] = (g < ngroups && i < hi) ? __ldcs(rids + i) : ~RidT(0);
     }
+    RidT key[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      key[u] = r[u];
+      const uint32_t g = g0 + u * kKWarps;
+      const uint64_t i = lo + 32 * (uint64_t)g + lane;
+      if (HASH && g < ngroups && i < hi) r[u] = (uint32_t)(r[u] * 0x9E3779B1u) >> (32 - a.hash_m);
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t g = g0 + u * kKWarps;
@@ -153,7 +165,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
       if (i < hi) {
         a.inv[i] = valid ? slot : 0xFFFFFFFFu;
-        if (valid) a.local[slot] = (uint32_t)(r[u] & lmask);
+        if (valid) a.local[slot] = HASH ? (uint32_t)key[u] : (uint32_t)(r[u] & lmask);
       }
     }
   }
@@ -164,7 +176,8 @@ uint32_t l2k_smem_bytes(uint32_t K) { return (kKWarps + 1) * K * 4 + 64; }
 cudaError_t launch_l2k_distribute(const L2KArgs& a, uint32_t grid, cudaStream_t st, uint32_t* nl) {
   ++*nl;
   const uint32_t smem = l2k_smem_bytes(a.K);
-  auto fn = a.rid_bytes == 8 ? k_l2k_distribute<uint64_t> : k_l2k_distribute<uint32_t>;
+  auto fn = a.hash_m ? k_l2k_distribute<uint32_t, true>
+                     : a.rid_bytes == 8 ? k_l2k_distribute<uint64_t, false> : k_l2k_distribute<uint32_t, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   L2KArgs arg = a;

@@ -427,6 +427,9 @@ cudaError_t launch_l2run(const L2RunArgs& a, uint32_t W, uint32_t grid, cudaStre
   const uint32_t smem = l2run_smem_bytes(a.chunk);
   if (W == 16) return launch_l2_w<16, 0>(a, grid, smem, st);
   if (W == 8) return launch_l2_w<8, 0>(a, grid, smem, st);
+  // rows of one 4-byte word (the rid gather of the batch lookup): the flat
+  // word loop, one row per lane
+  if (W == 4 && a.rec == 4) return launch_l2_w<4, 0>(a, grid, smem, st);
   if (a.rec <= 128) {
     const bool word4 = a.rec % 4 == 0 && reinterpret_cast<uintptr_t>(a.src) % 4 == 0;
     return word4 ? launch_l2_w<16, 1>(a, grid, smem, st) : launch_l2_w<16, 2>(a, grid, smem, st);

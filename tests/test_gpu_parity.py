@@ -671,3 +671,21 @@ def test_segments_errors(dpg):
         dpg.dpg_retrieve_segments(src, rids, [1] * 9 + [1], [b] * 10)  # more than 8
     with pytest.raises(dpg.DPGError):
         dpg.dpg_retrieve_segments(src, rids, [10], [src.data_ptr()])   # overlaps src
+
+
+# --------------------------------------------------------------------------
+# Batch lookup in a hash index: DPG and the direct lookup.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n_keys,m,n_q,log2_run", [(1 << 12, 13, 20000, 8), (1 << 12, 13, 20000, 0),
+                                                   (5000, 12, 7777, 5), (1 << 20, 21, 1 << 22, 0),
+                                                   (1 << 20, 21, 1 << 22, 17), (1, 1, 100, 0)])
+def test_hash_lookup_matches_oracle(dpg, n_keys, m, n_q, log2_run):
+    w = datagen.hash_workload(n_keys, m, n_q)
+    want = oracle.batch_lookup(w["keys"], w["queries"])
+    t = torch.from_numpy(w["table"].view(np.int32)).cuda()
+    p = torch.from_numpy(w["pool"].view(np.int32)).cuda()
+    q = dev(w["queries"])
+    got = dpg.dpg_hash_lookup(t, p, q, log2_run=log2_run)
+    assert np.array_equal(host(got).view(np.uint32), want)
+    got_d = dpg.dpg_hash_lookup(t, p, q, direct=True)
+    assert np.array_equal(host(got_d).view(np.uint32), want)

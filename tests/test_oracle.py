@@ -319,3 +319,49 @@ def test_exponential_fk_generator_shape():
     assert fk.min() >= int(np.floor(n_dim * np.exp(-1e-7 * ((2 ** 31 - 1) >> 10))))
     h = np.histogram(fk, bins=4, range=(int(0.8109 * n_dim), n_dim))[0]
     assert np.all(np.diff(h) < 0)
+
+
+def test_batch_lookup_against_dict():
+    """Batch lookup pinned to a Python dict over the same pairs,
+    with absent keys, repeated queries and the empty cases."""
+    rng = np.random.default_rng(3)
+    keys = rng.choice(1 << 32, 5000, replace=False).astype(np.uint32)
+    d = {int(k): j for j, k in enumerate(keys)}
+    q = np.concatenate([keys[rng.integers(0, 5000, 3000)],
+                        rng.integers(0, 1 << 32, 2000, dtype=np.uint64).astype(np.uint32),
+                        np.array([0, 0xFFFFFFFF], dtype=np.uint32)])
+    want = np.array([d.get(int(x), oracle.NOT_FOUND) for x in q], dtype=np.uint32)
+    assert np.array_equal(oracle.batch_lookup(keys, q), want)
+    assert oracle.batch_lookup(keys, q[:0]).size == 0
+    assert np.all(oracle.batch_lookup(keys[:0], q[:10]) == oracle.NOT_FOUND)
+    # a key equal to 0xFFFFFFFF is still found (the sentinel is a rid, not a key)
+    k2 = np.array([7, 0xFFFFFFFF, 3], dtype=np.uint32)
+    assert list(oracle.batch_lookup(k2, np.array([0xFFFFFFFF, 3, 8], np.uint32))) == \
+        [1, 2, oracle.NOT_FOUND]
+
+
+def test_hash_index_generator_holds_every_key():
+    """The batch-lookup input (datagen.hash_index): walking slot h(k) and its
+    overflow chain finds every key with its rid; absent keys are not found;
+    every entry is in exactly one place."""
+    keys = datagen.feistel(1 << 32, 0, 3000, 0x611).astype(np.uint32)
+    table, pool = datagen.hash_index(keys, 11)
+    E = 0xFFFFFFFF
+
+    def walk(k):
+        h = (int(k) * 0x9E3779B1 & 0xFFFFFFFF) >> (32 - 11)
+        s = table[h]
+        if s[1] == E:
+            return E
+        if s[0] == k:
+            return int(s[1])
+        nx = int(s[2])
+        while nx != E:
+            if pool[nx][0] == k:
+                return int(pool[nx][1])
+            nx = int(pool[nx][2])
+        return E
+    assert [walk(k) for k in keys] == list(range(3000))
+    absent = datagen.feistel(1 << 32, 3000, 200, 0x611).astype(np.uint32)
+    assert all(walk(k) == E for k in absent)
+    assert (table[:, 1] != E).sum() + len(pool) == 3000
