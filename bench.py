@@ -531,6 +531,9 @@ def main():
     torch.cuda.synchronize()
     dpg.dpg_sync_status()
 
+    step()
+    ran_path = dpg.last_path()       # the plan the calls ran (after the skew check)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -680,7 +683,7 @@ def main():
                        "l2": "flushed before every step (512 MiB write, then 512 MiB read)",
                        "parallelism": "replicas" if world > 1 else "single",
                        "run_len": plan["run_len"], "num_runs": plan["num_runs"],
-                       "pair_bytes": plan["pair_bytes"], "plan_path": plan["path"]},
+                       "pair_bytes": plan["pair_bytes"], "plan_path": ran_path},
             "records_per_s": world * n_out / (ms_per_step * 1e-3),
             "frac_of_hbm_peak": value / world / peak,
             "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
