@@ -207,6 +207,23 @@ def hash_workload(n_keys: int, m_log2: int, n_queries: int, absent_per_mille: in
     return {"keys": keys, "table": table, "pool": pool, "queries": q}
 
 
+BTREE_FANOUT = 16
+
+
+def btree_index(keys: np.ndarray):
+    """The enhanced B+-tree of the batch lookup (every slot used)
+    over (keys[j], rid j): level 0 = the keys sorted (with their rids), level
+    t = every 16th entry of level t-1 (the first key of each node below),
+    up to a top level of <= 16 entries.  Returns (levels, rids): levels[0] is
+    the sorted keys (uint32), rids[j] the rid of levels[0][j]."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    order = np.argsort(keys, kind="stable")
+    levels = [keys[order]]
+    while levels[-1].size > BTREE_FANOUT:
+        levels.append(np.ascontiguousarray(levels[-1][::BTREE_FANOUT]))
+    return levels, order.astype(np.uint32)
+
+
 def stable_key_argsort(recs: np.ndarray, key_len: int = 10) -> np.ndarray:
     """Stable argsort of the records' key bytes (offset 0, unsigned
     lexicographic), ties by ascending rid (reading A10).  Part of the input

@@ -256,6 +256,27 @@ dpg_status_t dpg_hash_lookup_direct(const void *table, uint32_t m_log2, const vo
                                     const uint32_t *keys, uint64_t n, uint32_t *out,
                                     dpg_stream_t stream);
 
+/* Batch lookup of keys in an enhanced B+-tree (section 4).  The
+ * index (device, built by the caller): levels[0] = the N indexed keys sorted
+ * ascending (distinct), rids[j] (device) the rid of levels[0][j]; levels[t]
+ * = every 16th entry of levels[t-1] (level_n[t] = ceil(level_n[t-1] / 16)),
+ * up to a top level of <= 16 entries; n_levels <= 10; each level 64-byte
+ * aligned and readable up to a multiple of 16 entries (host arrays `levels`
+ * of device pointers and `level_n` of counts).  out[i] (device, n) = the
+ * rid of keys[i] (device, n), 0xFFFFFFFF when absent.
+ * dpg_btree_lookup: the two-pass DPG lookup -- the top of the
+ * tree places every key in a run of consecutive subtrees (runs of 2^s
+ * level-0 entries within the L2 run budget, or 2^log2_run when > 0; at most
+ * 512 runs), each run's lower levels are staged into the L2 and its keys
+ * complete their descent there, the rids gathered back into query order.
+ * dpg_btree_lookup_direct: one full descent per key.  Asynchronous. */
+dpg_status_t dpg_btree_lookup(const uint32_t *const *levels, const uint64_t *level_n,
+                              uint32_t n_levels, const uint32_t *rids, const uint32_t *keys,
+                              uint64_t n, uint32_t *out, dpg_stream_t stream, uint32_t log2_run);
+dpg_status_t dpg_btree_lookup_direct(const uint32_t *const *levels, const uint64_t *level_n,
+                                     uint32_t n_levels, const uint32_t *rids, const uint32_t *keys,
+                                     uint64_t n, uint32_t *out, dpg_stream_t stream);
+
 /* Multi-GPU retrieval (north_star config 5; not in the paper: reading A14,
  * DESIGN.md section 8).  One process per GPU.  dpg_get_unique_id: an NCCL
  * unique id (128 bytes) made on one rank and sent to the others by the

@@ -23,6 +23,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libdpg.so")
 
@@ -101,6 +103,8 @@ _sigs = {
     "dpg_get_unique_id": [_P],
     "dpg_hash_lookup": [_P, ctypes.c_uint32, _P, _P, _U, _P, _P, ctypes.c_uint32],
     "dpg_hash_lookup_direct": [_P, ctypes.c_uint32, _P, _P, _U, _P, _P],
+    "dpg_btree_lookup": [_P, _P, ctypes.c_uint32, _P, _P, _U, _P, _P, ctypes.c_uint32],
+    "dpg_btree_lookup_direct": [_P, _P, ctypes.c_uint32, _P, _P, _U, _P, _P],
     "dpg_comm_create": [_P, ctypes.c_int, ctypes.c_int, _P],
     "dpg_retrieve_dist": [_P, _P, _S, _U, _P, _U, _P, _P],
     "dpg_comm_destroy": [_P],
@@ -420,6 +424,38 @@ def dpg_hash_lookup(table, pool, keys, out=None, stream=None, direct=False, log2
         _check(_lib.dpg_hash_lookup(table.data_ptr(), m, pool.data_ptr(), keys.data_ptr(),
                                     keys.numel(), out.data_ptr(), _stream_ptr(stream), log2_run),
                "dpg_hash_lookup")
+    return out
+
+
+def btree_to_device(levels, rids, device="cuda"):
+    """The B+-tree levels (numpy uint32 arrays, level 0 = sorted keys) and the
+    rids as CUDA tensors, each level padded to a multiple of 16 entries."""
+    torch = _torch()
+    out = []
+    for lv in levels:
+        pad = (-lv.size) % 16
+        a = np.concatenate([lv, np.full(pad, 0xFFFFFFFF, dtype=np.uint32)]) if pad else lv
+        out.append(torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(device))
+    r = torch.from_numpy(np.ascontiguousarray(rids, dtype=np.uint32).view(np.int32)).to(device)
+    return out, [int(lv.size) for lv in levels], r
+
+
+def dpg_btree_lookup(levels, level_n, rids, keys, out=None, stream=None, direct=False, log2_run=0):
+    """Batch lookup in an enhanced B+-tree: out[i] = rid of
+    keys[i], 0xFFFFFFFF if absent.  levels/level_n/rids from btree_to_device."""
+    torch = _torch()
+    keys = _rid_tensor(keys, "keys")
+    if out is None:
+        out = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+    L = len(levels)
+    ptrs = (ctypes.c_void_p * L)(*[t.data_ptr() for t in levels])
+    ns = (ctypes.c_uint64 * L)(*level_n)
+    args = [ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(ns, ctypes.c_void_p), L, rids.data_ptr(),
+            keys.data_ptr(), keys.numel(), out.data_ptr(), _stream_ptr(stream)]
+    if direct:
+        _check(_lib.dpg_btree_lookup_direct(*args), "dpg_btree_lookup_direct")
+    else:
+        _check(_lib.dpg_btree_lookup(*args, log2_run), "dpg_btree_lookup")
     return out
 
 

@@ -1433,6 +1433,110 @@ dpg_status_t dpg_hash_lookup(const void* table, uint32_t m_log2, const void* poo
   return cuda_status(e);
 }
 
+static dpg_status_t btree_args(const uint32_t* const* levels, const uint64_t* level_n,
+                               uint32_t n_levels, const uint32_t* rids, BTreeIdx* T) {
+  if (!levels || !level_n || !rids || n_levels == 0 || n_levels > (uint32_t)kBtMaxLevels)
+    return DPG_ERR_INVALID_ARG;
+  std::memset(T, 0, sizeof(*T));
+  T->levels = n_levels;
+  T->rids = rids;
+  for (uint32_t t = 0; t < n_levels; ++t) {
+    if (!levels[t] || level_n[t] == 0 || level_n[t] >= (1ull << 32) || (uintptr_t)levels[t] % 64)
+      return DPG_ERR_INVALID_ARG;
+    if (t && level_n[t] != (level_n[t - 1] + 15) / 16) return DPG_ERR_INVALID_ARG;
+    T->lv[t] = levels[t];
+    T->n[t] = (uint32_t)level_n[t];
+  }
+  if (level_n[n_levels - 1] > 16) return DPG_ERR_INVALID_ARG;
+  return DPG_OK;
+}
+
+dpg_status_t dpg_btree_lookup_direct(const uint32_t* const* levels, const uint64_t* level_n,
+                                     uint32_t n_levels, const uint32_t* rids, const uint32_t* keys,
+                                     uint64_t n, uint32_t* out, dpg_stream_t stream) {
+  t_launches = 0;
+  BTreeIdx T;
+  const dpg_status_t a = btree_args(levels, level_n, n_levels, rids, &T);
+  if (a != DPG_OK) return a;
+  if (n == 0) return DPG_OK;
+  if (!keys || !out) return DPG_ERR_INVALID_ARG;
+  uint32_t nl = 0;
+  const cudaError_t e = launch_bt_direct(T, keys, n, out, current_sm_count(), (cudaStream_t)stream, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
+dpg_status_t dpg_btree_lookup(const uint32_t* const* levels, const uint64_t* level_n,
+                              uint32_t n_levels, const uint32_t* rids, const uint32_t* keys,
+                              uint64_t n, uint32_t* out, dpg_stream_t stream, uint32_t log2_run) {
+  // the two-pass DPG lookup
+  t_launches = 0;
+  BTreeIdx T;
+  const dpg_status_t a = btree_args(levels, level_n, n_levels, rids, &T);
+  if (a != DPG_OK) return a;
+  if (n == 0) return DPG_OK;
+  if (!keys || !out) return DPG_ERR_INVALID_ARG;
+  if (n >= (1ull << 32) - 1) return DPG_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = current_sm_count();
+  const uint64_t N = level_n[0];
+  // run = 2^s consecutive level-0 entries (keys + rids, 8 bytes each) within
+  // one L2 run budget, rooted at a level whose entries span 16^stop <= 2^s
+  uint32_t s = 0;
+  while ((1ull << s) < N) ++s;
+  if (log2_run) {
+    s = std::min<uint32_t>(s, log2_run);
+  } else {
+    const uint64_t B1 = l2_run_budget(current_l2_bytes());
+    while (s > 4 && (1ull << s) * 8 > B1) --s;
+  }
+  uint32_t stop = std::min<uint32_t>(s / 4, n_levels - 1);
+  const uint32_t shift = s - 4 * stop;
+  const uint64_t K64 = (N + (1ull << s) - 1) >> s;
+  if (K64 > 512) return DPG_ERR_UNSUPPORTED;
+  const uint32_t K = (uint32_t)std::max<uint64_t>(1, K64);
+  uint32_t *gbar = nullptr, *total = nullptr;
+  void* ws = nullptr;
+  const uint64_t off_counts = 0;
+  const uint64_t off_rs = align_up((uint64_t)K * sm * 4, 256);
+  const uint64_t off_run = align_up(off_rs + (K + 1) * 4, 256);
+  const uint64_t off_q = align_up(off_run + n * 4 + 16, 256);
+  const uint64_t off_inv = align_up(off_q + n * 4 + 16, 256);
+  const uint64_t off_tmp = align_up(off_inv + n * 4 + 16, 256);
+  const uint64_t bytes = off_tmp + n * 4 + 64;
+  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+  if (w != DPG_OK) return w;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  uint8_t* wb = (uint8_t*)ws;
+  uint32_t* run = (uint32_t*)(wb + off_run);
+  uint32_t* tmp = (uint32_t*)(wb + off_tmp);
+  uint32_t nl = 0;
+  cudaError_t e = launch_bt_top(T, stop, shift, keys, n, run, sm, st, &nl);
+  L2KArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.rids = run;
+  d.rid_bytes = 4;
+  d.n_out = n;
+  d.n_src = K;
+  d.s = 0;
+  d.K = K;
+  d.chunk = align_up((n + sm - 1) / sm, 32);
+  d.counts = (uint32_t*)(wb + off_counts);
+  d.run_start = (uint32_t*)(wb + off_rs);
+  d.local = (uint32_t*)(wb + off_q);
+  d.inv = (uint32_t*)(wb + off_inv);
+  d.gbar = gbar + 16;
+  d.status = status;
+  d.payload = keys;
+  if (e == cudaSuccess) e = launch_l2k_distribute(d, (uint32_t)sm, st, &nl);
+  if (e == cudaSuccess)
+    e = launch_bt_probe(T, K, s, stop, d.local, d.run_start, tmp, gbar, sm, st, &nl);
+  if (e == cudaSuccess) e = launch_gather_u32(tmp, d.inv, n, out, sm, st, &nl);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
 dpg_status_t dpg_ipc_alloc(size_t bytes, void** ptr, uint8_t handle[64]) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   if (!ptr || !handle || bytes == 0) return DPG_ERR_INVALID_ARG;

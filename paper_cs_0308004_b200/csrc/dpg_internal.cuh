@@ -324,6 +324,17 @@ struct L2KArgs {
   unsigned long long* status;
   uint32_t hash_m;       // 0: rids; else the entries are uint32 keys, run of key k =
                          // hash slot (k * 0x9E3779B1) >> (32 - hash_m) >> s, local = k
+  const uint32_t* payload;   // rids mode: local[slot] = payload[i] instead of r & (L-1)
+};
+
+// Enhanced B+-tree of the batch lookup (btree.cu): level 0 = sorted keys,
+// level t = every 16th entry of level t-1, each level padded to 16 entries.
+constexpr int kBtMaxLevels = 10;
+struct BTreeIdx {
+  const uint32_t* lv[kBtMaxLevels];
+  uint32_t n[kBtMaxLevels];
+  uint32_t levels;
+  const uint32_t* rids;  // rid of each level-0 entry
 };
 
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion
@@ -479,6 +490,15 @@ cudaError_t launch_gather_u32(const uint32_t* tmp, const uint32_t* inv, uint64_t
 cudaError_t launch_hash_probe(const void* table, uint32_t m, uint32_t s, uint32_t K, const void* pool,
                               const uint32_t* qkeys, const uint32_t* run_start, uint32_t* tmp,
                               uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl);
+
+// Batch lookup in an enhanced B+-tree (btree.cu).
+cudaError_t launch_bt_direct(const BTreeIdx& T, const uint32_t* keys, uint64_t n, uint32_t* out,
+                             int sm, cudaStream_t st, uint32_t* nl);
+cudaError_t launch_bt_top(const BTreeIdx& T, uint32_t stop, uint32_t shift, const uint32_t* keys,
+                          uint64_t n, uint32_t* run, int sm, cudaStream_t st, uint32_t* nl);
+cudaError_t launch_bt_probe(const BTreeIdx& T, uint32_t K, uint32_t s, uint32_t stop,
+                            const uint32_t* qkeys, const uint32_t* run_start, uint32_t* tmp,
+                            uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl);
 
 // Launch count of the last call on this host thread (api.cu).
 uint32_t t_launches_get();

@@ -165,7 +165,9 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
       if (i < hi) {
         a.inv[i] = valid ? slot : 0xFFFFFFFFu;
-        if (valid) a.local[slot] = HASH ? (uint32_t)key[u] : (uint32_t)(r[u] & lmask);
+        if (valid)
+          a.local[slot] = HASH ? (uint32_t)key[u]
+                               : a.payload ? __ldcs(a.payload + i) : (uint32_t)(r[u] & lmask);
       }
     }
   }

@@ -689,3 +689,22 @@ def test_hash_lookup_matches_oracle(dpg, n_keys, m, n_q, log2_run):
     assert np.array_equal(host(got).view(np.uint32), want)
     got_d = dpg.dpg_hash_lookup(t, p, q, direct=True)
     assert np.array_equal(host(got_d).view(np.uint32), want)
+
+
+# --------------------------------------------------------------------------
+# Batch lookup in an enhanced B+-tree: DPG and the direct descent.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n_keys,n_q,log2_run", [(1 << 12, 20000, 8), (5000, 7777, 6), (5000, 7777, 0),
+                                                 (1 << 20, 1 << 22, 0), (1 << 20, 1 << 22, 16),
+                                                 (1, 100, 0), (17, 1000, 4)])
+def test_btree_lookup_matches_oracle(dpg, n_keys, n_q, log2_run):
+    w = datagen.hash_workload(n_keys, max(1, (n_keys - 1).bit_length()), n_q)
+    w["queries"][:3] = [0, 0xFFFFFFFF, w["keys"].min()]      # below, above, the smallest key
+    want = oracle.batch_lookup(w["keys"], w["queries"])
+    levels, rids = datagen.btree_index(w["keys"])
+    lv, ln, r = dpg.btree_to_device(levels, rids)
+    q = dev(w["queries"])
+    got = dpg.dpg_btree_lookup(lv, ln, r, q, log2_run=log2_run)
+    assert np.array_equal(host(got).view(np.uint32), want)
+    got_d = dpg.dpg_btree_lookup(lv, ln, r, q, direct=True)
+    assert np.array_equal(host(got_d).view(np.uint32), want)

@@ -365,3 +365,26 @@ def test_hash_index_generator_holds_every_key():
     absent = datagen.feistel(1 << 32, 3000, 200, 0x611).astype(np.uint32)
     assert all(walk(k) == E for k in absent)
     assert (table[:, 1] != E).sum() + len(pool) == 3000
+
+
+def test_btree_generator_descent_finds_every_key():
+    """The batch-lookup B+-tree input (datagen.btree_index): a descent from the
+    top (largest entry <= key in each 16-entry node) ends at every key with
+    its rid; absent keys end at a different key."""
+    keys = datagen.feistel(1 << 32, 0, 5000, 0x611).astype(np.uint32)
+    levels, rids = datagen.btree_index(keys)
+    assert levels[-1].size <= 16 and levels[0].size == 5000
+
+    def descend(q):
+        top = levels[-1]
+        c = int(np.sum(top <= q))
+        if c == 0:
+            return None
+        j = c - 1
+        for t in range(len(levels) - 2, -1, -1):
+            node = levels[t][16 * j:16 * j + 16]
+            j = 16 * j + int(np.sum(node <= q)) - 1
+        return j if levels[0][j] == q else None
+    assert all(rids[descend(k)] == i for i, k in enumerate(keys))
+    absent = datagen.feistel(1 << 32, 5000, 300, 0x611).astype(np.uint32)
+    assert all(descend(k) is None for k in absent)
