@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(const __grid_consta
   __syncwarp();
   }
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 1] = globaltimer();
-  if (a.stage) grid_barrier(a.gbar, G);
+  if (a.stage) grid_barrier_mono(a.gbar + 16, G);   // (one poller: CTA 0)
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 2] = globaltimer();
 
   // The rid run (this CTA's chunk of the rid list) is read group by group,
