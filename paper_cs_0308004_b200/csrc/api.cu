@@ -1394,41 +1394,36 @@ dpg_status_t dpg_hash_lookup(const void* table, uint32_t m_log2, const void* poo
   }
   const uint32_t K = 1u << (m_log2 - s);
   if (K > 512) return DPG_ERR_UNSUPPORTED;
+  // fixed run capacity: the hash spreads keys evenly (expectation + 6 sigma);
+  // the keys beyond it (duplicates of hot keys) are looked up directly
+  const double mean = (double)n / K;
+  const uint64_t cap64 = (uint64_t)(mean + 6.0 * std::sqrt(mean) + 64);
+  const uint32_t cap = (uint32_t)std::min<uint64_t>(cap64, UINT32_MAX / K);
   uint32_t *gbar = nullptr, *total = nullptr;
   void* ws = nullptr;
-  const uint64_t off_counts = 0;
-  const uint64_t off_rs = align_up((uint64_t)K * sm * 4, 256);
-  const uint64_t off_q = align_up(off_rs + (K + 1) * 4, 256);
-  const uint64_t off_inv = align_up(off_q + n * 4 + 16, 256);
+  const uint64_t slots = (uint64_t)K * cap;
+  const uint64_t off_cur = 0;                                   // [K] cursors + overflow count
+  const uint64_t off_q = align_up((K + 1) * 4, 256);
+  const uint64_t off_inv = align_up(off_q + slots * 4 + 16, 256);
   const uint64_t off_tmp = align_up(off_inv + n * 4 + 16, 256);
-  const uint64_t bytes = off_tmp + n * 4 + 64;
+  const uint64_t off_ovf = align_up(off_tmp + slots * 4 + 16, 256);
+  const uint64_t bytes = off_ovf + n * 8 + 64;
   dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws);
   if (w != DPG_OK) return w;
-  unsigned long long* status = device_status();
-  if (!status) return DPG_ERR_CUDA;
   uint8_t* wb = (uint8_t*)ws;
-  L2KArgs d;
-  std::memset(&d, 0, sizeof(d));
-  d.rids = keys;
-  d.rid_bytes = 4;
-  d.n_out = n;
-  d.n_src = 1ull << m_log2;
-  d.s = s;
-  d.K = K;
-  d.chunk = align_up((n + sm - 1) / sm, 32);
-  d.counts = (uint32_t*)(wb + off_counts);
-  d.run_start = (uint32_t*)(wb + off_rs);
-  d.local = (uint32_t*)(wb + off_q);
-  d.inv = (uint32_t*)(wb + off_inv);
-  d.gbar = gbar + 16;
-  d.status = status;
-  d.hash_m = m_log2;
+  uint32_t* cursor = (uint32_t*)(wb + off_cur);
+  uint32_t* qk = (uint32_t*)(wb + off_q);
+  uint32_t* inv = (uint32_t*)(wb + off_inv);
   uint32_t* tmp = (uint32_t*)(wb + off_tmp);
+  uint64_t* ovf = (uint64_t*)(wb + off_ovf);
   uint32_t nl = 0;
-  cudaError_t e = launch_l2k_distribute(d, (uint32_t)sm, st, &nl);
+  cudaError_t e = cudaMemsetAsync(cursor, 0, (K + 1) * 4, st);
   if (e == cudaSuccess)
-    e = launch_hash_probe(table, m_log2, s, K, pool, d.local, d.run_start, tmp, gbar, sm, st, &nl);
-  if (e == cudaSuccess) e = launch_gather_u32(tmp, d.inv, n, out, sm, st, &nl);
+    e = launch_hash_distribute(keys, n, m_log2, s, K, cap, cursor, qk, inv, ovf, cursor + K, sm, st, &nl);
+  if (e == cudaSuccess)
+    e = launch_hash_probe(table, m_log2, s, K, pool, qk, nullptr, tmp, gbar, sm, st, &nl, cursor, cap);
+  if (e == cudaSuccess) e = launch_gather_u32(tmp, inv, n, out, sm, st, &nl);
+  if (e == cudaSuccess) e = launch_hash_overflow(table, m_log2, pool, ovf, cursor + K, out, sm, st, &nl);
   t_launches = nl;
   return cuda_status(e);
 }

@@ -489,7 +489,15 @@ cudaError_t launch_gather_u32(const uint32_t* tmp, const uint32_t* inv, uint64_t
                               int sm, cudaStream_t st, uint32_t* nl);
 cudaError_t launch_hash_probe(const void* table, uint32_t m, uint32_t s, uint32_t K, const void* pool,
                               const uint32_t* qkeys, const uint32_t* run_start, uint32_t* tmp,
-                              uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl);
+                              uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl,
+                              const uint32_t* counts = nullptr, uint32_t cap = 0);
+cudaError_t launch_hash_distribute(const uint32_t* keys, uint64_t n, uint32_t m, uint32_t s, uint32_t K,
+                                   uint32_t cap, uint32_t* cursor, uint32_t* qkeys, uint32_t* inv,
+                                   uint64_t* ovf, uint32_t* n_ovf, int sm, cudaStream_t st,
+                                   uint32_t* nl);
+cudaError_t launch_hash_overflow(const void* table, uint32_t m, const void* pool, const uint64_t* ovf,
+                                 const uint32_t* n_ovf, uint32_t* out, int sm, cudaStream_t st,
+                                 uint32_t* nl);
 
 // Batch lookup in an enhanced B+-tree (btree.cu).
 cudaError_t launch_bt_direct(const BTreeIdx& T, const uint32_t* keys, uint64_t n, uint32_t* out,

@@ -83,6 +83,8 @@ struct HashProbeArgs {
   const uint32_t* run_start;   // [K + 1]
   uint32_t* tmp;           // rids, run-major
   uint32_t* gbar;          // grid barrier words (count, generation; zero-restored)
+  const uint32_t* counts;  // fixed-capacity layout: run b at [b*cap, b*cap + min(counts[b], cap))
+  uint32_t cap;            //   (counts == nullptr: run b at [run_start[b], run_start[b+1]))
 };
 
 // Phase II over all runs.  Lane 0 of warp 0 of every CTA streams its slice
@@ -112,7 +114,14 @@ __global__ void __launch_bounds__(kHThreads, 1) k_hash_probe(HashProbeArgs a) {
       __syncwarp();
     }
     grid_barrier(a.gbar, G);
-    const uint64_t e0 = __ldg(a.run_start + b), e1 = __ldg(a.run_start + b + 1);
+    uint64_t e0, e1;
+    if (a.counts) {
+      e0 = (uint64_t)b * a.cap;
+      e1 = e0 + min(__ldcg(a.counts + b), a.cap);
+    } else {
+      e0 = __ldg(a.run_start + b);
+      e1 = __ldg(a.run_start + b + 1);
+    }
     const uint64_t per = ((e1 - e0 + G - 1) / G + 31) & ~uint64_t(31);
     const uint64_t lo = min_u64(e1, e0 + (uint64_t)c * per), hi = min_u64(e1, lo + per);
     constexpr int U = 4;
@@ -144,11 +153,95 @@ __global__ void __launch_bounds__(256) k_gather_u32(const uint32_t* __restrict__
 #pragma unroll
     for (int u = 0; u < U; ++u) j[u] = i0 + u * stride < n ? __ldcs(inv + i0 + u * stride) : 0u;
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = i0 + u * stride < n ? __ldcg(tmp + j[u]) : 0u;
+    for (int u = 0; u < U; ++u) v[u] = i0 + u * stride < n && j[u] != kNotFound ? __ldcg(tmp + j[u]) : 0u;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i0 + u * stride < n) __stcs(out + i0 + u * stride, v[u]);
+    for (int u = 0; u < U; ++u)   // (inv = 0xFFFFFFFF: an overflow key, looked up directly)
+      if (i0 + u * stride < n && j[u] != kNotFound) __stcs(out + i0 + u * stride, v[u]);
   }
+}
+
+// Phase I in one pass (the hash spreads the keys evenly over the partitions,
+// so every run gets a fixed capacity): per tile of 8192 keys (16 per thread,
+// read once) a shared-memory rank inside (tile, run), one global reservation
+// per (tile, run), and each key written at b*cap + base + rank with its slot
+// in inv; a key beyond its run's capacity goes to an overflow list (looked up
+// directly after Phase III).
+static constexpr int kHdKpt = 16;
+__global__ void __launch_bounds__(kHThreads, 1) k_hash_distribute(
+    const uint32_t* __restrict__ keys, uint64_t n, uint64_t chunk, uint32_t m, uint32_t s, uint32_t K,
+    uint32_t cap, uint32_t* __restrict__ cursor, uint32_t* __restrict__ qkeys, uint32_t* __restrict__ inv,
+    uint64_t* __restrict__ ovf, uint32_t* __restrict__ n_ovf) {
+  __shared__ uint32_t cnt[512], base[512];
+  const int tid = threadIdx.x;
+  const uint64_t lo = min_u64(n, (uint64_t)blockIdx.x * chunk), hi = min_u64(n, lo + chunk);
+  for (uint64_t t0 = lo; t0 < hi; t0 += kHThreads * kHdKpt) {
+    for (uint32_t b = tid; b < K; b += kHThreads) cnt[b] = 0;
+    __syncthreads();
+    uint32_t k[kHdKpt], rk[kHdKpt];
+#pragma unroll
+    for (int u = 0; u < kHdKpt; ++u) {
+      const uint64_t i = t0 + (uint64_t)u * kHThreads + tid;
+      k[u] = i < hi ? __ldcs(keys + i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kHdKpt; ++u) {
+      const uint64_t i = t0 + (uint64_t)u * kHThreads + tid;
+      if (i < hi) rk[u] = atomicAdd(&cnt[hslot(k[u], m) >> s], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = tid; b < K; b += kHThreads) base[b] = cnt[b] ? atomicAdd(cursor + b, cnt[b]) : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kHdKpt; ++u) {
+      const uint64_t i = t0 + (uint64_t)u * kHThreads + tid;
+      if (i >= hi) continue;
+      const uint32_t b = hslot(k[u], m) >> s;
+      const uint32_t slot = base[b] + rk[u];
+      if (slot < cap) {
+        const uint32_t e = b * cap + slot;
+        qkeys[e] = k[u];
+        __stcs(inv + i, e);
+      } else {
+        const uint32_t o = atomicAdd(n_ovf, 1u);
+        ovf[o] = (i << 32) | k[u];
+        __stcs(inv + i, kNotFound);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// The overflow keys of the one-pass Phase I: looked up directly.
+__global__ void __launch_bounds__(256) k_hash_overflow(const uint4* __restrict__ table, uint32_t m,
+                                                        const uint4* __restrict__ pool,
+                                                        const uint64_t* __restrict__ ovf,
+                                                        const uint32_t* __restrict__ n_ovf,
+                                                        uint32_t* __restrict__ out) {
+  const uint32_t no = *n_ovf;
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < no; o += gridDim.x * blockDim.x) {
+    const uint64_t e = ovf[o];
+    const uint32_t key = (uint32_t)e;
+    out[e >> 32] = hash_chain(__ldg(table + hslot(key, m)), key, pool);
+  }
+}
+
+cudaError_t launch_hash_distribute(const uint32_t* keys, uint64_t n, uint32_t m, uint32_t s, uint32_t K,
+                                   uint32_t cap, uint32_t* cursor, uint32_t* qkeys, uint32_t* inv,
+                                   uint64_t* ovf, uint32_t* n_ovf, int sm, cudaStream_t st,
+                                   uint32_t* nl) {
+  ++*nl;
+  const uint64_t chunk = (n + sm - 1) / sm;
+  k_hash_distribute<<<sm, kHThreads, 0, st>>>(keys, n, chunk, m, s, K, cap, cursor, qkeys, inv, ovf,
+                                              n_ovf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash_overflow(const void* table, uint32_t m, const void* pool, const uint64_t* ovf,
+                                 const uint32_t* n_ovf, uint32_t* out, int sm, cudaStream_t st,
+                                 uint32_t* nl) {
+  ++*nl;
+  k_hash_overflow<<<sm * 2, 256, 0, st>>>((const uint4*)table, m, (const uint4*)pool, ovf, n_ovf, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gather_u32(const uint32_t* tmp, const uint32_t* inv, uint64_t n, uint32_t* out,
@@ -169,9 +262,12 @@ cudaError_t launch_hash_direct(const void* table, uint32_t m, const void* pool, 
 
 cudaError_t launch_hash_probe(const void* table, uint32_t m, uint32_t s, uint32_t K, const void* pool,
                               const uint32_t* qkeys, const uint32_t* run_start, uint32_t* tmp,
-                              uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl) {
+                              uint32_t* gbar, int sm, cudaStream_t st, uint32_t* nl,
+                              const uint32_t* counts, uint32_t cap) {
   ++*nl;
   HashProbeArgs a;
+  a.counts = counts;
+  a.cap = cap;
   a.table = (const uint4*)table;
   a.m = m;
   a.s = s;

@@ -708,3 +708,18 @@ def test_btree_lookup_matches_oracle(dpg, n_keys, n_q, log2_run):
     assert np.array_equal(host(got).view(np.uint32), want)
     got_d = dpg.dpg_btree_lookup(lv, ln, r, q, direct=True)
     assert np.array_equal(host(got_d).view(np.uint32), want)
+
+
+def test_hash_lookup_hot_key_overflow(dpg):
+    """Duplicates of one key fill its partition past the fixed run capacity:
+    the excess keys take the direct lookup (and absent hot keys too)."""
+    w = datagen.hash_workload(1 << 14, 15, 1 << 20)
+    q = w["queries"].copy()
+    q[: 1 << 19] = w["keys"][123]
+    q[1 << 19: (1 << 19) + 5000] = 0xDEADBEEF if 0xDEADBEEF not in set(w["keys"].tolist()) else 7
+    want = oracle.batch_lookup(w["keys"], q)
+    t = torch.from_numpy(w["table"].view(np.int32)).cuda()
+    p = torch.from_numpy(w["pool"].view(np.int32)).cuda()
+    for log2_run in (0, 10):
+        got = dpg.dpg_hash_lookup(t, p, dev(q), log2_run=log2_run)
+        assert np.array_equal(host(got).view(np.uint32), want), log2_run
