@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kHThreads, 1) k_hash_probe(HashProbeArgs a) {
     }
     const uint64_t per = ((e1 - e0 + G - 1) / G + 31) & ~uint64_t(31);
     const uint64_t lo = min_u64(e1, e0 + (uint64_t)c * per), hi = min_u64(e1, lo + per);
-    constexpr int U = 4;
+    constexpr int U = 16;     // keys in flight per thread (the probe is latency-bound)
     for (uint64_t e = lo + tid; e < hi; e += U * kHThreads) {
       uint32_t k[U];
       uint4 sl[U];
