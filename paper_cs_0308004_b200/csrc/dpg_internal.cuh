@@ -284,7 +284,10 @@ struct L2RunArgs {
   const uint32_t* dev_range;  // optional [2] on the device: rows [r0, r1) (rids, dst offset by r0)
   uint32_t rd_magic;     // ceil(2^32 / (rec / 4)): dword -> row division of the gather
   uint32_t dbg;          // tuning flags (dpg_debug_flags): bit0 LSU stores of the tile,
-                         // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first
+                         // bit1 no tile store, bit2 no Phase II load, bit3 L2 prefetch first,
+                         // bit16 Phase II by L2 bulk prefetches, bit17 no barrier after
+                         // Phase II (only with bit16), bits 20/21 skip consume/issue
+                         // (profiles/r01_l2_prefetch_staging.txt, r01_engine_probe.txt)
   OutSegs seg;           // output segments (seg.n = 0: dst); the window-gather path only
 };
 

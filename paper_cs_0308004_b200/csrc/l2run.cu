@@ -100,7 +100,12 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(const __grid_consta
     const uint32_t CH = a.ring_chunk ? a.ring_chunk : (32u << 10);
     const uint32_t NS = a.ring_slots ? a.ring_slots : 6;
     uint32_t j = 0;
-    if (a.stage)
+    if (a.stage && (a.dbg & 0x10000)) {
+      // experiment: L2 prefetches of the slice (no shared memory, no completion)
+      for (uint64_t off = b0; off < b1; off += CH)
+        bulk_prefetch_l2(reinterpret_cast<const void*>(s0 + off), (uint32_t)min_u64(CH, b1 - off),
+                         pol_stage);
+    } else if (a.stage)
     for (uint64_t off = b0; off < b1; off += CH, ++j) {
       const uint32_t slot = j % NS;
       if (j >= NS) mbar_wait(&bar[slot], ((j / NS) - 1) & 1);
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_dpg_l2run(const __grid_consta
   __syncwarp();
   }
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 1] = globaltimer();
-  if (a.stage) grid_barrier_mono(a.gbar + 16, G);   // (one poller: CTA 0)
+  if (a.stage && !(a.dbg & 0x20000)) grid_barrier_mono(a.gbar + 16, G);   // (one poller: CTA 0)
   if (a.ts && tid == 0) a.ts[(size_t)c * 16 + 2] = globaltimer();
 
   // The rid run (this CTA's chunk of the rid list) is read group by group,
