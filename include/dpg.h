@@ -379,7 +379,8 @@ uint32_t dpg_last_launch_count(void);
  * (section 2.3: 65,536 rids at evenly spaced positions, counted
  * per group of runs; one stream synchronisation); when the estimated rids
  * beyond the runs' fixed capacity exceed 2% of the input, the call runs the
- * count-based L2 runs (path 5) instead, whose run sizes are exact. */
+ * count-based L2 runs (path 5) instead, whose run sizes are exact.  (Not
+ * while the stream is being captured into a CUDA graph: no sampling then.) */
 uint32_t dpg_last_path(void);
 
 /* Phase timing (bench.py's roofline): while enabled, every dpg_retrieve /

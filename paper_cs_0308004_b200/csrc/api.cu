@@ -630,7 +630,10 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     const bool auto_plan = !opt || (opt->path == 0 && !opt->log2_run && !opt->grid_distribute &&
                                     !opt->grid_probe && !opt->hist_mode && !opt->gather &&
                                     !opt->pair_bytes);
-    if (auto_plan && p.path == 1 && pay == 0 && n_out >= kSkewMinRids && !(g_debug_flags & 64)) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);      // (a graph capture cannot synchronise: no sampling)
+    if (auto_plan && p.path == 1 && pay == 0 && n_out >= kSkewMinRids && !(g_debug_flags & 64) &&
+        cap == cudaStreamCaptureStatusNone) {
       uint64_t excess = 0;
       dpg_status_t ks = skew_excess(rids, n_out, n_src, p, st, &excess, &nl_skew);
       if (ks != DPG_OK) return ks;

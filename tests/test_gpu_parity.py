@@ -723,3 +723,27 @@ def test_hash_lookup_hot_key_overflow(dpg):
     for log2_run in (0, 10):
         got = dpg.dpg_hash_lookup(t, p, dev(q), log2_run=log2_run)
         assert np.array_equal(host(got).view(np.uint32), want), log2_run
+
+
+def test_graph_capture_of_a_large_fixed_run_plan(dpg):
+    """A CUDA graph can capture dpg_retrieve on a plan that would sample for
+    skew (the sampling synchronises, so it is skipped under capture); the
+    replayed graph gives the oracle's rows."""
+    rng = np.random.default_rng(8)
+    n_src = 3 << 20
+    src = dev(rng.integers(0, 256, (n_src, 64), dtype=np.uint8))
+    rids_np = rng.integers(0, n_src, 5 << 20).astype(np.uint32)
+    rids = dev(rids_np)
+    out = torch.empty((rids.numel(), 64), dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(src, rids, dst=out)                       # warm (workspace allocated)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    out.zero_()
+    with torch.cuda.graph(g, stream=s):
+        dpg.dpg_retrieve(src, rids, dst=out, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    idx = rng.integers(0, rids.numel(), 20000)
+    want = oracle.retrieve_at(host(src), rids_np, idx.astype(np.uint64))
+    assert np.array_equal(host(out)[idx], want)
