@@ -218,6 +218,32 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = args.config
+    if cfg == "h1":
+        import datagen
+        import oracle
+        w = datagen.hash_workload(1 << 24, 24, 1 << 26)
+        q = w["queries"][: 1 << 24]              # bounded sample: a quarter of the queries
+        times = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            oracle.batch_lookup(w["keys"], q)
+            times.append(time.perf_counter() - t0)
+            if sum(times) > 120:
+                break
+        t = sum(times) / len(times)
+        value = q.size / t
+        print(json.dumps({
+            "impl": "reference", "metric": "batch index lookups/s (hash index, DPG)", "value": value,
+            "unit": "lookups/s", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (datagen.hash_workload, seed 0)",
+            "config": {"workload": "h1 sample: 2^24 of the 2^26 queries"},
+            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+                             "sample": "2^24 queries, oracle.batch_lookup (sorted pairs + binary search)",
+                             "host_cpu": host_cpu()},
+            "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
     if cfg == "c5":
         # bounded sample of the c5 workload for the host oracle: 2^22 records
         # of the c5 source stream, rids = the c5 Feistel permutation of [0, 2^22)
@@ -427,6 +453,15 @@ def run_h1(args):
         ms, ok, launches = timed(False)
     dms, dok, _ = timed(True)
     alg = n * (4 + 16 + 4)        # key in, the key's 16-byte slot, rid out
+    cpu = None
+    if not args.no_cpu:
+        qs = w["queries"][: 1 << 22]
+        t0 = time.perf_counter()
+        oracle.batch_lookup(w["keys"], qs)
+        tc = time.perf_counter() - t0
+        cpu = {"value": qs.size / tc, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+               "sample": "2^22 of the queries, oracle.batch_lookup (sorted pairs + binary search)",
+               "host_cpu": host_cpu()}
     peak, peak_src = hbm_peak()
     print(json.dumps({
         "metric": "batch index lookups/s (hash index, DPG)", "value": n / (ms * 1e-3),
@@ -440,7 +475,8 @@ def run_h1(args):
         "effective_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak,
         "direct": {"value": n / (dms * 1e-3), "unit": "lookups/s", "ms_per_step": dms,
                    "parity_sampled_ok": bool(dok)},
-        "parity_sampled_ok": bool(ok), "gpu_launches": launches, "clocks": clk.summary()}),
+        "parity_sampled_ok": bool(ok), "gpu_launches": launches, "cpu_baseline": cpu,
+        "clocks": clk.summary()}),
         flush=True)
     return 0
 
