@@ -24,9 +24,8 @@ constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives 
 thread_local uint32_t t_launches = 0;
 thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
 thread_local const OutSegs* t_seg = nullptr;   // output segments of the current call (or none)
-thread_local bool g_seg_nostage = false;        // segmented call re-planned onto path 3 past the L2
-unsigned long long* g_debug_ts = nullptr;
-uint32_t g_debug_flags = 0;            // tuning experiments only (dpg_debug_flags)  // profiling: per-CTA phase stamps of the fused kernel
+unsigned long long* g_debug_ts = nullptr;   // profiling: per-CTA phase stamps (dpg_debug_phase_stamps)
+uint32_t g_debug_flags = 0;                 // tuning experiments only (dpg_debug_flags)
 
 // ---- optional phase timing (events on the call's stream) --------------------
 std::mutex g_timing_mu;
@@ -623,6 +622,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
   uint32_t nl_skew = 0;
+  bool seg_nostage = false;   // a segmented call re-planned onto path 3 past the L2 budget
   {
     // Data skew (section 2.3): a large input planned on fixed
     // shared-memory runs is sampled first; a rid list that would overflow the
@@ -657,7 +657,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       dpg_options_t o{};
       o.path = 3;
       if (make_plan(rec, n_src, n_out, 0, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
-      if (p.path == 3 && n_src * rec > l2_budget(current_l2_bytes())) g_seg_nostage = true;
+      if (p.path == 3 && n_src * rec > l2_budget(current_l2_bytes())) seg_nostage = true;
     } else {
       // any other record: the direct gather, one launch per segment
       uint32_t nl = 0;
@@ -822,8 +822,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       l.seg = *t_seg;
       l.dst = t_seg->out[0];
       W = 4;
-      if (g_seg_nostage) l.stage = 0;   // a source beyond the L2 budget: no Phase II
-      g_seg_nostage = false;
+      if (seg_nostage) l.stage = 0;   // a source beyond the L2 budget: no Phase II
     }
     uint32_t nl = 0;
     PhaseEvents pe;
