@@ -747,3 +747,57 @@ def test_graph_capture_of_a_large_fixed_run_plan(dpg):
     idx = rng.integers(0, rids.numel(), 20000)
     want = oracle.retrieve_at(host(src), rids_np, idx.astype(np.uint64))
     assert np.array_equal(host(out)[idx], want)
+
+
+# --------------------------------------------------------------------------
+# Edge cases across plans.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("rec", [108, 112, 116, 120, 124])
+@pytest.mark.parametrize("doff", [0, 4, 8])
+def test_window_gather_record_size_boundary(dpg, rec, doff):
+    """Around the largest record the window gather takes (116 bytes; larger
+    rows go to the realigning tile path), staged and unstaged, with output
+    offsets of 0/4/8 bytes and a ragged last group."""
+    rng = np.random.default_rng(rec * 10 + doff)
+    n_src, n_out = 3001, 4097
+    src = rng.integers(0, 256, (n_src, rec), dtype=np.uint8)
+    rids = rng.integers(0, n_src, n_out).astype(np.uint32)
+    want = oracle.retrieve(src, rids)
+    buf = torch.full((n_out * rec + doff + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+    out = buf[doff:doff + n_out * rec].view(n_out, rec)
+    for call in (lambda: dpg.dpg_retrieve(dev(src), dev(rids), dst=out, path=3),
+                 lambda: dpg.dpg_retrieve_direct_ex(dev(src), dev(rids), dst=out, hint=3)):
+        out.zero_()
+        call()
+        assert np.array_equal(host(out), want)
+        b = host(buf)
+        assert np.all(b[:doff] == 0x5A) and np.all(b[doff + n_out * rec:] == 0x5A)
+
+
+@pytest.mark.parametrize("path,gather", [(0, 0), (1, 1), (1, 2), (2, 0), (3, 0), (5, 0)])
+@pytest.mark.parametrize("n_out", [1, 31, 33])
+def test_single_record_source_every_plan(dpg, path, gather, n_out):
+    src = np.arange(100, dtype=np.uint8).reshape(1, 100)
+    rids = np.zeros(n_out, dtype=np.uint32)
+    try:
+        got = host(dpg.dpg_retrieve(dev(src), dev(rids), path=path, gather=gather))
+    except dpg.DPGError as e:
+        assert e.status == dpg.DPG_ERR_UNSUPPORTED, e   # a forced plan may not apply
+        return
+    assert np.array_equal(got, np.repeat(src, n_out, axis=0))
+
+
+def test_hash_and_btree_lookup_empty_and_tiny(dpg):
+    w = datagen.hash_workload(2, 1, 5)
+    t = torch.from_numpy(w["table"].view(np.int32)).cuda()
+    p = torch.from_numpy(w["pool"].view(np.int32)).cuda()
+    for direct in (False, True):
+        out = dpg.dpg_hash_lookup(t, p, dev(w["queries"][:0]), direct=direct)
+        assert out.numel() == 0
+        got = host(dpg.dpg_hash_lookup(t, p, dev(w["queries"]), direct=direct)).view(np.uint32)
+        assert np.array_equal(got, oracle.batch_lookup(w["keys"], w["queries"]))
+    levels, rids = datagen.btree_index(w["keys"])
+    lv, ln, r = dpg.btree_to_device(levels, rids)
+    for direct in (False, True):
+        got = host(dpg.dpg_btree_lookup(lv, ln, r, dev(w["queries"]), direct=direct)).view(np.uint32)
+        assert np.array_equal(got, oracle.batch_lookup(w["keys"], w["queries"]))
