@@ -64,9 +64,8 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       const bool valid = r[u] < a.n_src;
       if (!HASH && i < hi && !valid) report_bad(a.status, i);
-      const uint32_t b = valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, b);
-      if (valid && (peers & lanemask_lt()) == 0) my[b] += __popc(peers);
+      // (a count needs no rank: warp-private counters, shared-memory atomics)
+      if (valid) atomicAdd(&my[(uint32_t)(r[u] >> a.s)], 1u);
     }
   }
   __syncthreads();
@@ -151,6 +150,13 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       if (HASH && g < ngroups && i < hi) r[u] = (uint32_t)(r[u] * 0x9E3779B1u) >> (32 - a.hash_m);
     }
+    // the rank groups of all eight rows first (independent match.any issues)
+    uint32_t pm[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool valid = r[u] < a.n_src;
+      pm[u] = __match_any_sync(0xffffffffu, valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu);
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t g = g0 + u * kKWarps;
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(kKThreads, 1) k_l2k_distribute(L2KArgs a) {
       const uint64_t i = lo + 32 * (uint64_t)g + lane;
       const bool valid = r[u] < a.n_src;
       const uint32_t b = valid ? (uint32_t)(r[u] >> a.s) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      const uint32_t peers = pm[u];
       uint32_t slot = 0;
       if (valid) slot = my[b] + __popc(peers & lanemask_lt());
       __syncwarp();
