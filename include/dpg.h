@@ -326,10 +326,10 @@ dpg_status_t dpg_ipc_free(void *ptr);
  * multi-GPU exchange uses this to write an owner's replies straight into each
  * requester's receive window over NVLink, with no reply buffer and no
  * separate collective for the records (north_star config 5; SV 8(f) #1).
- * The plan is dpg_retrieve's: shared-memory runs write each staged record to
- * its segment row; the L2 run and the K-run L2 plan's last gather do the
- * same per 32-row group (4-byte-multiple records of 8..116 bytes); other
- * records use one direct gather per segment.  Errors as dpg_retrieve
+ * The plan is dpg_retrieve's: shared-memory runs (both kernels) write each
+ * staged record to its segment row; the L2 run and the K-run L2 plan's last
+ * gather do the same per 32-row group (4-byte-multiple records of 8..116
+ * bytes); other records use one direct gather per segment.  Errors as dpg_retrieve
  * (DPG_ERR_INVALID_ARG also for counts that do not sum to n_out, a NULL
  * segment with rows, or a segment overlapping src or rids).  Asynchronous. */
 dpg_status_t dpg_retrieve_segments(const void *src, size_t rec_bytes, uint64_t n_src,

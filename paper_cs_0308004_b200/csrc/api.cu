@@ -397,6 +397,14 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
       plan_fused(rec, n_src, n_out, pay, opt, sm, p))
     return DPG_OK;
   if (want_path == 1) return DPG_ERR_UNSUPPORTED;
+  // Beyond the single fused kernel, a source of >= 8 L2s with records the
+  // window gather takes runs faster as K L2-sized runs than as the
+  // multi-kernel shared-memory runs (the config-5 owner shard, 2^27 x 100 B:
+  // 11.4 vs 14.7 ms per 2^26 rids, profiles/r01_c5_owner_plans.txt)
+  if (want_path == 0 && !overrides && pay == 0 && rec % 4 == 0 && rec >= 8 && rec <= 116 &&
+      n_src * rec >= 8 * current_l2_bytes() &&
+      plan_l2k(rec, n_src, n_out, pay, false, 0, sm, current_l2_bytes(), p))
+    return DPG_OK;
   std::memset(p, 0, sizeof(*p));
   p->path = 2;
   p->nstages = 2;
@@ -652,6 +660,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     const bool agr_ok = rec % 4 == 0 && rec >= 8 && rec <= 116 && al4 && (uintptr_t)src % 4 == 0;
     if (p.path == 1 && pay == 0) {
       p.gather = 1;
+    } else if (p.path == 2 && pay == 0) {
     } else if (p.path == 5 && agr_ok) {
     } else if (agr_ok && n_src * rec <= ((uint64_t)1 << 32)) {
       dpg_options_t o{};
@@ -968,7 +977,12 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     a.slot_pairs = p.slot_pairs;
     a.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
     a.slot_bytes = (p.smem_bytes - kBarBytes) / 2;
-    uint32_t W = pow2_divisor(rec | pay | (uintptr_t)src | (uintptr_t)dst);
+    uintptr_t outs = (uintptr_t)dst;
+    if (t_seg) {
+      a.seg = *t_seg;   // the probe writes each row to its segment
+      for (uint32_t q = 0; q < t_seg->n; ++q) outs |= (uintptr_t)t_seg->out[q];
+    }
+    uint32_t W = pow2_divisor(rec | pay | (uintptr_t)src | outs);
     e = launch_probe_gather(a, W, p.grid_probe, p.smem_bytes, st, &nl);
   }
   if (timed) cudaEventRecord(pe.e2, st);

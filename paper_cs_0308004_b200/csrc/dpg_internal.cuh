@@ -180,24 +180,6 @@ struct DistArgs {
   unsigned long long* status;
 };
 
-struct ProbeArgs {
-  const uint8_t* src;     // staged source records
-  uint64_t n_src;
-  uint32_t rec;
-  uint32_t s;
-  uint32_t K;
-  const uint32_t* run_start;   // [K+1]
-  const void* pairs;
-  uint32_t pair_bytes;
-  const uint8_t* pay;          // [n_out * pay_bytes] or null
-  uint32_t pay_bytes;
-  uint8_t* dst;                // row r at dst + r*row_bytes
-  uint32_t row_bytes;          // pay_bytes + rec
-  uint32_t slot_pairs;         // pairs per stage
-  uint32_t region_cap;         // bytes reserved for a region in a stage
-  uint32_t slot_bytes;         // total bytes per stage
-};
-
 // Output split into segments (dpg_retrieve_segments; the multi-GPU exchange
 // writes each requester's replies straight into its window over NVLink):
 // output row k of segment q (start[q] <= k < start[q+1]) goes to
@@ -220,6 +202,25 @@ __device__ __forceinline__ uint8_t* seg_row(const OutSegs& o, uint8_t* dst, uint
   const uint32_t q = seg_of(o, k);
   return o.out[q] + (k - o.start[q]) * row_bytes;
 }
+
+struct ProbeArgs {
+  const uint8_t* src;     // staged source records
+  uint64_t n_src;
+  uint32_t rec;
+  uint32_t s;
+  uint32_t K;
+  const uint32_t* run_start;   // [K+1]
+  const void* pairs;
+  uint32_t pair_bytes;
+  const uint8_t* pay;          // [n_out * pay_bytes] or null
+  uint32_t pay_bytes;
+  uint8_t* dst;                // row r at dst + r*row_bytes
+  uint32_t row_bytes;          // pay_bytes + rec
+  uint32_t slot_pairs;         // pairs per stage
+  uint32_t region_cap;         // bytes reserved for a region in a stage
+  uint32_t slot_bytes;         // total bytes per stage
+  OutSegs seg;                 // output segments (seg.n = 0: dst)
+};
 
 // One persistent cooperative kernel for the whole path (fused.cu).
 struct FusedArgs {

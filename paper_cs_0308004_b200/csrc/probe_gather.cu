@@ -136,7 +136,7 @@ __device__ __forceinline__ void unpack(PairT p, uint32_t s, uint32_t& local, uin
 }
 
 template <int W, typename PairT, bool PAY>
-__global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(ProbeArgs a) {
+__global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_constant__ ProbeArgs a) {
   using T = typename Word<W>::T;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -212,14 +212,14 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(ProbeArgs a) 
               v = *reinterpret_cast<const T*>(pay + (size_t)(g0 + rr) * a.pay_bytes + lw * W);
             else
               v = *reinterpret_cast<const T*>(region + (size_t)loc * a.rec + (lw - PR) * W);
-            *reinterpret_cast<T*>(a.dst + (uint64_t)pos * a.row_bytes + lw * W) = v;
+            *reinterpret_cast<T*>(seg_row(a.seg, a.dst, pos, a.row_bytes) + lw * W) = v;
           }
         }
       } else {
         for (uint32_t rr = 0; rr < cnt; ++rr) {
           const uint32_t loc = __shfl_sync(0xffffffffu, my_local, rr);
           const uint32_t pos = __shfl_sync(0xffffffffu, my_pos, rr);
-          uint8_t* drow = a.dst + (uint64_t)pos * a.row_bytes;
+          uint8_t* drow = seg_row(a.seg, a.dst, pos, a.row_bytes);
           const uint8_t* srow = region + (size_t)loc * a.rec;
 #pragma unroll 4
           for (uint32_t w = lane; w < R; w += 32) {
@@ -242,6 +242,9 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(ProbeArgs a) 
     chave = cons.next(cit);
     ++it_idx;
   }
+  // rows written into peer memory (output segments mapped from other GPUs)
+  // are made visible system-wide before the kernel ends
+  if (a.seg.n) __threadfence_system();
 }
 
 template <int W, typename PairT, bool PAY>

@@ -801,3 +801,30 @@ def test_hash_and_btree_lookup_empty_and_tiny(dpg):
     for direct in (False, True):
         got = host(dpg.dpg_btree_lookup(lv, ln, r, dev(w["queries"]), direct=direct)).view(np.uint32)
         assert np.array_equal(got, oracle.batch_lookup(w["keys"], w["queries"]))
+
+
+def test_segments_multi_kernel_runs(dpg):
+    """A source too large for the single fused kernel with records the window
+    gather does not take (2^24 x 128 B: the multi-kernel plan, path 2) and
+    output segments.  The source is generated on the device; sampled rows are
+    checked against the generator's bytes at the rid (pointwise definition,
+    as for config 5)."""
+    n_src, rec = 1 << 24, 128
+    assert dpg.dpg_plan(rec, n_src, 1 << 22, 0, 148)["path"] == 2
+    src = torch.empty((n_src, rec), dtype=torch.uint8, device="cuda")
+    sid = datagen.STREAMS[("test", "src")]
+    datagen.random_bytes_cuda(src.view(-1), sid)
+    rng = np.random.default_rng(12)
+    rids = rng.integers(0, n_src, 1 << 22).astype(np.uint32)
+    sizes = [1 << 20, 17, 1 << 21, (1 << 22) - (1 << 20) - 17 - (1 << 21)]
+    bufs = [torch.full((n + 1, rec), 0xA5, dtype=torch.uint8, device="cuda") for n in sizes]
+    dpg.dpg_retrieve_segments(src, dev(rids), sizes, [b.data_ptr() for b in bufs])
+    assert dpg.last_path() == 2
+    k = 0
+    for n, b in zip(sizes, bufs):
+        h = host(b)
+        assert np.all(h[n:] == 0xA5)
+        for j in np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 200)])):
+            want = datagen.random_bytes(rec, sid, offset=int(rids[k + j]) * rec)  # 8-byte multiple
+            assert np.array_equal(h[j], want), (n, j)
+        k += n
