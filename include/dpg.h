@@ -329,7 +329,9 @@ dpg_status_t dpg_ipc_free(void *ptr);
  * The plan is dpg_retrieve's: shared-memory runs (both kernels) write each
  * staged record to its segment row; the L2 run and the K-run L2 plan's last
  * gather do the same per 32-row group (4-byte-multiple records of 8..116
- * bytes); other records use one direct gather per segment.  Errors as dpg_retrieve
+ * bytes); a plan that cannot (another record in an L2 run) is replaced by
+ * the shared-memory runs; only a record no plan takes falls back to one
+ * direct gather per segment.  Errors as dpg_retrieve
  * (DPG_ERR_INVALID_ARG also for counts that do not sum to n_out, a NULL
  * segment with rows, or a segment overlapping src or rids).  Asynchronous. */
 dpg_status_t dpg_retrieve_segments(const void *src, size_t rec_bytes, uint64_t n_src,

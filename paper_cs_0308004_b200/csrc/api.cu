@@ -652,8 +652,9 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     }
   }
   if (t_seg) {
-    // output segments: the plans whose last writer is the fused probe (mode 0)
-    // or the window gather; others take the window gather without staging
+    // output segments: every plan whose last writer can address rows anywhere
+    // (the fused probe in mode 0, the multi-kernel probe, the window gather);
+    // the others are re-planned onto one of those
     const OutSegs& sg = *t_seg;
     bool al4 = true;
     for (uint32_t q = 0; q < sg.n; ++q) al4 = al4 && ((uintptr_t)sg.out[q] % 4 == 0);
@@ -667,8 +668,20 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       o.path = 3;
       if (make_plan(rec, n_src, n_out, 0, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
       if (p.path == 3 && n_src * rec > l2_budget(current_l2_bytes())) seg_nostage = true;
+    } else if (dpg_plan_t q; pay == 0 && [&] {
+                 // the shared-memory runs, which write rows anywhere: fused, else multi-kernel
+                 dpg_options_t o{};
+                 o.path = 1;
+                 if (make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK) {
+                   q.gather = 1;
+                   return true;
+                 }
+                 o.path = 2;
+                 return make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK;
+               }()) {
+      p = q;
     } else {
-      // any other record: the direct gather, one launch per segment
+      // a record no DPG plan can write to segments: the direct gather, one launch per segment
       uint32_t nl = 0;
       for (uint32_t q = 0; q < sg.n; ++q) {
         const uint64_t k0 = sg.start[q], k1 = sg.start[q + 1];

@@ -624,11 +624,15 @@ def test_segments_l2_run(dpg, rec):
 
 
 @pytest.mark.parametrize("rec,shift", [(6, 0), (128, 0), (100, 2), (256, 0)])
-def test_segments_direct_fallback(dpg, rec, shift):
+def test_segments_other_records(dpg, rec, shift):
+    """Records the window gather does not take (odd sizes, > 116 bytes,
+    unaligned segments): re-planned onto the shared-memory runs, which write
+    rows anywhere."""
     rng = np.random.default_rng(rec + shift)
     src = rng.integers(0, 256, (3000, rec), dtype=np.uint8)
     rids = rng.integers(0, 3000, 9000).astype(np.uint32)
     _check_segments(dpg, src, rids, [4000, 1, 0, 4999], shift=shift)
+    assert dpg.last_path() in (1, 2)
 
 
 def test_segments_shared_memory_runs(dpg):
