@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c4x", "c5", "h1"],
                     help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
     ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
-    ap.add_argument("--c5-round-rows", type=int, default=1 << 26)
+    ap.add_argument("--c5-round-rows", type=int, default=1 << 27,
+                    help="c5 rows per exchange round (bounds the windows: 13.4 GB per rank)")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="c5: replies written into the requesters' windows over NVLink "
                          "(fused) or returned by an NCCL all-to-all")
