@@ -344,9 +344,11 @@ dpg_status_t dpg_retrieve_segments(const void *src, size_t rec_bytes, uint64_t n
  * temporary file in that order by DPG retrieval, then joined with dim (F)
  * read in rid_F order.  out (device, n_fact rows of fact_bytes + rec_bytes):
  * row j = fact[rid_R_j] ++ dim[rid_F_j], pairs in stable fk order -- the same
- * rows as dpg_fk_join, in fk order instead of fact order.  An fk >= n_dim
- * leaves its row unwritten and is reported at its fact position
- * (dpg_sync_status).  Same argument rules as dpg_fk_join.  Asynchronous. */
+ * rows as dpg_fk_join, in fk order instead of fact order.  Only the key bytes
+ * an fk below n_dim can have are sorted ("the lowest log N bits"),
+ * so an fk >= n_dim is reported at its fact position (dpg_sync_status) and
+ * leaves the content of out unspecified (reading A19).  Same argument rules
+ * as dpg_fk_join.  Asynchronous. */
 dpg_status_t dpg_fk_join_sort(const void *fact, size_t fact_bytes, uint64_t n_fact,
                               const uint32_t *fk_col, const void *dim, size_t rec_bytes,
                               uint64_t n_dim, void *out, dpg_stream_t stream);
