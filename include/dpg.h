@@ -12,10 +12,13 @@
  * or repeat rids (joins).  DPG computes exactly this result in
  * three phases (section 2.1, Fig. 1): Distribute the rids
  * into runs by their high bits, Probe each cache-resident run of the input,
- * Gather the probed records back into rid order.  On B200 the probe and
- * gather phases are fused: each source run is staged into shared
- * memory by TMA bulk copies and every record is written straight to its
- * destination position.
+ * Gather the probed records back into rid order.  On B200 the "cache" is
+ * the L2 or shared memory: a source within the L2 budget is one
+ * run, staged into the L2 by TMA bulk copies and probed in output order
+ * (path 3); larger sources are cut into shared-memory runs whose probe
+ * writes each record straight to its destination (paths 1/2) or into K
+ * L2-sized runs with an INTERNAL file (path 5, chosen after a skew sample or
+ * for very large sources).  dpg_plan_t.path below lists the plans.
  *
  * Conventions (all entry points):
  *  - Pointers named src/rids/dst/fact/fk_col/dim/out are DEVICE pointers
@@ -60,11 +63,12 @@ typedef enum {
 
 typedef void *dpg_stream_t; /* a cudaStream_t */
 
-/* Execution plan chosen for one call (host-side; no GPU needed).
- * Run length L = 2^log2_run records (runs sized to the cache,
- * power of two, identified by the high-order bits of the rid); on B200 a
- * run is sized so that one run plus its pair chunk fit one shared-memory
- * stage, two stages per SM. */
+/* Execution plan chosen for one call (host-side; no GPU needed; the skew
+ * sample of dpg_retrieve may still switch path 1 to path 5 at run time,
+ * dpg_last_path).  Run length L = 2^log2_run records (runs sized
+ * to the cache, power of two, identified by the high-order bits of the
+ * rid): the whole source for path 3, one shared-memory stage for paths 1/2,
+ * one L2 run budget for path 5. */
 typedef struct {
     uint32_t log2_run;      /* s: run of rid r is r >> s (reading A1)           */
     uint32_t pair_bytes;    /* 4 = packed (pos << s | local), 8 = (local, pos)  */
