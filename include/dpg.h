@@ -409,6 +409,12 @@ void dpg_debug_phase_stamps(void *device_buf);
  * the default and what every other caller gets. */
 void dpg_debug_flags(uint32_t flags);
 dpg_status_t dpg_phase_times(double *distribute_ms, double *probe_gather_ms, uint32_t *calls);
+/* Same record split by phase: Phase I (distribute), Phase II (probe) and
+ * Phase III (gather) of the three-kernel plan (path 6) are timed separately;
+ * for the other plans *phase2_ms covers the probe-gather kernel(s) and
+ * *phase3_ms is 0. */
+dpg_status_t dpg_phase_times_ex(double *phase1_ms, double *phase2_ms, double *phase3_ms,
+                                uint32_t *calls);
 
 int dpg_version(void);
 

@@ -126,6 +126,8 @@ _lib.dpg_phase_timing.argtypes = [ctypes.c_int]
 _lib.dpg_phase_timing.restype = None
 _lib.dpg_phase_times.argtypes = [_P, _P, _P]
 _lib.dpg_phase_times.restype = _st
+_lib.dpg_phase_times_ex.argtypes = [_P, _P, _P, _P]
+_lib.dpg_phase_times_ex.restype = _st
 
 
 def _check(status: int, where: str):
@@ -178,6 +180,16 @@ def dpg_phase_times() -> tuple[float, float, int]:
     _check(_lib.dpg_phase_times(ctypes.byref(d), ctypes.byref(p), ctypes.byref(c)),
            "dpg_phase_times")
     return d.value, p.value, c.value
+
+
+def dpg_phase_times_ex() -> tuple[float, float, float, int]:
+    """(phase1_ms, phase2_ms, phase3_ms, calls) summed since the last read;
+    phase3_ms is nonzero only for the three-kernel plan (path 6), whose Phase
+    II and Phase III are timed separately (else phase2_ms covers both)."""
+    a, b, c, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+    _check(_lib.dpg_phase_times_ex(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                   ctypes.byref(n)), "dpg_phase_times_ex")
+    return a.value, b.value, c.value, n.value
 
 
 # ---------------------------------------------------------------------------

@@ -24,13 +24,16 @@ constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives 
 thread_local uint32_t t_launches = 0;
 thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
 thread_local const OutSegs* t_seg = nullptr;   // output segments of the current call (or none)
+thread_local uint64_t* t_seq3_pairs = nullptr; // tests: path 6 Phase I pairs (dpg_distribute)
 unsigned long long* g_debug_ts = nullptr;   // profiling: per-CTA phase stamps (dpg_debug_phase_stamps)
 uint32_t g_debug_flags = 0;                 // tuning experiments only (dpg_debug_flags)
 
 // ---- optional phase timing (events on the call's stream) --------------------
 std::mutex g_timing_mu;
 bool g_timing = false;
-struct PhaseEvents { cudaEvent_t e0, e1, e2; };
+// e0 call start, e1 end of Phase I, e3 end of Phase II (path 6 only: has3),
+// e2 end of the call
+struct PhaseEvents { cudaEvent_t e0, e1, e2, e3; bool has3; };
 std::vector<PhaseEvents> g_pending, g_pool;
 
 bool timing_begin(cudaStream_t st, PhaseEvents* pe) {
@@ -39,10 +42,21 @@ bool timing_begin(cudaStream_t st, PhaseEvents* pe) {
   if (!g_pool.empty()) { *pe = g_pool.back(); g_pool.pop_back(); }
   else {
     cudaEventCreate(&pe->e0); cudaEventCreate(&pe->e1); cudaEventCreate(&pe->e2);
+    cudaEventCreate(&pe->e3);
   }
+  pe->has3 = false;
   cudaEventRecord(pe->e0, st);
   g_pending.push_back(*pe);
   return true;
+}
+
+// End of Phase II of a three-kernel plan (path 6): Phase II and Phase III are
+// then reported separately.
+void timing_phase2_end(const PhaseEvents& pe, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  cudaEventRecord(pe.e3, st);
+  for (auto& q : g_pending)
+    if (q.e0 == pe.e0) q.has3 = true;
 }
 
 int current_sm_count() {
@@ -365,6 +379,85 @@ bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool
   return true;
 }
 
+// Three sequential passes over shared-memory runs (seq3.cu): runs of L = 2^s
+// records, L * rec <= one stage (128 KB: one CTA per SM holds it, the next
+// run is prefetched into L2 meanwhile), 16-bit local offsets (s <= 16).
+uint64_t seq3_stage_bytes() {
+  static uint64_t env = [] {
+    const char* e = getenv("DPG_SEQ3_STAGE_KB");
+    return e ? (uint64_t)atoll(e) << 10 : 0ull;
+  }();
+  return env ? env : (128ull << 10);
+}
+
+// Largest record for which the three sequential passes are the automatic plan
+// beyond the L2 (measured).
+uint64_t seq3_auto_max_rec() {
+  static uint64_t env = [] {
+    const char* e = getenv("DPG_SEQ3_MAX_REC");
+    return e ? (uint64_t)atoll(e) : ~0ull;
+  }();
+  return env != ~0ull ? env : 32;
+}
+
+bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
+               const dpg_options_t* opt, int sm, dpg_plan_t* p) {
+  if (n_out == 0 || n_src == 0 || rec % 4 || pay % 4 || rec > 16384) return false;
+  if (n_out >= 0xFFFFFFFFull || n_out * ((rec + pay) / 4) >= (1ull << 32)) return false;
+  const bool forced = opt && opt->path == 6;
+  const uint64_t stage = std::min<uint64_t>(seq3_stage_bytes(), 128ull << 10);
+  uint32_t s = 0;
+  if (opt && opt->log2_run) {
+    s = opt->log2_run;
+    if (s > 16 || (1ull << s) * rec > (128ull << 10)) return false;
+  } else {
+    while (s < 16 && (2ull << s) * rec <= stage && (1ull << s) < n_src) ++s;
+  }
+  const uint64_t L = 1ull << s;
+  const uint64_t K = (n_src + L - 1) >> s;
+  if (K > 8192 || (L * rec) % 16) return false;    // each run one 16-byte aligned bulk copy
+  if (seq3_probe_smem(L * rec) > kSmemLimit) return false;
+  // tile T: the Phase III buffer (two of ~100 KB, else one of ~200 KB) and the
+  // Phase I tile (T rids + T offsets + 2 (K + 1) counters) both fit
+  auto tile_for = [&](uint64_t bytes) {
+    uint64_t T = std::min<uint64_t>(32768, bytes / (rec + 2)) & ~15ull;   // records + tinv
+    while (T >= 16 && seq3_dist_smem((uint32_t)T, (uint32_t)K) > kSmemLimit) T -= 16;
+    return T;
+  };
+  uint64_t T = tile_for(110ull << 10);
+  uint32_t nbuf = 2;
+  const uint32_t want_buf = opt ? opt->gather : 0;   // tuning: 1 or 2 Phase III buffers
+  if (want_buf == 1 || (want_buf != 2 && T * L < 2 * n_src)) {
+    T = tile_for(220ull << 10);
+    nbuf = 1;
+  }
+  if (opt && opt->grid_distribute) T = std::max<uint64_t>(16, std::min<uint64_t>(T, opt->grid_distribute * 16ull));
+  if (T < 16) return false;
+  const uint64_t nsub = (n_out + T - 1) / T;
+  // each piece (tile, run) should hold at least one entry on average
+  if (!forced && K * nsub > n_out) return false;
+  if (nsub * (K + 1) > (1ull << 31)) return false;
+  const uint32_t dsm = seq3_dist_smem((uint32_t)T, (uint32_t)K);
+  const uint64_t dctas = std::max<uint64_t>(1, std::min<uint64_t>(4, kSmemLimit / (dsm + 1024)));
+  std::memset(p, 0, sizeof(*p));
+  p->path = 6;
+  p->log2_run = s;
+  p->run_len = L;
+  p->num_runs = K;
+  p->pair_bytes = 2;
+  p->pay_bytes = (uint32_t)pay;
+  p->word_bytes = pow2_divisor(rec | pay);
+  p->tile = (uint32_t)T;
+  p->nstages = nbuf;
+  p->grid_distribute = (uint32_t)std::min<uint64_t>(nsub, dctas * (uint64_t)sm);
+  p->grid_probe = (uint32_t)std::min<uint64_t>(K, (opt && opt->grid_probe) ? opt->grid_probe
+                                                                           : (uint64_t)sm);
+  p->hist_in_smem = 1;
+  p->stage_bytes = (uint32_t)(L * rec);
+  p->smem_bytes = seq3_probe_smem(L * rec);
+  return true;
+}
+
 dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                        const dpg_options_t* opt, int sm, dpg_plan_t* p) {
   if (rec == 0 || !p) return DPG_ERR_INVALID_ARG;
@@ -387,6 +480,16 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
       return DPG_OK;
     if (want_path == 3) return DPG_ERR_UNSUPPORTED;
   }
+  if (want_path == 6) {
+    if (plan_seq3(rec, n_src, n_out, pay, opt, sm, p)) return DPG_OK;
+    return DPG_ERR_UNSUPPORTED;
+  }
+  // Beyond the L2, records up to seq3_auto_max_rec bytes take the three
+  // sequential passes (the paper's small-record case)
+  if (want_path == 0 && !overrides && rec <= seq3_auto_max_rec() &&
+      n_src * rec > l2_budget(current_l2_bytes()) &&
+      plan_seq3(rec, n_src, n_out, pay, opt, sm, p))
+    return DPG_OK;
   if (want_path == 5 || (want_path == 0 && !overrides && l2k_auto(rec))) {
     if (plan_l2k(rec, n_src, n_out, pay, want_path == 5, opt ? opt->log2_run : 0, sm,
                  current_l2_bytes(), p))
@@ -698,6 +801,68 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   }
   t_path = p.path;
 
+  if (p.path == 6 && ((uintptr_t)src % 16 != 0)) {
+    // the stage is one TMA bulk copy of the run: an unaligned source takes the
+    // multi-kernel shared-memory runs
+    if (opt && opt->path == 6) return DPG_ERR_UNSUPPORTED;
+    dpg_options_t o{};
+    o.path = 2;
+    if (make_plan(rec, n_src, n_out, pay, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
+    t_path = p.path;
+  }
+  if (p.path == 6) {
+    const uint64_t K = p.num_runs, T = p.tile;
+    const uint64_t nsub = (n_out + T - 1) / T;
+    uint32_t *gbar = nullptr, *total = nullptr;
+    void* ws = nullptr;
+    const uint64_t off_pre = 0;
+    const uint64_t off_preT = align_up(off_pre + nsub * (K + 1) * 2, 256);
+    const uint64_t off_loc = align_up(off_preT + nsub * (K + 1) * 2, 256);
+    const uint64_t off_tinv = align_up(off_loc + nsub * T * 2, 256);
+    const uint64_t off_int = align_up(off_tinv + nsub * T * 2 + 16, 256);
+    const uint64_t bytes = off_int + nsub * T * rec + 64;
+    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+    if (wst != DPG_OK) return wst;
+    uint8_t* wb = (uint8_t*)ws;
+    Seq3Args a;
+    std::memset(&a, 0, sizeof(a));
+    a.src = (const uint8_t*)src;
+    a.n_src = n_src;
+    a.rec = (uint32_t)rec;
+    a.rids = rids;
+    a.n_out = n_out;
+    a.s = p.log2_run;
+    a.K = (uint32_t)K;
+    a.T = (uint32_t)T;
+    a.nsub = (uint32_t)nsub;
+    a.pre = (uint16_t*)(wb + off_pre);
+    a.preT = (uint16_t*)(wb + off_preT);
+    a.loc = (uint16_t*)(wb + off_loc);
+    a.tinv = (uint16_t*)(wb + off_tinv);
+    a.dbg_pairs = t_seq3_pairs;
+    a.internal = wb + off_int;
+    a.dst = (uint8_t*)dst;
+    a.pay = (const uint8_t*)pay_src;
+    a.pay_bytes = (uint32_t)pay;
+    a.status = status;
+    a.dbg = g_debug_flags;
+    a.ts = g_debug_ts;
+    uint32_t nl = 0;
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    cudaError_t e = launch_seq3_distribute(a, p.grid_distribute, st, &nl);
+    if (timed) cudaEventRecord(pe.e1, st);
+    if (e == cudaSuccess)
+      e = launch_seq3_probe(a, pow2_divisor(rec), p.grid_probe, st, &nl);
+    if (timed) timing_phase2_end(pe, st);
+    if (e == cudaSuccess)
+      e = launch_seq3_gather(a, pow2_divisor(rec | pay | (uintptr_t)dst |
+                                             (pay ? (uintptr_t)pay_src : 0)),
+                             (uint32_t)std::min<uint64_t>(nsub, sm), p.nstages, st, &nl);
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_launches = nl + nl_skew;
+    return cuda_status(e);
+  }
   if (p.path == 5) {
     const uint32_t G = p.grid_probe, K = (uint32_t)p.num_runs;
     const uint64_t L = p.run_len;
@@ -1027,23 +1192,38 @@ void dpg_phase_timing(int enable) {
   g_timing = enable != 0;
 }
 
-dpg_status_t dpg_phase_times(double* distribute_ms, double* probe_gather_ms, uint32_t* calls) {
+dpg_status_t dpg_phase_times_ex(double* phase1_ms, double* phase2_ms, double* phase3_ms,
+                                uint32_t* calls) {
   std::lock_guard<std::mutex> lk(g_timing_mu);
-  double d = 0, p = 0;
+  double d = 0, p = 0, g = 0;
   for (auto& pe : g_pending) {
-    float a = 0, b = 0;
+    float a = 0, b = 0, c = 0;
     if (cudaEventSynchronize(pe.e2) != cudaSuccess) return cuda_status(cudaGetLastError());
     cudaEventElapsedTime(&a, pe.e0, pe.e1);
-    cudaEventElapsedTime(&b, pe.e1, pe.e2);
+    if (pe.has3) {
+      cudaEventElapsedTime(&b, pe.e1, pe.e3);
+      cudaEventElapsedTime(&c, pe.e3, pe.e2);
+    } else {
+      cudaEventElapsedTime(&b, pe.e1, pe.e2);
+    }
     d += a;
     p += b;
+    g += c;
     g_pool.push_back(pe);
   }
-  if (distribute_ms) *distribute_ms = d;
-  if (probe_gather_ms) *probe_gather_ms = p;
+  if (phase1_ms) *phase1_ms = d;
+  if (phase2_ms) *phase2_ms = p;
+  if (phase3_ms) *phase3_ms = g;
   if (calls) *calls = (uint32_t)g_pending.size();
   g_pending.clear();
   return DPG_OK;
+}
+
+dpg_status_t dpg_phase_times(double* distribute_ms, double* probe_gather_ms, uint32_t* calls) {
+  double p2 = 0, p3 = 0;
+  dpg_status_t r = dpg_phase_times_ex(distribute_ms, &p2, &p3, calls);
+  if (probe_gather_ms) *probe_gather_ms = p2 + p3;
+  return r;
 }
 
 const char* dpg_status_string(dpg_status_t s) {
@@ -1124,7 +1304,7 @@ dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact
   // payload instead carries the fact row through the distribute kernels.)
   t_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (fact_bytes == 0 || (opt && opt->path == 2))
+  if (fact_bytes == 0 || (opt && (opt->path == 2 || opt->path == 6)))
     return run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, fact, fact_bytes, out, st, opt);
   if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
   if (n_fact == 0) return DPG_OK;
@@ -1246,6 +1426,65 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   const uint64_t L = 1ull << log2_run;
   const uint64_t K = (n_src + L - 1) >> log2_run;
   if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
+  unsigned long long* status0 = device_status();
+  if (!status0) return DPG_ERR_CUDA;
+  if (opt && opt->path == 6 && n_out) {
+    // Phase I of the three sequential passes (seq3.cu): RID_RUN with the
+    // positions, tile by tile; returned run-major (run b = its pieces (t, b)
+    // in tile order), the reordering done here on the host (test entry)
+    dpg_options_t o = *opt;
+    o.log2_run = log2_run;
+    dpg_plan_t q;
+    if (log2_run > 16 || !plan_seq3(4, n_src, n_out, 0, &o, sm, &q)) return DPG_ERR_UNSUPPORTED;
+    const uint64_t T = q.tile, nsub = (n_out + T - 1) / T;
+    const uint64_t off_preT = align_up(nsub * (K + 1) * 2, 256);
+    const uint64_t off_loc = align_up(off_preT + nsub * (K + 1) * 2, 256);
+    const uint64_t off_tinv = align_up(off_loc + nsub * T * 2, 256);
+    const uint64_t off_pairs = align_up(off_tinv + nsub * T * 2 + 16, 256);
+    const uint64_t bytes = off_pairs + nsub * T * 8;
+    void* b = nullptr;
+    if (cudaMalloc(&b, bytes) != cudaSuccess) { cudaGetLastError(); return DPG_ERR_OOM; }
+    uint8_t* wb = (uint8_t*)b;
+    Seq3Args a;
+    std::memset(&a, 0, sizeof(a));
+    a.rids = rids;
+    a.n_out = n_out;
+    a.n_src = n_src;
+    a.s = log2_run;
+    a.K = (uint32_t)K;
+    a.T = (uint32_t)T;
+    a.nsub = (uint32_t)nsub;
+    a.pre = (uint16_t*)wb;
+    a.preT = (uint16_t*)(wb + off_preT);
+    a.loc = (uint16_t*)(wb + off_loc);
+    a.tinv = (uint16_t*)(wb + off_tinv);
+    a.dbg_pairs = (uint64_t*)(wb + off_pairs);
+    a.status = status0;
+    uint32_t nl = 0;
+    cudaError_t e = launch_seq3_distribute(a, q.grid_distribute, st, &nl);
+    std::vector<uint16_t> pre(nsub * (K + 1));
+    std::vector<uint64_t> tp(nsub * T), out(n_out);
+    std::vector<uint64_t> rs(K + 1, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pre.data(), a.pre, pre.size() * 2, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tp.data(), a.dbg_pairs, tp.size() * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+      uint64_t k = 0;
+      for (uint64_t r = 0; r < K; ++r) {
+        rs[r] = k;
+        for (uint64_t t = 0; t < nsub; ++t)
+          for (uint32_t j = pre[t * (K + 1) + r]; j < pre[t * (K + 1) + r + 1]; ++j) out[k++] = tp[t * T + j];
+      }
+      rs[K] = k;
+      e = cudaMemcpyAsync(pairs_out, out.data(), k * 8, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(run_start_out, rs.data(), (K + 1) * 8, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
+    cudaFree(b);
+    t_launches = nl;
+    return cuda_status(e);
+  }
   dpg_plan_t p;
   std::memset(&p, 0, sizeof(p));
   p.log2_run = log2_run;

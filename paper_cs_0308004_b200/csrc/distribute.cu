@@ -225,16 +225,13 @@ __global__ void k_unpack(const PairT* pairs, uint64_t n, uint32_t s, const uint3
   for (uint64_t b = t; b <= K; b += stride) rs_out[b] = rs[b];
 }
 
+// Steps (1) and (2): counts[b*G + c] become the first slot of (run b, chunk c)
+// in run-major order; run_start[K+1] the runs' boundaries.
 template <typename RidT>
-static cudaError_t launch_distribute_t(const DistArgs& a, cudaStream_t st, uint32_t* nl) {
+static cudaError_t launch_count_scan_t(const DistArgs& a, cudaStream_t st, uint32_t* nl) {
   size_t hsm = a.hist_smem ? (size_t)a.K * sizeof(uint32_t) : 0;
-  if (hsm > 48 * 1024) {
+  if (hsm > 48 * 1024)
     cudaFuncSetAttribute(k_count<RidT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-    cudaFuncSetAttribute(k_scatter<RidT, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)hsm);
-    cudaFuncSetAttribute(k_scatter<RidT, uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)hsm);
-  }
   k_count<RidT><<<a.G, kDistThreads, hsm, st>>>(a);
   ++*nl;
   const uint64_t M = (uint64_t)a.K * a.G;
@@ -245,6 +242,28 @@ static cudaError_t launch_distribute_t(const DistArgs& a, cudaStream_t st, uint3
   k_scan_partials<<<1, kScanThreads, 0, st>>>(partial, nt);
   k_scan_down<<<nt, kScanThreads, 0, st>>>(a.counts, M, partial, a.G, a.K, a.run_start);
   *nl += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_scan(const DistArgs& a, cudaStream_t st, uint32_t* nl) {
+  return launch_count_scan_t<uint32_t>(a, st, nl);
+}
+
+uint32_t count_scan_partials(uint64_t K, uint64_t G) {
+  return (uint32_t)((K * G + kScanTile - 1) / kScanTile);
+}
+
+template <typename RidT>
+static cudaError_t launch_distribute_t(const DistArgs& a, cudaStream_t st, uint32_t* nl) {
+  size_t hsm = a.hist_smem ? (size_t)a.K * sizeof(uint32_t) : 0;
+  if (hsm > 48 * 1024) {
+    cudaFuncSetAttribute(k_scatter<RidT, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)hsm);
+    cudaFuncSetAttribute(k_scatter<RidT, uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)hsm);
+  }
+  cudaError_t e = launch_count_scan_t<RidT>(a, st, nl);
+  if (e != cudaSuccess) return e;
   if (a.pair_bytes == 4)
     k_scatter<RidT, uint32_t><<<a.G, kDistThreads, hsm, st>>>(a);
   else

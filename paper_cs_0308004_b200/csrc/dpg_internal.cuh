@@ -527,6 +527,46 @@ cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t*
 uint64_t sort_ws_bytes(uint64_t n, int sm);
 uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);
+// Steps (1)-(2) of the distribute alone (32-bit rids): per-chunk run counts
+// and their run-major exclusive scan (partials: count_scan_partials words
+// past run_start[K]).
+cudaError_t launch_count_scan(const DistArgs& a, cudaStream_t st, uint32_t* nlaunch);
+uint32_t count_scan_partials(uint64_t K, uint64_t G);
+
+// DPG in three sequential passes over shared-memory runs (seq3.cu, path 6),
+// intermediates stored tile by tile (see seq3.cu).
+struct Seq3Args {
+  const uint8_t* src;      // n_src records of rec bytes (16-byte aligned)
+  uint64_t n_src;
+  uint32_t rec;
+  const uint32_t* rids;    // n_out rids
+  uint64_t n_out;
+  uint32_t s;              // run length L = 2^s records (L * rec <= one stage)
+  uint32_t K;              // runs
+  uint32_t T;              // rids per tile (multiple of 16, <= 32768)
+  uint32_t nsub;           // tiles = ceil(n_out / T)
+  uint16_t* pre;           // [nsub][K+1] exclusive run prefix of each tile
+  uint16_t* preT;          // [K+1][nsub] its transpose
+  uint16_t* loc;           // RID_RUN, tile by tile: [nsub * T] local offsets
+  uint16_t* tinv;          // [n_out] slot of row i inside its tile (0xFFFF: invalid rid)
+  uint64_t* dbg_pairs;     // tests only: (local | i << 32) per RID_RUN slot
+  uint8_t* internal;       // INTERNAL, tile by tile: [nsub * T * rec]
+  uint8_t* dst;            // n_out rows of pay_bytes + rec
+  const uint8_t* pay;      // join: n_out payload rows (pay_bytes each), or null
+  uint32_t pay_bytes;
+  unsigned long long* status;
+  uint32_t dbg;            // tuning experiments only (dpg_debug_flags): 0 normally
+  unsigned long long* ts;  // profiling only (dpg_debug_phase_stamps): per-CTA stamps
+};
+uint32_t seq3_dist_smem(uint32_t T, uint32_t K);
+uint32_t seq3_probe_smem(uint64_t stage_bytes);
+uint32_t seq3_gather_smem(uint32_t T, uint32_t rec, uint32_t nbuf);
+cudaError_t launch_seq3_distribute(const Seq3Args& a, uint32_t grid, cudaStream_t st,
+                                   uint32_t* nlaunch);
+cudaError_t launch_seq3_probe(const Seq3Args& a, uint32_t W, uint32_t grid, cudaStream_t st,
+                              uint32_t* nlaunch);
+cudaError_t launch_seq3_gather(const Seq3Args& a, uint32_t W, uint32_t grid, uint32_t nbuf,
+                               cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                                 cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,

@@ -106,12 +106,14 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
     (100, 65536, 3),                  # config 1: 6.6 MB source, one L2 run
     (100, 1048576, 3),                # config 2: 105 MB source <= 7/8 of the L2, one staged run
     (64, 16777216, 1),                # config 3 at rec 64: 1.07 GB, shared-memory runs
-    (8, 1 << 24, 1),                  # 134 MB source > budget: shared-memory runs
+    (8, 1 << 24, 6),                  # 134 MB source > budget, small records: three sequential passes
+    (32, 1 << 24, 6),
 ])
 def test_plan_l2_run_rule(dpg, rec, n, auto_path):
     """The run is sized to the cache: one run (path 3) when the
     whole source fits the L2 budget (7/8 of 126 MB with no device), else
-    shared-memory runs."""
+    shared-memory runs: for records up to 32 bytes the three sequential passes
+    (path 6), else the fused / multi-kernel plans."""
     run_budget = (126 << 20) // 16 * 7                 # one L2 run (measured retention)
     p = dpg.dpg_plan(rec, n, n, 0, 148)
     assert p["path"] == auto_path

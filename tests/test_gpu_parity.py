@@ -123,7 +123,7 @@ def test_retrieve_sweep(dpg, k, n_src, rec, n_out, kind, log2_run):
 
 
 @pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
-@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0), (4, 0), (5, 0)])
+@pytest.mark.parametrize("path,gather", [(1, 1), (1, 2), (2, 0), (3, 0), (4, 0), (5, 0), (6, 0)])
 def test_retrieve_sweep_forced_path(dpg, k, n_src, rec, n_out, kind, log2_run, path, gather):
     """Every execution path on the same cases: the fused cooperative kernel
     writing rows straight to dst (gather 1) or through INTERNAL (gather 2),

@@ -24,8 +24,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--lines", type=int, default=30)
+    ap.add_argument("--kernel", default=None, help="regex: only this kernel's launches")
     a = ap.parse_args()
-    rows = list(csv.reader(io.StringIO(ncu(a.rep, "--page", "raw", "--csv"))))
+    filt = ["--kernel-name", f"regex:{a.kernel}"] if a.kernel else []
+    rows = list(csv.reader(io.StringIO(ncu(a.rep, *filt, "--page", "raw", "--csv"))))
     d = dict(zip(rows[0], rows[2] if len(rows) > 2 else rows[1]))
     for k in KEYS:
         print(f"{k:60s} {d.get(k)}")
@@ -33,7 +35,7 @@ def main():
           if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")]
     print("stalls:", ", ".join(f"{k[34:-29]} {v:.2f}" for k, v in sorted(st, key=lambda x: -x[1])[:8]))
     cur, out = None, []
-    for r in csv.reader(io.StringIO(ncu(a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"))):
+    for r in csv.reader(io.StringIO(ncu(a.rep, *filt, "--page", "source", "--csv", "--print-source", "cuda,sass"))):
         if not r:
             continue
         if r[0] == "File Path":
