@@ -34,6 +34,12 @@
  *    n_src == 0 with n_out > 0, byte-size overflow, or dst overlapping an
  *    input (the paper always copies into a separate destination);
  *    DPG_ERR_UNSUPPORTED for n_out >= 2^32.
+ *  - Scratch comes from a private stream-ordered memory pool per device (the
+ *    process's default pool is not touched); the plans' persistent workspaces
+ *    are cached per (device, stream), at most 8 of them (least recently used
+ *    idle ones are freed).  A call holds its stream's workspace until its
+ *    kernels are enqueued, so two host threads may drive the same stream.
+ *    dpg_release_cache() frees every cached buffer and trims the pool.
  *  - n_out == 0 is a no-op returning DPG_OK.
  *  - Device-detected errors: a rid >= n_src (an fk >= n_dim) is skipped, its
  *    destination row is left unwritten, and the smallest offending position
@@ -228,16 +234,14 @@ dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t
 /* End-to-end entry with HOST buffers: copies src and rids host->device,
  * runs dpg_retrieve, copies dst device->host and synchronises `stream`.
  * Host buffers should be pinned for full PCIe bandwidth.  Device buffers are
- * library-owned and cached across calls (dpg_release_cache frees them). */
+ * library-owned and cached across calls, per device (dpg_release_cache frees
+ * them).  dpg_release_cache also frees the per-stream workspaces and trims
+ * the library's memory pool (it synchronises every device). */
 dpg_status_t dpg_retrieve_host(const void *src_host, size_t rec_bytes, uint64_t n_src,
                                const uint32_t *rids_host, uint64_t n_out, void *dst_host,
                                dpg_stream_t stream);
 void dpg_release_cache(void);
 
-/* Synchronise `stream`, then report and clear the device status word:
- * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
- * recorded since the last call, or DPG_OK.  The status word is per device,
- * shared by all streams. */
 /* Batch lookup of keys in a hash index (section 4).  The index
  * (device, built by the caller): `table` = 2^m_log2 primary slots and `pool`
  * = overflow entries, each 16 bytes {uint32 key, uint32 rid, uint32 next,
@@ -299,13 +303,36 @@ dpg_status_t dpg_btree_lookup_direct(const uint32_t *const *levels, const uint64
  * receive window (CUDA IPC, NVLink), a stream-ordered all-reduce, Phase III
  * from the window.  NCCL is loaded at run time (DPG_ERR_NCCL if absent or on
  * an NCCL failure).  Invalid rids as dpg_retrieve.  Synchronises `stream`
- * once (the counts size the exchange). */
+ * (the counts size the exchange).  Failure handling: before each collective
+ * the ranks agree on their local status (an all-reduce), so a rank that fails
+ * locally (allocation, IPC mapping, a launch) makes every rank return the
+ * error together; while waiting for the stream a rank polls NCCL's
+ * asynchronous error state and aborts the communicator on an error or after
+ * DPG_NCCL_TIMEOUT_S seconds (default 600) -- an aborted communicator then
+ * returns DPG_ERR_NCCL on every call and must be destroyed. */
 dpg_status_t dpg_get_unique_id(uint8_t id[128]);
 dpg_status_t dpg_comm_create(const uint8_t id[128], int nranks, int rank, void **comm);
 dpg_status_t dpg_retrieve_dist(void *comm, const void *src_shard, size_t rec_bytes,
                                uint64_t n_src_total, const uint64_t *rids, uint64_t n_out_local,
                                void *dst, dpg_stream_t stream);
 dpg_status_t dpg_comm_destroy(void *comm);
+
+/* The same global retrieval for P (<= 8) VIRTUAL ranks in one process on the
+ * current GPU (testing and single-GPU measurement of the exchange): rank r's
+ * source shard src_shards[r] (device; records [r*S, (r+1)*S) of the global
+ * source, S as for dpg_retrieve_dist), its rids rids[r] (uint64, device,
+ * n_out[r] of them) and its output dst[r] (device).  Host arrays of P
+ * entries.  Every step is dpg_retrieve_dist's -- owner partition, the count
+ * matrix, the owner-side offsets of the requests and of each requester's
+ * window rows (the same code), the owner's segmented DPG writing into the
+ * requesters' windows, Phase III from the window -- with NCCL replaced by a
+ * host read of the counts and one device-to-device copy per (requester,
+ * owner) pair.  Synchronises `stream` once.  Errors as dpg_retrieve_dist
+ * (no DPG_ERR_NCCL: no NCCL is used). */
+dpg_status_t dpg_retrieve_dist_loopback(int P, const void *const *src_shards, size_t rec_bytes,
+                                        uint64_t n_src_total, const uint64_t *const *rids,
+                                        const uint64_t *n_out, void *const *dst,
+                                        dpg_stream_t stream);
 
 /* Receive windows for the fused multi-GPU exchange (one process per GPU on
  * one node).  dpg_ipc_alloc: a device buffer of `bytes` on the current device
@@ -374,6 +401,10 @@ dpg_status_t dpg_sort_rids(const void *src, size_t rec_bytes, uint64_t n, size_t
 dpg_status_t dpg_sort(const void *src, size_t rec_bytes, uint64_t n, size_t key_off,
                       size_t key_bytes, void *dst, dpg_stream_t stream);
 
+/* Synchronise `stream`, then report and clear the device status word:
+ * DPG_ERR_RID_RANGE with *first_bad_index = smallest offending position
+ * recorded since the last call, or DPG_OK.  The status word is per device,
+ * shared by all streams. */
 dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t *first_bad_index);
 
 const char *dpg_status_string(dpg_status_t status);

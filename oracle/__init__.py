@@ -12,6 +12,8 @@ Each wrapper cites the passage the C function follows:
 * :func:`dpg_fig1`    -- the three phases of Fig. 1, INTERNAL materialised
 * :func:`fk_join`     -- DPG-Move join rows ``fact[i] ++ dim[fk[i]]``
 * :func:`retrieve_at` -- the definition evaluated at sampled output positions
+* :func:`retrieve_generated` -- the definition for a counter-generated source too
+  large for the host (config 5), at sampled rows
 * :func:`sort_rids`   -- phases 1-2 of three-phase key-pointer sorting:
   the rids in stable key order
 * :func:`sort`        -- the whole three-phase sort: sort_rids then retrieve
@@ -61,6 +63,8 @@ def _load():
         lib.oracle_dpg_fig1.argtypes = [P, U, U, P, U, U, P, P, P, P, P, P]
         lib.oracle_fk_join.argtypes = [P, U, U, P, P, U, U, P, P]
         lib.oracle_retrieve_at.argtypes = [P, U, U, P, P, U, P]
+        lib.oracle_retrieve_at_u64.argtypes = [P, U, U, P, P, U, P]
+        lib.oracle_retrieve_at_u64.restype = ctypes.c_int
         lib.oracle_sort_rids.argtypes = [P, U, U, U, U, P]
         lib.oracle_fk_join_sort.argtypes = [P, U, U, P, P, U, U, P, P]
         lib.oracle_batch_lookup.argtypes = [P, U, P, U, P]
@@ -108,15 +112,37 @@ def retrieve(src: np.ndarray, rids: np.ndarray) -> np.ndarray:
 
 
 def retrieve_at(src: np.ndarray, rids: np.ndarray, idx: np.ndarray) -> np.ndarray:
-    """Rows D[idx[j]] of the definition, for sampled parity at full sizes."""
+    """Rows D[idx[j]] of the definition, for sampled parity at full sizes
+    (uint32 or uint64 rids; no cast)."""
     src = _records(src)
     n_src, rec = src.shape
-    rids = np.ascontiguousarray(rids, dtype=np.uint32)
+    rids = np.ascontiguousarray(rids)
+    if rids.dtype not in (np.uint32, np.uint64):
+        rids = rids.astype(np.uint64)
     idx = np.ascontiguousarray(idx, dtype=np.uint64)
     out = np.zeros((idx.size, rec), dtype=np.uint8)
-    if _load().oracle_retrieve_at(_ptr(src), rec, n_src, _ptr(rids), _ptr(idx), idx.size, _ptr(out)):
+    fn = _load().oracle_retrieve_at if rids.dtype == np.uint32 else _load().oracle_retrieve_at_u64
+    if fn(_ptr(src), rec, n_src, _ptr(rids), _ptr(idx), idx.size, _ptr(out)):
         raise RidRangeError(-1)
     return out
+
+
+def retrieve_generated(rec: int, n_src: int, sid: int, rids: np.ndarray,
+                       seed: int = 0) -> np.ndarray:
+    """D[i] = R[rids[i]] for a source R too large to hold on the
+    host (config 5: 2^30 x 100 B) whose record r is bytes [r*rec, (r+1)*rec)
+    of the counter-based stream sid (datagen, reading A12): each needed record
+    is generated at its offset and handed to oracle_retrieve_u64 as a compact
+    source.  For sampled rows only (a Python loop over the rids)."""
+    import datagen
+    rids = np.ascontiguousarray(rids).astype(np.uint64)
+    bad = np.nonzero(rids >= np.uint64(n_src))[0]
+    if bad.size:
+        raise RidRangeError(int(bad[0]))
+    uniq, inv = np.unique(rids, return_inverse=True)
+    compact = np.stack([datagen.random_bytes(rec, sid, seed=seed, offset=int(r) * rec)
+                        for r in uniq]) if uniq.size else np.zeros((0, rec), np.uint8)
+    return retrieve(compact, inv.astype(np.uint64))
 
 
 def dpg_fig1(src: np.ndarray, rids: np.ndarray, L: int):

@@ -16,7 +16,9 @@
  * brute force over all permutations n<=6 via an independent inverse-scatter
  * formulation, all rid sequences of length <= 4 over n <= 3 against numpy
  * fancy indexing, identity / multiset / sorted-key invariants, the join's
- * nested-loop cross-check.  No function here is "parity unpinned".
+ * nested-loop cross-check; the 64-bit-rid entries against numpy indexing, the
+ * 32-bit entries and a no-truncation check (rids >= 2^32).  No function here
+ * is "parity unpinned".
  *
  * Return convention (reading A6 of DESIGN.md): 0 on success; -1 on an invalid
  * argument; 1 if some rid >= n_src, in which case *bad_index receives the
@@ -190,6 +192,19 @@ int oracle_fk_join(const uint8_t *fact, uint64_t fact_bytes, uint64_t n_fact,
 int oracle_retrieve_at(const uint8_t *src, uint64_t rec, uint64_t n_src,
                        const uint32_t *rids, const uint64_t *idx, uint64_t n_idx,
                        uint8_t *out)
+{
+    for (uint64_t j = 0; j < n_idx; ++j) {
+        uint64_t r = rids[idx[j]];
+        if (r >= n_src) return 1;
+        memcpy(out + j * rec, src + r * rec, rec);
+    }
+    return 0;
+}
+
+/* Same, 64-bit rids (the multi-GPU configuration's global rids). */
+int oracle_retrieve_at_u64(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                           const uint64_t *rids, const uint64_t *idx, uint64_t n_idx,
+                           uint8_t *out)
 {
     for (uint64_t j = 0; j < n_idx; ++j) {
         uint64_t r = rids[idx[j]];

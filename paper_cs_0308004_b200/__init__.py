@@ -44,6 +44,7 @@ EXPORTED = (
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
     "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
+    "dpg_phase_times_ex", "dpg_retrieve_dist_loopback",
 )
 
 
@@ -107,6 +108,7 @@ _sigs = {
     "dpg_btree_lookup_direct": [_P, _P, ctypes.c_uint32, _P, _P, _U, _P, _P],
     "dpg_comm_create": [_P, ctypes.c_int, ctypes.c_int, _P],
     "dpg_retrieve_dist": [_P, _P, _S, _U, _P, _U, _P, _P],
+    "dpg_retrieve_dist_loopback": [ctypes.c_int, _P, _S, _U, _P, _P, _P, _P],
     "dpg_comm_destroy": [_P],
     "dpg_ipc_open": [_P, _P],
     "dpg_ipc_close": [_P],
@@ -504,6 +506,32 @@ def dpg_retrieve_dist(comm: int, src_shard, n_src_total: int, rids, dst=None, st
                                   rids.data_ptr(), rids.numel(), dst.data_ptr(),
                                   _stream_ptr(stream)), "dpg_retrieve_dist")
     return dst
+
+
+def dpg_retrieve_dist_loopback(src_shards, n_src_total: int, rids_list, dsts=None, stream=None):
+    """The multi-GPU exchange for P = len(src_shards) virtual ranks on this GPU
+    (dpg_retrieve_dist_loopback): rank r owns src_shards[r] (uint8 [S_r, rec]),
+    asks for rids_list[r] (int64/uint64 CUDA) and receives dsts[r]."""
+    torch = _torch()
+    P = len(src_shards)
+    if len(rids_list) != P:
+        raise ValueError("one rid list per rank")
+    shards = [_records(t, "src_shard") for t in src_shards]
+    rec = shards[0].shape[1]
+    rl = []
+    for r in rids_list:
+        if r.dtype not in (torch.int64, torch.uint64) or not r.is_contiguous():
+            raise TypeError("rids must be contiguous CUDA int64/uint64")
+        rl.append(r)
+    if dsts is None:
+        dsts = [torch.empty((r.numel(), rec), dtype=torch.uint8, device=r.device) for r in rl]
+    arr_p = (ctypes.c_void_p * P)
+    arr_u = (ctypes.c_uint64 * P)
+    _check(_lib.dpg_retrieve_dist_loopback(
+        P, arr_p(*[t.data_ptr() for t in shards]), rec, n_src_total,
+        arr_p(*[r.data_ptr() for r in rl]), arr_u(*[r.numel() for r in rl]),
+        arr_p(*[d.data_ptr() for d in dsts]), _stream_ptr(stream)), "dpg_retrieve_dist_loopback")
+    return dsts
 
 
 def ipc_alloc(nbytes: int) -> tuple[int, bytes]:

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <list>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -98,12 +100,6 @@ unsigned long long* device_status() {
     if (cudaMalloc(&p, sizeof(*p)) != cudaSuccess) return nullptr;
     unsigned long long init = ~0ull;
     if (cudaMemcpy(p, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-    // keep freed workspace in the default pool (no release back to the OS)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
     ptr[dev] = p;
   }
   return ptr[dev];
@@ -586,7 +582,7 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
   uint64_t off_pay = align_up(off_pairs + n_out * p.pair_bytes + 64, 256);
   uint64_t total = align_up(off_pay + (p.pay_bytes ? n_out * p.pay_bytes + 64 : 0), 256);
   void* b = nullptr;
-  if (cudaMallocAsync(&b, total, st) != cudaSuccess) {
+  if (ws_malloc(&b, total, st) != cudaSuccess) {
     cudaGetLastError();
     return DPG_ERR_OOM;
   }
@@ -598,32 +594,117 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
   return DPG_OK;
 }
 
-// Persistent per-(device, stream) workspace of the fused kernel:
-// [grid barrier (2 u32) | run totals (K u32) | pairs].  The kernel leaves the
-// barrier and the totals zero on exit, so they are zeroed once, at allocation.
+// Persistent per-(device, stream) workspace: [grid barrier + counters (K
+// u32) | scratch].  The kernels leave the barrier and the counters zero on
+// exit, so they are zeroed once, at allocation.  Each entry has its own
+// (recursive) mutex, which the calling entry point holds (WsHold) from
+// persist_ws until its launches are enqueued: a second host thread driving the
+// same stream waits instead of freeing a base the first is about to use; a
+// nested call on the same thread (dpg_sort -> run_dpg) re-enters.  At most
+// kWsCached entries keep memory; the least recently used idle ones beyond
+// that are freed (synchronously: their stream may be gone).
 struct PersistWS {
+  int dev = 0;
+  cudaStream_t st = nullptr;
   uint8_t* base = nullptr;
   uint64_t counters = 0;  // bytes of the zero-invariant prefix
   uint64_t bytes = 0;
+  uint64_t last_use = 0;
+  std::unique_ptr<std::recursive_mutex> mu{new std::recursive_mutex};
 };
+constexpr size_t kWsCached = 8;
 std::mutex g_ws_mu;
-std::vector<std::pair<std::pair<int, cudaStream_t>, PersistWS>> g_ws;
+std::list<PersistWS> g_ws;      // entries are never erased (stable addresses)
+uint64_t g_ws_clock = 0;
+
+// Library scratch comes from a private stream-ordered pool per device (the
+// process's default pool is left alone); dpg_release_cache trims it.
+cudaMemPool_t ws_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps pr;
+    std::memset(&pr, 0, sizeof(pr));
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.handleTypes = cudaMemHandleTypeNone;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &pr) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    uint64_t thr = UINT64_MAX;      // freed scratch stays reserved for the next call
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
+
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = ws_pool();
+  if (!pool) return cudaMallocAsync(p, bytes, st);
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
+void ws_pool_trim() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return; }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < n && d < 64; ++d) {
+    cudaSetDevice(d);
+    if (cudaMemPool_t p = ws_pool()) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(p, 0);
+    }
+  }
+  cudaSetDevice(cur);
+  cudaGetLastError();
+}
 
 dpg_status_t persist_ws(cudaStream_t st, uint64_t K, uint64_t pair_bytes_total, uint32_t** gbar,
-                        uint32_t** total, void** pairs) {
+                        uint32_t** total, void** pairs, WsHold* hold) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return DPG_ERR_CUDA;
   const uint64_t need_ctr = align_up(256 + K * 4, 256);
   const uint64_t need = need_ctr + align_up(pair_bytes_total + 64, 256);
-  std::lock_guard<std::mutex> lk(g_ws_mu);
   PersistWS* w = nullptr;
-  for (auto& kv : g_ws)
-    if (kv.first.first == dev && kv.first.second == st) w = &kv.second;
-  if (!w) {
-    g_ws.push_back({{dev, st}, PersistWS()});
-    w = &g_ws.back().second;
+  std::vector<PersistWS*> evict;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& kv : g_ws)
+      if (kv.dev == dev && kv.st == st) w = &kv;
+    if (!w) {
+      g_ws.emplace_back();
+      w = &g_ws.back();
+      w->dev = dev;
+      w->st = st;
+    }
+    w->last_use = ++g_ws_clock;
+    std::vector<PersistWS*> live;
+    for (auto& kv : g_ws)
+      if (kv.base && &kv != w) live.push_back(&kv);
+    if (live.size() + 1 > kWsCached) {
+      std::sort(live.begin(), live.end(),
+                [](PersistWS* x, PersistWS* y) { return x->last_use < y->last_use; });
+      evict.assign(live.begin(), live.begin() + (live.size() + 1 - kWsCached));
+    }
   }
+  for (PersistWS* v : evict) {           // idle least recently used entries
+    std::unique_lock<std::recursive_mutex> vl(*v->mu, std::try_to_lock);
+    if (!vl.owns_lock() || !v->base) continue;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(v->dev);
+    cudaFree(v->base);                   // synchronous: its stream may be destroyed
+    cudaSetDevice(cur);
+    cudaGetLastError();
+    v->base = nullptr;
+    v->bytes = v->counters = 0;
+  }
+  *hold = WsHold(*w->mu);                // held until the caller's launches are enqueued
   const uint64_t need_pairs = need - need_ctr;
   const uint64_t have_pairs = w->bytes - w->counters;
   if (w->counters < need_ctr || have_pairs < need_pairs) {
@@ -633,7 +714,7 @@ dpg_status_t persist_ws(cudaStream_t st, uint64_t K, uint64_t pair_bytes_total, 
     w->base = nullptr;
     w->bytes = w->counters = 0;
     void* b = nullptr;
-    if (cudaMallocAsync(&b, bytes, st) != cudaSuccess) {
+    if (ws_malloc(&b, bytes, st) != cudaSuccess) {
       cudaGetLastError();
       return DPG_ERR_OOM;
     }
@@ -649,10 +730,23 @@ dpg_status_t persist_ws(cudaStream_t st, uint64_t K, uint64_t pair_bytes_total, 
 }
 
 void release_persist_ws() {
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  for (auto& kv : g_ws)
-    if (kv.second.base) cudaFreeAsync(kv.second.base, kv.first.second);
-  g_ws.clear();
+  std::vector<PersistWS*> all;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& kv : g_ws) all.push_back(&kv);
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (PersistWS* v : all) {
+    std::lock_guard<std::recursive_mutex> vl(*v->mu);
+    if (!v->base) continue;
+    cudaSetDevice(v->dev);
+    cudaFree(v->base);                   // synchronous: the stream may be destroyed
+    v->base = nullptr;
+    v->bytes = v->counters = 0;
+  }
+  cudaSetDevice(cur);
+  cudaGetLastError();
 }
 
 dpg_status_t cuda_status(cudaError_t e) {
@@ -702,6 +796,7 @@ dpg_status_t skew_excess(const uint32_t* rids, uint64_t n_out, uint64_t n_src, c
 dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32_t* rids,
                      uint64_t n_out, const void* pay_src, uint64_t pay, void* dst,
                      cudaStream_t st, const dpg_options_t* opt) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   t_launches = 0;
   if (rec == 0) return DPG_ERR_INVALID_ARG;
   if (n_out == 0) return DPG_OK;
@@ -821,7 +916,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     const uint64_t off_tinv = align_up(off_loc + nsub * T * 2, 256);
     const uint64_t off_int = align_up(off_tinv + nsub * T * 2 + 16, 256);
     const uint64_t bytes = off_int + nsub * T * rec + 64;
-    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws, &ws_hold);
     if (wst != DPG_OK) return wst;
     uint8_t* wb = (uint8_t*)ws;
     Seq3Args a;
@@ -874,7 +969,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     const uint64_t off_inv = align_up(off_local + n_out * 4 + 16, 256);
     const uint64_t off_int = align_up(off_inv + n_out * 4 + 16, 256);
     const uint64_t bytes = off_int + n_out * rec + 64;
-    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+    dpg_status_t wst = persist_ws(st, 1, bytes, &gbar, &total, &ws, &ws_hold);
     if (wst != DPG_OK) return wst;
     uint8_t* wb = (uint8_t*)ws;
     L2KArgs d;
@@ -953,7 +1048,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     uint32_t *gbar = nullptr, *total = nullptr;
     void* internal = nullptr;
     const uint64_t int_bytes = (uint64_t)p.grid_probe * p.tile * rec;
-    dpg_status_t ws = persist_ws(st, 1, int_bytes + 64, &gbar, &total, &internal);
+    dpg_status_t ws = persist_ws(st, 1, int_bytes + 64, &gbar, &total, &internal, &ws_hold);
     if (ws != DPG_OK) return ws;
     L2PairArgs l;
     std::memset(&l, 0, sizeof(l));
@@ -983,7 +1078,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (p.path == 3) {
     uint32_t *gbar = nullptr, *total = nullptr;
     void* pairs = nullptr;
-    dpg_status_t ws = persist_ws(st, 1, 64, &gbar, &total, &pairs);
+    dpg_status_t ws = persist_ws(st, 1, 64, &gbar, &total, &pairs, &ws_hold);
     if (ws != DPG_OK) return ws;
     L2RunArgs l;
     std::memset(&l, 0, sizeof(l));
@@ -1035,7 +1130,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     const uint64_t inv_sz = p.gather == 2 ? align_up(n_out * 4, 256) : 0;
     const uint64_t int_sz = p.gather == 2 ? align_up(slots * rec + 64, 256) : 0;
     dpg_status_t ws = persist_ws(st, p.num_runs, pairs_sz + ovf_sz + inv_sz + int_sz, &gbar,
-                                 &total, &pairs);
+                                 &total, &pairs, &ws_hold);
     if (ws != DPG_OK) return ws;
     f.mode = p.gather == 2 ? 1 : 0;
     if (f.mode == 1) {
@@ -1321,7 +1416,7 @@ dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact
       overlaps(out, out_bytes, fk_col, n_fact * 4))
     return DPG_ERR_INVALID_ARG;
   void* tmp = nullptr;
-  if (cudaMallocAsync(&tmp, tmp_bytes + 256, st) != cudaSuccess) {
+  if (ws_malloc(&tmp, tmp_bytes + 256, st) != cudaSuccess) {
     cudaGetLastError();
     return DPG_ERR_OOM;
   }
@@ -1332,7 +1427,8 @@ dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact
                                     (uintptr_t)out);
     cudaError_t e = launch_zip_rows((const uint8_t*)fact, (uint32_t)fact_bytes,
                                     (const uint8_t*)tmp, (uint32_t)rec_bytes, n_fact,
-                                    (uint8_t*)out, W, current_sm_count(), st, &nl);
+                                    (uint8_t*)out, W, current_sm_count(), st, &nl,
+                                    fk_col, n_dim);   // an fk >= n_dim: row left unwritten
     s = cuda_status(e);
   }
   cudaFreeAsync(tmp, st);
@@ -1366,6 +1462,7 @@ dpg_status_t dpg_l2_prefetch(const void* ptr, uint64_t bytes, dpg_stream_t strea
 dpg_status_t dpg_retrieve_direct_ex(const void* src, size_t rec_bytes, uint64_t n_src,
                                     const uint32_t* rids, uint64_t n_out, void* dst,
                                     dpg_stream_t stream, int hint) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   t_launches = 0;
   if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
   if (n_out == 0) return DPG_OK;
@@ -1387,7 +1484,7 @@ dpg_status_t dpg_retrieve_direct_ex(const void* src, size_t rec_bytes, uint64_t 
     // realigned in shared memory, coalesced 16-byte row stores), no staging
     uint32_t *gbar = nullptr, *total = nullptr;
     void* pairs = nullptr;
-    dpg_status_t ws = persist_ws((cudaStream_t)stream, 1, 64, &gbar, &total, &pairs);
+    dpg_status_t ws = persist_ws((cudaStream_t)stream, 1, 64, &gbar, &total, &pairs, &ws_hold);
     if (ws != DPG_OK) return ws;
     const int sm = current_sm_count();
     L2RunArgs l;
@@ -1585,6 +1682,7 @@ dpg_status_t dpg_partition_inv(const void* rids, uint32_t rid_bytes, uint64_t n,
                                uint64_t n_src_total, uint32_t log2_span, uint32_t parts,
                                uint32_t* local_out, uint32_t* inv_out, uint64_t* counts_out,
                                dpg_stream_t stream) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // Phase I of the multi-GPU path with Phase III's map: requests grouped by
   // owner (owner = rid >> log2_span), and for every row the slot of its request
   // (the replies come back in request order, so dst[i] = reply[inv[i]]).
@@ -1603,7 +1701,7 @@ dpg_status_t dpg_partition_inv(const void* rids, uint32_t rid_bytes, uint64_t n,
   uint32_t *gbar = nullptr, *total = nullptr;
   void* ws = nullptr;
   const uint64_t cbytes = align_up((uint64_t)parts * sm * 4, 256) + align_up((parts + 1) * 4, 256);
-  dpg_status_t w = persist_ws(st, 1, cbytes, &gbar, &total, &ws);
+  dpg_status_t w = persist_ws(st, 1, cbytes, &gbar, &total, &ws, &ws_hold);
   if (w != DPG_OK) return w;
   L2KArgs d;
   std::memset(&d, 0, sizeof(d));
@@ -1659,6 +1757,7 @@ dpg_status_t dpg_ipc_free(void* ptr) { return cuda_status(cudaFree(ptr)); }
 
 dpg_status_t dpg_gather_rows(const void* rows, size_t rec_bytes, uint64_t n_rows, const uint32_t* inv,
                              uint64_t n, void* dst, dpg_stream_t stream) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // dst[i] = rows[inv[i]] (rows with inv[i] >= n_rows stay unwritten): the
   // multi-GPU path's Phase III over the replies, in output order.
   t_launches = 0;
@@ -1669,7 +1768,7 @@ dpg_status_t dpg_gather_rows(const void* rows, size_t rec_bytes, uint64_t n_rows
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t *gbar = nullptr, *total = nullptr;
   void* ws = nullptr;
-  dpg_status_t w = persist_ws(st, 1, 64, &gbar, &total, &ws);
+  dpg_status_t w = persist_ws(st, 1, 64, &gbar, &total, &ws, &ws_hold);
   if (w != DPG_OK) return w;
   const int sm = current_sm_count();
   L2RunArgs l;
@@ -1725,21 +1824,24 @@ dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
 
 // ---- end-to-end entry with host buffers --------------------------------------
 static std::mutex g_host_mu;
-static void* g_host_buf[3] = {nullptr, nullptr, nullptr};
-static size_t g_host_cap[3] = {0, 0, 0};
+// device buffers of dpg_retrieve_host, cached per device
+static void* g_host_buf[64][3] = {};
+static size_t g_host_cap[64][3] = {};
 
 static dpg_status_t host_buf(int k, size_t bytes, void** out) {
-  if (g_host_cap[k] < bytes) {
-    if (g_host_buf[k]) cudaFree(g_host_buf[k]);
-    g_host_buf[k] = nullptr;
-    g_host_cap[k] = 0;
-    if (cudaMalloc(&g_host_buf[k], bytes) != cudaSuccess) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DPG_ERR_CUDA;
+  if (g_host_cap[dev][k] < bytes) {
+    if (g_host_buf[dev][k]) cudaFree(g_host_buf[dev][k]);
+    g_host_buf[dev][k] = nullptr;
+    g_host_cap[dev][k] = 0;
+    if (cudaMalloc(&g_host_buf[dev][k], bytes) != cudaSuccess) {
       cudaGetLastError();
       return DPG_ERR_OOM;
     }
-    g_host_cap[k] = bytes;
+    g_host_cap[dev][k] = bytes;
   }
-  *out = g_host_buf[k];
+  *out = g_host_buf[dev][k];
   return DPG_OK;
 }
 
@@ -1772,12 +1874,20 @@ dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t 
 
 void dpg_release_cache(void) {
   std::lock_guard<std::mutex> lk(g_host_mu);
-  for (int k = 0; k < 3; ++k) {
-    if (g_host_buf[k]) cudaFree(g_host_buf[k]);
-    g_host_buf[k] = nullptr;
-    g_host_cap[k] = 0;
-  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < 64; ++d)
+    for (int k = 0; k < 3; ++k) {
+      if (!g_host_buf[d][k]) continue;
+      cudaSetDevice(d);
+      cudaFree(g_host_buf[d][k]);
+      g_host_buf[d][k] = nullptr;
+      g_host_cap[d][k] = 0;
+    }
+  cudaSetDevice(cur);
+  cudaGetLastError();
   release_persist_ws();
+  ws_pool_trim();
 }
 
 }  // extern "C"

@@ -36,6 +36,7 @@ extern "C" {
 
 dpg_status_t dpg_sort_rids(const void* src, size_t rec_bytes, uint64_t n, size_t key_off,
                            size_t key_bytes, uint32_t* rids_out, dpg_stream_t stream) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // Phases 1-2 of three-phase sorting: stable rid order by key.
   t_launches = 0;
   if (rec_bytes == 0 || key_bytes == 0 || key_bytes > 12 || key_off + key_bytes > rec_bytes)
@@ -50,7 +51,7 @@ dpg_status_t dpg_sort_rids(const void* src, size_t rec_bytes, uint64_t n, size_t
   const int sm = current_sm_count();
   uint32_t *gbar = nullptr, *total = nullptr;
   void* ws = nullptr;
-  dpg_status_t w = persist_ws(st, 1, sort_ws_bytes(n, sm), &gbar, &total, &ws);
+  dpg_status_t w = persist_ws(st, 1, sort_ws_bytes(n, sm), &gbar, &total, &ws, &ws_hold);
   if (w != DPG_OK) return w;
   uint32_t nl = 0;
   cudaError_t e = launch_sort_rids((const uint8_t*)src, (uint32_t)rec_bytes, n, (uint32_t)key_off,
@@ -73,7 +74,7 @@ dpg_status_t dpg_sort(const void* src, size_t rec_bytes, uint64_t n, size_t key_
   if (overlaps(dst, bytes, src, bytes)) return DPG_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   void* rids = nullptr;
-  if (cudaMallocAsync(&rids, n * 4 + 64, st) != cudaSuccess) {
+  if (ws_malloc(&rids, n * 4 + 64, st) != cudaSuccess) {
     cudaGetLastError();
     return DPG_ERR_OOM;
   }
@@ -91,6 +92,7 @@ dpg_status_t dpg_sort(const void* src, size_t rec_bytes, uint64_t n, size_t key_
 dpg_status_t dpg_fk_join_sort(const void* fact, size_t fact_bytes, uint64_t n_fact,
                               const uint32_t* fk_col, const void* dim, size_t rec_bytes,
                               uint64_t n_dim, void* out, dpg_stream_t stream) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // DPG-Sort join: sort the pairs (rid_R = i, rid_F =
   // fk[i]) by rid_F (stable radix sort, sort.cu), move the records of R (the
   // fact rows) into a temporary file in that order by DPG retrieval, then join
@@ -119,7 +121,7 @@ dpg_status_t dpg_fk_join_sort(const void* fact, size_t fact_bytes, uint64_t n_fa
   const uint64_t o_fk = align_up(n_fact * 4 + 16, 256);
   const uint64_t o_tmp = o_fk + align_up(n_fact * 4 + 16, 256);
   void* buf = nullptr;
-  if (cudaMallocAsync(&buf, o_tmp + n_fact * fact_bytes + 64, st) != cudaSuccess) {
+  if (ws_malloc(&buf, o_tmp + n_fact * fact_bytes + 64, st) != cudaSuccess) {
     cudaGetLastError();
     return DPG_ERR_OOM;
   }
@@ -129,7 +131,7 @@ dpg_status_t dpg_fk_join_sort(const void* fact, size_t fact_bytes, uint64_t n_fa
   uint32_t *gbar = nullptr, *total = nullptr;
   void* ws = nullptr;
   uint32_t nl = 0;
-  dpg_status_t s = persist_ws(st, 1, sort_ws_bytes(n_fact, sm), &gbar, &total, &ws);
+  dpg_status_t s = persist_ws(st, 1, sort_ws_bytes(n_fact, sm), &gbar, &total, &ws, &ws_hold);
   cudaError_t e = cudaSuccess;
   if (s == DPG_OK)
     e = launch_sort_rids(nullptr, 4, n_fact, 0, 4, (uint8_t*)ws, rid_r, gbar + 16, sm, st, &nl,
@@ -167,6 +169,7 @@ dpg_status_t dpg_hash_lookup_direct(const void* table, uint32_t m_log2, const vo
 dpg_status_t dpg_hash_lookup(const void* table, uint32_t m_log2, const void* pool,
                              const uint32_t* keys, uint64_t n, uint32_t* out, dpg_stream_t stream,
                              uint32_t log2_run) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // DPG batch lookup: Phase I distributes the keys by partition
   // of the hash array, Phase II probes partition by partition with the
   // partition L2-resident, Phase III gathers the rids back into query order.
@@ -201,7 +204,7 @@ dpg_status_t dpg_hash_lookup(const void* table, uint32_t m_log2, const void* poo
   const uint64_t off_tmp = align_up(off_inv + n * 4 + 16, 256);
   const uint64_t off_ovf = align_up(off_tmp + slots * 4 + 16, 256);
   const uint64_t bytes = off_ovf + n * 8 + 64;
-  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws, &ws_hold);
   if (w != DPG_OK) return w;
   uint8_t* wb = (uint8_t*)ws;
   uint32_t* cursor = (uint32_t*)(wb + off_cur);
@@ -239,6 +242,7 @@ dpg_status_t dpg_btree_lookup_direct(const uint32_t* const* levels, const uint64
 dpg_status_t dpg_btree_lookup(const uint32_t* const* levels, const uint64_t* level_n,
                               uint32_t n_levels, const uint32_t* rids, const uint32_t* keys,
                               uint64_t n, uint32_t* out, dpg_stream_t stream, uint32_t log2_run) {
+  WsHold ws_hold;   // the stream's workspace stays ours until the launches are enqueued
   // the two-pass DPG lookup
   t_launches = 0;
   BTreeIdx T;
@@ -274,7 +278,7 @@ dpg_status_t dpg_btree_lookup(const uint32_t* const* levels, const uint64_t* lev
   const uint64_t off_inv = align_up(off_q + n * 4 + 16, 256);
   const uint64_t off_tmp = align_up(off_inv + n * 4 + 16, 256);
   const uint64_t bytes = off_tmp + n * 4 + 64;
-  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws);
+  dpg_status_t w = persist_ws(st, 1, bytes, &gbar, &total, &ws, &ws_hold);
   if (w != DPG_OK) return w;
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;

@@ -3,6 +3,7 @@
 // Internal to libdpg.so; not part of include/dpg.h.
 #pragma once
 #include <cstdint>
+#include <mutex>
 
 #include "dpg.h"
 #include "dpg_internal.cuh"
@@ -20,8 +21,17 @@ bool overlaps(const void* a, uint64_t na, const void* b, uint64_t nb);
 uint64_t l2_run_budget(uint64_t l2_bytes);
 // Library-owned workspace, persistent per (device, stream): grid-barrier and
 // counter words (zero-restored by the kernels) and `bytes` of scratch.
+// *hold keeps the (device, stream) entry locked until the caller's launches
+// are enqueued (declare it before the call, in the entry point's scope).
+using WsHold = std::unique_lock<std::recursive_mutex>;
 dpg_status_t persist_ws(cudaStream_t st, uint64_t K, uint64_t bytes, uint32_t** gbar,
-                        uint32_t** total, void** scratch);
+                        uint32_t** total, void** scratch, WsHold* hold);
+// Stream-ordered scratch from the library's private pool (cudaFreeAsync frees it).
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t st);
+template <typename T>
+inline cudaError_t ws_malloc(T** p, size_t bytes, cudaStream_t st) {
+  return ws_malloc(reinterpret_cast<void**>(p), bytes, st);
+}
 dpg_status_t cuda_status(cudaError_t e);
 dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32_t* rids,
                      uint64_t n_out, const void* pay_src, uint64_t pay, void* dst, cudaStream_t st,

@@ -206,7 +206,8 @@ cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cuda
 template <int W>
 __global__ void __launch_bounds__(256) k_zip_rows(const uint8_t* __restrict__ a, uint32_t a_bytes,
                                                   const uint8_t* __restrict__ b, uint32_t b_bytes,
-                                                  uint64_t n, uint8_t* __restrict__ out) {
+                                                  uint64_t n, uint8_t* __restrict__ out,
+                                                  const uint32_t* __restrict__ key, uint64_t key_limit) {
   using T = typename Word<W>::T;
   const uint32_t AW = a_bytes / W, R = (a_bytes + b_bytes) / W;
   const uint64_t words = n * R;
@@ -214,6 +215,8 @@ __global__ void __launch_bounds__(256) k_zip_rows(const uint8_t* __restrict__ a,
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < words; k += stride) {
     const uint64_t row = k / R;
     const uint32_t w = (uint32_t)(k - row * R);
+    // a row whose key failed the integrity check has no b part: left unwritten
+    if (key && (uint64_t)__ldg(key + row) >= key_limit) continue;
     const T v = w < AW ? __ldg(reinterpret_cast<const T*>(a + row * a_bytes) + w)
                        : __ldg(reinterpret_cast<const T*>(b + row * b_bytes) + (w - AW));
     reinterpret_cast<T*>(out)[k] = v;
@@ -222,16 +225,16 @@ __global__ void __launch_bounds__(256) k_zip_rows(const uint8_t* __restrict__ a,
 
 cudaError_t launch_zip_rows(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                             uint64_t n, uint8_t* out, uint32_t W, int sm_count, cudaStream_t st,
-                            uint32_t* nl) {
+                            uint32_t* nl, const uint32_t* key, uint64_t key_limit) {
   const uint64_t words = n * ((a_bytes + b_bytes) / W);
   const uint32_t grid = (uint32_t)max_u64(1, min_u64((words + 255) / 256, (uint64_t)sm_count * 8));
   ++*nl;
   switch (W) {
-    case 16: k_zip_rows<16><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out); break;
-    case 8: k_zip_rows<8><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out); break;
-    case 4: k_zip_rows<4><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out); break;
-    case 2: k_zip_rows<2><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out); break;
-    default: k_zip_rows<1><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out); break;
+    case 16: k_zip_rows<16><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out, key, key_limit); break;
+    case 8: k_zip_rows<8><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out, key, key_limit); break;
+    case 4: k_zip_rows<4><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out, key, key_limit); break;
+    case 2: k_zip_rows<2><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out, key, key_limit); break;
+    default: k_zip_rows<1><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n, out, key, key_limit); break;
   }
   return cudaGetLastError();
 }

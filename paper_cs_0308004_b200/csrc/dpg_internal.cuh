@@ -577,7 +577,8 @@ cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cuda
                                uint32_t* nlaunch);
 cudaError_t launch_zip_rows(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                             uint64_t n, uint8_t* out, uint32_t W, int sm_count, cudaStream_t st,
-                            uint32_t* nlaunch);
+                            uint32_t* nlaunch, const uint32_t* key = nullptr,
+                            uint64_t key_limit = 0);
 cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos,
                                 uint64_t n, uint8_t* dst, uint64_t n_dst, uint32_t W,
                                 int sm_count, cudaStream_t st, uint32_t* nlaunch);

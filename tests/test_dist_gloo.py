@@ -151,7 +151,7 @@ def test_retrieve_dist_matches_oracle(world, n_total, rec, n_out, round_rows, fu
     src = rng.integers(0, 256, (n_total, rec), dtype=np.uint8)
     rids = rng.integers(0, n_total, n_out).astype(np.int64)
     rids[: min(n_out, n_total)] = rng.permutation(n_total)[: min(n_out, n_total)]
-    assert np.array_equal(got, oracle.retrieve(src, rids.astype(np.uint32)))
+    assert np.array_equal(got, oracle.retrieve(src, rids.astype(np.uint64)))
 
 
 def test_span_and_ranges():

@@ -8,6 +8,7 @@ import socket
 import numpy as np
 import pytest
 
+import datagen
 import oracle
 
 pytestmark = pytest.mark.gpu
@@ -91,7 +92,7 @@ def test_retrieve_dist_single_rank_nccl(dpg):
         out = retrieve_dist(torch.from_numpy(src).cuda(), torch.from_numpy(rids).cuda(), 50000,
                             max_rows_per_round=30000)
         torch.cuda.synchronize()
-        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint64)))
     finally:
         dist.destroy_process_group()
 
@@ -114,7 +115,7 @@ def test_retrieve_dist_fused_single_rank_nccl(dpg):
         out = retrieve_dist(torch.from_numpy(src).cuda(), torch.from_numpy(rids).cuda(), 50000,
                             max_rows_per_round=30000, fused=True)
         torch.cuda.synchronize()
-        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+        assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint64)))
     finally:
         dist.destroy_process_group()
 
@@ -185,7 +186,7 @@ def test_c_abi_retrieve_dist_single_rank(dpg):
             out = dpg.dpg_retrieve_dist(comm, torch.from_numpy(src).cuda(), n_total,
                                         torch.from_numpy(rids).cuda())
             torch.cuda.synchronize()
-            assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint32)))
+            assert np.array_equal(out.cpu().numpy(), oracle.retrieve(src, rids.astype(np.uint64)))
         rids = np.arange(100, dtype=np.int64)
         rids[37] = 5000
         dpg.dpg_retrieve_dist(comm, torch.zeros((100, 8), dtype=torch.uint8, device="cuda"), 100,
@@ -195,3 +196,57 @@ def test_c_abi_retrieve_dist_single_rank(dpg):
         assert e.value.index == 37
     finally:
         dpg.dpg_comm_destroy(comm)
+
+
+def _owner_span(n_total, P):
+    per = max(1, -(-n_total // P))
+    return 1 << (per - 1).bit_length()
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_loopback_exchange_config5_down_scaled(dpg, P):
+    """The multi-GPU exchange for P virtual ranks on one GPU
+    (dpg_retrieve_dist_loopback): config 5's shape down-scaled -- 2^20 records
+    of 100 B from the c5 source stream, rids = the c5 Feistel permutation
+    (uint64), block-partitioned by output position -- through the same owner
+    partition, count matrix, request and window-row offsets, segmented owner
+    DPG and Phase III as dpg_retrieve_dist; every rank's output against the
+    oracle (64-bit rids)."""
+    n_total, rec = 1 << 20, 100
+    src = datagen.records(n_total, rec, datagen.STREAMS[("c5", "src")])
+    rids = datagen.feistel(n_total, 0, n_total, datagen.STREAMS[("c5", "rids")])
+    S = _owner_span(n_total, P)
+    shards = [torch.from_numpy(src[r * S:min(n_total, (r + 1) * S)]).cuda() for r in range(P)]
+    blocks = [rids[r * n_total // P:(r + 1) * n_total // P] for r in range(P)]
+    outs = dpg.dpg_retrieve_dist_loopback(shards, n_total,
+                                          [torch.from_numpy(b.view(np.int64)).cuda() for b in blocks])
+    torch.cuda.synchronize()
+    for b, o in zip(blocks, outs):
+        assert np.array_equal(o.cpu().numpy(), oracle.retrieve(src, b))
+
+
+@pytest.mark.parametrize("P,rec", [(2, 12), (5, 8), (8, 64), (3, 100)])
+def test_loopback_exchange_uneven_and_repeated(dpg, P, rec):
+    """Uneven output blocks (one empty), repeated rids (with replacement), a
+    source size that is not a multiple of P (the last owner's shard short),
+    and an invalid rid (reported, row left unwritten)."""
+    rng = np.random.default_rng(P * 100 + rec)
+    n_total = 100_003
+    src = rng.integers(0, 256, (n_total, rec), dtype=np.uint8)
+    S = _owner_span(n_total, P)
+    shards = [torch.from_numpy(src[r * S:min(n_total, (r + 1) * S)]).cuda() for r in range(P)]
+    sizes = [int(x) for x in rng.integers(0, 60_000, P)]
+    sizes[1] = 0
+    blocks = [rng.integers(0, n_total, n).astype(np.uint64) for n in sizes]
+    blocks[0][7] = n_total + 5                         # invalid rid at rank 0, row 7
+    outs = [torch.full((n, rec), 0x6B, dtype=torch.uint8, device="cuda") for n in sizes]
+    dpg.dpg_retrieve_dist_loopback(shards, n_total,
+                                   [torch.from_numpy(b.view(np.int64)).cuda() for b in blocks], outs)
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == 7
+    for r, (b, o) in enumerate(zip(blocks, outs)):
+        got = o.cpu().numpy()
+        ok = b < np.uint64(n_total)
+        assert np.array_equal(got[ok], oracle.retrieve(src, b[ok])), r
+        assert np.all(got[~ok] == 0x6B)

@@ -388,3 +388,64 @@ def test_btree_generator_descent_finds_every_key():
     assert all(rids[descend(k)] == i for i, k in enumerate(keys))
     absent = datagen.feistel(1 << 32, 5000, 300, 0x611).astype(np.uint32)
     assert all(descend(k) is None for k in absent)
+
+
+# --------------------------------------------------------------------------
+# 64-bit rids (config 5's global rids): oracle_retrieve_u64,
+# oracle_retrieve_at_u64 and the generated-source definition.
+# --------------------------------------------------------------------------
+def test_u64_retrieve_matches_numpy_indexing():
+    """D[i] = R[rid[i]] with uint64 rids against numpy fancy indexing (an
+    independent definition), every length <= 3 sequence over n <= 3 plus a
+    seeded large case."""
+    for n in range(1, 4):
+        src = _distinct_records(n, 5, seed=n)
+        for k in range(0, 4):
+            for seq in itertools.product(range(n), repeat=k):
+                rids = np.array(seq, dtype=np.uint64)
+                got = oracle.retrieve(src, rids)
+                assert np.array_equal(got, src[rids.astype(np.int64)] if k else np.zeros((0, 5), np.uint8))
+    rng = np.random.default_rng(9)
+    src = rng.integers(0, 256, size=(5000, 100), dtype=np.uint8)
+    rids = rng.integers(0, 5000, 20000).astype(np.uint64)
+    assert np.array_equal(oracle.retrieve(src, rids), src[rids.astype(np.int64)])
+    # the same bytes through the 32-bit entry (a different code path)
+    assert np.array_equal(oracle.retrieve(src, rids), oracle.retrieve(src, rids.astype(np.uint32)))
+
+
+def test_u64_rids_are_not_truncated():
+    """A rid >= 2^32 is out of range for a small source; a 32-bit truncation
+    would silently copy record rid mod 2^32 instead."""
+    src = _distinct_records(10, 8)
+    rids = np.array([1, 2, (1 << 32) + 3, 4, (1 << 33) + 1], dtype=np.uint64)
+    with pytest.raises(oracle.RidRangeError) as e:
+        oracle.retrieve(src, rids)
+    assert e.value.index == 2
+    with pytest.raises(oracle.RidRangeError):
+        oracle.retrieve_at(src, rids, np.array([2], dtype=np.uint64))
+    assert np.array_equal(oracle.retrieve_at(src, rids, np.array([0, 3], dtype=np.uint64)),
+                          src[[1, 4]])
+
+
+def test_u64_retrieve_at_samples_the_definition():
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, 256, size=(3000, 12), dtype=np.uint8)
+    rids = rng.integers(0, 3000, 7000).astype(np.uint64)
+    idx = np.unique(rng.integers(0, 7000, 500)).astype(np.uint64)
+    full = src[rids.astype(np.int64)]
+    assert np.array_equal(oracle.retrieve_at(src, rids, idx), full[idx.astype(np.int64)])
+    assert np.array_equal(oracle.retrieve_at(src, rids.astype(np.uint32), idx),
+                          full[idx.astype(np.int64)])
+
+
+def test_retrieve_generated_matches_materialised_source():
+    """The generated-source definition (config 5's records made pointwise at
+    their byte offsets) equals the retrieval from the materialised stream."""
+    n, rec, sid = 4096, 100, datagen.STREAMS[("c5", "src")]
+    src = datagen.records(n, rec, sid)
+    rids = datagen.feistel(n, 0, n, datagen.STREAMS[("c5", "rids")])[:300]
+    rids = np.concatenate([rids, rids[:7]])                 # repeats
+    assert np.array_equal(oracle.retrieve_generated(rec, n, sid, rids), src[rids.astype(np.int64)])
+    with pytest.raises(oracle.RidRangeError) as e:
+        oracle.retrieve_generated(rec, n, sid, np.array([5, n, 1], dtype=np.uint64))
+    assert e.value.index == 1
