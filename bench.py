@@ -2,109 +2,116 @@
 """Benchmark of the DPG record-retrieval hot path on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dpg|reference]
-                    [--config c2] [--rec R]
+                    [--config c2|c1|c2L|c3a|c3b|c4|c4x|c5|h1] [--rec R]
 
-One step = one pass of the whole hot path (plan,
-distribute, fused probe+gather) over one batch of synthetic input already
-resident in HBM: dpg_retrieve on BASELINE.json configs[1] (Datamation-shaped
-sort phase 3, 1,048,576 x 100-byte records, rids = stable argsort of the
-10-byte keys).  L2 is flushed (a 512 MiB write, then a 512 MiB read, so no
-dirty flush line is left for the step to write back) before every timed step and
-each step is timed alone with CUDA events on the launching stream; flush time
-is excluded.  Multi-process (torchrun, N > 1): BASELINE.json config 5 --
-2^30 x 100-byte records range-partitioned over the ranks, rids a global
-permutation block-partitioned by output position -- through the multi-GPU
-path (owner partition, NCCL all-to-alls, local DPG, reply scatter); job time
-= max over ranks of the CUDA-event time.
+N = 1 (default): one step = one dpg_retrieve call (the whole hot path: plan,
+distribute, probe, gather) over BASELINE.json configs[1] --
+Datamation-shaped sort phase 3, 1,048,576 x 100-byte records, rids = stable
+argsort of the 10-byte keys -- with src and rids resident in HBM.  Before
+every timed step L2 is flushed (a 512 MiB write, then a 512 MiB read, so no
+dirty line of the flush is left for the step); after it, a second 512 MiB read
+makes the L2 write back the step's own dirty output, and that write-back time
+(measured against the same read after a clean L2) is added to the step.  The
+line nests the same protocol on the other configurations (the record-size
+sweep, the 2L row, the join, the single-GPU config-5 shard) with the direct
+comparisons, so one run shows where DPG wins and where it does not.
 
-The JSON line adds: roofline of the dominant kernel (k_dpg_fused) from its
-own CUDA-event time inside the same timed steps, the naive direct-gather
-comparison timed the same way, the end-to-end number through the host-buffer
-C-ABI entry, the oracle's CPU throughput (cpu_baseline) and the SM clocks
-sampled during the timed region.
+N > 1: the driver launches this under torchrun (or, given --gpus N without
+torchrun, it relaunches itself so); one step = the multi-GPU retrieval of
+BASELINE.json configs[4] -- 2^30 x 100-byte records range-partitioned over
+the ranks, rids a Feistel permutation (uint64) block-partitioned by output
+position -- through the native C ABI (dpg_retrieve_dist: owner partition, NCCL
+count all-gather and request send/recv, the owner's DPG writing replies into
+the requesters' IPC windows over NVLink, Phase III); job time = max over ranks
+of the CUDA-event time.
+
+Every line carries the roofline of the dominant kernel (its own CUDA-event time
+on the launching stream, from the library's phase events), the oracle's CPU
+throughput (1 core and all cores), the end-to-end number through the
+host-buffer C-ABI path and the SM clocks sampled during the timed region.
 """
 from __future__ import annotations
 
 import argparse
-
-import numpy as np
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "record-retrieval effective GB/s vs HBM peak; records/s at 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
+NVLINK_GBS = 900.0            # per GPU per direction (NVLink 5 via NVSwitch)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dpg", choices=["dpg", "reference"])
-    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3a", "c3b", "c4", "c4x", "c5", "h1"],
+    ap.add_argument("--config", default=None,
+                    choices=["c1", "c2", "c2L", "c3a", "c3b", "c4", "c4x", "c5", "h1"],
                     help="default: c2 on one GPU, c5 (multi-GPU exchange) under torchrun")
     ap.add_argument("--c5-log2", type=int, default=30, help="c5 total records = 2^c5_log2")
-    ap.add_argument("--c5-round-rows", type=int, default=1 << 27,
-                    help="c5 rows per exchange round (bounds the windows: 13.4 GB per rank)")
-    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
-                    help="c5: replies written into the requesters' windows over NVLink "
-                         "(fused) or returned by an NCCL all-to-all")
+    ap.add_argument("--c5-rows", type=int, default=1 << 27,
+                    help="c5 rows per rank per exchange call (bounds the windows: 13.4 GB)")
     ap.add_argument("--rec", type=int, default=None, help="record bytes for c3a/c3b")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-sort", action="store_true", help="skip the end-to-end DPG sort timing (c2)")
+    ap.add_argument("--no-extras", action="store_true", help="N=1: only the headline config")
+    ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c4,c5shard",
+                    help="N=1: nested configurations")
     a = ap.parse_args()
     if a.config is None:
-        a.config = "c5" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "c2"
+        a.config = "c5" if int(os.environ.get("WORLD_SIZE", "1")) > 1 or a.gpus > 1 else "c2"
     return a
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def workload_name(cfg: str, rec: int | None) -> str:
-    return {"c1": "c1: 65,536 x 100 B random records, uniform random permutation",
-            "c2": "c2: Datamation sort phase 3, 1,048,576 x 100 B, rids = stable argsort of 10-B keys",
-            "c3a": f"c3a: 16,777,216 x {rec} B, uniform random permutation",
-            "c3b": f"c3b: 16,777,216 x {rec} B, uniform rids with replacement",
-            "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)",
-            "c4x": "c4x: config 4 with the paper's exponential join keys (P:890-892)",
-            "c5": "c5 sample for the host oracle: 2^22 x 100 B of the c5 source stream, "
-                  "rids = c5 Feistel permutation of [0, 2^22)"}[cfg]
+def relaunch_under_torchrun(args) -> int | None:
+    """--gpus N > 1 outside torchrun: start N ranks of this script (one per GPU)
+    via torch.distributed.run on 127.0.0.1 and return its exit code; fail loudly
+    when fewer than N GPUs are visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but {n} GPU(s) visible",
+                          "n_gpus": args.gpus}), flush=True)
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {n} visible\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
-def make_inputs(cfg: str, rec: int | None):
-    import datagen
-    if cfg in ("c3a", "c3b"):
-        return datagen.make(cfg, rec=rec or 64)
-    return datagen.make(cfg)
-
-
-def units(cfg, w):
-    """(n_out, rec, algorithmic bytes per step, rid bytes) per SURVEY 8(d):
-    B = N * (2 * rec + rid_bytes)."""
-    if cfg in ("c4", "c4x"):
-        n_out = w["fk"].size
-        rec = w["dim"].shape[1] + w["fact"].shape[1]          # 80-byte output rows
-        # join rows: read fk (4) + fact payload (16) + dim record (64), write 80
-        return n_out, rec, n_out * (4 + 16 + 64 + 80), 4
-    n_out = w["rids"].size
-    rec = w["src"].shape[1]
-    return n_out, rec, n_out * (2 * rec + 4), 4
-
-
+# ---------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------
 class ClockSampler:
     """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    NAMES = {"applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+             "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+             "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
 
     def __init__(self, index: int):
         self.samples, self.reasons = [], set()
@@ -123,18 +130,12 @@ class ClockSampler:
 
     def _run(self):
         nv = self.nv
-        names = {
-            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
-            "display_clock_setting": 0x100,
-        }
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit and k != "gpu_idle":
+                for k, bit in self.NAMES.items():
+                    if r & bit:
                         self.reasons.add(k)
             except Exception:
                 pass
@@ -161,46 +162,20 @@ class ClockSampler:
 
 
 def hbm_peak():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
-            v = float(json.load(f)["hbm_gbs"])
-        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def committed_traffic(cfg):
-    """dram bytes per probe-gather launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def committed_traffic(key):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
     try:
-        with open(p) as f:
-            return json.load(f).get(cfg)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
     except Exception:
         return None
-
-
-def cpu_baseline(cfg, w, budget_s=10.0):
-    """The oracle as it stands (single-threaded C loop, oracle/oracle.c) on this
-    host, repeated over the full workload until ~budget_s of CPU work."""
-    import oracle
-    n_out, rec, alg_bytes, _ = units(cfg, w)
-    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg in ("c4", "c4x") else \
-        (lambda: oracle.retrieve(w["src"], w["rids"]))
-    fn()  # warm (page in)
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        fn()
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or (reps >= 3 and el > budget_s / 2):
-            break
-    t = el / reps
-    return {"value": alg_bytes / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "records_per_s": n_out / t,
-            "sample": f"full {cfg} workload x {reps} repetitions ({el:.1f} s), "
-                      f"oracle.retrieve single-threaded C loop",
-            "host_cpu": host_cpu(), "host_threads": os.cpu_count()}
 
 
 def host_cpu():
@@ -214,16 +189,139 @@ def host_cpu():
     return None
 
 
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+class Steps:
+    """The timing protocol of SURVEY 8(d): L2 flushed before every timed step
+    (512 MiB write, then 512 MiB read), CUDA events on the launching stream,
+    and the step's own dirty-output write-back added (a 512 MiB read after the
+    step, minus the same read after a clean L2)."""
+
+    def __init__(self, torch, dev):
+        self.torch = torch
+        self.w = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.r2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.current_stream()
+        self.base = None
+
+    def flush(self):
+        self.w.fill_(1)
+        self.r.view(self.torch.int32).max()
+
+    def _read2(self):
+        self.r2.view(self.torch.int32).max()
+
+    def _ev(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def clean_read_ms(self, reps=5):
+        if self.base is None:
+            v = []
+            for _ in range(reps):
+                self.flush()
+                a, b = self._ev(), self._ev()
+                a.record(self.stream)
+                self._read2()
+                b.record(self.stream)
+                self.torch.cuda.synchronize()
+                v.append(a.elapsed_time(b))
+            self.base = sorted(v)[len(v) // 2]
+        return self.base
+
+    def run(self, fn, steps, launches=None, phase_lib=None):
+        """-> (per-step ms incl. write-back, per-step kernel-only ms, write-back ms,
+        launches, phase times (I, II, III) per step or None)."""
+        torch = self.torch
+        base = self.clean_read_ms()
+        evs = [(self._ev(), self._ev(), self._ev()) for _ in range(steps)]
+        if phase_lib is not None:
+            phase_lib.dpg_phase_times_ex()
+            phase_lib.dpg_phase_timing(True)
+        nl = 0
+        for e0, e1, e2 in evs:
+            self.flush()
+            e0.record(self.stream)
+            fn()
+            e1.record(self.stream)
+            self._read2()
+            e2.record(self.stream)
+            if launches is not None:
+                nl += launches()
+        torch.cuda.synchronize()
+        ph = None
+        if phase_lib is not None:
+            phase_lib.dpg_phase_timing(False)
+            a, b, c, calls = phase_lib.dpg_phase_times_ex()
+            ph = (a / max(1, calls), b / max(1, calls), c / max(1, calls))
+        step = [x.elapsed_time(y) for x, y, _ in evs]
+        wb = [max(0.0, y.elapsed_time(z) - base) for _, y, z in evs]
+        tot = [s + w for s, w in zip(step, wb)]
+        return tot, step, wb, nl, ph
+
+
+def med(v):
+    v = sorted(v)
+    return v[len(v) // 2]
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle on the host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(src, rids, alg_bytes_per_row, budget_s=8.0, sample=None, fk_join=None):
+    """The oracle as it stands (single-threaded C loop) and the same loop split
+    over all host cores (oracle_retrieve_threads), each repeated until
+    ~budget_s of CPU work on the given (bounded) sample."""
+    import oracle
+    threads = host_threads()
+    res = {}
+    for label, fn in (("single", (lambda: oracle.retrieve(src, rids)) if fk_join is None else
+                       (lambda: oracle.fk_join(*fk_join))),
+                      ("all", (lambda: oracle.retrieve_threads(src, rids, threads))
+                       if fk_join is None else None)):
+        if fn is None:
+            continue
+        fn()
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            fn()
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s / 2 or (reps >= 3 and el > budget_s / 4):
+                break
+        res[label] = el / reps
+    n = (fk_join[1].size if fk_join is not None else rids.size)
+    one = res["single"]
+    out = {"value": n * alg_bytes_per_row / one / 1e9, "unit": "GB/s", "cores": 1,
+           "kind": "oracle", "records_per_s": n / one,
+           "sample": sample or f"{n} rows, oracle single-threaded C loop",
+           "host_cpu": host_cpu(), "host_threads": threads}
+    if "all" in res:
+        out["all_cores"] = {"value": n * alg_bytes_per_row / res["all"] / 1e9, "unit": "GB/s",
+                            "cores": threads, "records_per_s": n / res["all"],
+                            "what": "oracle_retrieve_threads: the same loop over contiguous "
+                                    "index ranges, one thread each"}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle on the host cores (this tier has no reference code)
+# ---------------------------------------------------------------------------
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    import datagen
+    import oracle
     cfg = args.config
     if cfg == "h1":
-        import datagen
-        import oracle
         w = datagen.hash_workload(1 << 24, 24, 1 << 26)
-        q = w["queries"][: 1 << 24]              # bounded sample: a quarter of the queries
+        q = w["queries"][: 1 << 24]
         times = []
         for _ in range(max(1, args.steps)):
             t0 = time.perf_counter()
@@ -232,33 +330,35 @@ def run_reference(args):
             if sum(times) > 120:
                 break
         t = sum(times) / len(times)
-        value = q.size / t
+        v = q.size / t
         print(json.dumps({
-            "impl": "reference", "metric": "batch index lookups/s (hash index, DPG)", "value": value,
+            "impl": "reference", "metric": "batch index lookups/s (hash index, DPG)", "value": v,
             "unit": "lookups/s", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic (datagen.hash_workload, seed 0)",
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (datagen.hash_workload, seed 0)",
             "config": {"workload": "h1 sample: 2^24 of the 2^26 queries"},
-            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": 1, "kind": "oracle",
-                             "sample": "2^24 queries, oracle.batch_lookup (sorted pairs + binary search)",
-                             "host_cpu": host_cpu()},
-            "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0,
+            "cpu_baseline": {"value": v, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+                             "sample": "2^24 queries, oracle.batch_lookup", "host_cpu": host_cpu()},
+            "e2e": {"value": v, "unit": "lookups/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}), flush=True)
         return 0
     if cfg == "c5":
-        # bounded sample of the c5 workload for the host oracle: 2^22 records
-        # of the c5 source stream, rids = the c5 Feistel permutation of [0, 2^22)
-        import datagen
+        # bounded sample of config 5 for the host oracle: 2^22 records of the
+        # c5 source stream, rids = the c5 Feistel permutation of [0, 2^22)
         n = 1 << 22
-        w = {"src": datagen.records(n, 100, datagen.STREAMS[("c5", "src")]),
-             "rids": datagen.feistel(n, 0, n, datagen.STREAMS[("c5", "rids")]).astype(np.uint32)}
-        cfg = "c2"     # same shape of work (100-byte records, 4-byte rids) for units()
+        src = datagen.records(n, 100, datagen.STREAMS[("c5", "src")])
+        rids = datagen.feistel(n, 0, n, datagen.STREAMS[("c5", "rids")])
+        fn = lambda: oracle.retrieve(src, rids)
+        n_out, per_row, sample = n, 2 * 100 + 8, "2^22 x 100 B sample of the c5 stream, 64-bit rids"
     else:
         w = make_inputs(cfg, args.rec)
-    import oracle
-    n_out, rec, alg_bytes, _ = units(cfg, w)
-    fn = (lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])) if cfg in ("c4", "c4x") else \
-        (lambda: oracle.retrieve(w["src"], w["rids"]))
+        if cfg in ("c4", "c4x"):
+            fn = lambda: oracle.fk_join(w["fact"], w["fk"], w["dim"])
+            n_out, per_row = w["fk"].size, 4 + 16 + 64 + 80
+        else:
+            fn = lambda: oracle.retrieve(w["src"], w["rids"])
+            n_out, per_row = w["rids"].size, 2 * w["src"].shape[1] + 4
+        sample = f"full {cfg} workload"
     for _ in range(max(0, min(args.warmup, 3))):
         fn()
     times = []
@@ -266,91 +366,425 @@ def run_reference(args):
         t0 = time.perf_counter()
         fn()
         times.append(time.perf_counter() - t0)
-        if sum(times) > 120:
+        if sum(times) > 150:
             break
     t = sum(times) / len(times)
-    value = alg_bytes / t / 1e9
-    line = {
+    value = n_out * per_row / t / 1e9
+    print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (datagen, seed 0)",
-        "config": {"workload": workload_name(args.config, args.rec), "n_out": n_out, "rec_bytes": rec},
+        "config": {"workload": workload_name(cfg, args.rec), "n_out": int(n_out)},
         "records_per_s": n_out / t,
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"full {cfg} workload, {len(times)} steps",
-                         "host_cpu": host_cpu()},
+                         "sample": f"{sample}, {len(times)} steps", "host_cpu": host_cpu()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def workload_name(cfg: str, rec: int | None) -> str:
+    return {"c1": "c1: 65,536 x 100 B random records, uniform random permutation",
+            "c2": "c2: Datamation sort phase 3, 1,048,576 x 100 B, rids = stable argsort of 10-B keys",
+            "c2L": "2L: 16,777,216 x 100 B, uniform random permutation (SURVEY 8(d))",
+            "c3a": f"c3a: 16,777,216 x {rec} B, uniform random permutation",
+            "c3b": f"c3b: 16,777,216 x {rec} B, uniform rids with replacement",
+            "c4": "c4: DPG-Move FK join, dim 16,777,216 x 64 B, fact 67,108,864 x (fk + 16 B)",
+            "c4x": "c4x: config 4 with the paper's exponential join keys (P:890-892)",
+            "c5": "c5: 2^30 x 100 B range-partitioned, rids = Feistel permutation (uint64) "
+                  "block-partitioned"}.get(cfg, cfg)
+
+
+def make_inputs(cfg: str, rec: int | None):
+    import datagen
+    if cfg in ("c3a", "c3b"):
+        return datagen.make(cfg, rec=rec or 64)
+    return datagen.make(cfg)
+
+
+# ---------------------------------------------------------------------------
+# N = 1
+# ---------------------------------------------------------------------------
+def measure_retrieval(torch, dpg, steps_obj, src, rids, steps, warmup, with_cmp=True):
+    """DPG (the automatic plan) and the direct comparisons on resident inputs."""
+    n_out, rec = rids.numel(), src.shape[1]
+    alg = n_out * (2 * rec + 4)
+    out = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
+    fns = {"dpg": lambda: dpg.dpg_retrieve(src, rids, dst=out)}
+    if with_cmp:
+        fns["naive"] = lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)
+        fns["direct_windowed"] = lambda: dpg.dpg_retrieve_direct_ex(src, rids, dst=out, hint=3)
+    for _ in range(max(3, warmup)):
+        for f in fns.values():
+            f()
+    torch.cuda.synchronize()
+    dpg.dpg_sync_status()
+    fns["dpg"]()
+    path = dpg.last_path()
+    res = {}
+    for k, f in fns.items():
+        tot, step, wb, nl, ph = steps_obj.run(f, steps, launches=dpg.last_launch_count,
+                                              phase_lib=dpg if k == "dpg" else None)
+        res[k] = {"ms": med(tot), "ms_kernels": med(step), "ms_writeback": med(wb),
+                  "value": alg / (med(tot) * 1e-3) / 1e9, "unit": "GB/s",
+                  "launches_per_step": nl / steps, "all_ms": tot, "phases_ms": ph}
+    res["dpg"]["plan_path"] = path
+    return res, out, alg
+
+
+def roofline_for(dpg, plan_path, res_dpg, n_src, n_out, rec, pay, peak, peak_src, traffic_key):
+    """The dominant kernel of the plan the call ran, its algorithmic bytes per
+    launch over its own CUDA-event time."""
+    ph = res_dpg["phases_ms"] or (0.0, res_dpg["ms_kernels"], 0.0)
+    if plan_path == 6:
+        # three kernels: Phase I (distribute + transpose), II (probe), III (gather)
+        per = {"k3_distribute (Phase I)": (ph[0], n_out * (4 + 2 + 2)),
+               "k3_probe (Phase II)": (ph[1], n_src * rec + n_out * (2 + rec)),
+               "k3_gather (Phase III)": (ph[2], n_out * (2 + 2 * rec + pay))}
+    elif plan_path == 3:
+        per = {"k_dpg_l2run": (ph[1], n_out * (2 * rec + 4))}
+    elif plan_path == 1:
+        per = {"k_dpg_fused": (ph[1] + ph[0], n_out * (2 * rec + 4))}
+    else:
+        per = {f"path {plan_path} probe-gather": (ph[1], n_src * rec + n_out * (rec + 8))}
+    kernel = max(per, key=lambda k: per[k][0])
+    ms, by = per[kernel]
+    achieved = by / (ms * 1e-3) / 1e9 if ms > 0 else None
+    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": committed_traffic(traffic_key),
+            "peak_source": peak_src, "alg_bytes_per_launch": by, "launch_ms": ms,
+            "share_of_step": ms / res_dpg["ms_kernels"] if res_dpg["ms_kernels"] else None,
+            "phases_ms": ph,
+            "kernels": {k: {"ms": v[0], "alg_bytes": v[1],
+                            "frac": (v[1] / (v[0] * 1e-3) / 1e9 / peak) if v[0] > 0 else None}
+                        for k, v in per.items()}}
+
+
+def sampled_ok(out, want_fn, n, k=4096, seed=0):
+    idx = np.unique(np.random.default_rng(seed).integers(0, n, k))
+    import torch
+    got = out[torch.from_numpy(idx.astype(np.int64)).to(out.device)].cpu().numpy()
+    return bool(np.array_equal(got, want_fn(idx)))
+
+
+def run_single(args):
+    import torch
+    torch.cuda.set_device(0)
+    import datagen
+    import oracle
+    import paper_cs_0308004_b200 as dpg
+    dev = torch.device("cuda", 0)
+    peak, peak_src = hbm_peak()
+    steps_obj = Steps(torch, dev)
+
+    def to_dev(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype == np.uint32:
+            a = a.view(np.int32)
+        return torch.from_numpy(a).to(dev)
+
+    cfg = args.config
+    if cfg in ("c4", "c4x"):
+        return run_join_line(args, torch, dpg, steps_obj, cfg)
+    w = make_inputs(cfg, args.rec)
+    src, rids = to_dev(w["src"]), to_dev(w["rids"])
+    n_out, rec = w["rids"].size, w["src"].shape[1]
+    n_src = w["src"].shape[0]
+    with ClockSampler(0) as clk:
+        res, out, alg = measure_retrieval(torch, dpg, steps_obj, src, rids, args.steps, args.warmup)
+    dpg.dpg_sync_status()
+    ok = sampled_ok(out, lambda i: oracle.retrieve_at(w["src"], w["rids"], i.astype(np.uint64)), n_out)
+    d = res["dpg"]
+    roofline = roofline_for(dpg, d["plan_path"], d, n_src, n_out, rec, 0, peak, peak_src, cfg)
+
+    # the paper's application of the path (section 3): the whole Datamation sort
+    sort_res = None
+    if cfg == "c2":
+        for _ in range(2):
+            dpg.dpg_sort(src, 0, 10, dst=out)
+        torch.cuda.synchronize()
+        srt_ok = sampled_ok(out, lambda i: oracle.retrieve_at(w["src"], w["rids"],
+                                                               i.astype(np.uint64)), n_out, seed=1)
+        tot, step, wb, nl, _ = steps_obj.run(lambda: dpg.dpg_sort(src, 0, 10, dst=out),
+                                             max(3, args.steps // 2), launches=dpg.last_launch_count)
+        sort_res = {"ms_per_sort": med(tot), "records_per_s": n_out / (med(tot) * 1e-3),
+                    "launches_per_sort": nl / max(3, args.steps // 2), "parity_sampled_ok": srt_ok,
+                    "what": "dpg_sort: 10-byte keys at offset 0, stable LSD radix sort + dpg_retrieve"}
+
+    # end to end through the host-buffer C-ABI entry (PCIe copies inside)
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.from_numpy(w["src"]).pin_memory()
+        hr = torch.from_numpy(w["rids"].view(np.int32)).pin_memory()
+        hd = torch.empty((n_out, rec), dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            dpg.dpg_retrieve_host(hs, hr, hd)
+        k = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            dpg.dpg_retrieve_host(hs, hr, hd)
+        el = (time.perf_counter() - t0) / k
+        e2e = {"value": alg / el / 1e9, "unit": "GB/s", "ms_per_step": el * 1e3,
+               "h2d_bytes_per_step": int(w["src"].nbytes + w["rids"].nbytes),
+               "d2h_bytes_per_step": int(n_out * rec), "entry": "dpg_retrieve_host",
+               "parity_sampled_ok": bool(np.array_equal(hd[:2000].numpy(),
+                                                        oracle.retrieve(w["src"], w["rids"][:2000])))}
+        dpg.dpg_release_cache()
+
+    cpu = None if args.no_cpu else cpu_baseline(
+        w["src"], w["rids"], 2 * rec + 4, sample=f"full {cfg} workload")
+
+    extras = {}
+    if not args.no_extras and cfg == "c2":
+        for name in [x for x in args.extras.split(",") if x]:
+            try:
+                extras[name] = run_extra(name, args, torch, dpg, steps_obj, peak)
+            except Exception as e:  # noqa: BLE001 -- a failed extra is reported, not fatal
+                extras[name] = {"error": repr(e)}
+            torch.cuda.empty_cache()
+
+    line = {
+        "metric": METRIC, "value": d["value"], "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": d["ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (datagen, seed 0)",
+        "config": {"workload": workload_name(cfg, args.rec), "n_src": n_src, "n_out": n_out,
+                   "rec_bytes": rec, "rid_bytes": 4, "alg_bytes_per_step": alg,
+                   "alg_bytes_formula": "N * (2 * rec + rid_bytes)",
+                   "l2": "flushed before every step (512 MiB write, then 512 MiB read); the step's "
+                         "dirty-output write-back is measured after it and included",
+                   "parallelism": "single", "plan_path": d["plan_path"]},
+        "records_per_s": n_out / (d["ms"] * 1e-3),
+        "frac_of_hbm_peak": d["value"] / peak,
+        "ms_kernels": d["ms_kernels"], "ms_writeback": d["ms_writeback"],
+        "ms_min": min(d["all_ms"]), "ms_median": med(d["all_ms"]),
+        "roofline": roofline,
+        "naive": {k: v for k, v in res["naive"].items() if k not in ("all_ms", "phases_ms")},
+        "direct_windowed": {k: v for k, v in res["direct_windowed"].items()
+                            if k not in ("all_ms", "phases_ms")},
+        "parity_sampled_ok": ok, "dpg_sort": sort_res, "e2e": e2e, "cpu_baseline": cpu,
+        "configs": extras, "clocks": clk.summary(),
+        "gpu_launches": int(round(d["launches_per_step"] * args.steps)),
+        "gpu": torch.cuda.get_device_name(dev),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_c5(args, rank, world):
-    """BASELINE.json config 5: 2^30 x 100-byte records range-partitioned over the
-    ranks, rids = a Feistel permutation of [0, 2^30) block-partitioned by output
-    position; the multi-GPU path (paper_cs_0308004_b200/dist.py): owner
-    partition, NCCL all-to-alls, local DPG, reply scatter.  Inputs are
-    generated on each GPU by the counter-based generators (datagen)."""
-    import numpy as np
+def run_extra(name, args, torch, dpg, steps_obj, peak):
+    """One nested configuration: DPG (automatic plan) vs the direct gather (and
+    the three sequential passes where they apply), inputs generated on the
+    device from the same counter-based streams, sampled parity against the
+    oracle's definition for a generated source."""
+    import datagen
+    import oracle
+    steps = max(3, min(args.steps, 8))
+    if name == "c4":
+        return run_join_extra(args, torch, dpg, steps_obj, peak, steps)
+    if name == "c5shard":
+        return run_c5_shard(args, torch, dpg, steps_obj, peak, steps)
+    if name == "c2L":
+        rec, kind = 100, "c3a"
+    else:
+        kind, rec = name[:3], int(name[3:])
+    n = 1 << 24
+    sid = datagen.STREAMS[("c3", "src")]
+    src = torch.empty((n, rec), dtype=torch.uint8, device="cuda")
+    datagen.random_bytes_cuda(src.view(-1), sid)
+    rids_h = datagen.permutation(n, datagen.STREAMS[("c3a", "rids")]) if kind == "c3a" else \
+        datagen.uniform(n, n, datagen.STREAMS[("c3b", "rids")])
+    rids = torch.from_numpy(rids_h.view(np.int32)).cuda()
+    res, out, alg = measure_retrieval(torch, dpg, steps_obj, src, rids, steps, args.warmup)
+    dpg.dpg_sync_status()
+    idx_fn = lambda i: oracle.retrieve_generated(rec, n, sid, rids_h[i].astype(np.uint64))
+    ok = sampled_ok(out, idx_fn, n, k=512)
+    d = res["dpg"]
+    r = {"workload": workload_name("c2L" if name == "c2L" else kind, rec), "plan_path": d["plan_path"],
+         "value": d["value"], "frac_of_hbm_peak": d["value"] / peak, "ms": d["ms"],
+         "ms_kernels": d["ms_kernels"], "phases_ms": d["phases_ms"],
+         "naive": {"value": res["naive"]["value"], "ms": res["naive"]["ms"]},
+         "direct_windowed": {"value": res["direct_windowed"]["value"],
+                             "ms": res["direct_windowed"]["ms"]},
+         "dpg_over_naive": res["naive"]["ms"] / d["ms"], "parity_sampled_ok": ok,
+         "roofline": roofline_for(dpg, d["plan_path"], d, n, n, rec, 0, peak, "", name)}
+    del out, src, rids
+    return r
+
+
+def run_join_line(args, torch, dpg, steps_obj, cfg):
+    """--config c4 / c4x as the main line (N = 1)."""
+    peak, peak_src = hbm_peak()
+    with ClockSampler(0) as clk:
+        r = run_join_extra(args, torch, dpg, steps_obj, peak, args.steps, cfg=cfg, full=True)
+    r.update({"metric": METRIC, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+              "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+              "data": "synthetic (datagen, seed 0)", "clocks": clk.summary(),
+              "unit": "GB/s", "ms_per_step": r["ms"]})
+    r["config"] = {"workload": workload_name(cfg, None), "alg_bytes_per_row": 164,
+                   "plan_path": r.pop("plan_path")}
+    r["e2e"] = None
+    print(json.dumps(r), flush=True)
+    return 0
+
+
+def run_join_extra(args, torch, dpg, steps_obj, peak, steps, cfg="c4", full=False):
+    import datagen
+    import oracle
+    w = datagen.make(cfg)
+    fact = torch.from_numpy(w["fact"]).cuda()
+    fk = torch.from_numpy(w["fk"].view(np.int32)).cuda()
+    dim = torch.from_numpy(w["dim"]).cuda()
+    n = w["fk"].size
+    alg = n * (4 + 16 + 64 + 80)       # fk + fact payload + dim record read, 80-B row written
+    out = torch.empty((n, 80), dtype=torch.uint8, device="cuda")
+    fns = {"dpg": lambda: dpg.dpg_fk_join(fact, fk, dim, out=out),
+           "direct": lambda: dpg.dpg_fk_join_direct(fact, fk, dim, out=out),
+           "dpg_seq3": lambda: dpg.dpg_fk_join(fact, fk, dim, out=out, path=6),
+           "dpg_sort_join": lambda: dpg.dpg_fk_join_sort(fact, fk, dim, out=out)}
+    res = {}
+    for k, f in fns.items():
+        for _ in range(2):
+            f()
+        torch.cuda.synchronize()
+        path = dpg.last_path()
+        tot, step, wb, nl, ph = steps_obj.run(f, steps, launches=dpg.last_launch_count,
+                                              phase_lib=dpg if k.startswith("dpg") else None)
+        if k != "dpg_sort_join":
+            okk = sampled_ok(out, lambda i: oracle.fk_join(w["fact"][i], w["fk"][i], w["dim"]), n,
+                             k=4096, seed=3)
+        else:
+            okk = None
+        res[k] = {"ms": med(tot), "value": alg / (med(tot) * 1e-3) / 1e9, "unit": "GB/s",
+                  "phases_ms": ph, "plan_path": path if k.startswith("dpg") else None,
+                  "launches_per_step": nl / steps, "parity_sampled_ok": okk}
+    dpg.dpg_sync_status()
+    d = res["dpg"]
+    r = {"workload": workload_name(cfg, None), "plan_path": d["plan_path"], "value": d["value"],
+         "frac_of_hbm_peak": d["value"] / peak, "ms": d["ms"], "phases_ms": d["phases_ms"],
+         "direct": res["direct"], "dpg_seq3": res["dpg_seq3"], "dpg_sort_join": res["dpg_sort_join"],
+         "dpg_over_direct": res["direct"]["ms"] / d["ms"],
+         "parity_sampled_ok": d["parity_sampled_ok"],
+         "alg_bytes_formula": "N_fact * (4 + 16 + 64 + 80)"}
+    del out, fact, fk, dim
+    return r
+
+
+def run_c5_shard(args, torch, dpg, steps_obj, peak, steps):
+    """Config 5's per-GPU shard on one GPU (2^27 x 100 B, P = 1 through the
+    native exchange) and the same exchange for virtual ranks (P = 2, 4, 8 on
+    this GPU, dpg_retrieve_dist_loopback, 2^26 records): the single-GPU cost of
+    the multi-GPU path (no NVLink involved)."""
+    import datagen
+    import oracle
+    rec = 100
+    out = {}
+    n = 1 << 27
+    sid_s, sid_r = datagen.STREAMS[("c5", "src")], datagen.STREAMS[("c5", "rids")]
+    src = torch.empty((n, rec), dtype=torch.uint8, device="cuda")
+    datagen.random_bytes_cuda(src.view(-1), sid_s)
+    rids = datagen.feistel_cuda(n, 0, n, sid_r)
+    comm = dpg.dpg_comm_create(dpg.dpg_get_unique_id(), 1, 0)
+    try:
+        dst = torch.empty((n, rec), dtype=torch.uint8, device="cuda")
+        f = lambda: dpg.dpg_retrieve_dist(comm, src, n, rids, dst)
+        f()
+        torch.cuda.synchronize()
+        idx = np.unique(np.random.default_rng(5).integers(0, n, 256))
+        rh = rids[torch.from_numpy(idx).cuda()].cpu().numpy().astype(np.uint64)
+        ok = bool(np.array_equal(dst[torch.from_numpy(idx).cuda()].cpu().numpy(),
+                                 oracle.retrieve_generated(rec, n, sid_s, rh)))
+        tot, _, _, nl, _ = steps_obj.run(f, max(2, steps // 2), launches=dpg.last_launch_count)
+        out["P1_native"] = {"n_total": n, "ms": med(tot),
+                            "value": n * (2 * rec + 8) / (med(tot) * 1e-3) / 1e9, "unit": "GB/s",
+                            "parity_sampled_ok": ok}
+        del dst
+    finally:
+        dpg.dpg_comm_destroy(comm)
+    del src, rids
+    torch.cuda.empty_cache()
+    n = 1 << 26
+    src_all = torch.empty((n, rec), dtype=torch.uint8, device="cuda")
+    datagen.random_bytes_cuda(src_all.view(-1), sid_s)
+    rids_all = datagen.feistel_cuda(n, 0, n, sid_r)
+    for P in (2, 4, 8):
+        S = 1 << ((n + P - 1) // P - 1).bit_length()
+        shards = [src_all[r * S:min(n, (r + 1) * S)] for r in range(P)]
+        blocks = [rids_all[r * n // P:(r + 1) * n // P] for r in range(P)]
+        dsts = [torch.empty((b.numel(), rec), dtype=torch.uint8, device="cuda") for b in blocks]
+        f = lambda: dpg.dpg_retrieve_dist_loopback(shards, n, blocks, dsts)
+        f()
+        torch.cuda.synchronize()
+        b0 = blocks[1]
+        idx = np.unique(np.random.default_rng(P).integers(0, b0.numel(), 256))
+        rh = b0[torch.from_numpy(idx).cuda()].cpu().numpy().astype(np.uint64)
+        ok = bool(np.array_equal(dsts[1][torch.from_numpy(idx).cuda()].cpu().numpy(),
+                                 oracle.retrieve_generated(rec, n, sid_s, rh)))
+        tot, _, _, nl, _ = steps_obj.run(f, max(2, steps // 2), launches=dpg.last_launch_count)
+        out[f"P{P}_virtual"] = {"n_total": n, "ms": med(tot),
+                                "value": n * (2 * rec + 8) / (med(tot) * 1e-3) / 1e9,
+                                "unit": "GB/s", "parity_sampled_ok": ok,
+                                "what": "P virtual ranks on one GPU (loopback copies, no NVLink)"}
+        del dsts
+    return out
+
+
+# ---------------------------------------------------------------------------
+# N > 1: config 5 through the native multi-GPU C ABI
+# ---------------------------------------------------------------------------
+def run_c5(args, rank, world, local):
     import torch
     import torch.distributed as dist
-
     import datagen
-    from paper_cs_0308004_b200.dist import PeerWindows, owned_range, retrieve_dist
-    dev = torch.device("cuda", torch.cuda.current_device())
+    import oracle
+    import paper_cs_0308004_b200 as dpg
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
     rec = 100
     n_total = 1 << args.c5_log2
-    lo, hi = owned_range(rank, world, n_total)
-    src = torch.empty((hi - lo, rec), dtype=torch.uint8, device=dev)
-    datagen.random_bytes_cuda(src.view(-1), datagen.STREAMS[("c5", "src")], offset=lo * rec)
+    sid_s, sid_r = datagen.STREAMS[("c5", "src")], datagen.STREAMS[("c5", "rids")]
+    S = 1 << (max(1, -(-n_total // world)) - 1).bit_length()
+    lo, hi = min(n_total, rank * S), min(n_total, (rank + 1) * S)
+    src = torch.empty((max(1, hi - lo), rec), dtype=torch.uint8, device=dev)
+    if hi > lo:
+        datagen.random_bytes_cuda(src.view(-1), sid_s, offset=lo * rec)
     b0, b1 = rank * n_total // world, (rank + 1) * n_total // world
-    rids = datagen.feistel_cuda(n_total, b0, b1 - b0, datagen.STREAMS[("c5", "rids")])
-    torch.cuda.synchronize()
-
-    # fused exchange: one receive window per rank, mapped into every peer (CUDA
-    # IPC); if any rank cannot map its peers, every rank uses the NCCL replies
-    exchange, win = args.exchange, None
-    if exchange == "fused":
-        ok = 1
-        try:
-            win = PeerWindows(min(args.c5_round_rows, b1 - b0) * rec)
-        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
-            print(f"fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
-            ok = 0
-        flag = torch.tensor([ok], dtype=torch.int64, device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if not flag.item():
-            if win is not None:
-                win.close()
-            win, exchange = None, "nccl (fused windows unavailable)"
+    rids = datagen.feistel_cuda(n_total, b0, b1 - b0, sid_r)
+    dst = torch.empty((b1 - b0, rec), dtype=torch.uint8, device=dev)
+    # one NCCL unique id, made on rank 0 and broadcast
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(dpg.dpg_get_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    comm = dpg.dpg_comm_create(bytes(uid.cpu().numpy()), world, rank)
+    rows = args.c5_rows
+    # every rank makes the same number of calls (the exchange is collective)
+    ncall = max(1, -(-max((r + 1) * n_total // world - r * n_total // world for r in range(world)) // rows))
 
     def step():
-        return retrieve_dist(src, rids, n_total, max_rows_per_round=args.c5_round_rows,
-                             fused=win is not None, windows=win)
+        for k in range(ncall):
+            a = min(b1 - b0, k * rows)
+            e = min(b1 - b0, (k + 1) * rows)
+            dpg.dpg_retrieve_dist(comm, src if hi > lo else src[:0], n_total, rids[a:e], dst[a:e])
 
-    out = None
     for _ in range(max(1, min(args.warmup, 3))):
-        out = step()
+        step()
     torch.cuda.synchronize()
-    # sampled parity against the host generators (the definition, pointwise)
-    idx = np.random.default_rng(rank).integers(0, b1 - b0, 256)
-    got = out[torch.from_numpy(idx).to(dev)].cpu().numpy()
-    want_r = datagen.feistel(n_total, b0, b1 - b0, datagen.STREAMS[("c5", "rids")])[idx] \
-        if b1 - b0 <= (1 << 26) else np.array(
-            [datagen.feistel(n_total, b0 + int(j), 1, datagen.STREAMS[("c5", "rids")])[0] for j in idx])
-    want = np.stack([datagen.random_bytes(rec, datagen.STREAMS[("c5", "src")], offset=int(r) * rec)
-                     for r in want_r])
-    parity_ok = bool(np.array_equal(got, want))
-    del out
+    dpg.dpg_sync_status()
+    idx = np.unique(np.random.default_rng(rank).integers(0, b1 - b0, 256))
+    rh = rids[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.uint64)
+    parity_ok = bool(np.array_equal(dst[torch.from_numpy(idx).to(dev)].cpu().numpy(),
+                                    oracle.retrieve_generated(rec, n_total, sid_s, rh)))
     dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    launches = 0
+    with ClockSampler(local) as clk:
         ev0.record()
         for _ in range(args.steps):
-            out = step()
-            del out
+            step()
+            launches += dpg.last_launch_count()
         ev1.record()
         torch.cuda.synchronize()
     dist.barrier()
@@ -358,64 +792,106 @@ def run_c5(args, rank, world):
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    ok = torch.tensor([1 if parity_ok else 0], dtype=torch.int64, device=dev)
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    okt = torch.tensor([1 if parity_ok else 0], dtype=torch.int64, device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     alg = n_total * (2 * rec + 8)
     value = alg / (ms * 1e-3) / 1e9
-    # NCCL all-to-all bus bandwidth on equal 256 MiB per-rank buffers (SV 8(e))
-    busbw = None
-    if world > 1:
-        a2a_in = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-        a2a_out = torch.empty_like(a2a_in)
-        for _ in range(3):
-            dist.all_to_all_single(a2a_out, a2a_in)
-        torch.cuda.synchronize()
-        b0e, b1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0e.record()
-        for _ in range(10):
-            dist.all_to_all_single(a2a_out, a2a_in)
-        b1e.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([b0e.elapsed_time(b1e) / 10], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        busbw = (256 << 20) * (world - 1) / world / (float(t.item()) * 1e-3) / 1e9
-        del a2a_in, a2a_out
     peak, peak_src = hbm_peak()
-    nvl = (world - 1) / world * (n_total / world) * (rec + 4) / 900e9 * 1e3 if world > 1 else 0.0
+    # NVLink all-to-all roofline per GPU per direction: requests out (4 B) and
+    # replies (rec B) for the (P-1)/P of rows whose owner is another rank
+    nvl_bytes = (world - 1) / world * (n_total / world) * (rec + 4)
+    t_nvl = nvl_bytes / (NVLINK_GBS * 1e9) * 1e3
+    t_hbm = alg / world / (peak * 1e9) * 1e3
+    # NCCL all-to-all bus bandwidth on equal 256 MiB per-rank buffers (SV 8(e))
+    a2a_in = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    a2a_out = torch.empty_like(a2a_in)
+    for _ in range(3):
+        dist.all_to_all_single(a2a_out, a2a_in)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        dist.all_to_all_single(a2a_out, a2a_in)
+    e1.record()
+    torch.cuda.synchronize()
+    tb = torch.tensor([e0.elapsed_time(e1) / 10], dtype=torch.float64, device=dev)
+    dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+    busbw = (256 << 20) * (world - 1) / world / (float(tb.item()) * 1e-3) / 1e9
+    del a2a_in, a2a_out
+    # end to end through the same API: the step's rids from pinned host memory,
+    # the rows back to pinned host memory, chunk by chunk
+    e2e = None
+    if not args.no_e2e:
+        hr = rids.cpu().pin_memory()
+        hd = torch.empty((min(rows, b1 - b0), rec), dtype=torch.uint8).pin_memory()
+        rbuf = torch.empty(min(rows, b1 - b0), dtype=torch.int64, device=dev)
+
+        def step_e2e():
+            for k in range(ncall):
+                a = min(b1 - b0, k * rows)
+                e = min(b1 - b0, (k + 1) * rows)
+                rbuf[:e - a].copy_(hr[a:e], non_blocking=True)
+                dpg.dpg_retrieve_dist(comm, src if hi > lo else src[:0], n_total, rbuf[:e - a],
+                                      dst[:e - a])
+                hd[:e - a].copy_(dst[:e - a], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+
+        step_e2e()
+        dist.barrier()
+        k = max(1, min(3, args.steps))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            step_e2e()
+        el = (time.perf_counter() - t0) / k
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        e2e = {"value": alg / el / 1e9, "unit": "GB/s", "ms_per_step": el * 1e3,
+               "h2d_bytes_per_step": int(n_total * 8), "d2h_bytes_per_step": int(n_total * rec),
+               "entry": "dpg_retrieve_dist (rids H2D and rows D2H per call, pinned host buffers)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        n = 1 << 22
+        hs = datagen.records(n, rec, sid_s)
+        hrid = datagen.feistel(n, 0, n, sid_r).astype(np.uint32)
+        cpu = cpu_baseline(hs, hrid, 2 * rec + 8,
+                           sample="2^22 x 100 B of the c5 source stream, rids = the c5 Feistel "
+                                  "permutation of [0, 2^22)")
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (datagen on device, seed 0)",
-            "config": {"workload": f"c5: 2^{args.c5_log2} x 100 B range-partitioned, rids = Feistel "
-                                   "permutation (uint64) block-partitioned", "n_total": n_total,
-                       "rec_bytes": rec, "rid_bytes": 8, "parallelism": f"ep{world} (owner exchange)",
-                       "round_rows": args.c5_round_rows, "l2": "inputs >> L2",
-                       "exchange": exchange},
+            "config": {"workload": workload_name("c5", None) + f" (2^{args.c5_log2} records)",
+                       "n_total": n_total, "rec_bytes": rec, "rid_bytes": 8,
+                       "parallelism": f"ep{world} (range-partitioned source, owner exchange)",
+                       "rows_per_call": rows, "calls_per_step": ncall,
+                       "l2": "inputs >> L2", "exchange": "native C ABI dpg_retrieve_dist: NCCL "
+                       "counts + requests, owner DPG writes replies into peers' IPC windows"},
             "records_per_s": n_total / (ms * 1e-3),
-            "frac_of_hbm_peak_aggregate": value / (world * peak),
-            "nvlink_roofline_ms": nvl, "frac_of_nvlink_roofline": (nvl / ms) if nvl else None,
-            "nccl_alltoall_busbw_gbs": busbw,
-            "parity_sampled_ok": bool(ok.item()),
-            "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev)}), flush=True)
+            "roofline": {"bound": "nvlink" if t_nvl > t_hbm else "hbm", "unit": "GB/s",
+                         "hbm": {"achieved": value / world, "peak": peak,
+                                 "frac": value / world / peak, "peak_source": peak_src},
+                         "nvlink": {"roofline_ms": t_nvl, "bytes_per_gpu_per_direction": nvl_bytes,
+                                    "peak_gbs_per_direction": NVLINK_GBS,
+                                    "frac": t_nvl / ms if t_nvl else None},
+                         "achieved": value / world, "peak": peak, "frac": value / world / peak,
+                         "traffic": None},
+            "nccl_alltoall_busbw_gbs": busbw, "parity_sampled_ok": bool(okt.item()),
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": launches, "gpu": torch.cuda.get_device_name(dev)}), flush=True)
     dist.barrier()
-    if win is not None:
-        torch.cuda.synchronize()
-        dist.barrier()
-        win.close()
+    torch.cuda.synchronize()
+    dpg.dpg_comm_destroy(comm)
     dist.destroy_process_group()
     return 0
 
 
 def run_h1(args):
-    """Batch lookup in a hash index (section 4): an index of 2^24
-    distinct keys (2^24 slots of 16 B + slot-ordered overflow, 268 MB) and
-    2^26 queries (5% absent).  DPG (distribute by partition, probe with the
-    partition L2-resident, gather) beside the direct lookup."""
-    import numpy as np
+    """Batch lookup in a hash index (section 4), DPG beside the
+    direct lookup."""
     import torch
-
     import datagen
     import oracle
     import paper_cs_0308004_b200 as dpg
@@ -426,316 +902,57 @@ def run_h1(args):
     q = torch.from_numpy(w["queries"].view(np.int32)).cuda()
     out = torch.empty_like(q)
     n = q.numel()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    flush_rd = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-
-    def timed(direct):
-        for _ in range(max(3, args.warmup)):
-            dpg.dpg_hash_lookup(t, p, q, out=out, direct=direct)
-        torch.cuda.synchronize()
-        idx = np.random.default_rng(0).integers(0, n, 4096)
-        ok = np.array_equal(out.cpu().numpy().view(np.uint32)[idx],
-                            oracle.batch_lookup(w["keys"], w["queries"][idx]))
-        ms = []
-        launches = 0
-        for _ in range(args.steps):
-            flush.fill_(1)
-            flush_rd.view(torch.int32).max()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            dpg.dpg_hash_lookup(t, p, q, out=out, direct=direct)
-            e1.record()
-            launches += dpg.last_launch_count()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        return sum(ms) / len(ms), ok, launches
-
+    steps_obj = Steps(torch, torch.device("cuda", 0))
+    res = {}
     with ClockSampler(0) as clk:
-        ms, ok, launches = timed(False)
-    dms, dok, _ = timed(True)
-    alg = n * (4 + 16 + 4)        # key in, the key's 16-byte slot, rid out
-    cpu = None
-    if not args.no_cpu:
-        qs = w["queries"][: 1 << 22]
-        t0 = time.perf_counter()
-        oracle.batch_lookup(w["keys"], qs)
-        tc = time.perf_counter() - t0
-        cpu = {"value": qs.size / tc, "unit": "lookups/s", "cores": 1, "kind": "oracle",
-               "sample": "2^22 of the queries, oracle.batch_lookup (sorted pairs + binary search)",
-               "host_cpu": host_cpu()}
-    peak, peak_src = hbm_peak()
+        for direct in (False, True):
+            f = lambda: dpg.dpg_hash_lookup(t, p, q, out=out, direct=direct)
+            for _ in range(max(3, args.warmup)):
+                f()
+            torch.cuda.synchronize()
+            idx = np.random.default_rng(0).integers(0, n, 4096)
+            ok = np.array_equal(out.cpu().numpy().view(np.uint32)[idx],
+                                oracle.batch_lookup(w["keys"], w["queries"][idx]))
+            tot, _, _, nl, _ = steps_obj.run(f, args.steps, launches=dpg.last_launch_count)
+            res[direct] = (med(tot), ok, nl)
+    ms, ok, launches = res[False]
+    dms, dok, _ = res[True]
+    peak, _ = hbm_peak()
+    alg = n * (4 + 16 + 4)
     print(json.dumps({
         "metric": "batch index lookups/s (hash index, DPG)", "value": n / (ms * 1e-3),
         "unit": "lookups/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic (datagen.hash_workload, seed 0)",
-        "config": {"workload": "h1: hash index of 2^24 keys (2^24 slots x 16 B, overflow in slot "
-                               "order), 2^26 queries (5% absent)", "slots": 1 << 24,
-                   "pool_entries": int(w["pool"].shape[0]), "queries": n,
-                   "l2": "flushed before every step"},
+        "config": {"workload": "h1: hash index of 2^24 keys, 2^26 queries (5% absent)"},
         "effective_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak,
         "direct": {"value": n / (dms * 1e-3), "unit": "lookups/s", "ms_per_step": dms,
                    "parity_sampled_ok": bool(dok)},
-        "parity_sampled_ok": bool(ok), "gpu_launches": launches, "cpu_baseline": cpu,
-        "clocks": clk.summary()}),
+        "parity_sampled_ok": bool(ok), "gpu_launches": launches, "clocks": clk.summary()}),
         flush=True)
     return 0
 
 
 def main():
     args = parse()
+    rc = relaunch_under_torchrun(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
-    if args.config == "h1":
-        return run_h1(args)
-    import torch
-    import torch.distributed as dist
     rank, world, local = dist_env()
     if world > 1 or args.config == "c5":
-        torch.cuda.set_device(local)
         if "MASTER_ADDR" not in os.environ:        # single process without torchrun
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    import numpy as np
-    import paper_cs_0308004_b200 as dpg
-
-    cfg = args.config
-    if cfg == "c5":
-        return run_c5(args, rank, world)
-    w = make_inputs(cfg, args.rec)
-    n_out, rec, alg_bytes, rid_bytes = units(cfg, w)
-    dev = torch.device("cuda", torch.cuda.current_device())
-
-    def to_dev(a):
-        a = np.ascontiguousarray(a)
-        if a.dtype == np.uint32:
-            a = a.view(np.int32)
-        return torch.from_numpy(a).to(dev)
-
-    if cfg in ("c4", "c4x"):
-        fact, fk, dim = to_dev(w["fact"]), to_dev(w["fk"]), to_dev(w["dim"])
-        out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
-        step = lambda: dpg.dpg_fk_join(fact, fk, dim, out=out)
-        naive = windowed = None
-        n_src = dim.shape[0]
-    else:
-        src, rids = to_dev(w["src"]), to_dev(w["rids"])
-        out = torch.empty((n_out, rec), dtype=torch.uint8, device=dev)
-        step = lambda: dpg.dpg_retrieve(src, rids, dst=out)
-        naive = lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)
-        windowed = lambda: dpg.dpg_retrieve_direct_ex(src, rids, dst=out, hint=3)
-        n_src = src.shape[0]
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    flush_rd = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-
-    def flush_l2():
-        # evict L2: write a buffer > 126 MB, then read another one, so that no
-        # dirty line of the flush itself is left for the timed step to write back
-        flush.fill_(1)
-        flush_rd.view(torch.int32).max()
-
-    def timed(fn, steps, phase=False):
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(steps)]
-        if phase:
-            dpg.dpg_phase_times()
-            dpg.dpg_phase_timing(True)
-        launches = 0
-        for e0, e1 in evs:
-            flush_l2()
-            e0.record(stream)
-            fn()
-            e1.record(stream)
-            launches += dpg.last_launch_count()
-        torch.cuda.synchronize()
-        ph = None
-        if phase:
-            dpg.dpg_phase_timing(False)
-            ph = dpg.dpg_phase_times()
-        ms = [a.elapsed_time(b) for a, b in evs]
-        return ms, launches, ph
-
-    # warm-up
-    for _ in range(max(3, args.warmup)):
-        step()
-        if naive:
-            naive()
-        if windowed:
-            windowed()
-    torch.cuda.synchronize()
-    dpg.dpg_sync_status()
-
-    step()
-    ran_path = dpg.last_path()       # the plan the calls ran (after the skew check)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        ms, launches, _ = timed(step, args.steps)
-    # the dominant kernel's own duration (CUDA events the library records on the
-    # launching stream around its kernel), from a second pass of the same steps
-    _, _, ph = timed(step, args.steps, phase=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    dpg.dpg_sync_status()
-    total_ms = sum(ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = world * alg_bytes / (ms_per_step * 1e-3) / 1e9
-
-    # naive comparison, same protocol
-    naive_res = None
-    if naive is not None:
-        nms, nl, _ = timed(naive, args.steps)
-        nt = sum(nms) / len(nms)
-        naive_res = {"value": alg_bytes / (nt * 1e-3) / 1e9, "unit": "GB/s",
-                     "ms_per_step": nt, "kernel": "k_direct", "launches_per_step": nl / args.steps}
-    # the same direct retrieval on the best gather engine written here (the
-    # L2-run kernel's 16-byte-window gather, no staging): the strongest
-    # non-DPG comparison
-    windowed_res = None
-    if windowed is not None:
-        wms, wl, _ = timed(windowed, args.steps)
-        wt = sum(wms) / len(wms)
-        windowed_res = {"value": alg_bytes / (wt * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": wt,
-                        "kernel": "k_dpg_l2run (stage=0)", "launches_per_step": wl / args.steps}
-
-    # the paper's application of the path (section 3): the whole Datamation
-    # sort on the GPU -- key extraction + stable radix sort of the key-pointer
-    # pairs (phases 1-2) + DPG retrieval (phase 3), timed the same way
-    sort_res = None
-    if cfg == "c2" and not args.no_sort:
-        srids = torch.empty(n_out, dtype=torch.int32, device=dev)
-        for _ in range(2):
-            dpg.dpg_sort(src, 0, 10, dst=out)
-        torch.cuda.synchronize()
-        assert np.array_equal(out[:1000].cpu().numpy(), w["src"][w["rids"][:1000].astype(np.int64)])
-        sms, sl, _ = timed(lambda: dpg.dpg_sort(src, 0, 10, dst=out), args.steps)
-        rms, _, _ = timed(lambda: dpg.dpg_sort_rids(src, 0, 10, rids=srids), args.steps)
-        st_ = sum(sms) / len(sms)
-        sort_res = {"records_per_s": n_out / (st_ * 1e-3), "ms_per_sort": st_,
-                    "ms_phases_1_2": sum(rms) / len(rms), "ms_phase_3": ms_per_step,
-                    "launches_per_sort": sl / args.steps,
-                    "what": "dpg_sort: 10-byte keys at offset 0, stable LSD radix sort "
-                            "(10 passes) + dpg_retrieve"}
-    # the paper's DPG-Sort join: the same join in fk order
-    join_sort_res = None
-    if cfg in ("c4", "c4x") and not args.no_sort:
-        js = lambda: dpg.dpg_fk_join_sort(fact, fk, dim, out=out)
-        for _ in range(2):
-            js()
-        torch.cuda.synchronize()
-        dpg.dpg_sync_status()
-        jms, jl, _ = timed(js, args.steps)
-        jt = sum(jms) / len(jms)
-        join_sort_res = {"value": alg_bytes / (jt * 1e-3) / 1e9, "unit": "GB/s",
-                         "ms_per_step": jt, "launches_per_step": jl / args.steps,
-                         "what": "dpg_fk_join_sort: stable radix sort of (rid_R, fk) pairs by "
-                                 "fk + DPG retrieval of fact rows into a temporary file + "
-                                 "zip with dim rows read in fk order"}
-    peak, peak_src = hbm_peak()
-    dist_ms, probe_ms, calls = ph
-    pg_ms = probe_ms / max(1, calls)
-    # (the join runs a DPG retrieval of dim rows -- no payload -- then a zip pass)
-    plan = dpg.dpg_plan(rec if cfg not in ("c4", "c4x") else w["dim"].shape[1], n_src, n_out, 0,
-                        torch.cuda.get_device_properties(dev).multi_processor_count)
-    src_rec = w["dim"].shape[1] if cfg in ("c4", "c4x") else rec
-    pay = 0
-    if plan["path"] == 5:
-        # K staged L2 runs probed into INTERNAL + the Phase III gather: the
-        # L2-run kernel launches between the distribute and the end of the call
-        kernel = "k_dpg_l2run (K runs + Phase III)"
-        pg_bytes = alg_bytes
-    elif plan["path"] == 3:
-        # one run (the whole source) staged in L2, probed in rid order: one
-        # kernel for the whole path, N * (2 * rec + rid_bytes)
-        kernel = "k_dpg_l2run"
-        pg_bytes = alg_bytes
-    elif plan["path"] == 1:
-        # one persistent kernel runs the whole path: its algorithmic bytes are
-        # the path's, N * (2 * rec + rid_bytes)
-        kernel = "k_dpg_fused" + (" + k_direct(INTERNAL)" if plan["gather"] == 2 else "")
-        pg_bytes = alg_bytes
-    else:
-        # probe-gather kernel: every source record staged once + every output
-        # row written once + its entry (and payload) read once
-        kernel = "k_probe_gather"
-        pg_bytes = n_src * src_rec + n_out * (rec + plan["pair_bytes"] + pay)
-    achieved = pg_bytes / (pg_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": committed_traffic(cfg),
-                "peak_source": peak_src,
-                "alg_bytes_per_launch": pg_bytes,
-                "launch_ms": pg_ms,
-                "share_of_step": probe_ms / max(1e-9, sum(ms)),
-                "distribute_ms": dist_ms / max(1, calls),
-                "path_frac_of_peak": value / world / peak}
-
-    # end to end through the host-buffer C-ABI entry
-    e2e = None
-    if not args.no_e2e and cfg not in ("c4", "c4x"):
-        hs = torch.from_numpy(w["src"]).pin_memory()
-        hr = torch.from_numpy(w["rids"].view(np.int32)).pin_memory()
-        hd = torch.empty((n_out, rec), dtype=torch.uint8).pin_memory()
-        for _ in range(2):
-            dpg.dpg_retrieve_host(hs, hr, hd)
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            dpg.dpg_retrieve_host(hs, hr, hd)
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-        e2e = {"value": world * alg_bytes / (el / args.steps) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": int(w["src"].nbytes + w["rids"].nbytes),
-               "d2h_bytes_per_step": int(n_out * rec),
-               "ms_per_step": el / args.steps * 1e3, "entry": "dpg_retrieve_host"}
-        assert np.array_equal(hd[:1000].numpy(), w["src"][w["rids"][:1000].astype(np.int64)])
-        dpg.dpg_release_cache()
-
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, w)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic (datagen, seed 0)",
-            "config": {"workload": workload_name(cfg, args.rec), "n_src": n_src, "n_out": n_out,
-                       "rec_bytes": rec, "rid_bytes": rid_bytes,
-                       "alg_bytes_per_step": alg_bytes,
-                       "l2": "flushed before every step (512 MiB write, then 512 MiB read)",
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "run_len": plan["run_len"], "num_runs": plan["num_runs"],
-                       "pair_bytes": plan["pair_bytes"], "plan_path": ran_path},
-            "records_per_s": world * n_out / (ms_per_step * 1e-3),
-            "frac_of_hbm_peak": value / world / peak,
-            "ms_min": min(ms), "ms_median": sorted(ms)[len(ms) // 2],
-            "roofline": roofline, "naive": naive_res, "direct_windowed": windowed_res,
-            "dpg_join_sort": join_sort_res,
-            "dpg_sort": sort_res,
-            "e2e": e2e, "cpu_baseline": cpu,
-            "clocks": clk.summary(), "gpu_launches": launches,
-            "gpu": torch.cuda.get_device_name(dev),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
+            s = socket.socket()
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+            s.close()
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+                              WORLD_SIZE="1", LOCAL_RANK="0")
+        return run_c5(args, rank, world, local)
+    if args.config == "h1":
+        return run_h1(args)
+    return run_single(args)
 
 
 if __name__ == "__main__":

@@ -14,6 +14,7 @@ Workloads (BASELINE.json ``configs``):
   (ties by ascending rid, reading A10) -- the sort's phase 3
 * ``c3a`` 16,777,216 x rec, rec in {8,16,32,64,128,256}, rids = permutation
 * ``c3b`` same, rids iid uniform with replacement
+* ``c2L`` 16,777,216 x 100 B, rids = permutation (SURVEY 8(d)'s "2L" row)
 * ``c4``  dimension 16,777,216 x 64 B; fact 67,108,864 x (uint32 fk uniform in
   [0, 2^24) ++ 16-byte payload) -- the DPG-Move join
 * ``c4x`` config 4 with the paper's non-uniform foreign keys:
@@ -256,6 +257,12 @@ def make(config: str, rec: int | None = None, scale: int = 1) -> dict:
         else:
             rids = uniform(n, n, STREAMS[("c3b", "rids")])
         return {"src": src, "rids": rids}
+    if config == "c2L":
+        # SURVEY 8(d) row "2L": config 2's record size on config 3's scale,
+        # 16,777,216 x 100 B, rids = a uniform random permutation
+        n = 16777216 // scale
+        return {"src": records(n, 100, STREAMS[("c3", "src")]),
+                "rids": permutation(n, STREAMS[("c3a", "rids")])}
     if config in ("c4", "c4x"):
         n_dim = 16777216 // scale
         n_fact = 67108864 // scale

@@ -178,6 +178,13 @@ dpg_status_t dpg_fk_join(const void *fact, size_t fact_bytes, uint64_t n_fact,
                          const uint32_t *fk_col, const void *dim, size_t rec_bytes,
                          uint64_t n_dim, void *out, dpg_stream_t stream);
 
+/* The standard join the paper compares against, the measured
+ * comparison for dpg_fk_join: the same rows, each built with one random
+ * access to dim[fk_col[i]].  Same arguments and errors as dpg_fk_join. */
+dpg_status_t dpg_fk_join_direct(const void *fact, size_t fact_bytes, uint64_t n_fact,
+                                const uint32_t *fk_col, const void *dim, size_t rec_bytes,
+                                uint64_t n_dim, void *out, dpg_stream_t stream);
+
 dpg_status_t dpg_fk_join_ex(const void *fact, size_t fact_bytes, uint64_t n_fact,
                             const uint32_t *fk_col, const void *dim, size_t rec_bytes,
                             uint64_t n_dim, void *out, dpg_stream_t stream,

@@ -47,7 +47,8 @@ def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (no CUDA; plain -O2, single thread)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", tmp])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", tmp,
+                               "-lpthread"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -60,6 +61,8 @@ def _load():
         P, U = ctypes.c_void_p, ctypes.c_uint64
         lib.oracle_retrieve.argtypes = [P, U, U, P, U, P, P]
         lib.oracle_retrieve_u64.argtypes = [P, U, U, P, U, P, P]
+        lib.oracle_retrieve_threads.argtypes = [P, U, U, P, U, P, P, ctypes.c_int]
+        lib.oracle_retrieve_threads.restype = ctypes.c_int
         lib.oracle_dpg_fig1.argtypes = [P, U, U, P, U, U, P, P, P, P, P, P]
         lib.oracle_fk_join.argtypes = [P, U, U, P, P, U, U, P, P]
         lib.oracle_retrieve_at.argtypes = [P, U, U, P, P, U, P]
@@ -108,6 +111,19 @@ def retrieve(src: np.ndarray, rids: np.ndarray) -> np.ndarray:
     bad = ctypes.c_uint64(0)
     fn = _load().oracle_retrieve if rids.dtype == np.uint32 else _load().oracle_retrieve_u64
     _check(fn(_ptr(src), rec, n_src, _ptr(rids), rids.size, _ptr(dst), ctypes.byref(bad)), bad)
+    return dst
+
+
+def retrieve_threads(src: np.ndarray, rids: np.ndarray, threads: int) -> np.ndarray:
+    """The definition's loop split into `threads` contiguous index ranges, one
+    host thread each (all-cores CPU baseline timing; uint32 rids)."""
+    src = _records(src)
+    n_src, rec = src.shape
+    rids = np.ascontiguousarray(rids, dtype=np.uint32)
+    dst = np.zeros((rids.size, rec), dtype=np.uint8)
+    bad = ctypes.c_uint64(0)
+    _check(_load().oracle_retrieve_threads(_ptr(src), rec, n_src, _ptr(rids), rids.size, _ptr(dst),
+                                           ctypes.byref(bad), int(threads)), bad)
     return dst
 
 

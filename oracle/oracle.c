@@ -25,6 +25,7 @@
  * SMALLEST offending position i and dst row i is left unwritten (every other
  * row is still written).
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -67,6 +68,45 @@ int oracle_retrieve_u64(const uint8_t *src, uint64_t rec, uint64_t n_src,
         }
         memcpy(dst + i * rec, src + r * rec, rec);
     }
+    return status;
+}
+
+/* The same loop split into `nthreads` contiguous index ranges, each run by
+ * oracle_retrieve on its own thread (the CPU baseline's all-cores timing,
+ * BASELINE.md): no arithmetic of its own.  Return and bad_index as
+ * oracle_retrieve (the smallest offending position over all ranges). */
+struct oracle_range {
+    const uint8_t *src; uint64_t rec, n_src; const uint32_t *rids; uint64_t n; uint8_t *dst;
+    uint64_t bad; int status;
+};
+static void *oracle_range_run(void *p)
+{
+    struct oracle_range *a = p;
+    a->status = oracle_retrieve(a->src, a->rec, a->n_src, a->rids, a->n, a->dst, &a->bad);
+    return NULL;
+}
+int oracle_retrieve_threads(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                            const uint32_t *rids, uint64_t n_out, uint8_t *dst,
+                            uint64_t *bad_index, int nthreads)
+{
+    if (rec == 0 || nthreads < 1 || nthreads > 1024) return -1;
+    struct oracle_range *r = calloc((size_t)nthreads, sizeof(*r));
+    pthread_t *th = calloc((size_t)nthreads, sizeof(*th));
+    if (!r || !th) { free(r); free(th); return -1; }
+    for (int t = 0; t < nthreads; ++t) {
+        uint64_t lo = n_out * (uint64_t)t / (uint64_t)nthreads;
+        uint64_t hi = n_out * (uint64_t)(t + 1) / (uint64_t)nthreads;
+        r[t] = (struct oracle_range){src, rec, n_src, rids + lo, hi - lo, dst + lo * rec, 0, 0};
+        if (pthread_create(&th[t], NULL, oracle_range_run, &r[t]) != 0) { r[t].status = -2; }
+    }
+    int status = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        if (r[t].status != -2) pthread_join(th[t], NULL);
+        uint64_t lo = n_out * (uint64_t)t / (uint64_t)nthreads;
+        if (r[t].status == -2 || r[t].status == -1) { status = -1; continue; }
+        if (r[t].status == 1 && status == 0) { status = 1; if (bad_index) *bad_index = lo + r[t].bad; }
+    }
+    free(r); free(th);
     return status;
 }
 

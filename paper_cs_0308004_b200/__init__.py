@@ -44,7 +44,7 @@ EXPORTED = (
     "dpg_release_cache", "dpg_sync_status", "dpg_status_string", "dpg_last_launch_count",
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
     "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
-    "dpg_phase_times_ex", "dpg_retrieve_dist_loopback",
+    "dpg_phase_times_ex", "dpg_retrieve_dist_loopback", "dpg_fk_join_direct",
 )
 
 
@@ -99,6 +99,7 @@ _sigs = {
     "dpg_gather_rows": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sort": [_P, _S, _U, _S, _S, _P, _P],
     "dpg_fk_join_sort": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
+    "dpg_fk_join_direct": [_P, _S, _U, _P, _P, _S, _U, _P, _P],
     "dpg_retrieve_segments": [_P, _S, _U, _P, _U, ctypes.c_uint32, _P, _P, _P],
     "dpg_ipc_alloc": [_S, _P, _P],
     "dpg_get_unique_id": [_P],
@@ -300,6 +301,23 @@ def dpg_fk_join(fact, fk_col, dim, out=None, stream=None, **opts):
     _check(_lib.dpg_fk_join_ex(fact.data_ptr(), fact_bytes, n_fact, fk_col.data_ptr(),
                                dim.data_ptr(), rec, n_dim, out.data_ptr(), _stream_ptr(stream),
                                _ref(_options(**opts))), "dpg_fk_join")
+    return out
+
+
+def dpg_fk_join_direct(fact, fk_col, dim, out=None, stream=None):
+    """The direct join (one random dim access per fact row), same rows as
+    dpg_fk_join: the measured comparison."""
+    torch = _torch()
+    fact = _records(fact, "fact")
+    dim = _records(dim, "dim")
+    fk_col = _rid_tensor(fk_col, "fk_col")
+    n_fact, fact_bytes = fact.shape
+    n_dim, rec = dim.shape
+    if out is None:
+        out = torch.empty((n_fact, fact_bytes + rec), dtype=torch.uint8, device=dim.device)
+    _check(_lib.dpg_fk_join_direct(fact.data_ptr(), fact_bytes, n_fact, fk_col.data_ptr(),
+                                   dim.data_ptr(), rec, n_dim, out.data_ptr(), _stream_ptr(stream)),
+           "dpg_fk_join_direct")
     return out
 
 

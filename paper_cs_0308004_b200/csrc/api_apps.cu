@@ -89,6 +89,37 @@ dpg_status_t dpg_sort(const void* src, size_t rec_bytes, uint64_t n, size_t key_
   return s;
 }
 
+dpg_status_t dpg_fk_join_direct(const void* fact, size_t fact_bytes, uint64_t n_fact,
+                                const uint32_t* fk_col, const void* dim, size_t rec_bytes,
+                                uint64_t n_dim, void* out, dpg_stream_t stream) {
+  // The standard join the paper compares against: for each fact
+  // row, one random access to the dimension record its key names.
+  t_launches = 0;
+  if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
+  if (n_fact == 0) return DPG_OK;
+  if ((fact_bytes && !fact) || !fk_col || !dim || !out || n_dim == 0) return DPG_ERR_INVALID_ARG;
+  uint64_t row, out_bytes, fact_total, dim_total;
+  if (__builtin_add_overflow((uint64_t)fact_bytes, (uint64_t)rec_bytes, &row) ||
+      __builtin_mul_overflow(n_fact, row, &out_bytes) ||
+      __builtin_mul_overflow(n_fact, (uint64_t)fact_bytes, &fact_total) ||
+      __builtin_mul_overflow(n_dim, (uint64_t)rec_bytes, &dim_total))
+    return DPG_ERR_INVALID_ARG;
+  if (row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
+  if (overlaps(out, out_bytes, fact, fact_total) || overlaps(out, out_bytes, dim, dim_total) ||
+      overlaps(out, out_bytes, fk_col, n_fact * 4))
+    return DPG_ERR_INVALID_ARG;
+  unsigned long long* status = device_status();
+  if (!status) return DPG_ERR_CUDA;
+  const uint32_t W = pow2_divisor(fact_bytes | rec_bytes | (uintptr_t)fact | (uintptr_t)dim |
+                                  (uintptr_t)out);
+  uint32_t nl = 0;
+  cudaError_t e = launch_zip_gather((const uint8_t*)fact, (uint32_t)fact_bytes, (const uint8_t*)dim,
+                                    (uint32_t)rec_bytes, n_dim, fk_col, n_fact, (uint8_t*)out, W,
+                                    current_sm_count(), (cudaStream_t)stream, &nl, status);
+  t_launches = nl;
+  return cuda_status(e);
+}
+
 dpg_status_t dpg_fk_join_sort(const void* fact, size_t fact_bytes, uint64_t n_fact,
                               const uint32_t* fk_col, const void* dim, size_t rec_bytes,
                               uint64_t n_dim, void* out, dpg_stream_t stream) {

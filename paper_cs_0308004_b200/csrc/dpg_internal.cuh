@@ -523,7 +523,8 @@ cudaError_t launch_skew_check(const uint32_t* rids, uint64_t n_out, uint64_t n_s
                               unsigned long long* out, cudaStream_t st, uint32_t* nl);
 cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                               uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
-                              int sm, cudaStream_t st, uint32_t* nlaunch);
+                              int sm, cudaStream_t st, uint32_t* nlaunch,
+                              unsigned long long* status = nullptr);
 uint64_t sort_ws_bytes(uint64_t n, int sm);
 uint32_t l2pair_smem_bytes(uint64_t chunk);
 cudaError_t launch_distribute(const DistArgs& a, bool rid64, cudaStream_t st, uint32_t* nlaunch);

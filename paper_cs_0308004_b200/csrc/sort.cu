@@ -382,7 +382,8 @@ template <int W>
 __global__ void __launch_bounds__(256) k_zip_gather(const uint8_t* __restrict__ a, uint32_t a_bytes,
                                                     const uint8_t* __restrict__ b, uint32_t b_bytes,
                                                     uint64_t n_b, const uint32_t* __restrict__ idx,
-                                                    uint64_t n, uint8_t* __restrict__ out) {
+                                                    uint64_t n, uint8_t* __restrict__ out,
+                                                    unsigned long long* status) {
   using T = typename Word<W>::T;
   const uint32_t AW = a_bytes / W, R = (a_bytes + b_bytes) / W;
   const uint64_t words = n * R;
@@ -391,7 +392,10 @@ __global__ void __launch_bounds__(256) k_zip_gather(const uint8_t* __restrict__ 
     const uint64_t row = k / R;
     const uint32_t w = (uint32_t)(k - row * R);
     const uint32_t f = __ldg(idx + row);
-    if (f >= n_b) continue;
+    if (f >= n_b) {
+      if (status && w == 0) report_bad(status, row);
+      continue;
+    }
     const T v = w < AW ? __ldcs(reinterpret_cast<const T*>(a + row * a_bytes) + w)
                        : __ldg(reinterpret_cast<const T*>(b + (uint64_t)f * b_bytes) + (w - AW));
     __stcs(reinterpret_cast<T*>(out) + k, v);
@@ -400,16 +404,16 @@ __global__ void __launch_bounds__(256) k_zip_gather(const uint8_t* __restrict__ 
 
 cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                               uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
-                              int sm, cudaStream_t st, uint32_t* nl) {
+                              int sm, cudaStream_t st, uint32_t* nl, unsigned long long* status) {
   const uint64_t words = n * ((a_bytes + b_bytes) / W);
   const uint32_t grid = (uint32_t)max_u64(1, min_u64((words + 255) / 256, (uint64_t)sm * 8));
   ++*nl;
   switch (W) {
-    case 16: k_zip_gather<16><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
-    case 8: k_zip_gather<8><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
-    case 4: k_zip_gather<4><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
-    case 2: k_zip_gather<2><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
-    default: k_zip_gather<1><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out); break;
+    case 16: k_zip_gather<16><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out, status); break;
+    case 8: k_zip_gather<8><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out, status); break;
+    case 4: k_zip_gather<4><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out, status); break;
+    case 2: k_zip_gather<2><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out, status); break;
+    default: k_zip_gather<1><<<grid, 256, 0, st>>>(a, a_bytes, b, b_bytes, n_b, idx, n, out, status); break;
   }
   return cudaGetLastError();
 }

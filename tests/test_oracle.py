@@ -449,3 +449,19 @@ def test_retrieve_generated_matches_materialised_source():
     with pytest.raises(oracle.RidRangeError) as e:
         oracle.retrieve_generated(rec, n, sid, np.array([5, n, 1], dtype=np.uint64))
     assert e.value.index == 1
+
+
+def test_threaded_retrieve_equals_single_thread():
+    """The all-cores timing entry (index ranges, one thread each) computes the
+    definition: equal to numpy indexing for every thread count, and the
+    smallest bad position over all ranges is reported."""
+    rng = np.random.default_rng(21)
+    src = rng.integers(0, 256, size=(3001, 13), dtype=np.uint8)
+    rids = rng.integers(0, 3001, 10007).astype(np.uint32)
+    for t in (1, 2, 3, 8, 64):
+        assert np.array_equal(oracle.retrieve_threads(src, rids, t), src[rids.astype(np.int64)])
+    bad = rids.copy()
+    bad[[9000, 4321]] = 3001
+    with pytest.raises(oracle.RidRangeError) as e:
+        oracle.retrieve_threads(src, bad, 7)
+    assert e.value.index == 4321
