@@ -423,7 +423,10 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   uint64_t T = tile_for(110ull << 10);
   uint32_t nbuf = 2;
   const uint32_t want_buf = opt ? opt->gather : 0;   // tuning: 1 or 2 Phase III buffers
-  if (want_buf == 1 || (want_buf != 2 && T * L < 2 * n_src)) {
+  // (two buffers overlap Phase III's loads with its writes, but halve the
+  // tile, so every piece (tile, run) of Phase II is half as long: measured,
+  // two buffers pay only when pieces keep >= 8 entries on average)
+  if (want_buf == 1 || (want_buf != 2 && T * L < 8 * n_src)) {
     T = tile_for(220ull << 10);
     nbuf = 1;
   }

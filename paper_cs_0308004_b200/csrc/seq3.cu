@@ -336,14 +336,16 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
           for (uint32_t e = 0; e < len; ++e) reg[rinc - len + e] = st + e;
         __syncwarp();
         const uint32_t nw = __shfl_sync(0xffffffffu, rinc, hi - 1) * m;
-        constexpr int U = 4;
+        constexpr int U = 12;   // a list's RID_RUN loads in flight together
         for (uint32_t j0 = lane; j0 < nw; j0 += 32 * U) {
           uint32_t sl[U], l[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t j = j0 + 32 * u;
             sl[u] = j < nw ? reg[M == 1 ? j : j / m] : 0u;
-            l[u] = j < nw ? (uint32_t)__ldcs(a.loc + sl[u]) : 0u;
+            // (dbg 0x10000 / 0x20000: tuning experiments that drop the RID_RUN
+            // loads / the INTERNAL stores; the output is then wrong)
+            l[u] = j < nw ? ((a.dbg & 0x10000) ? (sl[u] & 1023u) : (uint32_t)__ldcs(a.loc + sl[u])) : 0u;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -351,7 +353,11 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
             if (j >= nw) continue;
             const uint32_t w = M == 1 ? 0 : j - (j / m) * m;
             const W v = reinterpret_cast<const W*>(stage + l[u] * rec)[w];
-            reinterpret_cast<W*>(a.internal + (uint64_t)sl[u] * rec)[w] = v;
+            if (a.dbg & 0x20000) {
+              if (l[u] == 0xFFFFFFFFu) reinterpret_cast<W*>(a.internal)[0] = v;
+            } else {
+              reinterpret_cast<W*>(a.internal + (uint64_t)sl[u] * rec)[w] = v;
+            }
           }
         }
         __syncwarp();

@@ -20,7 +20,7 @@ fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for rec in (8, 16):
     src = torch.randint(0, 256, (n, rec), dtype=torch.uint8, device="cuda", generator=g)
     out = torch.empty_like(src)
-    ts = torch.zeros(148 * 16 * 4, dtype=torch.int64, device="cuda")
+    ts = torch.zeros(148 * 16 * 4 + 148 * 16 * 2 * 4, dtype=torch.int64, device="cuda")
     dpg.dpg_retrieve(src, rids, dst=out, path=6)
     fl.fill_(1)
     torch.cuda.synchronize()
@@ -28,7 +28,9 @@ for rec in (8, 16):
     dpg.dpg_retrieve(src, rids, dst=out, path=6)
     torch.cuda.synchronize()
     lib.dpg_debug_phase_stamps(None)
-    t = ts.view(148, 16, 4).cpu().numpy().astype("float64")
+    allts = ts.cpu().numpy().astype("float64")
+    t = allts[:148 * 16 * 4].reshape(148, 16, 4)
+
     t0 = t[:, 0, 0][t[:, 0, 0] > 0].min()
     wait, work, gap = [], [], []
     for c in range(148):
