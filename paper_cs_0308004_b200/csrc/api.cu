@@ -26,9 +26,6 @@ constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives 
 thread_local uint32_t t_launches = 0;
 thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
 thread_local const OutSegs* t_seg = nullptr;   // output segments of the current call (or none)
-// rows of the current call written `t_dst_stride` bytes apart (0: packed) --
-// the DPG-Move join writes each dim record straight into its wider output row
-thread_local uint64_t t_dst_stride = 0;
 thread_local uint64_t* t_seq3_pairs = nullptr; // tests: path 6 Phase I pairs (dpg_distribute)
 unsigned long long* g_debug_ts = nullptr;   // profiling: per-CTA phase stamps (dpg_debug_phase_stamps)
 uint32_t g_debug_flags = 0;                 // tuning experiments only (dpg_debug_flags)
@@ -815,7 +812,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (__builtin_mul_overflow(n_out, row, &dst_bytes)) return DPG_ERR_INVALID_ARG;
   if (__builtin_mul_overflow(n_out, pay, &pay_bytes_total)) return DPG_ERR_INVALID_ARG;
   if (rec > UINT32_MAX / 2 || row > UINT32_MAX / 2) return DPG_ERR_UNSUPPORTED;
-  if (!t_seg && !t_dst_stride &&   // (segments / strided rows: the caller checked them)
+  if (!t_seg &&   // (segmented output: each segment was checked by dpg_retrieve_segments)
       (overlaps(dst, dst_bytes, src, src_bytes) || overlaps(dst, dst_bytes, rids, n_out * 4) ||
        (pay && overlaps(dst, dst_bytes, pay_src, pay_bytes_total))))
     return DPG_ERR_INVALID_ARG;
@@ -823,7 +820,6 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   const int sm = current_sm_count();
   dpg_plan_t p;
   dpg_status_t ps = make_plan(rec, n_src, n_out, pay, opt, sm, &p);
-  if (ps == DPG_ERR_UNSUPPORTED && t_dst_stride) return ps;
   if (ps == DPG_ERR_UNSUPPORTED && pay == 0 && !(opt && opt->log2_run) &&
       rec * 2 + 64 > kSmemLimit / 2) {
     // A record larger than a shared-memory stage is itself one sequential
@@ -902,8 +898,6 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     }
   }
   t_path = p.path;
-  if (t_dst_stride && !(p.path == 1 && p.gather == 1 && pay == 0 && !t_seg))
-    return DPG_ERR_UNSUPPORTED;   // (the caller takes another way)
 
   if (p.path == 6 && ((uintptr_t)src % 16 != 0)) {
     // the stage is one TMA bulk copy of the run: an unaligned source takes the
@@ -1162,7 +1156,6 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     f.dst = (uint8_t*)dst;
     if (t_seg) f.seg = *t_seg;   // mode 0 writes each row to its segment
     f.row_bytes = (uint32_t)row;
-    f.dst_stride = t_dst_stride ? t_dst_stride : row;
     f.slot_pairs = p.slot_pairs;
     f.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
     f.stage_bytes = p.stage_bytes;
@@ -1425,27 +1418,6 @@ dpg_status_t dpg_fk_join_ex(const void* fact, size_t fact_bytes, uint64_t n_fact
   if (overlaps(out, out_bytes, fact, fact_total) || overlaps(out, out_bytes, dim, dim_total) ||
       overlaps(out, out_bytes, fk_col, n_fact * 4))
     return DPG_ERR_INVALID_ARG;
-  {
-    // DPG-Move with the rows built in place: the DPG retrieval writes dim[fk[i]]
-    // straight into out row i (after the fact bytes; the fused shared-memory
-    // runs), then one sequential pass writes the fact parts -- no temporary
-    // file.  Plans that cannot write strided rows take the temporary file.
-    t_dst_stride = row;
-    dpg_status_t s = run_dpg(dim, rec_bytes, n_dim, fk_col, n_fact, nullptr, 0,
-                             (uint8_t*)out + fact_bytes, st, opt);
-    t_dst_stride = 0;
-    if (s != DPG_ERR_UNSUPPORTED) {
-      uint32_t nl = t_launches;
-      if (s == DPG_OK) {
-        const uint32_t W = pow2_divisor(fact_bytes | row | (uintptr_t)fact | (uintptr_t)out);
-        s = cuda_status(launch_put_rows((const uint8_t*)fact, (uint32_t)fact_bytes, n_fact,
-                                        (uint8_t*)out, row, W, fk_col, n_dim,
-                                        current_sm_count(), st, &nl));
-      }
-      t_launches = nl;
-      return s;
-    }
-  }
   void* tmp = nullptr;
   if (ws_malloc(&tmp, tmp_bytes + 256, st) != cudaSuccess) {
     cudaGetLastError();

@@ -239,42 +239,6 @@ cudaError_t launch_zip_rows(const uint8_t* a, uint32_t a_bytes, const uint8_t* b
   return cudaGetLastError();
 }
 
-// out[i * out_stride, + a_bytes) = a[i] for rows whose key passes (the fact
-// part of the DPG-Move join's rows; rows with key >= key_limit untouched).
-template <int W>
-__global__ void __launch_bounds__(256) k_put_rows(const uint8_t* __restrict__ a, uint32_t a_bytes,
-                                                  uint64_t n, uint8_t* __restrict__ out,
-                                                  uint64_t out_stride, const uint32_t* __restrict__ key,
-                                                  uint64_t key_limit) {
-  using T = typename Word<W>::T;
-  const uint32_t R = a_bytes / W;
-  const uint64_t words = n * R;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < words; k += stride) {
-    const uint64_t row = R == 1 ? k : k / R;
-    const uint32_t w = (uint32_t)(k - row * R);
-    if (key && (uint64_t)__ldg(key + row) >= key_limit) continue;
-    const T v = __ldcs(reinterpret_cast<const T*>(a + row * a_bytes) + w);
-    *reinterpret_cast<T*>(out + row * out_stride + (uint64_t)w * W) = v;
-  }
-}
-
-cudaError_t launch_put_rows(const uint8_t* a, uint32_t a_bytes, uint64_t n, uint8_t* out,
-                            uint64_t out_stride, uint32_t W, const uint32_t* key, uint64_t key_limit,
-                            int sm_count, cudaStream_t st, uint32_t* nl) {
-  const uint64_t words = n * (a_bytes / W);
-  const uint32_t grid = (uint32_t)max_u64(1, min_u64((words + 255) / 256, (uint64_t)sm_count * 8));
-  ++*nl;
-  switch (W) {
-    case 16: k_put_rows<16><<<grid, 256, 0, st>>>(a, a_bytes, n, out, out_stride, key, key_limit); break;
-    case 8: k_put_rows<8><<<grid, 256, 0, st>>>(a, a_bytes, n, out, out_stride, key, key_limit); break;
-    case 4: k_put_rows<4><<<grid, 256, 0, st>>>(a, a_bytes, n, out, out_stride, key, key_limit); break;
-    case 2: k_put_rows<2><<<grid, 256, 0, st>>>(a, a_bytes, n, out, out_stride, key, key_limit); break;
-    default: k_put_rows<1><<<grid, 256, 0, st>>>(a, a_bytes, n, out, out_stride, key, key_limit); break;
-  }
-  return cudaGetLastError();
-}
-
 cudaError_t launch_scatter_rows(const uint8_t* rows, uint32_t rec, const uint32_t* pos, uint64_t n,
                                 uint8_t* dst, uint64_t n_dst, uint32_t W, int sm_count,
                                 cudaStream_t st, uint32_t* nl) {

@@ -241,8 +241,6 @@ struct FusedArgs {
   uint32_t pair_bytes;
   uint8_t* dst;
   uint32_t row_bytes;
-  uint64_t dst_stride;   // mode 0: bytes between output rows (row_bytes, or a wider row
-                         // whose first row_bytes... at dst are this record: the join)
   uint32_t slot_pairs;   // pairs per stage
   uint32_t region_cap;   // bytes of a stage reserved for the run's records
   uint32_t stage_bytes;  // bytes per stage
@@ -578,9 +576,6 @@ cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, cons
                           int hint = 0);
 cudaError_t launch_l2_prefetch(const void* p, uint64_t bytes, int sm_count, cudaStream_t st,
                                uint32_t* nlaunch);
-cudaError_t launch_put_rows(const uint8_t* a, uint32_t a_bytes, uint64_t n, uint8_t* out,
-                            uint64_t out_stride, uint32_t W, const uint32_t* key, uint64_t key_limit,
-                            int sm_count, cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_zip_rows(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                             uint64_t n, uint8_t* out, uint32_t W, int sm_count, cudaStream_t st,
                             uint32_t* nlaunch, const uint32_t* key = nullptr,

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
               const uint32_t rr = k0 + u * RPI + lr;
               if (lane_on && rr < cnt) {
                 uint8_t* d = (MODE == 1 ? obase + (uint64_t)ps[u] * a.row_bytes
-                                        : seg_row(a.seg, a.dst, ps[u], a.dst_stride)) + lw * W;
+                                        : seg_row(a.seg, a.dst, ps[u], a.row_bytes)) + lw * W;
                 // rows with L2 evict_last: a row's partially written sectors stay
                 // in L2 until the neighbouring rows complete them (measured: -15%)
                 if (!(a.dbg & 1)) HintIO<W>::st(d, v[u], pol_last);
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
             const uint32_t pos = MODE == 1 ? rr : __shfl_sync(0xFFFFFFFFu, my_pos, rr);
             const uint8_t* srow = region + (size_t)loc * a.rec;
             uint8_t* drow = MODE == 1 ? obase + (uint64_t)pos * a.row_bytes
-                                      : seg_row(a.seg, a.dst, pos, a.dst_stride);
+                                      : seg_row(a.seg, a.dst, pos, a.row_bytes);
 #pragma unroll 4
             for (uint32_t w = lane; w < R; w += 32) {
               const T v = *reinterpret_cast<const T*>(srow + w * W);
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
         const uint64_t e = __ldcg(a.ovf + j);
         const uint64_t i = (uint32_t)e, r = e >> 32;
         const uint8_t* s = a.src + r * a.rec;
-        uint8_t* d = seg_row(a.seg, a.dst, i, a.dst_stride);
+        uint8_t* d = seg_row(a.seg, a.dst, i, a.row_bytes);
         for (uint32_t w = lane; w < R; w += 32)
           *reinterpret_cast<T*>(d + w * W) = *reinterpret_cast<const T*>(s + w * W);
       }
