@@ -291,22 +291,25 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
     for (uint32_t t = bulk + tid; t < bytes; t += blockDim.x) stage[t] = gsrc[t];   // < 16 B
     const uint16_t* colA = a.preT + (uint64_t)b * nsub;
     const uint16_t* colB = colA + nsub;
-    // this warp's first group of pieces, loaded before the stage wait
-    uint32_t g = warp;
-    uint32_t t = g * 32 + lane;
-    uint32_t pa = t < nsub ? colA[t] : 0u, pb = t < nsub ? colB[t] : 0u;
+    // this warp's pieces: an equal share [p_lo, p_hi) of the run's nsub pieces,
+    // 32 at a time; the first group's column entries loaded before the stage wait
+    const uint32_t ppw = (nsub + nwarp - 1) / nwarp;
+    const uint32_t p_lo = min(nsub, warp * ppw), p_hi = min(nsub, p_lo + ppw);
+    uint32_t g = p_lo;
+    uint32_t t = g + lane;
+    uint32_t pa = t < p_hi ? colA[t] : 0u, pb = t < p_hi ? colB[t] : 0u;
     mbar_wait(bar, phase);
     phase ^= 1;
     __syncthreads();   // (the tail bytes)
     if (a.ts && tid == 0 && it < 16) a.ts[(blockIdx.x * 16 + it) * 4 + 1] = globaltimer();
     // "For each rid r in RID_RUN[i]: append INPUT_REC[r] to RECORD_RUN[i]"
     //
-    for (; g * 32 < nsub; g += nwarp) {
+    for (; g < p_hi; g += 32) {
       const uint32_t len = pb - pa, st = t * T + pa;
       // the next group's column entries, in flight during this group
-      const uint32_t tn = (g + nwarp) * 32 + lane;
-      pa = tn < nsub ? colA[tn] : 0u;
-      pb = tn < nsub ? colB[tn] : 0u;
+      const uint32_t tn = g + 32 + lane;
+      pa = tn < p_hi ? colA[tn] : 0u;
+      pb = tn < p_hi ? colB[tn] : 0u;
       t = tn;
       uint32_t inc = len;
 #pragma unroll
