@@ -67,7 +67,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N=1: only the headline config")
-    ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c4,c5shard",
+    ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c3a8n26,c3a8n27,"
+                                        "c3a16n26,c4,c5shard",
                     help="N=1: nested configurations")
     a = ap.parse_args()
     if a.config is None:
@@ -584,11 +585,14 @@ def run_extra(name, args, torch, dpg, steps_obj, peak):
         return run_join_extra(args, torch, dpg, steps_obj, peak, steps)
     if name == "c5shard":
         return run_c5_shard(args, torch, dpg, steps_obj, peak, steps)
+    log2n = 24
+    if "n" in name[3:]:                       # e.g. c3a8n26: config 3's shape at 2^26 records
+        name, log2n = name.split("n")[0], int(name.split("n")[1])
     if name == "c2L":
         rec, kind = 100, "c3a"
     else:
         kind, rec = name[:3], int(name[3:])
-    n = 1 << 24
+    n = 1 << log2n
     sid = datagen.STREAMS[("c3", "src")]
     src = torch.empty((n, rec), dtype=torch.uint8, device="cuda")
     datagen.random_bytes_cuda(src.view(-1), sid)
@@ -600,7 +604,11 @@ def run_extra(name, args, torch, dpg, steps_obj, peak):
     idx_fn = lambda i: oracle.retrieve_generated(rec, n, sid, rids_h[i].astype(np.uint64))
     ok = sampled_ok(out, idx_fn, n, k=512)
     d = res["dpg"]
-    r = {"workload": workload_name("c2L" if name == "c2L" else kind, rec), "plan_path": d["plan_path"],
+    wl = workload_name("c2L" if name == "c2L" else kind, rec)
+    if log2n != 24:
+        wl = wl.replace("16,777,216", f"2^{log2n} = {n:,}") + \
+            f" (source {n * rec / 1e6:.0f} MB, {n * rec / (126 << 20):.1f}x the L2)"
+    r = {"workload": wl, "plan_path": d["plan_path"],
          "value": d["value"], "frac_of_hbm_peak": d["value"] / peak, "ms": d["ms"],
          "ms_kernels": d["ms_kernels"], "phases_ms": d["phases_ms"],
          "naive": {"value": res["naive"]["value"], "ms": res["naive"]["ms"]},
