@@ -107,7 +107,9 @@ typedef struct {
     uint32_t npre;          /* source runs prefetched before Phase I (fused)    */
     uint32_t rid_cache;     /* 1: each CTA's rid chunk is staged in smem (fused) */
     uint32_t hist_warps;    /* warps owning private 16-bit run counters (fused) */
-    uint32_t tile;          /* rids per Phase I tile of a CTA (fused)           */
+    uint32_t tile;          /* rids per Phase I tile of a CTA (fused, path 6)   */
+    uint32_t cluster;       /* path 6: CTAs (SMs) whose shared memory holds one
+                               run together (thread-block cluster, DSMEM)      */
 } dpg_plan_t;
 
 /* Optional overrides for tests and tuning (zero = automatic).  The output
@@ -124,7 +126,8 @@ typedef struct {
                                5 K L2 runs (log2_run, if set, fixes the run
                                  length)                                        */
     uint32_t gather;        /* 0 auto, 1 force direct-to-dst, 2 force INTERNAL  */
-    uint32_t reserved;
+    uint32_t cluster;       /* path 6: CTAs holding one run together (1, 2, 4,
+                               8; 0 = automatic)                                */
 } dpg_options_t;
 
 /* Build the plan the library would use (host only; sm_count <= 0 queries the

@@ -64,16 +64,16 @@ class Plan(ctypes.Structure):
                                        "grid_distribute", "grid_probe", "hist_in_smem",
                                        "pay_bytes", "path", "nstages", "stage_bytes",
                                        "gather", "npre", "rid_cache", "hist_warps",
-                                       "tile")]
+                                       "tile", "cluster")]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("log2_run", "grid_distribute", "grid_probe",
                                                "pair_bytes", "hist_mode", "path", "gather",
-                                               "reserved")]
+                                               "cluster")]
 
 
 _P, _U, _S, _I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
@@ -234,7 +234,7 @@ def _rid_tensor(t, name="rids"):
 
 
 def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0, grid_probe=0,
-                 pair_bytes=0, hist_mode=0, path=0, gather=0):
+                 pair_bytes=0, hist_mode=0, path=0, gather=0, cluster=0):
     """``dst[i] = src[rids[i]]`` by DPG.  src: uint8 CUDA [n_src, rec]; rids:
     int32/uint32 CUDA [n_out].  Returns dst (uint8 [n_out, rec])."""
     torch = _torch()
@@ -245,7 +245,8 @@ def dpg_retrieve(src, rids, dst=None, stream=None, log2_run=0, grid_distribute=0
     if dst is None:
         dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
     o = _options(log2_run=log2_run, grid_distribute=grid_distribute, grid_probe=grid_probe,
-                 pair_bytes=pair_bytes, hist_mode=hist_mode, path=path, gather=gather)
+                 pair_bytes=pair_bytes, hist_mode=hist_mode, path=path, gather=gather,
+                 cluster=cluster)
     _check(_lib.dpg_retrieve_ex(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
                                 dst.data_ptr(), _stream_ptr(stream), _ref(o)), "dpg_retrieve")
     return dst

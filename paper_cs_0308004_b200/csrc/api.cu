@@ -378,6 +378,14 @@ bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool
 // Three sequential passes over shared-memory runs (seq3.cu): runs of L = 2^s
 // records, L * rec <= one stage (128 KB: one CTA per SM holds it, the next
 // run is prefetched into L2 meanwhile), 16-bit local offsets (s <= 16).
+uint32_t seq3_cluster_env() {
+  static uint32_t env = [] {
+    const char* e = getenv("DPG_SEQ3_CLUSTER");
+    return e ? (uint32_t)atoi(e) : 0u;
+  }();
+  return env;
+}
+
 uint64_t seq3_stage_bytes() {
   static uint64_t env = [] {
     const char* e = getenv("DPG_SEQ3_STAGE_KB");
@@ -402,17 +410,35 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   if (n_out >= 0xFFFFFFFFull || n_out * ((rec + pay) / 4) >= (1ull << 32)) return false;
   const bool forced = opt && opt->path == 6;
   const uint64_t stage = std::min<uint64_t>(seq3_stage_bytes(), 128ull << 10);
-  uint32_t s = 0;
+  // one run = `cl` slices of Ls = 2^ls records, slice i in the shared memory
+  // of CTA i of a thread-block cluster (cl = 1: one CTA)
+  uint32_t cl = opt && opt->cluster ? opt->cluster : seq3_cluster_env();
+  if (cl != 0 && cl != 1 && cl != 2 && cl != 4 && cl != 8) return false;
+  const uint32_t lcl = cl == 8 ? 3 : cl == 4 ? 2 : cl == 2 ? 1 : 0;
+  uint32_t ls = 0;
+  while (ls < 16 && (2ull << ls) * rec <= stage && (1ull << ls) < n_src) ++ls;
+  if (cl == 0) {
+    // automatic: one CTA per run, or two (a cluster sharing the run through
+    // distributed shared memory) when one CTA's runs would leave pieces
+    // (tile, run) of fewer than 2 entries on average -- measured: the remote
+    // lookups cost more than the shorter pieces save unless the pieces are
+    // that short (profiles/r02_seq3_cluster.md)
+    const uint64_t T0 = std::min<uint64_t>(32768, (220ull << 10) / (rec + 2));
+    cl = (T0 << ls) < 2 * n_src && ls < 16 && (2ull << ls) < 2 * n_src ? 2 : 1;
+  }
+  const uint32_t lc = cl == 8 ? 3 : cl == 4 ? 2 : cl == 2 ? 1 : 0;
+  (void)lcl;
+  uint32_t s = ls + lc;
   if (opt && opt->log2_run) {
     s = opt->log2_run;
-    if (s > 16 || (1ull << s) * rec > (128ull << 10)) return false;
-  } else {
-    while (s < 16 && (2ull << s) * rec <= stage && (1ull << s) < n_src) ++s;
+    if (s > 16 || s < lc || (1ull << (s - lc)) * rec > (128ull << 10)) return false;
   }
+  if (s > 16) return false;                         // 16-bit local offsets
   const uint64_t L = 1ull << s;
+  const uint64_t Ls = L >> lc;
   const uint64_t K = (n_src + L - 1) >> s;
-  if (K > 8192 || (L * rec) % 16) return false;    // each run one 16-byte aligned bulk copy
-  if (seq3_probe_smem(L * rec) > kSmemLimit) return false;
+  if (K > 8192 || (Ls * rec) % 16) return false;   // each slice one 16-byte aligned bulk copy
+  if (seq3_probe_smem(Ls * rec) > kSmemLimit) return false;
   // tile T: the Phase III buffer (two of ~100 KB, else one of ~200 KB) and the
   // Phase I tile (T rids + T offsets + 2 (K + 1) counters) both fit
   auto tile_for = [&](uint64_t bytes) {
@@ -452,8 +478,11 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   p->grid_probe = (uint32_t)std::min<uint64_t>(K, (opt && opt->grid_probe) ? opt->grid_probe
                                                                            : (uint64_t)sm);
   p->hist_in_smem = 1;
-  p->stage_bytes = (uint32_t)(L * rec);
-  p->smem_bytes = seq3_probe_smem(L * rec);
+  p->stage_bytes = (uint32_t)(Ls * rec);
+  p->smem_bytes = seq3_probe_smem(Ls * rec);
+  p->cluster = cl;
+  if (cl > 1)
+    p->grid_probe = (uint32_t)std::max<uint64_t>(cl, std::min<uint64_t>(K * cl, (uint64_t)sm) / cl * cl);
   return true;
 }
 
@@ -945,6 +974,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     a.status = status;
     a.dbg = g_debug_flags;
     a.ts = g_debug_ts;
+    a.cl = p.cluster ? p.cluster : 1;
     uint32_t nl = 0;
     PhaseEvents pe;
     const bool timed = timing_begin(st, &pe);

@@ -558,6 +558,7 @@ struct Seq3Args {
   unsigned long long* status;
   uint32_t dbg;            // tuning experiments only (dpg_debug_flags): 0 normally
   unsigned long long* ts;  // profiling only (dpg_debug_phase_stamps): per-CTA stamps
+  uint32_t cl;             // Phase II: CTAs of a cluster holding one run (1, 2, 4, 8)
 };
 uint32_t seq3_dist_smem(uint32_t T, uint32_t K);
 uint32_t seq3_probe_smem(uint64_t stage_bytes);

@@ -42,6 +42,8 @@
 // memory atomic order (reading A15): the pieces are in tile order, the set of
 // each piece is unique, and every row's slot is recorded, so the output does
 // not depend on the order.
+#include <algorithm>
+
 #include "dpg_internal.cuh"
 
 namespace dpg {
@@ -251,7 +253,32 @@ uint32_t seq3_probe_smem(uint64_t stage_bytes) {
 // (Measured alternatives -- per-warp mbarrier pipelines over the stage, lists
 // filled by cp.async, one lane group per piece, CTA-wide entry windows -- were
 // slower: profiles/r02_seq3_phase2_variants.md.)
-template <int WB, int M>
+// Cluster-wide barrier (all threads of every CTA of the cluster), release /
+// acquire: the shared memory of every CTA is then visible cluster-wide.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// Generic address of `p` (this CTA's shared memory) in CTA `rank` of the cluster.
+__device__ __forceinline__ const uint8_t* map_cluster(const uint8_t* p, uint32_t rank) {
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+  return reinterpret_cast<const uint8_t*>(r);
+}
+
+// CL > 1 (section 8(f) #1 of the survey: larger on-chip regions): a cluster
+// of CL CTAs on CL SMs holds one run of L = 2^s records together, CTA r its
+// slice [r L/CL, (r+1) L/CL) in its own stage; a lookup of local offset l
+// reads the stage of CTA l / (L/CL) through distributed shared memory.  The
+// run's pieces are shared among all the cluster's warps; cluster barriers
+// order every slice's landing before the lookups and every lookup before the
+// next run's bulk copies.
+template <int WB, int M, int CL>
 __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
   using W = typename Word<WB>::T;
   extern __shared__ __align__(128) uint8_t smp[];
@@ -259,6 +286,11 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   uint32_t* reg = reinterpret_cast<uint32_t*>(smp + 256) + warp * k3Reg;
   uint8_t* stage = smp + 256 + (k3ProbeThreads / 32) * k3Reg * 4;
+  const uint32_t cr = CL > 1 ? cluster_ctarank() : 0;
+  const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const uint8_t* sbase[CL];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) sbase[r] = CL > 1 ? map_cluster(stage, r) : stage;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -266,11 +298,13 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
   __syncthreads();
   const uint64_t pol_first = policy_evict_first();
   const uint64_t L = 1ull << a.s;
+  const uint64_t Ls = L / CL;                     // records of one CTA's slice
+  const uint32_t ls_shift = a.s - (CL == 8 ? 3 : CL == 4 ? 2 : CL == 2 ? 1 : 0);
   const uint32_t rec = a.rec, m = M ? M : rec / WB, T = a.T, nsub = a.nsub;
   uint32_t phase = 0, it = 0;
-  for (uint32_t b = blockIdx.x; b < a.K; b += gridDim.x, ++it) {
-    const uint64_t r0 = (uint64_t)b << a.s;
-    const uint32_t bytes = (uint32_t)(min_u64(L, a.n_src - r0) * rec);
+  for (uint32_t b = cid; b < a.K; b += ncl, ++it) {
+    const uint64_t r0 = ((uint64_t)b << a.s) + cr * Ls;      // this CTA's slice of run b
+    const uint32_t bytes = r0 < a.n_src ? (uint32_t)(min_u64(Ls, a.n_src - r0) * rec) : 0u;
     const uint32_t bulk = bytes & ~15u;
     const uint8_t* gsrc = a.src + r0 * rec;
     if (a.ts && tid == 0 && it < 16) a.ts[(blockIdx.x * 16 + it) * 4 + 0] = globaltimer();
@@ -280,10 +314,10 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
       mbar_arrive_expect_tx(bar, bulk);
       for (uint32_t off = 0; off < bulk; off += 32768)
         bulk_g2s(stage + off, gsrc + off, min(32768u, bulk - off), bar, pol_first);
-      const uint32_t bn = b + gridDim.x;     // the CTA's next run, on its way to L2
+      const uint32_t bn = b + ncl;           // the cluster's next run, on its way to L2
       if (bn < a.K) {
-        const uint64_t rn = (uint64_t)bn << a.s;
-        const uint32_t nb = (uint32_t)(min_u64(L, a.n_src - rn) * rec) & ~15u;
+        const uint64_t rn = ((uint64_t)bn << a.s) + cr * Ls;
+        const uint32_t nb = rn < a.n_src ? (uint32_t)(min_u64(Ls, a.n_src - rn) * rec) & ~15u : 0u;
         for (uint32_t off = 0; off < nb; off += 32768)
           bulk_prefetch_l2(a.src + rn * rec + off, min(32768u, nb - off), pol_first);
       }
@@ -291,16 +325,19 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
     for (uint32_t t = bulk + tid; t < bytes; t += blockDim.x) stage[t] = gsrc[t];   // < 16 B
     const uint16_t* colA = a.preT + (uint64_t)b * nsub;
     const uint16_t* colB = colA + nsub;
-    // this warp's pieces: an equal share [p_lo, p_hi) of the run's nsub pieces,
-    // 32 at a time; the first group's column entries loaded before the stage wait
-    const uint32_t ppw = (nsub + nwarp - 1) / nwarp;
-    const uint32_t p_lo = min(nsub, warp * ppw), p_hi = min(nsub, p_lo + ppw);
+    // this warp's pieces: an equal share [p_lo, p_hi) of the run's nsub pieces
+    // among the cluster's warps, 32 at a time; the first group's column
+    // entries loaded before the stage wait
+    const uint32_t gw = cr * nwarp + warp, ngw = nwarp * CL;
+    const uint32_t ppw = (nsub + ngw - 1) / ngw;
+    const uint32_t p_lo = min(nsub, gw * ppw), p_hi = min(nsub, p_lo + ppw);
     uint32_t g = p_lo;
     uint32_t t = g + lane;
     uint32_t pa = t < p_hi ? colA[t] : 0u, pb = t < p_hi ? colB[t] : 0u;
     mbar_wait(bar, phase);
     phase ^= 1;
-    __syncthreads();   // (the tail bytes)
+    if (CL > 1) cluster_sync_all();   // every slice of run b landed (and the tail bytes)
+    else __syncthreads();             // (the tail bytes)
     if (a.ts && tid == 0 && it < 16) a.ts[(blockIdx.x * 16 + it) * 4 + 1] = globaltimer();
     // "For each rid r in RID_RUN[i]: append INPUT_REC[r] to RECORD_RUN[i]"
     //
@@ -329,8 +366,10 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
           for (uint32_t j = lane; j < lq * m; j += 32) {
             const uint32_t e = j / m, w = j - e * m;
             const uint32_t l = __ldcs(a.loc + sq + e);
+            const uint8_t* from = CL > 1 ? sbase[l >> ls_shift] + (l & (Ls - 1)) * rec
+                                         : stage + l * rec;
             reinterpret_cast<W*>(a.internal + (uint64_t)(sq + e) * rec)[w] =
-                reinterpret_cast<const W*>(stage + l * rec)[w];
+                reinterpret_cast<const W*>(from)[w];
           }
           ++lo;
           continue;
@@ -355,7 +394,9 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
             const uint32_t j = j0 + 32 * u;
             if (j >= nw) continue;
             const uint32_t w = M == 1 ? 0 : j - (j / m) * m;
-            const W v = reinterpret_cast<const W*>(stage + l[u] * rec)[w];
+            const uint8_t* from = CL > 1 ? sbase[l[u] >> ls_shift] + (l[u] & (Ls - 1)) * rec
+                                         : stage + l[u] * rec;
+            const W v = reinterpret_cast<const W*>(from)[w];
             if (a.dbg & 0x20000) {
               if (l[u] == 0xFFFFFFFFu) reinterpret_cast<W*>(a.internal)[0] = v;
             } else {
@@ -367,23 +408,64 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
         lo = hi;
       }
     }
-    __syncthreads();   // the stage is rewritten for the next run
+    // the stage is rewritten for the next run (CL > 1: once no CTA of the
+    // cluster reads it any more)
+    if (CL > 1) cluster_sync_all();
+    else __syncthreads();
     if (a.ts && tid == 0 && it < 16) a.ts[(blockIdx.x * 16 + it) * 4 + 2] = globaltimer();
   }
+}
+
+template <int WB, int M, int CL>
+static cudaError_t launch_probe_wc(const Seq3Args& a, uint32_t grid, uint32_t smem,
+                                   cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k3_probe<WB, M, CL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (CL == 1) {
+    k3_probe<WB, M, 1><<<grid, k3ProbeThreads, smem, st>>>(a);
+    return cudaSuccess;
+  }
+  // clusters of CL CTAs, as many as can be resident at once
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(k3ProbeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(CL);
+  int nclusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&nclusters, (void*)k3_probe<WB, M, CL>, &cfg);
+  if (e != cudaSuccess || nclusters <= 0) {
+    cudaGetLastError();
+    nclusters = (int)(grid / CL);
+  }
+  const uint32_t runs = a.K;
+  const uint32_t ncl = (uint32_t)std::max(1, std::min<int>(nclusters, (int)std::max(1u, runs)));
+  cfg.gridDim = dim3(ncl * CL);
+  return cudaLaunchKernelEx(&cfg, k3_probe<WB, M, CL>, a);
 }
 
 template <int WB, int M>
 static cudaError_t launch_probe_w(const Seq3Args& a, uint32_t grid, uint32_t smem,
                                   cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k3_probe<WB, M>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) k3_probe<WB, M><<<grid, k3ProbeThreads, smem, st>>>(a);
-  return e;
+  switch (a.cl) {
+    case 2: return launch_probe_wc<WB, M, 2>(a, grid, smem, st);
+    case 4: return launch_probe_wc<WB, M, 4>(a, grid, smem, st);
+    case 8: return launch_probe_wc<WB, M, 8>(a, grid, smem, st);
+    default: return launch_probe_wc<WB, M, 1>(a, grid, smem, st);
+  }
 }
 
 cudaError_t launch_seq3_probe(const Seq3Args& a, uint32_t W, uint32_t grid, cudaStream_t st,
                               uint32_t* nl) {
-  const uint32_t smem = seq3_probe_smem(((uint64_t)1 << a.s) * a.rec);
+  // each CTA stages a slice of L / cl records
+  const uint32_t smem = seq3_probe_smem((((uint64_t)1 << a.s) / std::max(1u, a.cl)) * a.rec);
   cudaError_t e;
   const uint32_t m = a.rec / W;
   if (W == 4 && m == 1) e = launch_probe_w<4, 1>(a, grid, smem, st);

@@ -168,3 +168,25 @@ def test_seq3_unaligned_source_falls_back(dpg):
         dpg.dpg_retrieve(s, dev(rids), path=6)
     got = host(dpg.dpg_retrieve(s, dev(rids)))
     assert np.array_equal(got, oracle.retrieve(src, rids))
+
+
+@pytest.mark.parametrize("cl", [2, 4, 8])
+@pytest.mark.parametrize("rec,n_src,n_out,kind", [(8, 300_001, 250_000, "repl"), (16, 200_000, 200_000, "perm"),
+                                                  (4, 50_000, 120_001, "sorted"), (32, 123_457, 99_999, "equal")])
+def test_seq3_cluster_runs(dpg, cl, rec, n_src, n_out, kind):
+    """Runs held by a thread-block cluster of cl CTAs (each a slice of the run
+    in its shared memory, lookups across the cluster through distributed
+    shared memory): bit-exact on duplicates, permutations, sorted and
+    all-equal rids, with short runs (many runs per cluster) and the automatic
+    slice length."""
+    src, rids = _case(cl * 10 + rec, n_src, rec, n_out, kind)
+    for s in (0, 10):
+        try:
+            p = dpg.dpg_plan(rec, n_src, n_out, path=6, cluster=cl, log2_run=s)
+        except dpg.DPGError:
+            continue
+        assert p["cluster"] == cl
+        out = torch.full((n_out, rec), 0x77, dtype=torch.uint8, device="cuda")
+        dpg.dpg_retrieve(dev(src), dev(rids), dst=out, path=6, cluster=cl, log2_run=s)
+        assert np.array_equal(host(out), oracle.retrieve(src, rids)), s
+        dpg.dpg_sync_status()
