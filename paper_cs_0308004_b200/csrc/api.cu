@@ -38,8 +38,10 @@ bool g_timing = false;
 struct PhaseEvents { cudaEvent_t e0, e1, e2, e3; bool has3; };
 std::vector<PhaseEvents> g_pending, g_pool;
 
+thread_local bool t_nested = false;   // inside path 7's level-2 calls: no events of their own
+
 bool timing_begin(cudaStream_t st, PhaseEvents* pe) {
-  if (!g_timing) return false;
+  if (!g_timing || t_nested) return false;
   std::lock_guard<std::mutex> lk(g_timing_mu);
   if (!g_pool.empty()) { *pe = g_pool.back(); g_pool.pop_back(); }
   else {
@@ -378,6 +380,17 @@ bool plan_l2run(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay, bool
 // Three sequential passes over shared-memory runs (seq3.cu): runs of L = 2^s
 // records, L * rec <= one stage (128 KB: one CTA per SM holds it, the next
 // run is prefetched into L2 meanwhile), 16-bit local offsets (s <= 16).
+// Smallest source (bytes) for which the automatic plan takes two levels.
+uint64_t twolevel_min_bytes() {
+  static uint64_t env = [] {
+    const char* e = getenv("DPG_TWOLEVEL_MIN_MB");
+    return e ? (uint64_t)atoll(e) << 20 : 0ull;
+  }();
+  // measured slower than the single level with clusters at every size tried
+  // (profiles/r02_twolevel.md): on request only unless DPG_TWOLEVEL_MIN_MB is set
+  return env ? env : ~0ull;
+}
+
 uint32_t seq3_cluster_env() {
   static uint32_t env = [] {
     const char* e = getenv("DPG_SEQ3_CLUSTER");
@@ -424,7 +437,9 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     // lookups cost more than the shorter pieces save unless the pieces are
     // that short (profiles/r02_seq3_cluster.md)
     const uint64_t T0 = std::min<uint64_t>(32768, (220ull << 10) / (rec + 2));
-    cl = (T0 << ls) < 2 * n_src && ls < 16 && (2ull << ls) < 2 * n_src ? 2 : 1;
+    cl = 1;
+    while (cl < 4 && ((T0 * cl) << ls) < 2 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
+      cl *= 2;
   }
   const uint32_t lc = cl == 8 ? 3 : cl == 4 ? 2 : cl == 2 ? 1 : 0;
   (void)lcl;
@@ -486,6 +501,37 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   return true;
 }
 
+// Two-level DPG (path 7; the paper's multi-pass DPG: "useful
+// when there is a very small cache in relation to the size of main memory"):
+// the rids are first distributed into super-runs of 2^s1 source records
+// (<= 512 MB each, the regime where the three sequential passes win), the
+// three sequential passes retrieve each super-run's records in its request
+// order, and one gather puts the rows back in output order.  s1 may be forced
+// (log2_run, tests).
+bool plan_twolevel(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
+                   const dpg_options_t* opt, int sm, dpg_plan_t* p) {
+  if (pay || n_out == 0 || n_src < 2 || rec % 4 || rec > 32) return false;
+  if (n_out >= 0xFFFFFFFFull || n_src > (1ull << 32)) return false;
+  uint32_t s1 = 0;
+  if (opt && opt->log2_run) {
+    s1 = opt->log2_run;
+  } else {
+    while ((2ull << s1) * rec <= (512ull << 20)) ++s1;
+  }
+  if (s1 > 31) return false;
+  const uint64_t C = (n_src + (1ull << s1) - 1) >> s1;
+  if (C < 2 || C > 512) return false;
+  std::memset(p, 0, sizeof(*p));
+  p->path = 7;
+  p->log2_run = s1;
+  p->run_len = 1ull << s1;
+  p->num_runs = C;
+  p->word_bytes = pow2_divisor(rec);
+  p->grid_probe = (uint32_t)sm;
+  p->grid_distribute = (uint32_t)sm;
+  return true;
+}
+
 dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
                        const dpg_options_t* opt, int sm, dpg_plan_t* p) {
   if (rec == 0 || !p) return DPG_ERR_INVALID_ARG;
@@ -512,6 +558,15 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
     if (plan_seq3(rec, n_src, n_out, pay, opt, sm, p)) return DPG_OK;
     return DPG_ERR_UNSUPPORTED;
   }
+  if (want_path == 7) {
+    if (plan_twolevel(rec, n_src, n_out, pay, opt, sm, p)) return DPG_OK;
+    return DPG_ERR_UNSUPPORTED;
+  }
+  // Sources of more than 512 MB of small records: two levels (measured:
+  // profiles/r02_twolevel.md)
+  if (want_path == 0 && !overrides && rec <= seq3_auto_max_rec() &&
+      n_src * rec > twolevel_min_bytes() && plan_twolevel(rec, n_src, n_out, pay, opt, sm, p))
+    return DPG_OK;
   // Beyond the L2, records up to seq3_auto_max_rec bytes take the three
   // sequential passes (the paper's small-record case)
   if (want_path == 0 && !overrides && rec <= seq3_auto_max_rec() &&
@@ -928,6 +983,63 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   }
   t_path = p.path;
 
+  if (p.path == 7) {
+    // level 1: the rids by super-run (rid >> s1), every row's slot (inv)
+    const uint32_t s1 = p.log2_run, C = (uint32_t)p.num_runs;
+    uint32_t *local = nullptr, *inv = nullptr;
+    uint64_t* counts = nullptr;
+    uint8_t* internal = nullptr;
+    auto fail = [&](dpg_status_t r) {
+      if (local) cudaFreeAsync(local, st);
+      if (inv) cudaFreeAsync(inv, st);
+      if (counts) cudaFreeAsync(counts, st);
+      if (internal) cudaFreeAsync(internal, st);
+      return r;
+    };
+    if (ws_malloc(&local, n_out * 4 + 64, st) != cudaSuccess ||
+        ws_malloc(&inv, n_out * 4 + 64, st) != cudaSuccess ||
+        ws_malloc(&counts, (uint64_t)C * 8 + 64, st) != cudaSuccess ||
+        ws_malloc(&internal, n_out * rec + 64, st) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DPG_ERR_OOM);
+    }
+    PhaseEvents pe;
+    const bool timed = timing_begin(st, &pe);
+    dpg_status_t r = dpg_partition_inv(rids, 4, n_out, n_src, s1, C, local, inv, counts,
+                                       (dpg_stream_t)st);
+    uint32_t nl = t_launches;
+    if (timed) cudaEventRecord(pe.e1, st);
+    std::vector<uint64_t> cnt(C);
+    if (r == DPG_OK &&
+        (cudaMemcpyAsync(cnt.data(), counts, (uint64_t)C * 8, cudaMemcpyDeviceToHost, st) !=
+             cudaSuccess ||
+         cudaStreamSynchronize(st) != cudaSuccess))
+      r = DPG_ERR_CUDA;
+    // level 2: every super-run's records in its request order (its own plan:
+    // the three sequential passes, or one L2 run for a small last super-run)
+    uint64_t start = 0;
+    for (uint32_t c = 0; c < C && r == DPG_OK; ++c) {
+      const uint64_t lo = (uint64_t)c << s1;
+      const uint64_t n_c = std::min<uint64_t>(1ull << s1, n_src - lo);
+      t_nested = true;
+      if (cnt[c])
+        r = run_dpg((const uint8_t*)src + lo * rec, rec, n_c, local + start, cnt[c], nullptr, 0,
+                    internal + start * rec, st, nullptr);
+      t_nested = false;
+      nl += t_launches;
+      start += cnt[c];
+    }
+    if (timed) timing_phase2_end(pe, st);
+    // level-1 Phase III: dst[i] = INTERNAL[inv[i]] in output order (C streams)
+    if (r == DPG_OK)
+      r = cuda_status(launch_direct(internal, start, (uint32_t)rec, inv, n_out, (uint8_t*)dst,
+                                    pow2_divisor(rec | (uintptr_t)dst), sm, nullptr, st, &nl));
+    if (timed) cudaEventRecord(pe.e2, st);
+    t_path = 7;
+    t_launches = nl + nl_skew;
+    fail(DPG_OK);
+    return r;
+  }
   if (p.path == 6 && ((uintptr_t)src % 16 != 0)) {
     // the stage is one TMA bulk copy of the run: an unaligned source takes the
     // multi-kernel shared-memory runs

@@ -190,3 +190,29 @@ def test_seq3_cluster_runs(dpg, cl, rec, n_src, n_out, kind):
         dpg.dpg_retrieve(dev(src), dev(rids), dst=out, path=6, cluster=cl, log2_run=s)
         assert np.array_equal(host(out), oracle.retrieve(src, rids)), s
         dpg.dpg_sync_status()
+
+
+@pytest.mark.parametrize("rec,n_src,n_out,kind,s1", [(8, 300_001, 250_000, "repl", 16),
+                                                      (16, 200_000, 200_000, "perm", 15),
+                                                      (4, 70_000, 90_001, "sorted", 14),
+                                                      (32, 123_457, 99_999, "equal", 15),
+                                                      (12, 100_000, 150_000, "repl", 12)])
+def test_twolevel(dpg, rec, n_src, n_out, kind, s1):
+    """Two-level DPG (path 7; the paper's multi-pass DPG): the
+    rids distributed into super-runs of 2^s1 records, each super-run retrieved
+    by its own plan, the rows gathered back in output order -- bit-exact,
+    including an invalid rid (reported, row unwritten)."""
+    src, rids = _case(rec + s1, n_src, rec, n_out, kind)
+    rids[n_out // 3] = n_src + 1
+    p = dpg.dpg_plan(rec, n_src, n_out, path=7, log2_run=s1)
+    assert p["path"] == 7 and p["num_runs"] == (n_src + (1 << s1) - 1) >> s1
+    out = torch.full((n_out, rec), 0x3D, dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=out, path=7, log2_run=s1)
+    assert dpg.last_path() == 7
+    with pytest.raises(dpg.DPGError) as e:
+        dpg.dpg_sync_status()
+    assert e.value.index == n_out // 3
+    got = host(out)
+    ok = rids < n_src
+    assert np.array_equal(got[ok], oracle.retrieve(src, rids[ok]))
+    assert (got[~ok] == 0x3D).all()

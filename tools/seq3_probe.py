@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--kinds", default="perm,repl")
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--stage-kb", default="")
+    ap.add_argument("--twolevel", action="store_true", help="also time path 7")
     args = ap.parse_args()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -82,6 +83,15 @@ def main():
                              f" [{ph[0]:.0f}/{ph[1]:.0f}/{ph[2]:.0f}]")
                 except dpg.DPGError as e:
                     line += f"  nbuf{nb} -- {e}"
+            if args.twolevel:
+                out.zero_()
+                try:
+                    t, ph = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out, path=7), phases=True)
+                    ok = torch.equal(out, want)
+                    line += (f"  two-level {t:7.1f}us {'ok' if ok else 'BAD'}"
+                             f" [{ph[0]:.0f}/{ph[1]:.0f}/{ph[2]:.0f}]")
+                except dpg.DPGError as e:
+                    line += f"  two-level -- {e}"
             out.zero_()
             t, _ = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out))
             ok = torch.equal(out, want)
