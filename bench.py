@@ -831,7 +831,8 @@ def run_c5(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         hr = rids.cpu().pin_memory()
-        hd = torch.empty((min(rows, b1 - b0), rec), dtype=torch.uint8).pin_memory()
+        sub = min(rows, b1 - b0, 1 << 24)          # pinned host rows buffer: 1.7 GB at most
+        hd = torch.empty((max(1, sub), rec), dtype=torch.uint8).pin_memory()
         rbuf = torch.empty(min(rows, b1 - b0), dtype=torch.int64, device=dev)
 
         def step_e2e():
@@ -841,8 +842,10 @@ def run_c5(args, rank, world, local):
                 rbuf[:e - a].copy_(hr[a:e], non_blocking=True)
                 dpg.dpg_retrieve_dist(comm, src if hi > lo else src[:0], n_total, rbuf[:e - a],
                                       dst[:e - a])
-                hd[:e - a].copy_(dst[:e - a], non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                for c0 in range(0, e - a, sub):     # the rows back to the host, chunk by chunk
+                    c1 = min(e - a, c0 + sub)
+                    hd[:c1 - c0].copy_(dst[c0:c1], non_blocking=True)
+                    torch.cuda.current_stream().synchronize()
 
         step_e2e()
         dist.barrier()
