@@ -431,14 +431,16 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   uint32_t ls = 0;
   while (ls < 16 && (2ull << ls) * rec <= stage && (1ull << ls) < n_src) ++ls;
   if (cl == 0) {
-    // automatic: one CTA per run, or two (a cluster sharing the run through
-    // distributed shared memory) when one CTA's runs would leave pieces
-    // (tile, run) of fewer than 2 entries on average -- measured: the remote
+    // automatic: one CTA per run, or a cluster of 2-4 sharing the run through
+    // distributed shared memory while one CTA's runs would leave pieces
+    // (tile, run) of fewer than 4 entries on average -- measured: the remote
     // lookups cost more than the shorter pieces save unless the pieces are
     // that short (profiles/r02_seq3_cluster.md)
     const uint64_t T0 = std::min<uint64_t>(32768, (220ull << 10) / (rec + 2));
     cl = 1;
-    while (cl < 4 && ((T0 * cl) << ls) < 2 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
+    // (records of <= 16 bytes; a remote lookup of a 32-byte record already
+    // costs more than it saves -- DSMEM moves ~20 B per cycle per SM)
+    while (rec <= 16 && cl < 4 && ((T0 * cl) << ls) < 4 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
       cl *= 2;
   }
   const uint32_t lc = cl == 8 ? 3 : cl == 4 ? 2 : cl == 2 ? 1 : 0;
