@@ -442,6 +442,12 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     // costs more than it saves -- DSMEM moves ~20 B per cycle per SM)
     while (rec <= 16 && cl < 4 && ((T0 * cl) << ls) < 4 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
       cl *= 2;
+    // more runs than Phase I takes (8192), or pieces of under one entry:
+    // larger runs, whatever the record
+    auto runs = [&](uint32_t c) { return (n_src + ((uint64_t)c << ls) - 1) / ((uint64_t)c << ls); };
+    while (cl < 8 && (runs(cl) > 8192 || runs(cl) * ((n_out + T0 - 1) / T0) > n_out) &&
+           ls + bit_length(cl) < 17)
+      cl *= 2;
   }
   const uint32_t lc = cl == 8 ? 3 : cl == 4 ? 2 : cl == 2 ? 1 : 0;
   (void)lcl;
