@@ -73,6 +73,12 @@ def _load():
         lib.oracle_batch_lookup.argtypes = [P, U, P, U, P]
         lib.oracle_batch_lookup.restype = ctypes.c_int
         lib.oracle_fk_join_sort.restype = ctypes.c_int
+        lib.oracle_splitmix64.argtypes = [U, U]
+        lib.oracle_splitmix64.restype = ctypes.c_uint64
+        lib.oracle_skew_partition.argtypes = [P, U, U, U, U, U, P, P]
+        lib.oracle_skew_partition.restype = ctypes.c_int
+        lib.oracle_dpg_bounds.argtypes = [P, U, U, P, U, P, U, P, P, P, P]
+        lib.oracle_dpg_bounds.restype = ctypes.c_int
         for f in (lib.oracle_retrieve, lib.oracle_retrieve_u64, lib.oracle_dpg_fig1,
                   lib.oracle_fk_join, lib.oracle_retrieve_at, lib.oracle_sort_rids):
             f.restype = ctypes.c_int
@@ -245,3 +251,41 @@ def batch_lookup(keys: np.ndarray, queries: np.ndarray) -> np.ndarray:
     if _load().oracle_batch_lookup(_ptr(keys), keys.size, _ptr(q), q.size, _ptr(out)) != 0:
         raise ValueError("invalid argument")
     return out
+
+
+def splitmix64(seed: int, k: int) -> int:
+    """Draw k of the SplitMix64 sequence started at seed (reading A23)."""
+    return int(_load().oracle_splitmix64(seed, k))
+
+
+def skew_partition(rids: np.ndarray, n_src: int, num_runs: int, sample_size: int,
+                   seed: int) -> np.ndarray:
+    """Run boundaries from a sorted sample of the rids (section 2.3, P:466-475;
+    S:162-170): uint32 [n_runs + 1], 0 < cuts < n_src strictly ascending."""
+    rids = np.ascontiguousarray(rids, dtype=np.uint32)
+    bounds = np.zeros(num_runs + 1, dtype=np.uint32)
+    n = ctypes.c_uint64(0)
+    if _load().oracle_skew_partition(_ptr(rids), rids.size, n_src, num_runs, sample_size, seed,
+                                     _ptr(bounds), ctypes.byref(n)) != 0:
+        raise ValueError("invalid argument")
+    return bounds[:n.value + 1].copy()
+
+
+def dpg_bounds(src: np.ndarray, rids: np.ndarray, bounds: np.ndarray):
+    """Fig. 1 with runs [bounds[k], bounds[k+1]).  Returns a dict
+    with ``dst``, ``run_start`` (n_runs + 1) and ``rid_pos`` (the positions of
+    each run's entries, in Phase I order)."""
+    src = _records(src)
+    n_src, rec = src.shape
+    rids = np.ascontiguousarray(rids, dtype=np.uint32)
+    bounds = np.ascontiguousarray(bounds, dtype=np.uint32)
+    n_runs = bounds.size - 1
+    dst = np.zeros((rids.size, rec), dtype=np.uint8)
+    run_start = np.zeros(n_runs + 1, dtype=np.uint64)
+    rid_pos = np.zeros(rids.size, dtype=np.uint64)
+    bad = ctypes.c_uint64(0)
+    st = _load().oracle_dpg_bounds(_ptr(src), rec, n_src, _ptr(rids), rids.size, _ptr(bounds),
+                                   n_runs, _ptr(dst), _ptr(run_start), _ptr(rid_pos),
+                                   ctypes.byref(bad))
+    _check(st, bad)
+    return {"dst": dst, "run_start": run_start, "rid_pos": rid_pos}

@@ -17,8 +17,11 @@
  * formulation, all rid sequences of length <= 4 over n <= 3 against numpy
  * fancy indexing, identity / multiset / sorted-key invariants, the join's
  * nested-loop cross-check; the 64-bit-rid entries against numpy indexing, the
- * 32-bit entries and a no-truncation check (rids >= 2^32).  No function here
- * is "parity unpinned".
+ * 32-bit entries and a no-truncation check (rids >= 2^32); the skew
+ * partition (tests/test_oracle_skew.py) against SplitMix64's published
+ * sequence, S:166-169's statistical examples and exhaustive tiny cases, and
+ * the boundary-mode Fig. 1 against (2) on multiples of L and the Fig. 2
+ * example.  No function here is "parity unpinned".
  *
  * Return convention (reading A6 of DESIGN.md): 0 on success; -1 on an invalid
  * argument; 1 if some rid >= n_src, in which case *bad_index receives the
@@ -379,5 +382,130 @@ int oracle_batch_lookup(const uint32_t *keys, uint64_t n_keys, const uint32_t *q
                                                                        : 0xFFFFFFFFu;
     }
     free(pairs);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ *
+ * (8) Data skew (section 2.3): "sample the rids from the rid     *
+ *     sequence.  The sampled set of rids is then sorted, and partitions of  *
+ *     the rids are chosen so as to evenly partition the sampled set."       *
+ *     The paper leaves the draw unspecified (reading A23): sample_size      *
+ *     positions are drawn uniformly, with replacement, by the SplitMix64    *
+ *     sequence started at `seed` (draw k = mix(seed + (k+1) * gamma), the   *
+ *     position floor(draw * n_out / 2^64)).  A sampled rid >= n_src counts  *
+ *     as n_src (it never becomes a cut).  The sorted sample s[0..S) gives   *
+ *     the cut candidates s[floor(i * S / num_runs)], i = 1 .. num_runs-1    *
+ *     (S:162-170); a candidate is kept when it is below n_src and larger   *
+ *     than the last kept cut (at first: than the smallest sampled rid), so  *
+ *     equal quantiles collapse, fewer runs may result, and every run holds  *
+ *     at least one sampled rid.  bounds_out[0..n_runs] = 0, cuts..., n_src *
+ *     (room for num_runs + 1 entries); run k = rids in                     *
+ *     [bounds[k], bounds[k+1]).                                            *
+ * ------------------------------------------------------------------------ */
+static uint64_t splitmix64_draw(uint64_t seed, uint64_t k)
+{
+    uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t oracle_splitmix64(uint64_t seed, uint64_t k) { return splitmix64_draw(seed, k); }
+
+static int cmp_u32(const void *a, const void *b)
+{
+    const uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return x < y ? -1 : x > y;
+}
+
+int oracle_skew_partition(const uint32_t *rids, uint64_t n_out, uint64_t n_src,
+                          uint64_t num_runs, uint64_t sample_size, uint64_t seed,
+                          uint32_t *bounds_out, uint64_t *n_runs_out)
+{
+    if (n_out == 0 || n_src == 0 || n_src > 0xFFFFFFFFull || num_runs < 1 ||
+        sample_size < num_runs)
+        return -1;
+    uint32_t *sample = malloc(sample_size * sizeof(uint32_t));
+    if (!sample) return -1;
+    for (uint64_t k = 0; k < sample_size; ++k) {           /* sample the rids */
+        const uint64_t z = splitmix64_draw(seed, k);
+        const uint64_t pos = (uint64_t)(((unsigned __int128)z * n_out) >> 64);
+        const uint32_t r = rids[pos];
+        sample[k] = r < n_src ? r : (uint32_t)n_src;
+    }
+    qsort(sample, sample_size, sizeof(uint32_t), cmp_u32);  /* the sampled set is sorted */
+    uint64_t n = 0;
+    uint32_t last = sample[0];                             /* run 0 holds the smallest sampled rid */
+    bounds_out[n++] = 0;
+    for (uint64_t i = 1; i < num_runs; ++i) {              /* evenly partition the sample */
+        const uint32_t q = sample[i * sample_size / num_runs];
+        if (q > last && q < n_src) bounds_out[n++] = last = q;
+    }
+    bounds_out[n] = (uint32_t)n_src;
+    *n_runs_out = n;
+    free(sample);
+    return 0;
+}
+
+/* Fig. 1 (as in (2)) with the runs given by boundaries instead of the high-   *
+ * order bits ("the N/L partitions of the input sequence of rids must be       *
+ * chosen on some other basis"): run k = [bounds[k], bounds[k+1]),  *
+ * bounds ascending from 0 to n_src (an empty run is allowed).  Phase I finds  *
+ * each rid's run by binary search; Phase II reads run k's records            *
+ * [bounds[k], bounds[k+1]); Phase III as in (2).  run_start_out[n_runs + 1]   *
+ * (may be NULL) receives the RID runs' offsets; rid_pos_out[n_out] (may be    *
+ * NULL) the positions of the entries of each run, in Phase I order.           */
+int oracle_dpg_bounds(const uint8_t *src, uint64_t rec, uint64_t n_src,
+                      const uint32_t *rids, uint64_t n_out, const uint32_t *bounds,
+                      uint64_t n_runs, uint8_t *dst, uint64_t *run_start_out,
+                      uint64_t *rid_pos_out, uint64_t *bad_index)
+{
+    if (rec == 0 || n_runs == 0 || bounds[0] != 0 || bounds[n_runs] != n_src) return -1;
+    for (uint64_t k = 0; k < n_runs; ++k)
+        if (bounds[k] > bounds[k + 1]) return -1;
+    for (uint64_t i = 0; i < n_out; ++i)
+        if ((uint64_t)rids[i] >= n_src) { if (bad_index) *bad_index = i; return 1; }
+    uint64_t *run_of = malloc((n_out ? n_out : 1) * sizeof(uint64_t));
+    uint64_t *run_start = calloc(n_runs + 1, sizeof(uint64_t));
+    uint64_t *cursor = calloc(n_runs + 1, sizeof(uint64_t));
+    uint32_t *RID_RUN = malloc((n_out ? n_out : 1) * sizeof(uint32_t));
+    uint64_t *RID_POS = malloc((n_out ? n_out : 1) * sizeof(uint64_t));
+    uint8_t *RECORD_RUN = malloc((n_out ? n_out : 1) * rec);
+    if (!run_of || !run_start || !cursor || !RID_RUN || !RID_POS || !RECORD_RUN) {
+        free(run_of); free(run_start); free(cursor); free(RID_RUN); free(RID_POS); free(RECORD_RUN);
+        return -1;
+    }
+    for (uint64_t i = 0; i < n_out; ++i) {                 /* the run k with b_k <= r < b_k+1 */
+        uint64_t lo = 0, hi = n_runs;                      /* (the last such k, if runs are empty) */
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (bounds[mid] <= rids[i]) lo = mid; else hi = mid;
+        }
+        run_of[i] = lo;
+        run_start[lo + 1] += 1;
+    }
+    for (uint64_t k = 0; k < n_runs; ++k) run_start[k + 1] += run_start[k];
+    /* Phase I: Append r to RID_RUN[run] */
+    for (uint64_t k = 0; k < n_runs; ++k) cursor[k] = run_start[k];
+    for (uint64_t i = 0; i < n_out; ++i) {
+        RID_RUN[cursor[run_of[i]]] = rids[i];
+        RID_POS[cursor[run_of[i]]] = i;
+        cursor[run_of[i]] += 1;
+    }
+    /* Phase II: run k of INPUT = records [bounds[k], bounds[k+1]) */
+    for (uint64_t k = 0; k < n_runs; ++k) {
+        const uint8_t *input_run = src + (uint64_t)bounds[k] * rec;
+        for (uint64_t j = run_start[k]; j < run_start[k + 1]; ++j)
+            memcpy(RECORD_RUN + j * rec, input_run + (uint64_t)(RID_RUN[j] - bounds[k]) * rec, rec);
+    }
+    /* Phase III: the next record of the rid's run, in RID order */
+    for (uint64_t k = 0; k < n_runs; ++k) cursor[k] = run_start[k];
+    for (uint64_t i = 0; i < n_out; ++i) {
+        memcpy(dst + i * rec, RECORD_RUN + cursor[run_of[i]] * rec, rec);
+        cursor[run_of[i]] += 1;
+    }
+    if (run_start_out) memcpy(run_start_out, run_start, (n_runs + 1) * sizeof(uint64_t));
+    if (rid_pos_out) memcpy(rid_pos_out, RID_POS, n_out * sizeof(uint64_t));
+    free(run_of); free(run_start); free(cursor); free(RID_RUN); free(RID_POS); free(RECORD_RUN);
     return 0;
 }
