@@ -205,6 +205,55 @@ dpg_status_t dpg_distribute(const uint32_t *rids, uint64_t n_out, uint64_t n_src
                             uint64_t *run_start_out, dpg_stream_t stream,
                             const dpg_options_t *opt);
 
+/* ---- Data skew: runs from a sorted sample of the rids (section 2.3) ----
+ * "If there is a great deal of data skew ... the N/L partitions of the input
+ * sequence of rids must be chosen on some other basis than the high order
+ * bits ... sample the rids from the rid sequence.  The sampled set of rids is
+ * then sorted, and partitions of the rids are chosen so as to evenly
+ * partition the sampled set" (reading A23).
+ *
+ * dpg_skew_partition: draws sample_size rids of rids[n_out] (device) at
+ * uniform positions (with replacement; the SplitMix64 sequence started at
+ * `seed`, so the result is a function of its arguments), sorts them, and
+ * takes the cut candidates sample[i * sample_size / num_runs], i = 1 ..
+ * num_runs - 1; a candidate is kept when it is below n_src and above the last
+ * kept cut (at first: above the smallest sampled rid), so ties collapse.
+ * bounds_out (HOST, room for num_runs + 1 uint32) receives 0, the cuts, n_src
+ * -- strictly ascending; *n_runs_out (host) the number of runs (<= num_runs;
+ * every run holds at least one sampled rid).  A sampled rid >= n_src counts as
+ * n_src.  Synchronous (one stream synchronisation).  Errors: n_out == 0,
+ * num_runs == 0 or sample_size < num_runs -> DPG_ERR_INVALID_ARG;
+ * sample_size > 32768 or n_src >= 2^32 -> DPG_ERR_UNSUPPORTED. */
+dpg_status_t dpg_skew_partition(const uint32_t *rids, uint64_t n_out, uint64_t n_src,
+                                uint32_t num_runs, uint32_t sample_size, uint64_t seed,
+                                uint32_t *bounds_out, uint32_t *n_runs_out,
+                                dpg_stream_t stream);
+
+/* dpg_retrieve with the runs given by boundaries: run k holds the rids in
+ * [bounds[k], bounds[k+1]) (bounds: HOST, n_runs + 1 uint32, bounds[0] = 0,
+ * bounds[n_runs] = n_src < 2^32, non-decreasing -- else DPG_ERR_INVALID_ARG).
+ * Runs wider than a shared-memory stage are split at the multiples of the
+ * plan's L = 2^s (constraint (1)); the multi-kernel plan (path 2)
+ * runs them.  Result, device buffers and error rules as dpg_retrieve; records
+ * too large for a shared-memory stage -> DPG_ERR_UNSUPPORTED.  The layout is
+ * uploaded with a pageable copy (the call may wait for the stream). */
+dpg_status_t dpg_retrieve_bounds(const void *src, size_t rec_bytes, uint64_t n_src,
+                                 const uint32_t *rids, uint64_t n_out, const uint32_t *bounds,
+                                 uint64_t n_runs, void *dst, dpg_stream_t stream);
+
+/* Phase I alone over boundary runs (tests): the runs are the caller's bounds
+ * (HOST, as dpg_retrieve_bounds) merged with the multiples of L = 2^log2_run,
+ * a caller bound equal to a multiple of L leaving an empty run before it;
+ * *num_runs_out (host) receives their number K = n_runs + ceil(n_src / L) - 1.
+ * pairs_out[n_out] (device) = (rid - start of its run) | (pos << 32), the
+ * entries of run b in [run_start_out[b], run_start_out[b+1]) (device, K + 1
+ * uint64), unordered within a run as dpg_distribute.  run_start_out == NULL:
+ * only *num_runs_out is set. */
+dpg_status_t dpg_distribute_bounds(const uint32_t *rids, uint64_t n_out, uint64_t n_src,
+                                   const uint32_t *bounds, uint64_t n_runs, uint32_t log2_run,
+                                   uint64_t *pairs_out, uint64_t *run_start_out,
+                                   uint64_t *num_runs_out, dpg_stream_t stream);
+
 /* Multi-GPU Phase I by owner: rids (uint32 or uint64,
  * rid_bytes = 4 or 8, device) are distributed to owners r >> log2_span
  * (parts owners, each owning 2^log2_span consecutive source records of the

@@ -45,6 +45,7 @@ EXPORTED = (
     "dpg_version", "dpg_phase_timing", "dpg_phase_times", "dpg_debug_phase_stamps",
     "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
     "dpg_phase_times_ex", "dpg_retrieve_dist_loopback", "dpg_fk_join_direct",
+    "dpg_skew_partition", "dpg_retrieve_bounds", "dpg_distribute_bounds",
 )
 
 
@@ -114,6 +115,9 @@ _sigs = {
     "dpg_ipc_open": [_P, _P],
     "dpg_ipc_close": [_P],
     "dpg_ipc_free": [_P],
+    "dpg_skew_partition": [_P, _U, _U, ctypes.c_uint32, ctypes.c_uint32, _U, _P, _P, _P],
+    "dpg_retrieve_bounds": [_P, _S, _U, _P, _U, _P, _U, _P, _P],
+    "dpg_distribute_bounds": [_P, _U, _U, _P, _U, ctypes.c_uint32, _P, _P, _P, _P],
 }
 for _name, _args in _sigs.items():
     _f = getattr(_lib, _name)
@@ -334,6 +338,66 @@ def dpg_distribute(rids, n_src: int, log2_run: int, stream=None, **opts):
     _check(_lib.dpg_distribute(rids.data_ptr(), n_out, n_src, log2_run, pairs.data_ptr(),
                                rs.data_ptr(), _stream_ptr(stream), _ref(_options(**opts))),
            "dpg_distribute")
+    return pairs[:n_out], rs
+
+
+def _host_bounds(bounds):
+    import numpy as np
+    b = np.ascontiguousarray(np.asarray(bounds), dtype=np.uint32)
+    if b.ndim != 1 or b.size < 2:
+        raise ValueError("bounds: 1-D, at least two entries (0 ... n_src)")
+    return b
+
+
+def dpg_skew_partition(rids, n_src: int, num_runs: int, sample_size: int = 16384, seed: int = 0,
+                       stream=None):
+    """Run boundaries from a sorted sample of the rids (section 2.3):
+    numpy uint32 [n_runs + 1] = 0, cuts..., n_src (synchronous)."""
+    import numpy as np
+    rids = _rid_tensor(rids)
+    out = np.zeros(num_runs + 1, dtype=np.uint32)
+    n = ctypes.c_uint32(0)
+    _check(_lib.dpg_skew_partition(rids.data_ptr(), rids.numel(), n_src, num_runs, sample_size,
+                                   seed, out.ctypes.data, ctypes.addressof(n),
+                                   _stream_ptr(stream)), "dpg_skew_partition")
+    return out[:n.value + 1].copy()
+
+
+def dpg_retrieve_bounds(src, rids, bounds, dst=None, stream=None):
+    """``dst[i] = src[rids[i]]`` by DPG with runs [bounds[k], bounds[k+1])
+    (host array; bounds[0] = 0, bounds[-1] = n_src)."""
+    torch = _torch()
+    src = _records(src, "src")
+    rids = _rid_tensor(rids)
+    n_src, rec = src.shape
+    n_out = rids.numel()
+    b = _host_bounds(bounds)
+    if dst is None:
+        dst = torch.empty((n_out, rec), dtype=torch.uint8, device=src.device)
+    _check(_lib.dpg_retrieve_bounds(src.data_ptr(), rec, n_src, rids.data_ptr(), n_out,
+                                    b.ctypes.data, b.size - 1, dst.data_ptr(),
+                                    _stream_ptr(stream)), "dpg_retrieve_bounds")
+    return dst
+
+
+def dpg_distribute_bounds(rids, n_src: int, bounds, log2_run: int, stream=None):
+    """Phase I over the bounds merged with the multiples of 2^log2_run.
+    Returns (pairs int64 [n_out] = (rid - run start) | pos << 32, run_start
+    int64 [K+1]) as CUDA tensors."""
+    torch = _torch()
+    rids = _rid_tensor(rids)
+    n_out = rids.numel()
+    b = _host_bounds(bounds)
+    K = ctypes.c_uint64(0)
+    _check(_lib.dpg_distribute_bounds(None, n_out, n_src, b.ctypes.data, b.size - 1, log2_run,
+                                      None, None, ctypes.addressof(K), None),
+           "dpg_distribute_bounds")
+    pairs = torch.empty(max(n_out, 1), dtype=torch.int64, device=rids.device)
+    rs = torch.empty(K.value + 1, dtype=torch.int64, device=rids.device)
+    _check(_lib.dpg_distribute_bounds(rids.data_ptr(), n_out, n_src, b.ctypes.data, b.size - 1,
+                                      log2_run, pairs.data_ptr(), rs.data_ptr(),
+                                      ctypes.addressof(K), _stream_ptr(stream)),
+           "dpg_distribute_bounds")
     return pairs[:n_out], rs
 
 

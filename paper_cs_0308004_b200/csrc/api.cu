@@ -27,6 +27,7 @@ thread_local uint32_t t_launches = 0;
 thread_local uint32_t t_path = 0;        // plan path of the last retrieval on this thread
 thread_local const OutSegs* t_seg = nullptr;   // output segments of the current call (or none)
 thread_local uint64_t* t_seq3_pairs = nullptr; // tests: path 6 Phase I pairs (dpg_distribute)
+thread_local const BoundsLayout* t_bounds = nullptr;   // boundary-mode runs of the current call
 unsigned long long* g_debug_ts = nullptr;   // profiling: per-CTA phase stamps (dpg_debug_phase_stamps)
 uint32_t g_debug_flags = 0;                 // tuning experiments only (dpg_debug_flags)
 
@@ -920,6 +921,14 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     return dpg_retrieve_direct(src, rec, n_src, rids, n_out, dst, (dpg_stream_t)st);
   }
   if (ps != DPG_OK) return ps;
+  if (t_bounds) {
+    // runs from boundaries (dpg_retrieve_bounds): the multi-kernel plan over
+    // the merged layout's K runs
+    if (p.path != 2) return DPG_ERR_UNSUPPORTED;
+    p.num_runs = t_bounds->K;
+    dpg_status_t gs = dist_geometry(p.num_runs, n_out, opt, sm, &p);
+    if (gs != DPG_OK) return gs;
+  }
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
   uint32_t nl_skew = 0;
@@ -1381,6 +1390,8 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   d.pay_bytes = (uint32_t)pay;
   d.hist_smem = p.hist_in_smem;
   d.status = status;
+  d.bmap = t_bounds ? t_bounds->bmap : nullptr;
+  d.btab = t_bounds ? t_bounds->btab : nullptr;
   PhaseEvents pe;
   const bool timed = timing_begin(st, &pe);
   cudaError_t e = launch_distribute(d, false, st, &nl);
@@ -1403,6 +1414,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     a.slot_pairs = p.slot_pairs;
     a.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
     a.slot_bytes = (p.smem_bytes - kBarBytes) / 2;
+    a.bmap = d.bmap;
     uintptr_t outs = (uintptr_t)dst;
     if (t_seg) {
       a.seg = *t_seg;   // the probe writes each row to its segment
@@ -1674,8 +1686,9 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   cudaStream_t st = (cudaStream_t)stream;
   const int sm = current_sm_count();
   const uint64_t L = 1ull << log2_run;
-  const uint64_t K = (n_src + L - 1) >> log2_run;
+  const uint64_t K = t_bounds ? t_bounds->K : (n_src + L - 1) >> log2_run;
   if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
+  if (t_bounds && opt && opt->path == 6) return DPG_ERR_UNSUPPORTED;
   unsigned long long* status0 = device_status();
   if (!status0) return DPG_ERR_CUDA;
   if (opt && opt->path == 6 && n_out) {
@@ -1767,6 +1780,8 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   d.pair_bytes = p.pair_bytes;
   d.hist_smem = p.hist_in_smem;
   d.status = status;
+  d.bmap = t_bounds ? t_bounds->bmap : nullptr;
+  d.btab = t_bounds ? t_bounds->btab : nullptr;
   if (e == cudaSuccess && n_out) e = launch_distribute(d, false, st, &nl);
   if (e == cudaSuccess) {
     if (!n_out) {

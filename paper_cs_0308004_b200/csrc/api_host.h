@@ -33,6 +33,16 @@ inline cudaError_t ws_malloc(T** p, size_t bytes, cudaStream_t st) {
   return ws_malloc(reinterpret_cast<void**>(p), bytes, st);
 }
 dpg_status_t cuda_status(cudaError_t e);
+dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
+                       const dpg_options_t* opt, int sm, dpg_plan_t* p);
+// Boundary-mode runs (section 2.3): the device layout of the current call on
+// this thread (set around run_dpg / dpg_distribute by the bounds entry points).
+struct BoundsLayout {
+  const uint32_t* bmap;   // [K+1] run starts: the caller's bounds merged with the multiples of L
+  const uint32_t* btab;   // [ceil(n_src/L)+1] index in bmap of the run starting at h*L
+  uint64_t K;
+};
+extern thread_local const BoundsLayout* t_bounds;
 dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32_t* rids,
                      uint64_t n_out, const void* pay_src, uint64_t pay, void* dst, cudaStream_t st,
                      const dpg_options_t* opt);

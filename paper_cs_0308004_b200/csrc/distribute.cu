@@ -2,7 +2,9 @@
 //
 // "One distributes the rids of RID_LIST into appropriate RID runs according
 // to the values of the rids"; the run of rid r is given by its
-// high-order bits: run(r) = r >> s, L = 2^s (reading A1).
+// high-order bits: run(r) = r >> s, L = 2^s (reading A1) -- or,
+// under data skew, by boundaries from a sorted sample of the rids merged with
+// the multiples of L (section 2.3; bounds_run, reading A23).
 //
 // B200 form: a counting distribution over K runs and G contiguous chunks of
 // the rid list (one CTA per chunk), in three steps:
@@ -52,7 +54,8 @@ __global__ void __launch_bounds__(kDistThreads) k_count(DistArgs a) {
       uint64_t i = base + (uint64_t)u * blockDim.x;
       if (i >= hi) continue;
       if (r[u] >= a.n_src) { report_bad(a.status, i); continue; }
-      uint32_t b = (uint32_t)(r[u] >> a.s);
+      uint32_t b0;
+      uint32_t b = a.bmap ? bounds_run(a.bmap, a.btab, a.s, r[u], &b0) : (uint32_t)(r[u] >> a.s);
       if (a.hist_smem) atomicAdd(&hist[b], 1u);
       else atomicAdd(&a.counts[(uint64_t)b * a.G + c], 1u);
     }
@@ -194,10 +197,11 @@ __global__ void __launch_bounds__(kDistThreads) k_scatter(DistArgs a) {
     for (int u = 0; u < U; ++u) {
       uint64_t i = base + (uint64_t)u * blockDim.x;
       if (i >= hi || r[u] >= a.n_src) continue;
-      uint32_t b = (uint32_t)(r[u] >> a.s);
+      uint32_t b0 = 0;
+      uint32_t b = a.bmap ? bounds_run(a.bmap, a.btab, a.s, r[u], &b0) : (uint32_t)(r[u] >> a.s);
       uint32_t slot = a.hist_smem ? atomicAdd(&cur[b], 1u)
                                   : atomicAdd(&a.counts[(uint64_t)b * a.G + c], 1u);
-      uint64_t local = r[u] & lmask;
+      uint64_t local = a.bmap ? r[u] - b0 : r[u] & lmask;
       if (sizeof(PairT) == 4)
         pairs[slot] = (PairT)((i << a.s) | local);
       else

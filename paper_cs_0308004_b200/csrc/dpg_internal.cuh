@@ -178,7 +178,27 @@ struct DistArgs {
   uint32_t pay_bytes;
   uint32_t hist_smem;     // 1: shared-memory histogram of K counters
   unsigned long long* status;
+  // Boundary-mode runs (section 2.3; null: run = r >> s):
+  // run b = [bmap[b], bmap[b+1]), at most L = 2^s records wide; btab[h] =
+  // the run starting at h*L (a multiple of L is always a run start).
+  const uint32_t* bmap;   // [K+1]
+  const uint32_t* btab;   // [ceil(n_src / L) + 1], btab[last] = K
 };
+
+// Run of rid r in boundary mode: the last b in [btab[h], btab[h+1]) with
+// bmap[b] <= r, h = r >> s (the multiples of L bound the search).
+__device__ __forceinline__ uint32_t bounds_run(const uint32_t* __restrict__ bmap,
+                                               const uint32_t* __restrict__ btab, uint32_t s,
+                                               uint64_t r, uint32_t* start) {
+  const uint32_t h = (uint32_t)(r >> s);
+  uint32_t lo = __ldg(btab + h), hi = __ldg(btab + h + 1);
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((uint64_t)__ldg(bmap + mid) <= r) lo = mid; else hi = mid;
+  }
+  *start = __ldg(bmap + lo);
+  return lo;
+}
 
 // Output split into segments (dpg_retrieve_segments; the multi-GPU exchange
 // writes each requester's replies straight into its window over NVLink):
@@ -220,6 +240,7 @@ struct ProbeArgs {
   uint32_t region_cap;         // bytes reserved for a region in a stage
   uint32_t slot_bytes;         // total bytes per stage
   OutSegs seg;                 // output segments (seg.n = 0: dst)
+  const uint32_t* bmap;        // boundary-mode runs [K+1] (DistArgs), or null
 };
 
 // One persistent cooperative kernel for the whole path (fused.cu).
@@ -521,6 +542,12 @@ void t_launches_set(uint32_t n);
 cudaError_t launch_skew_check(const uint32_t* rids, uint64_t n_out, uint64_t n_src, uint32_t s,
                               uint32_t K, uint32_t cap, uint32_t S, uint32_t* hist,
                               unsigned long long* out, cudaStream_t st, uint32_t* nl);
+// Run boundaries from a sorted sample of S <= 32768 rids (skew.cu, reading
+// A23): bounds[0..*n_runs] (room for K + 1), one CTA.
+constexpr uint32_t kSkewMaxSample = 32768;
+cudaError_t launch_skew_partition(const uint32_t* rids, uint64_t n_out, uint32_t n_src, uint32_t K,
+                                  uint32_t S, uint64_t seed, uint32_t* bounds, uint32_t* n_runs,
+                                  cudaStream_t st, uint32_t* nl);
 cudaError_t launch_zip_gather(const uint8_t* a, uint32_t a_bytes, const uint8_t* b, uint32_t b_bytes,
                               uint64_t n_b, const uint32_t* idx, uint64_t n, uint8_t* out, uint32_t W,
                               int sm, cudaStream_t st, uint32_t* nlaunch,

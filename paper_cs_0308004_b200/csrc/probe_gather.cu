@@ -80,8 +80,8 @@ struct Ranges {
 
 __device__ __forceinline__ Ranges item_ranges(const ProbeArgs& a, const Item& it) {
   Ranges g;
-  uint64_t rec0 = (uint64_t)it.b << a.s;
-  uint64_t rec1 = min_u64(a.n_src, rec0 + (1ull << a.s));
+  uint64_t rec0 = a.bmap ? (uint64_t)__ldg(a.bmap + it.b) : (uint64_t)it.b << a.s;
+  uint64_t rec1 = a.bmap ? (uint64_t)__ldg(a.bmap + it.b + 1) : min_u64(a.n_src, rec0 + (1ull << a.s));
   g.r0 = a.src + rec0 * a.rec;
   g.r1 = a.src + rec1 * a.rec;
   const uint8_t* pb = reinterpret_cast<const uint8_t*>(a.pairs);

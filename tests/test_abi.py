@@ -145,3 +145,43 @@ def test_plan_pair_packing_and_overrides(dpg):
         dpg.dpg_plan(0, 10, 10)
     j = dpg.dpg_plan(64, 1 << 24, 1 << 26, pay_bytes=16)
     assert j["pay_bytes"] == 16 and j["word_bytes"] == 16
+
+
+def test_bounds_entry_points_host_checks(dpg):
+    """Boundary-mode runs (section 2.3): host-side validation and the merged
+    layout's size (bounds merged with the multiples of L), no CUDA call."""
+    lib = dpg.raw_lib()
+    U32 = ctypes.c_uint32
+    p = ctypes.c_void_p(0x10000)
+    q = ctypes.c_void_p(0x90000000)
+    r = ctypes.c_void_p(0x40000000)
+    K = ctypes.c_uint64(0)
+
+    def b(*v):
+        return (U32 * len(v))(*v)
+
+    # size query: K = n_runs + ceil(n_src / L) - 1
+    assert lib.dpg_distribute_bounds(None, 0, 1000, b(0, 10, 500, 1000), 3, 8, None, None,
+                                     ctypes.byref(K), None) == dpg.DPG_OK
+    assert K.value == 3 + 4 - 1
+    assert lib.dpg_distribute_bounds(None, 0, 100, b(0, 100), 1, 10, None, None,
+                                     ctypes.byref(K), None) == dpg.DPG_OK
+    assert K.value == 1
+    for bad in [b(1, 100), b(0, 99), b(0, 60, 50, 100)]:
+        n = len(bad) - 1
+        assert lib.dpg_distribute_bounds(None, 0, 100, bad, n, 4, None, None, ctypes.byref(K),
+                                         None) == dpg.DPG_ERR_INVALID_ARG
+        assert lib.dpg_retrieve_bounds(p, 8, 100, r, 10, bad, n, q, None) == \
+            dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve_bounds(p, 8, 100, r, 10, None, 1, q, None) == dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve_bounds(p, 0, 100, r, 10, b(0, 100), 1, q, None) == \
+        dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_retrieve_bounds(p, 8, 100, r, 0, b(0, 100), 1, q, None) == dpg.DPG_OK
+    n_runs = U32(0)
+    out = (U32 * 10)()
+    assert lib.dpg_skew_partition(r, 0, 100, 4, 16, 0, out, ctypes.byref(n_runs), None) == \
+        dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_skew_partition(r, 10, 100, 8, 4, 0, out, ctypes.byref(n_runs), None) == \
+        dpg.DPG_ERR_INVALID_ARG
+    assert lib.dpg_skew_partition(r, 10, 100, 4, 40000, 0, out, ctypes.byref(n_runs), None) == \
+        dpg.DPG_ERR_UNSUPPORTED
