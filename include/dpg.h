@@ -110,6 +110,9 @@ typedef struct {
     uint32_t tile;          /* rids per Phase I tile of a CTA (fused, path 6)   */
     uint32_t cluster;       /* path 6: CTAs (SMs) whose shared memory holds one
                                run together (thread-block cluster, DSMEM)      */
+    uint32_t dist_radix;    /* path 2: Phase I as this many stable 8-bit radix
+                               passes over the run index (0 = counting
+                               distribute with atomics)                        */
 } dpg_plan_t;
 
 /* Optional overrides for tests and tuning (zero = automatic).  The output
@@ -119,7 +122,8 @@ typedef struct {
     uint32_t grid_distribute;
     uint32_t grid_probe;
     uint32_t pair_bytes;    /* force 8-byte pairs                               */
-    uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global    */
+    uint32_t hist_mode;     /* 0 auto, 1 force shared-memory, 2 force global,
+                               3 force radix passes (path 2, no payload)       */
     uint32_t path;          /* 0 auto, 1 force fused kernel, 2 force multi-kernel,
                                3 force the L2-run kernel (any source size),
                                4 two L2 runs (rec % 4 == 0, 8..116 bytes),

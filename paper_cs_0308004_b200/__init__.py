@@ -65,7 +65,7 @@ class Plan(ctypes.Structure):
                                        "grid_distribute", "grid_probe", "hist_in_smem",
                                        "pay_bytes", "path", "nstages", "stage_bytes",
                                        "gather", "npre", "rid_cache", "hist_warps",
-                                       "tile", "cluster")]
+                                       "tile", "cluster", "dist_radix")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

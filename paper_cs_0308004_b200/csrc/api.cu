@@ -142,7 +142,7 @@ dpg_status_t dist_geometry(uint64_t K, uint64_t n_out, const dpg_options_t* opt,
   uint64_t G = std::min<uint64_t>((uint64_t)2 * sm, std::max<uint64_t>(1, (n_out + 2047) / 2048));
   uint32_t hist_mode = opt ? opt->hist_mode : 0;
   bool smem_hist = hist_mode == 1 ? (K * 4 <= kSmemLimit)
-                 : hist_mode == 2 ? false
+                 : hist_mode >= 2 ? false
                                   : (K <= kHistSmemMax);
   if (hist_mode == 1 && !smem_hist) return DPG_ERR_UNSUPPORTED;
   if (!smem_hist) G = std::min<uint64_t>(G, (uint64_t)sm);
@@ -634,7 +634,13 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   const uint64_t L = 1ull << s;
   const uint64_t K = (nsrc + L - 1) >> s;
   if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
-  const uint32_t pb = pair_bytes_for(s);
+  // Phase I: counting distribute with per-CTA run histograms in shared memory
+  // while K counters fit, else stable radix passes over the run index (their
+  // 8-byte elements carry the rid; reading A24)
+  const uint32_t hm = opt ? opt->hist_mode : 0;
+  if (hm == 3 && pay) return DPG_ERR_UNSUPPORTED;
+  const bool radix = pay == 0 && (hm == 3 || (hm == 0 && K > kHistSmemMax));
+  const uint32_t pb = radix ? 8u : pair_bytes_for(s);
   // Pair chunk per stage: 2L when it fits (Poisson slack for with-replacement
   // rids), else 1.5L, else L; a heavier run is processed in several chunks.
   uint32_t sp = 0;
@@ -652,8 +658,13 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   p->num_runs = K;
   p->word_bytes = pow2_divisor(rec | pay);
   p->pay_bytes = (uint32_t)pay;
-  dpg_status_t ds = dist_geometry(K, n_out, opt, sm, p);
+  dpg_status_t ds = radix ? DPG_OK : dist_geometry(K, n_out, opt, sm, p);
   if (ds != DPG_OK) return ds;
+  if (radix) {
+    p->hist_in_smem = 0;
+    p->grid_distribute = (uint32_t)sm;     // cooperative passes: one CTA per SM
+    p->dist_radix = radix_passes(K);
+  }
   uint64_t gp = std::min<uint64_t>(K, (uint64_t)sm);
   if (opt && opt->grid_probe) gp = opt->grid_probe;
   p->grid_probe = (uint32_t)std::max<uint64_t>(1, gp);
@@ -666,17 +677,28 @@ struct Workspace {
   uint32_t* run_start = nullptr;
   void* pairs = nullptr;
   uint8_t* pay = nullptr;
+  // probe work items (path 2): chunk counts, scan partials, first item per run, run per item
+  uint32_t *item_cnt = nullptr, *item_part = nullptr, *item_start = nullptr, *item_run = nullptr;
+  uint64_t* tmp = nullptr;   // radix Phase I ping-pong buffer (n_out elements)
 };
 
 dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t st, Workspace* w) {
   const uint64_t K = p.num_runs, G = p.grid_distribute;
-  const uint64_t M = K * G;
+  const uint64_t M = (p.dist_radix ? 256 : K) * G;   // counts: per (run or digit, CTA)
   const uint64_t ntiles = (M + 4095) / 4096;
   uint64_t off_counts = 0;
   uint64_t off_rs = align_up(off_counts + M * 4, 256);
   uint64_t off_pairs = align_up(off_rs + (K + 1 + ntiles) * 4, 256);
   uint64_t off_pay = align_up(off_pairs + n_out * p.pair_bytes + 64, 256);
-  uint64_t total = align_up(off_pay + (p.pay_bytes ? n_out * p.pay_bytes + 64 : 0), 256);
+  uint64_t end = align_up(off_pay + (p.pay_bytes ? n_out * p.pay_bytes + 64 : 0), 256);
+  uint64_t off_items = end;
+  if (p.slot_pairs) {   // K chunk counts | partials | K+1 item starts | items (<= K + n_out/SP)
+    const uint64_t items = K + (n_out + p.slot_pairs - 1) / p.slot_pairs + 1;
+    end = align_up(off_items + (K + (K + 4095) / 4096 + K + 1 + items) * 4, 256);
+  }
+  const uint64_t off_tmp = end;
+  if (p.dist_radix >= 2) end = align_up(off_tmp + n_out * 8 + 64, 256);
+  const uint64_t total = end;
   void* b = nullptr;
   if (ws_malloc(&b, total, st) != cudaSuccess) {
     cudaGetLastError();
@@ -687,6 +709,13 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
   w->run_start = (uint32_t*)(w->base + off_rs);
   w->pairs = w->base + off_pairs;
   w->pay = p.pay_bytes ? w->base + off_pay : nullptr;
+  if (p.dist_radix >= 2) w->tmp = (uint64_t*)(w->base + off_tmp);
+  if (p.slot_pairs) {
+    w->item_cnt = (uint32_t*)(w->base + off_items);
+    w->item_part = w->item_cnt + K;
+    w->item_start = w->item_part + (K + 4095) / 4096;
+    w->item_run = w->item_start + K + 1;
+  }
   return DPG_OK;
 }
 
@@ -926,6 +955,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     // the merged layout's K runs
     if (p.path != 2) return DPG_ERR_UNSUPPORTED;
     p.num_runs = t_bounds->K;
+    p.dist_radix = 0;
     dpg_status_t gs = dist_geometry(p.num_runs, n_out, opt, sm, &p);
     if (gs != DPG_OK) return gs;
   }
@@ -1368,9 +1398,16 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   if (as != DPG_OK) return as;
   uint32_t nl = 0;
   const uint64_t M = p.num_runs * (uint64_t)p.grid_distribute;
-  if (!p.hist_in_smem) {
+  if (!p.hist_in_smem && !p.dist_radix) {
     cudaError_t e = cudaMemsetAsync(w.counts, 0, M * 4, st);
     if (e != cudaSuccess) { cudaFreeAsync(w.base, st); return cuda_status(e); }
+  }
+  uint32_t* gbar = nullptr;
+  if (p.dist_radix) {
+    uint32_t* tot = nullptr;
+    void* scr = nullptr;
+    dpg_status_t gs = persist_ws(st, 1, 0, &gbar, &tot, &scr, &ws_hold);
+    if (gs != DPG_OK) { cudaFreeAsync(w.base, st); return gs; }
   }
   DistArgs d;
   std::memset(&d, 0, sizeof(d));
@@ -1394,7 +1431,14 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   d.btab = t_bounds ? t_bounds->btab : nullptr;
   PhaseEvents pe;
   const bool timed = timing_begin(st, &pe);
-  cudaError_t e = launch_distribute(d, false, st, &nl);
+  cudaError_t e = p.dist_radix
+                      ? launch_radix_distribute(rids, n_out, n_src, p.log2_run, d.K, w.tmp,
+                                                (uint64_t*)w.pairs, w.counts, gbar + 16,
+                                                w.run_start, sm, st, &nl, status)
+                      : launch_distribute(d, false, st, &nl);
+  if (e == cudaSuccess)
+    e = launch_items(w.run_start, d.K, p.slot_pairs, w.item_cnt, w.item_part, w.item_start,
+                     w.item_run, st, &nl);
   if (timed) cudaEventRecord(pe.e1, st);
   if (e == cudaSuccess) {
     ProbeArgs a;
@@ -1415,6 +1459,9 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     a.region_cap = (uint32_t)align_up(p.run_len * rec + 32, 16);
     a.slot_bytes = (p.smem_bytes - kBarBytes) / 2;
     a.bmap = d.bmap;
+    a.item_start = w.item_start;
+    a.item_run = w.item_run;
+    a.rid_pairs = p.dist_radix ? 1u : 0u;
     uintptr_t outs = (uintptr_t)dst;
     if (t_seg) {
       a.seg = *t_seg;   // the probe writes each row to its segment
@@ -1757,12 +1804,35 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   p.pair_bytes = (!force8 && log2_run + bit_length(n_out ? n_out - 1 : 0) <= 32) ? 4 : 8;
   dpg_status_t ds = dist_geometry(K, n_out, opt, sm, &p);
   if (ds != DPG_OK) return ds;
+  if (opt && opt->hist_mode == 3 && !t_bounds) {   // radix passes (reading A24)
+    p.dist_radix = radix_passes(K);
+    p.grid_distribute = (uint32_t)sm;
+    p.hist_in_smem = 0;
+    p.pair_bytes = 8;
+  }
   unsigned long long* status = device_status();
   if (!status) return DPG_ERR_CUDA;
   Workspace w;
   dpg_status_t as = alloc_workspace(p, n_out, st, &w);
   if (as != DPG_OK) return as;
   uint32_t nl = 0;
+  if (p.dist_radix) {
+    WsHold hold;
+    uint32_t *gbar = nullptr, *tot = nullptr;
+    void* scr = nullptr;
+    dpg_status_t gs = persist_ws(st, 1, 0, &gbar, &tot, &scr, &hold);
+    cudaError_t e = gs == DPG_OK ? cudaSuccess : cudaErrorMemoryAllocation;
+    if (e == cudaSuccess)
+      e = launch_radix_distribute(rids, n_out, n_src, log2_run, (uint32_t)K, w.tmp,
+                                  (uint64_t*)w.pairs, w.counts, gbar + 16, w.run_start, sm, st,
+                                  &nl, status);
+    if (e == cudaSuccess)
+      e = launch_radix_unpack((const uint64_t*)w.pairs, n_out, log2_run, w.run_start, (uint32_t)K,
+                              pairs_out, run_start_out, st, &nl);
+    cudaFreeAsync(w.base, st);
+    t_launches = nl;
+    return gs != DPG_OK ? gs : cuda_status(e);
+  }
   cudaError_t e = cudaSuccess;
   if (!p.hist_in_smem) e = cudaMemsetAsync(w.counts, 0, K * (uint64_t)p.grid_distribute * 4, st);
   DistArgs d;

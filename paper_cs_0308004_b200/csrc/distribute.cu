@@ -257,6 +257,36 @@ uint32_t count_scan_partials(uint64_t K, uint64_t G) {
   return (uint32_t)((K * G + kScanTile - 1) / kScanTile);
 }
 
+// Work items of the probe-gather kernel: ic[b] = chunks of SP pairs in run b,
+// item_start = their exclusive scan, item_run[item_start[b] + j] = b.
+__global__ void k_item_counts(const uint32_t* __restrict__ rs, uint32_t K, uint32_t sp,
+                              uint32_t* __restrict__ ic) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < K; b += gridDim.x * blockDim.x)
+    ic[b] = (rs[b + 1] - rs[b] + sp - 1) / sp;
+}
+
+__global__ void k_item_expand(const uint32_t* __restrict__ is, uint32_t K,
+                              uint32_t* __restrict__ ir) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < K;
+       b += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t j = is[b] + lane; j < is[b + 1]; j += 32) ir[j] = b;
+}
+
+cudaError_t launch_items(const uint32_t* run_start, uint32_t K, uint32_t sp, uint32_t* item_cnt,
+                         uint32_t* partial, uint32_t* item_start, uint32_t* item_run,
+                         cudaStream_t st, uint32_t* nl) {
+  const uint32_t g = (uint32_t)min_u64(1024, (K + 255) / 256);
+  k_item_counts<<<g, 256, 0, st>>>(run_start, K, sp, item_cnt);
+  const uint32_t nt = count_scan_partials(K, 1);
+  k_scan_reduce<<<nt, kScanThreads, 0, st>>>(item_cnt, K, partial);
+  k_scan_partials<<<1, kScanThreads, 0, st>>>(partial, nt);
+  k_scan_down<<<nt, kScanThreads, 0, st>>>(item_cnt, K, partial, 1, K, item_start);
+  k_item_expand<<<(uint32_t)min_u64(4096, (K + 7) / 8), 256, 0, st>>>(item_start, K, item_run);
+  *nl += 5;
+  return cudaGetLastError();
+}
+
 template <typename RidT>
 static cudaError_t launch_distribute_t(const DistArgs& a, cudaStream_t st, uint32_t* nl) {
   size_t hsm = a.hist_smem ? (size_t)a.K * sizeof(uint32_t) : 0;

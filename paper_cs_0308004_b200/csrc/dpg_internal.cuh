@@ -241,6 +241,9 @@ struct ProbeArgs {
   uint32_t slot_bytes;         // total bytes per stage
   OutSegs seg;                 // output segments (seg.n = 0: dst)
   const uint32_t* bmap;        // boundary-mode runs [K+1] (DistArgs), or null
+  const uint32_t* item_start;  // [K+1] first item (pair chunk) of each run (launch_items)
+  const uint32_t* item_run;    // [items] run of each item
+  uint32_t rid_pairs;          // 8-byte pairs are radix Phase I elements (rid << 32) | position
 };
 
 // One persistent cooperative kernel for the whole path (fused.cu).
@@ -596,6 +599,22 @@ cudaError_t launch_seq3_probe(const Seq3Args& a, uint32_t W, uint32_t grid, cuda
                               uint32_t* nlaunch);
 cudaError_t launch_seq3_gather(const Seq3Args& a, uint32_t W, uint32_t grid, uint32_t nbuf,
                                cudaStream_t st, uint32_t* nlaunch);
+// Phase I of the multi-kernel plan as stable radix passes over rid >> s
+// (sort.cu): out[n] = (rid << 32) | position by run, run_start[K+1].
+uint32_t radix_passes(uint64_t K);
+cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n_src, uint32_t s,
+                                    uint32_t K, uint64_t* tmp, uint64_t* out, uint32_t* counts,
+                                    uint32_t* gbar, uint32_t* run_start, int sm, cudaStream_t st,
+                                    uint32_t* nl, unsigned long long* status);
+cudaError_t launch_radix_unpack(const uint64_t* e, uint64_t n, uint32_t s, const uint32_t* rs,
+                                uint32_t K, uint64_t* out, uint64_t* rs_out, cudaStream_t st,
+                                uint32_t* nl);
+// Pair chunks of the runs as work items (distribute.cu): item_cnt[K] and
+// partial[count_scan_partials(K, 1)] scratch, item_start[K+1], item_run[up to
+// K + n_out / sp] (the run of each item).
+cudaError_t launch_items(const uint32_t* run_start, uint32_t K, uint32_t sp, uint32_t* item_cnt,
+                         uint32_t* partial, uint32_t* item_start, uint32_t* item_run,
+                         cudaStream_t st, uint32_t* nl);
 cudaError_t launch_probe_gather(const ProbeArgs& a, uint32_t W, uint32_t grid, uint32_t smem,
                                 cudaStream_t st, uint32_t* nlaunch);
 cudaError_t launch_direct(const uint8_t* src, uint64_t n_src, uint32_t rec, const uint32_t* rids,

@@ -8,8 +8,8 @@
 // run is copied to the destination array".
 //
 // B200 form: one persistent CTA per SM walks
-// runs b = blockIdx.x, blockIdx.x + grid, ...; each run's source records
-// [bL, (b+1)L) and its pair chunk are staged into one of two shared-memory
+// the items (run b, pair chunk j) i = blockIdx.x, blockIdx.x + grid, ...; each
+// item's source records [bL, (b+1)L) and its pair chunk are staged into one of two shared-memory
 // stages by TMA bulk copies (cp.async.bulk + mbarrier complete_tx, L2
 // evict-first), double buffered so the next run streams in while this one is
 // written out.  Each pair (local, pos) then copies the staged record straight
@@ -26,34 +26,39 @@ static constexpr int kProbeThreads = 512;
 static constexpr uint32_t kBarBytes = 128;
 
 struct Item {
-  uint32_t b;       // run
+  uint32_t b;       // run (kItemDone: no more items)
   uint32_t chunk;   // pair chunk within the run
   uint32_t p0, p1;  // pair range [p0, p1)
 };
+constexpr uint32_t kItemDone = 0xFFFFFFFFu;
+constexpr uint32_t kNoLocal = 0xFFFFFFFFu;   // a pair whose rid was out of range
 
-// Sequence of non-empty (run, chunk) items of this CTA.
+// The items are the (run, chunk) pairs in run order -- chunk j of run b holds
+// its pairs [rs[b] + j*SP, min(rs[b+1], rs[b] + (j+1)*SP)) -- and item i runs
+// on CTA i mod G, so a run with many rids (data skew) is spread
+// over the CTAs instead of queueing on one.  item_run[i] = the run of item i,
+// item_start[b] = the first item of run b (launch_items, distribute.cu).
 struct ItemIter {
-  uint32_t b, chunk, stride, K, slot_pairs;
-  const uint32_t* rs;
-  __device__ bool first(uint32_t b0, uint32_t G, uint32_t K_, uint32_t sp, const uint32_t* rs_,
-                        Item& it) {
-    stride = G; K = K_; slot_pairs = sp; rs = rs_;
-    b = b0; chunk = 0;
+  uint32_t i, stride, n, sp;
+  const uint32_t *rs, *ir, *is;
+  __device__ bool first(uint32_t c, uint32_t G, const ProbeArgs& a, Item& it) {
+    stride = G; sp = a.slot_pairs; rs = a.run_start; ir = a.item_run; is = a.item_start;
+    n = __ldg(is + a.K);
+    i = c;
     return settle(it);
   }
   __device__ bool settle(Item& it) {
-    while (b < K) {
-      uint32_t s0 = __ldg(rs + b), s1 = __ldg(rs + b + 1);
-      uint32_t p0 = s0 + chunk * slot_pairs;
-      if (p0 < s1) {
-        it.b = b; it.chunk = chunk; it.p0 = p0; it.p1 = min(s1, p0 + slot_pairs);
-        return true;
-      }
-      b += stride; chunk = 0;
-    }
-    return false;
+    if (i >= n) return false;
+    const uint32_t b = __ldg(ir + i);
+    const uint32_t j = i - __ldg(is + b);
+    const uint32_t s1 = __ldg(rs + b + 1);
+    it.b = b;
+    it.chunk = j;
+    it.p0 = __ldg(rs + b) + j * sp;
+    it.p1 = min(s1, it.p0 + sp);
+    return true;
   }
-  __device__ bool next(Item& it) { ++chunk; return settle(it); }
+  __device__ bool next(Item& it) { i += stride; return settle(it); }
 };
 
 struct SlotPtrs {
@@ -146,6 +151,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
   const uint32_t PR = PAY ? a.pay_bytes / W : 0;
   const uint32_t recW = a.rec / W;
 
+  __shared__ Item sit[2];   // the item staged in each slot (written by thread 0 before its arrive)
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -154,15 +160,25 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
   __syncthreads();
 
   uint64_t pol = policy_evict_first();
-  ItemIter prod, cons;
-  Item pit, cit;
+  ItemIter prod;
+  Item pit;
   bool phave = false;
+  // thread 0 fills a slot: the next item's copies, or the end mark
+  auto post = [&](int slot) {
+    if (phave) {
+      sit[slot] = pit;
+      issue(a, pit, smem, slot, &bars[slot], pol);
+      phave = prod.next(pit);   // (loads in flight while the CTA copies rows)
+    } else {
+      sit[slot].b = kItemDone;
+      mbar_arrive(&bars[slot]);
+    }
+  };
   if (tid == 0) {
-    phave = prod.first(blockIdx.x, gridDim.x, a.K, a.slot_pairs, a.run_start, pit);
-    if (phave) { issue(a, pit, smem, 0, &bars[0], pol); phave = prod.next(pit); }
-    if (phave) { issue(a, pit, smem, 1, &bars[1], pol); phave = prod.next(pit); }
+    phave = prod.first(blockIdx.x, gridDim.x, a, pit);
+    post(0);
+    post(1);
   }
-  bool chave = cons.first(blockIdx.x, gridDim.x, a.K, a.slot_pairs, a.run_start, cit);
 
   // Per-lane word mapping for rows of R <= 32 words: RPI rows per warp step.
   const uint32_t RPI = R <= 32 ? 32 / R : 1;
@@ -171,10 +187,12 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
   const bool lane_on = R <= 32 ? (uint32_t)lane < RPI * R : true;
 
   uint32_t it_idx = 0;
-  while (chave) {
+  while (true) {
     const int slot = it_idx & 1;
     const uint32_t parity = (it_idx >> 1) & 1;
     mbar_wait(&bars[slot], parity);
+    const Item cit = sit[slot];
+    if (cit.b == kItemDone) break;
     SlotPtrs sp = slot_ptrs(smem, a, slot);
     Ranges g = item_ranges(a, cit);
     const uint8_t* rb = align_dn(g.r0);
@@ -198,7 +216,17 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
 
     for (uint32_t g0 = (uint32_t)warp * 32; g0 < n; g0 += (uint32_t)nwarps * 32) {
       uint32_t my_local = 0, my_pos = 0;
-      if (g0 + lane < n) unpack<PairT>(prs[g0 + lane], a.s, my_local, my_pos);
+      if (g0 + lane < n) {
+        if (sizeof(PairT) == 8 && a.rid_pairs) {
+          // radix Phase I elements (rid << 32) | position; a bad rid is skipped
+          const uint64_t e = (uint64_t)prs[g0 + lane];
+          const uint32_t r = (uint32_t)(e >> 32);
+          my_pos = (uint32_t)e;
+          my_local = r < a.n_src ? (r & ((1u << a.s) - 1u)) : kNoLocal;
+        } else {
+          unpack<PairT>(prs[g0 + lane], a.s, my_local, my_pos);
+        }
+      }
       const uint32_t cnt = min(32u, n - g0);
       if (R <= 32) {
 #pragma unroll 4
@@ -206,7 +234,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
           const uint32_t rr = k + lr;
           const uint32_t loc = __shfl_sync(0xffffffffu, my_local, rr & 31);
           const uint32_t pos = __shfl_sync(0xffffffffu, my_pos, rr & 31);
-          if (lane_on && rr < cnt) {
+          if (lane_on && rr < cnt && loc != kNoLocal) {
             T v;
             if (PAY && lw < PR)
               v = *reinterpret_cast<const T*>(pay + (size_t)(g0 + rr) * a.pay_bytes + lw * W);
@@ -219,6 +247,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
         for (uint32_t rr = 0; rr < cnt; ++rr) {
           const uint32_t loc = __shfl_sync(0xffffffffu, my_local, rr);
           const uint32_t pos = __shfl_sync(0xffffffffu, my_pos, rr);
+          if (loc == kNoLocal) continue;
           uint8_t* drow = seg_row(a.seg, a.dst, pos, a.row_bytes);
           const uint8_t* srow = region + (size_t)loc * a.rec;
 #pragma unroll 4
@@ -234,12 +263,8 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
       }
     }
     (void)recW;
-    __syncthreads();  // every thread is done reading this stage
-    if (tid == 0 && phave) {
-      issue(a, pit, smem, slot, &bars[slot], pol);
-      phave = prod.next(pit);
-    }
-    chave = cons.next(cit);
+    __syncthreads();  // every thread is done reading this stage (and its item)
+    if (tid == 0) post(slot);
     ++it_idx;
   }
   // rows written into peer memory (output segments mapped from other GPUs)

@@ -16,6 +16,8 @@
 //            running count of the digit -- so equal digits keep their order
 //            (stable), which makes the LSD sort correct.
 //   phase 3  dpg_retrieve of the records in the sorted rid order (api.cu).
+#include <cstring>
+
 #include "dpg_internal.cuh"
 
 namespace dpg {
@@ -63,6 +65,14 @@ struct SortPassArgs {
   uint32_t byte;         // key byte of this pass (0 = most significant)
   uint32_t* counts;      // [grid * 256]
   uint32_t* gbar;        // monotonic grid barrier words
+  // Phase I as radix passes (launch_radix_distribute): shift >= 0 takes the
+  // digit (key word >> shift) & 255 instead of key byte `byte`; SRC passes
+  // read the rid list and form the key word (rid << 32) | position, a rid
+  // >= n_src becoming 0xFFFFFFFF (reported at its position).
+  int32_t shift;
+  const uint32_t* rids_in;
+  uint64_t n_src;
+  unsigned long long* status;
 };
 
 static constexpr int kSKpt = 16;                         // elements per lane in a tile
@@ -98,7 +108,7 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 //           to its stable position there (rank among equal digits of the same
 //           32 elements from ballots); the staged tile then leaves as one
 //           contiguous run per digit.  Four CTA barriers per tile.
-template <bool LO, bool RID>
+template <bool LO, bool RID, bool SRC>
 __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   extern __shared__ __align__(16) uint8_t sdyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kSTile]
@@ -117,6 +127,14 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
   const uint64_t hi = min_u64(a.n, lo + a.chunk);
   const uint32_t byte = a.byte;
+  const int32_t shift = a.shift;
+  auto dig = [&](uint64_t kh, uint32_t kl) -> uint32_t {
+    return shift >= 0 ? (uint32_t)(kh >> shift) & 255u : digit_of(kh, kl, byte);
+  };
+  // SRC: the key word of element i (rid << 32 | i; 0xFFFFFFFF for a bad rid)
+  auto src_word = [&](uint64_t i, uint32_t r) -> uint64_t {
+    return (uint64_t)(r < a.n_src ? r : 0xFFFFFFFFu) << 32 | (uint32_t)i;
+  };
   for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
   __syncthreads();
   // ---- count (only the key word that holds the digit is read) ----
@@ -126,8 +144,16 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     for (int u = 0; u < 16; ++u) {
       const uint64_t i = i0 + u * kSThreads;
       dg[u] = 256;
-      if (i < hi) dg[u] = (!LO || byte < 8) ? digit_of(__ldcg(a.khi_in + i), 0u, byte)
-                                            : digit_of(0ull, __ldcg(a.klo_in + i), byte);
+      if (SRC) {
+        if (i < hi) {
+          const uint32_t r = __ldcg(a.rids_in + i);
+          if (r >= a.n_src) report_bad(a.status, i);
+          dg[u] = dig(src_word(i, r), 0u);
+        }
+      } else if (i < hi) {
+        dg[u] = (!LO || byte < 8) ? dig(__ldcg(a.khi_in + i), 0u)
+                                  : digit_of(0ull, __ldcg(a.klo_in + i), byte);
+      }
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u)
@@ -185,7 +211,9 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
       kh[k] = 0;
       kl[k] = 0;
       rd[k] = 0;
-      if (e < cnt) {
+      if (SRC && e < cnt) {
+        kh[k] = src_word(t0 + e, __ldcs(a.rids_in + t0 + e));
+      } else if (e < cnt) {
         kh[k] = __ldcs(a.khi_in + t0 + e);
         if (LO) kl[k] = __ldcs(a.klo_in + t0 + e);
         if (RID) rd[k] = __ldcs(a.rid_in + t0 + e);
@@ -202,7 +230,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kSKpt; ++k)
-      if (wb + k * 32 + lane < cnt) atomicAdd(&wo[digit_of(kh[k], kl[k], byte)], 1u);
+      if (wb + k * 32 + lane < cnt) atomicAdd(&wo[dig(kh[k], kl[k])], 1u);
     __syncthreads();
     // ---- per-digit tile totals, their scan (staging bases), per-warp offsets ----
     if (tid < 256) {
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
 #pragma unroll
     for (int k = 0; k < kSKpt; ++k) {
       const bool on = wb + k * 32 + lane < cnt;
-      const uint32_t d = digit_of(kh[k], kl[k], byte);
+      const uint32_t d = dig(kh[k], kl[k]);
       const uint32_t pm = match_digit(d, __ballot_sync(0xffffffffu, on));
       if (on) {
         const uint32_t pos = tl[d] + wo[d] + __popc(pm & lt);
@@ -255,7 +283,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     for (uint32_t p = tid; p < cnt; p += kSThreads) {
       const uint64_t k = sk[p];
       const uint32_t l = LO ? sl[p] : 0u;
-      const uint32_t d = digit_of(k, l, byte);
+      const uint32_t d = dig(k, l);
       const uint32_t slot = delta[d] + p;
       __stcg(a.khi_out + slot, k);
       if (LO) __stcg(a.klo_out + slot, l);
@@ -283,14 +311,14 @@ __global__ void k_unpack(const uint64_t* __restrict__ khi, uint64_t n, uint32_t*
   }
 }
 
-template <bool LO, bool RID>
+template <bool LO, bool RID, bool SRC = false>
 static cudaError_t set_pass_smem() {
   static int set_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_dev == dev) return cudaSuccess;
   const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSTile;
-  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID>,
+  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) set_dev = dev;
   return e;
@@ -336,8 +364,9 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     e = packed ? set_pass_smem<false, false>() : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
   const uint64_t chunk = ((n + sm - 1) / sm + kSTile - 1) / kSTile * kSTile;
   const uint32_t dyn = (8 + (lo_w ? 4 : 0) + (packed ? 0 : 4)) * kSTile;
-  const void* fn = packed ? (const void*)k_sort_pass<false, false>
-                          : lo_w ? (const void*)k_sort_pass<true, true> : (const void*)k_sort_pass<false, true>;
+  const void* fn = packed ? (const void*)k_sort_pass<false, false, false>
+                          : lo_w ? (const void*)k_sort_pass<true, true, false>
+                                 : (const void*)k_sort_pass<false, true, false>;
   uint32_t in = 0;
   for (int byte = (int)key_bytes - 1; byte >= (int)first && e == cudaSuccess; --byte, in ^= 1) {
     SortPassArgs s;
@@ -352,6 +381,10 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     s.byte = (uint32_t)byte;
     s.counts = counts;
     s.gbar = gbar;
+    s.shift = -1;
+    s.rids_in = nullptr;
+    s.n_src = 0;
+    s.status = nullptr;
     void* params[] = {&s};
     ++*nl;
     e = cudaLaunchCooperativeKernel(fn, dim3(sm), dim3(kSThreads), params, dyn, st);
@@ -367,6 +400,100 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     e = cudaGetLastError();
   }
   return e;
+}
+
+// Phase I of the multi-kernel plan as stable radix passes over the run index
+// b = rid >> s (Fig. 1's "Append r to RID_RUN[run_num]", as a
+// counting sort; reading A24): P = ceil(bits(K-1) / 8) passes of
+// 8 bits, the first reading the rid list, each writing every element as one
+// contiguous run per digit from a shared-memory staged tile.  out[n] (8-byte
+// elements (rid << 32) | position, by run, positions ascending inside a run;
+// a rid >= n_src is 0xFFFFFFFF and sorts last, into run K-1 at the latest),
+// tmp[n] a ping-pong buffer (P >= 2), counts[256 * sm], then run_start[K+1]
+// from the boundaries of the sorted runs.
+__global__ void k_run_bounds(const uint64_t* __restrict__ e, uint64_t n, uint32_t s,
+                             uint32_t bits, uint32_t K, uint32_t* __restrict__ rs) {
+  auto run = [&](uint64_t j) -> uint32_t {
+    uint32_t b = (uint32_t)(e[j] >> 32) >> s;
+    if (bits < 32) b &= (1u << bits) - 1u;
+    return min(b, K);
+  };
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lo = j == 0 ? 0u : run(j - 1) + 1u;
+    const uint32_t hi = j == n ? K : run(j);
+    for (uint32_t b = lo; b <= hi; ++b) rs[b] = (uint32_t)j;
+  }
+}
+
+uint32_t radix_passes(uint64_t K) {
+  uint32_t bits = 0;
+  for (uint64_t m = K > 1 ? K - 1 : 0; m; m >>= 1) ++bits;
+  return bits ? (bits + 7) / 8 : 1;
+}
+
+cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n_src, uint32_t s,
+                                    uint32_t K, uint64_t* tmp, uint64_t* out, uint32_t* counts,
+                                    uint32_t* gbar, uint32_t* run_start, int sm, cudaStream_t st,
+                                    uint32_t* nl, unsigned long long* status) {
+  const uint32_t P = radix_passes(K);
+  cudaError_t e = set_pass_smem<false, false, true>();
+  if (e == cudaSuccess) e = set_pass_smem<false, false, false>();
+  const uint64_t chunk = ((n + sm - 1) / sm + kSTile - 1) / kSTile * kSTile;
+  const uint32_t dyn = 8 * kSTile;
+  const uint64_t* in = nullptr;
+  for (uint32_t k = 0; k < P && e == cudaSuccess; ++k) {
+    uint64_t* o = ((P - 1 - k) % 2 == 0) ? out : tmp;
+    SortPassArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.khi_in = in;
+    a.khi_out = o;
+    a.n = n;
+    a.chunk = chunk;
+    a.counts = counts;
+    a.gbar = gbar;
+    a.shift = (int32_t)(32 + s + 8 * k);
+    a.rids_in = rids;
+    a.n_src = n_src;
+    a.status = status;
+    void* params[] = {&a};
+    ++*nl;
+    e = cudaLaunchCooperativeKernel(k ? (const void*)k_sort_pass<false, false, false>
+                                      : (const void*)k_sort_pass<false, false, true>,
+                                    dim3(sm), dim3(kSThreads), params, dyn, st);
+    in = o;
+  }
+  if (e == cudaSuccess) {
+    ++*nl;
+    const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 256) / 256, (uint64_t)sm * 8));
+    k_run_bounds<<<g, 256, 0, st>>>(out, n, s, 8 * P, K, run_start);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+// Test helper (dpg_distribute): radix elements -> (local | pos << 32) with
+// local = rid & (L - 1) (0xFFFFFFFF for a bad rid), run_start -> uint64.
+__global__ void k_radix_unpack(const uint64_t* __restrict__ e, uint64_t n, uint32_t s,
+                               const uint32_t* __restrict__ rs, uint32_t K,
+                               uint64_t* __restrict__ out, uint64_t* __restrict__ rs_out) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = t; j < n; j += stride) {
+    const uint32_t r = (uint32_t)(e[j] >> 32);
+    const uint64_t local = r == 0xFFFFFFFFu ? 0xFFFFFFFFull : (r & ((1ull << s) - 1));
+    out[j] = local | (e[j] << 32);
+  }
+  for (uint64_t b = t; b <= K; b += stride) rs_out[b] = rs[b];
+}
+
+cudaError_t launch_radix_unpack(const uint64_t* e, uint64_t n, uint32_t s, const uint32_t* rs,
+                                uint32_t K, uint64_t* out, uint64_t* rs_out, cudaStream_t st,
+                                uint32_t* nl) {
+  ++*nl;
+  const uint32_t g = (uint32_t)min_u64(4096, (max_u64(n, K + 1) + 255) / 256);
+  k_radix_unpack<<<g, 256, 0, st>>>(e, n, s, rs, K, out, rs_out);
+  return cudaGetLastError();
 }
 
 uint64_t sort_ws_bytes(uint64_t n, int sm) {

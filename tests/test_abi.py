@@ -100,6 +100,15 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
     assert p["run_len"] * rec <= (p["smem_bytes"] - 128) // p["nstages"]
     m = dpg.dpg_plan(rec, n, n, 0, 148, path=2)
     assert m["path"] == 2 and m["nstages"] == 2
+    # Phase I: shared-memory histograms while K counters fit, else radix
+    # passes of 8 bits over the run index (8-byte elements carrying the rid)
+    if m["num_runs"] > 24576:
+        assert m["dist_radix"] == (int(m["num_runs"] - 1).bit_length() + 7) // 8
+        assert m["pair_bytes"] == 8 and m["grid_distribute"] == 148
+    else:
+        assert m["dist_radix"] == 0
+    r = dpg.dpg_plan(rec, n, n, 0, 148, path=2, hist_mode=3)
+    assert r["dist_radix"] >= 1 and r["pair_bytes"] == 8
 
 
 @pytest.mark.parametrize("rec,n,auto_path", [

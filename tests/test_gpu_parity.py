@@ -269,7 +269,7 @@ def test_plan_picks_l2run_when_the_source_fits_l2(dpg):
     assert dpg.dpg_plan(100, 1 << 24, 1 << 24)["path"] in (1, 2)
 
 
-@pytest.mark.parametrize("hist_mode", [1, 2])
+@pytest.mark.parametrize("hist_mode", [1, 2, 3])
 def test_histogram_modes_agree(dpg, hist_mode):
     src, rids = _case(7, 50000, 24, 70000, "repl")
     got = host(dpg.dpg_retrieve(dev(src), dev(rids), log2_run=6, hist_mode=hist_mode))
@@ -359,6 +359,56 @@ def test_distribute_runs_match_fig1_phase1(dpg):
                 assert np.array_equal(pos[a0:a1][o], ref["rid_pos"][a0:a1])
                 assert np.array_equal(local[a0:a1][o] + np.uint64(b << log2_run),
                                       ref["rid_runs"][a0:a1].astype(np.uint64))
+
+
+def test_radix_distribute_is_fig1_phase1_in_order(dpg):
+    """Phase I as stable radix passes (hist_mode 3, reading A24): every RID run
+    holds its entries in input order -- Fig. 1's RID_RUN exactly,
+    not just the same set -- at 1, 2 and 3 passes, ragged sizes."""
+    for seed, kind, n_src, log2_run in ((1, "perm", 20000, 6), (2, "repl", 20000, 0),
+                                        (3, "equal", 5000, 4), (4, "repl", 3_000_001, 3),
+                                        (5, "sorted", 777, 2), (6, "repl", 70000, 8)):
+        n_out = n_src if kind == "perm" else min(2 * n_src, 400_000)
+        src, rids = _case(seed, n_src, 1, n_out, kind)
+        ref = oracle.dpg_fig1(src, rids, 1 << log2_run)
+        pairs, rs = dpg.dpg_distribute(dev(rids), n_src, log2_run, hist_mode=3)
+        pairs, rs = host(pairs).astype(np.uint64), host(rs).astype(np.uint64)
+        assert np.array_equal(rs, ref["run_start"]), (seed, kind)
+        assert np.array_equal(pairs >> np.uint64(32), ref["rid_pos"])
+        run = np.repeat(np.arange(len(rs) - 1, dtype=np.uint64), np.diff(rs).astype(np.int64))
+        assert np.array_equal((pairs & np.uint64(0xffffffff)) + (run << np.uint64(log2_run)),
+                              ref["rid_runs"].astype(np.uint64))
+
+
+@pytest.mark.parametrize("k,n_src,rec,n_out,kind,log2_run", _sweep()[::2])
+def test_retrieve_sweep_radix_phase1(dpg, k, n_src, rec, n_out, kind, log2_run):
+    src, rids = _case(k, n_src, rec, n_out, kind)
+    try:
+        got = host(dpg.dpg_retrieve(dev(src), dev(rids), log2_run=log2_run, path=2, hist_mode=3))
+    except dpg.DPGError as e:
+        assert e.status == dpg.DPG_ERR_UNSUPPORTED
+        pytest.skip("plan refused")
+    assert np.array_equal(got, oracle.retrieve(src, rids))
+    dpg.dpg_sync_status()
+
+
+@pytest.mark.parametrize("n_src,log2_run", [(65536 * 4, 2), (256 * 16, 4), (100_000, 0)])
+def test_radix_phase1_invalid_rids(dpg, n_src, log2_run):
+    """Bad rids sort behind every run (K = 2^16 and 2^8: inside the last run's
+    digits, where the probe skips them): reported, rows left unwritten."""
+    rec, n = 12, 300_000
+    src, rids = _case(9, n_src, rec, n, "repl")
+    bad = np.array([17, 5, 299_999, 150_000])
+    rids[bad] = [n_src, 2**32 - 1, n_src + 5, 2**31]
+    out = torch.full((n, rec), 0x5A, dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=out, log2_run=log2_run, path=2, hist_mode=3)
+    with pytest.raises(dpg.DPGError) as ei:
+        dpg.dpg_sync_status()
+    assert ei.value.index == 5
+    got = host(out)
+    good = np.setdiff1d(np.arange(n), bad)
+    assert np.array_equal(got[good], oracle.retrieve(src, rids[good]))
+    assert (got[bad] == 0x5A).all()
 
 
 # --------------------------------------------------------------------------

@@ -40,18 +40,29 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-    def timed(fn):
-        ms = []
+    phases = {}
+
+    def timed(fn, name=None):
+        ms, ph = [], []
         for _ in range(args.reps):
             flush.fill_(1)
             flush2.view(torch.int32).max()
+            if name:
+                dpg.dpg_phase_times_ex()
+                dpg.dpg_phase_timing(True)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
             b.record()
             torch.cuda.synchronize()
+            if name:
+                dpg.dpg_phase_timing(False)
+                ph.append(dpg.dpg_phase_times_ex()[:3])
             ms.append(a.elapsed_time(b))
-        return sorted(ms)[len(ms) // 2] * 1e3
+        o = sorted(range(len(ms)), key=lambda i: ms[i])[len(ms) // 2]
+        if name:
+            phases[name] = "/".join(f"{x * 1e3:.0f}" for x in ph[o])
+        return ms[o] * 1e3
 
     n_src, n_out = args.n_src, args.n_out
     rng = np.random.default_rng(0)
@@ -81,9 +92,9 @@ def main():
             line += f"  auto(p{dpg.last_path()}) {t:8.1f}{'' if ok else ' MISMATCH'}"
             for name, kw in (("p2", dict(path=2)), ("p5", dict(path=5))):
                 try:
-                    t = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out, **kw))
+                    t = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out, **kw), name)
                     ok = torch.equal(out, ref)
-                    line += f"  {name} {t:8.1f}{'' if ok else ' MISMATCH'}"
+                    line += f"  {name} {t:8.1f} [{phases[name]}]{'' if ok else ' MISMATCH'}"
                 except dpg.DPGError as e:
                     line += f"  {name} --({e})"
             for K in [int(x) for x in args.runs.split(",")]:
@@ -92,10 +103,10 @@ def main():
                 t_part = timed(lambda: holder.__setitem__(
                     "b", dpg.dpg_skew_partition(rids, n_src, K, sample_size=S, seed=1)))
                 b = holder["b"]
-                t = timed(lambda: dpg.dpg_retrieve_bounds(src, rids, b, dst=out))
+                t = timed(lambda: dpg.dpg_retrieve_bounds(src, rids, b, dst=out), "bounds")
                 ok = torch.equal(out, ref)
                 line += f"  part {t_part:6.1f} (K {K} -> {b.size - 1}) bounds {t:8.1f}" \
-                        f"{'' if ok else ' MISMATCH'}"
+                        f" [{phases['bounds']}]{'' if ok else ' MISMATCH'}"
             print(line, flush=True)
             del src, out, ref
 
