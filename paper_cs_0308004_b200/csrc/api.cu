@@ -641,10 +641,13 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   if (hm == 3 && pay) return DPG_ERR_UNSUPPORTED;
   const bool radix = pay == 0 && (hm == 3 || (hm == 0 && K > kHistSmemMax));
   const uint32_t pb = radix ? 8u : pair_bytes_for(s);
-  // Pair chunk per stage: 2L when it fits (Poisson slack for with-replacement
-  // rids), else 1.5L, else L; a heavier run is processed in several chunks.
+  // Pair chunk per stage: the expected rids of a run with Poisson slack (at
+  // least 2L) when it fits, else 2L, 1.5L, L, ...; a heavier run is processed
+  // in several chunks, each staging the run's records again.
   uint32_t sp = 0;
-  for (uint64_t cand : {2 * L, L + L / 2, L, L / 2, L / 4, (uint64_t)32}) {
+  const uint64_t per_run = n_out / std::max<uint64_t>(1, K);
+  const uint64_t want = std::max<uint64_t>(2 * L, per_run + per_run / 4 + 64);
+  for (uint64_t cand : {want, 2 * L, L + L / 2, L, L / 2, L / 4, (uint64_t)32}) {
     cand = std::max<uint64_t>(32, cand);
     dpg_plan_t t;
     stage_geometry(rec, s, pb, pay, (uint32_t)std::min<uint64_t>(cand, 1u << 24), &t);
@@ -694,7 +697,7 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
   uint64_t off_items = end;
   if (p.slot_pairs) {   // K chunk counts | partials | K+1 item starts | items (<= K + n_out/SP)
     const uint64_t items = K + (n_out + p.slot_pairs - 1) / p.slot_pairs + 1;
-    end = align_up(off_items + (K + (K + 4095) / 4096 + K + 1 + items) * 4, 256);
+    end = align_up(off_items + align_up((K + (K + 4095) / 4096 + K + 1) * 4, 16) + items * 16, 256);
   }
   const uint64_t off_tmp = end;
   if (p.dist_radix >= 2) end = align_up(off_tmp + n_out * 8 + 64, 256);
@@ -714,7 +717,7 @@ dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t s
     w->item_cnt = (uint32_t*)(w->base + off_items);
     w->item_part = w->item_cnt + K;
     w->item_start = w->item_part + (K + 4095) / 4096;
-    w->item_run = w->item_start + K + 1;
+    w->item_run = (uint32_t*)(w->base + off_items + align_up((K + (K + 4095) / 4096 + K + 1) * 4, 16));
   }
   return DPG_OK;
 }
@@ -966,7 +969,8 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   {
     // Data skew (section 2.3): a large input planned on fixed
     // shared-memory runs is sampled first; a rid list that would overflow the
-    // runs' capacity takes the count-based L2 runs (exact run sizes) instead.
+    // runs' capacity takes the multi-kernel plan instead (exact run sizes from
+    // the count, heavy runs split into work items over all CTAs).
     const bool auto_plan = !opt || (opt->path == 0 && !opt->log2_run && !opt->grid_distribute &&
                                     !opt->grid_probe && !opt->hist_mode && !opt->gather &&
                                     !opt->pair_bytes);
@@ -978,9 +982,10 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
       dpg_status_t ks = skew_excess(rids, n_out, n_src, p, st, &excess, &nl_skew);
       if (ks != DPG_OK) return ks;
       dpg_plan_t q;
-      if (excess > n_out / 50 &&
-          plan_l2k(rec, n_src, n_out, 0, false, 0, sm, current_l2_bytes(), &q))
-        p = q;
+      dpg_options_t o2;
+      std::memset(&o2, 0, sizeof(o2));
+      o2.path = 2;
+      if (excess > n_out / 50 && make_plan(rec, n_src, n_out, pay, &o2, sm, &q) == DPG_OK) p = q;
     }
   }
   if (t_seg) {

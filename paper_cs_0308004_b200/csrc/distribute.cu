@@ -258,19 +258,26 @@ uint32_t count_scan_partials(uint64_t K, uint64_t G) {
 }
 
 // Work items of the probe-gather kernel: ic[b] = chunks of SP pairs in run b,
-// item_start = their exclusive scan, item_run[item_start[b] + j] = b.
+// item_start = their exclusive scan, items[item_start[b] + j] = {b, j | more << 31, p0, p1}
+// (more: a later chunk of the run follows).
 __global__ void k_item_counts(const uint32_t* __restrict__ rs, uint32_t K, uint32_t sp,
                               uint32_t* __restrict__ ic) {
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < K; b += gridDim.x * blockDim.x)
     ic[b] = (rs[b + 1] - rs[b] + sp - 1) / sp;
 }
 
-__global__ void k_item_expand(const uint32_t* __restrict__ is, uint32_t K,
-                              uint32_t* __restrict__ ir) {
+__global__ void k_item_expand(const uint32_t* __restrict__ is, const uint32_t* __restrict__ rs,
+                              uint32_t K, uint32_t sp, uint4* __restrict__ items) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < K;
-       b += (gridDim.x * blockDim.x) >> 5)
-    for (uint32_t j = is[b] + lane; j < is[b + 1]; j += 32) ir[j] = b;
+       b += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t i0 = is[b], r0 = rs[b], r1 = rs[b + 1];
+    for (uint32_t j = lane; i0 + j < is[b + 1]; j += 32) {
+      const uint32_t p0 = r0 + j * sp;
+      const uint32_t more = p0 + sp < r1 ? 0x80000000u : 0u;   // a later chunk restages the region
+      items[i0 + j] = make_uint4(b, j | more, p0, min(r1, p0 + sp));
+    }
+  }
 }
 
 cudaError_t launch_items(const uint32_t* run_start, uint32_t K, uint32_t sp, uint32_t* item_cnt,
@@ -282,7 +289,8 @@ cudaError_t launch_items(const uint32_t* run_start, uint32_t K, uint32_t sp, uin
   k_scan_reduce<<<nt, kScanThreads, 0, st>>>(item_cnt, K, partial);
   k_scan_partials<<<1, kScanThreads, 0, st>>>(partial, nt);
   k_scan_down<<<nt, kScanThreads, 0, st>>>(item_cnt, K, partial, 1, K, item_start);
-  k_item_expand<<<(uint32_t)min_u64(4096, (K + 7) / 8), 256, 0, st>>>(item_start, K, item_run);
+  k_item_expand<<<(uint32_t)min_u64(4096, (K + 7) / 8), 256, 0, st>>>(
+      item_start, run_start, K, sp, reinterpret_cast<uint4*>(item_run));
   *nl += 5;
   return cudaGetLastError();
 }

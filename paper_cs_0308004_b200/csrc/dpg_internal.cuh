@@ -242,7 +242,7 @@ struct ProbeArgs {
   OutSegs seg;                 // output segments (seg.n = 0: dst)
   const uint32_t* bmap;        // boundary-mode runs [K+1] (DistArgs), or null
   const uint32_t* item_start;  // [K+1] first item (pair chunk) of each run (launch_items)
-  const uint32_t* item_run;    // [items] run of each item
+  const uint32_t* item_run;    // [items] uint4 {run, chunk, p0, p1} of each item (16-aligned)
   uint32_t rid_pairs;          // 8-byte pairs are radix Phase I elements (rid << 32) | position
 };
 
@@ -610,8 +610,8 @@ cudaError_t launch_radix_unpack(const uint64_t* e, uint64_t n, uint32_t s, const
                                 uint32_t K, uint64_t* out, uint64_t* rs_out, cudaStream_t st,
                                 uint32_t* nl);
 // Pair chunks of the runs as work items (distribute.cu): item_cnt[K] and
-// partial[count_scan_partials(K, 1)] scratch, item_start[K+1], item_run[up to
-// K + n_out / sp] (the run of each item).
+// partial[count_scan_partials(K, 1)] scratch, item_start[K+1], item_run[4 x
+// (up to K + n_out / sp)] (16-byte aligned: uint4 {run, chunk, p0, p1} per item).
 cudaError_t launch_items(const uint32_t* run_start, uint32_t K, uint32_t sp, uint32_t* item_cnt,
                          uint32_t* partial, uint32_t* item_start, uint32_t* item_run,
                          cudaStream_t st, uint32_t* nl);

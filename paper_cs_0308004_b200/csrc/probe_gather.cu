@@ -29,6 +29,7 @@ struct Item {
   uint32_t b;       // run (kItemDone: no more items)
   uint32_t chunk;   // pair chunk within the run
   uint32_t p0, p1;  // pair range [p0, p1)
+  uint32_t more;    // 1: a later chunk of the run stages the same region
 };
 constexpr uint32_t kItemDone = 0xFFFFFFFFu;
 constexpr uint32_t kNoLocal = 0xFFFFFFFFu;   // a pair whose rid was out of range
@@ -36,26 +37,27 @@ constexpr uint32_t kNoLocal = 0xFFFFFFFFu;   // a pair whose rid was out of rang
 // The items are the (run, chunk) pairs in run order -- chunk j of run b holds
 // its pairs [rs[b] + j*SP, min(rs[b+1], rs[b] + (j+1)*SP)) -- and item i runs
 // on CTA i mod G, so a run with many rids (data skew) is spread
-// over the CTAs instead of queueing on one.  item_run[i] = the run of item i,
-// item_start[b] = the first item of run b (launch_items, distribute.cu).
+// over the CTAs instead of queueing on one.  items[i] = {b, j, p0, p1}
+// (launch_items, distribute.cu): one independent load per item, so thread 0
+// fetches the item after next while the CTA copies rows.
 struct ItemIter {
-  uint32_t i, stride, n, sp;
-  const uint32_t *rs, *ir, *is;
+  uint32_t i, stride, n;
+  const uint4* items;
   __device__ bool first(uint32_t c, uint32_t G, const ProbeArgs& a, Item& it) {
-    stride = G; sp = a.slot_pairs; rs = a.run_start; ir = a.item_run; is = a.item_start;
-    n = __ldg(is + a.K);
+    stride = G;
+    items = reinterpret_cast<const uint4*>(a.item_run);
+    n = __ldg(a.item_start + a.K);
     i = c;
     return settle(it);
   }
   __device__ bool settle(Item& it) {
     if (i >= n) return false;
-    const uint32_t b = __ldg(ir + i);
-    const uint32_t j = i - __ldg(is + b);
-    const uint32_t s1 = __ldg(rs + b + 1);
-    it.b = b;
-    it.chunk = j;
-    it.p0 = __ldg(rs + b) + j * sp;
-    it.p1 = min(s1, it.p0 + sp);
+    const uint4 d = __ldg(items + i);
+    it.b = d.x;
+    it.chunk = d.y & 0x7FFFFFFFu;
+    it.more = d.y >> 31;
+    it.p0 = d.z;
+    it.p1 = d.w;
     return true;
   }
   __device__ bool next(Item& it) { i += stride; return settle(it); }
@@ -109,7 +111,7 @@ __device__ __forceinline__ const uint8_t* align_up(const uint8_t* p) {
 // after the wait.  Pair and payload arrays live in padded workspace, so their
 // chunks are bulk-copied from aligned-down to aligned-up addresses.
 __device__ __forceinline__ void issue(const ProbeArgs& a, const Item& it, uint8_t* smem, int slot,
-                                      uint64_t* bar, uint64_t pol) {
+                                      uint64_t* bar, uint64_t pol, uint64_t pol_keep) {
   SlotPtrs sp = slot_ptrs(smem, a, slot);
   Ranges g = item_ranges(a, it);
   const uint8_t* rb = align_dn(g.r0);
@@ -124,7 +126,9 @@ __device__ __forceinline__ void issue(const ProbeArgs& a, const Item& it, uint8_
   tx = rbytes + qbytes + ybytes;
   fence_proxy_async_smem();
   mbar_arrive_expect_tx(bar, tx);
-  if (rbytes) bulk_g2s(sp.region + (ra0 - rb), ra0, rbytes, bar, pol);
+  // a region another chunk of the run will stage again (on a neighbouring
+  // CTA, at about the same time) is kept in L2 until that chunk reads it
+  if (rbytes) bulk_g2s(sp.region + (ra0 - rb), ra0, rbytes, bar, it.more ? pol_keep : pol);
   bulk_g2s(sp.pairs, qa0, qbytes, bar, pol);
   if (ybytes) bulk_g2s(sp.pay, ya0, ybytes, bar, pol);
 }
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
   __syncthreads();
 
   uint64_t pol = policy_evict_first();
+  uint64_t pol_keep = policy_evict_last();
   ItemIter prod;
   Item pit;
   bool phave = false;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) k_probe_gather(const __grid_
   auto post = [&](int slot) {
     if (phave) {
       sit[slot] = pit;
-      issue(a, pit, smem, slot, &bars[slot], pol);
+      issue(a, pit, smem, slot, &bars[slot], pol, pol_keep);
       phave = prod.next(pit);   // (loads in flight while the CTA copies rows)
     } else {
       sit[slot].b = kItemDone;

@@ -647,8 +647,9 @@ def test_fk_join_sort_exponential_keys(dpg):
 def test_skew_check_switches_plan(dpg):
     """Section 2.3: a large rid list that would overflow the fixed
     shared-memory runs (the exponential join keys) is detected by sampling and
-    runs on the count-based L2 runs; a uniform list keeps the fixed runs."""
-    for cfg, want in (("c4x", 5), ("c4", 1)):
+    runs on the multi-kernel plan (exact run sizes, heavy runs split into work
+    items); a uniform list keeps the fixed runs."""
+    for cfg, want in (("c4x", 2), ("c4", 1)):
         w = datagen.make(cfg, scale=4)
         d = dpg.dpg_fk_join(dev(w["fact"]), dev(w["fk"]), dev(w["dim"]))
         assert dpg.last_path() == want, cfg
@@ -708,16 +709,16 @@ def test_segments_shared_memory_runs(dpg):
     assert dpg.last_path() == 1
 
 
-def test_segments_skewed_k_runs(dpg):
-    """A skewed list (exponential keys) switches to the K-run L2 plan, whose
-    last gather writes the segments."""
+def test_segments_skewed(dpg):
+    """A skewed list (exponential keys) switches to the multi-kernel plan,
+    whose probe writes the segments."""
     w = datagen.make("c4x", scale=8)
     rids = w["fk"][: (1 << 22) + 77]
     sizes = [1 << 20, 12345, (1 << 21), len(rids) - (1 << 20) - 12345 - (1 << 21)]
     want = oracle.retrieve(w["dim"], rids)
     bufs = [torch.empty((n, 64), dtype=torch.uint8, device="cuda") for n in sizes]
     dpg.dpg_retrieve_segments(dev(w["dim"]), dev(rids), sizes, bufs)
-    assert dpg.last_path() == 5
+    assert dpg.last_path() == 2
     k = 0
     for n, b in zip(sizes, bufs):
         assert np.array_equal(host(b), want[k:k + n])

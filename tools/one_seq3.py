@@ -1,5 +1,5 @@
-"""One path-6 retrieval (after a warm-up) on the c3 shape, for ncu captures:
-    python tools/one_seq3.py --rec 8 [--n 16777216] [--kind perm] [--path 6]"""
+"""One retrieval (after a warm-up) on the c3 shape, for ncu captures:
+    python tools/one_seq3.py --rec 8 [--n 16777216] [--kind perm] [--path 6] [--hist-mode 3]"""
 import argparse
 import os
 import sys
@@ -15,6 +15,7 @@ ap.add_argument("--rec", type=int, default=8)
 ap.add_argument("--kind", default="perm")
 ap.add_argument("--path", type=int, default=6)
 ap.add_argument("--direct", action="store_true")
+ap.add_argument("--hist-mode", type=int, default=0)
 a = ap.parse_args()
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
@@ -24,7 +25,7 @@ rids = (torch.randperm(n, device="cuda", generator=g) if a.kind == "perm"
 src = torch.randint(0, 256, (n, a.rec), dtype=torch.uint8, device="cuda", generator=g)
 out = torch.empty_like(src)
 fn = (lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)) if a.direct else \
-    (lambda: dpg.dpg_retrieve(src, rids, dst=out, path=a.path))
+    (lambda: dpg.dpg_retrieve(src, rids, dst=out, path=a.path, hist_mode=a.hist_mode))
 fn()
 torch.cuda.synchronize()
 fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")

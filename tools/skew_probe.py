@@ -5,7 +5,8 @@ a hot set (90% of the rids on 1% of the records), floor(n_src u^6) ("zipf":
 6% of the rids on record 0) or uniform.  Lines:
   direct       dpg_retrieve_direct
   auto         dpg_retrieve (plan + skew check; path 5 when the sample shows skew)
-  p2           the multi-kernel plan on high-bit runs (path 2)
+  p1 / p2      the fused / multi-kernel plan on high-bit runs (path 1 / 2)
+  p2r / p2g    path 2 with Phase I as radix passes / global-atomic counting (hist_mode 3 / 2)
   p5           the K L2 runs (path 5)
   bounds       dpg_retrieve_bounds over runs from dpg_skew_partition (the
                partition timed separately: 'part')
@@ -36,6 +37,7 @@ def main():
     ap.add_argument("--runs", default="1024,8192", help="quantile runs asked for")
     ap.add_argument("--sample", type=int, default=32768)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--variants", default="p2,p5", help="of p1,p2,p2r,p5")
     args = ap.parse_args()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -73,6 +75,8 @@ def main():
             h = rng.integers(0, n_src, n_out).astype(np.uint32)
             hot = rng.random(n_out) < 0.9
             h[hot] = rng.integers(0, max(1, n_src // 100), int(hot.sum())).astype(np.uint32)
+        elif kind == "perm":
+            h = rng.permutation(n_src)[:n_out].astype(np.uint32)
         elif kind == "zipf":    # floor(n_src * u^6): 6% of the rids on record 0
             u = rng.random(n_out)
             h = np.minimum(n_src - 1, np.floor(n_src * u ** 6)).astype(np.uint32)
@@ -90,14 +94,19 @@ def main():
             t = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out))
             ok = torch.equal(out, ref)
             line += f"  auto(p{dpg.last_path()}) {t:8.1f}{'' if ok else ' MISMATCH'}"
-            for name, kw in (("p2", dict(path=2)), ("p5", dict(path=5))):
+            variants = [("p1", dict(path=1)), ("p2", dict(path=2)),
+                        ("p2r", dict(path=2, hist_mode=3)), ("p2g", dict(path=2, hist_mode=2)),
+                        ("p5", dict(path=5))]
+            for name, kw in variants:
+                if name not in args.variants.split(","):
+                    continue
                 try:
                     t = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out, **kw), name)
                     ok = torch.equal(out, ref)
                     line += f"  {name} {t:8.1f} [{phases[name]}]{'' if ok else ' MISMATCH'}"
                 except dpg.DPGError as e:
                     line += f"  {name} --({e})"
-            for K in [int(x) for x in args.runs.split(",")]:
+            for K in [int(x) for x in args.runs.split(",") if x]:
                 S = max(args.sample, K)
                 holder = {}
                 t_part = timed(lambda: holder.__setitem__(
