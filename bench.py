@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N=1: only the headline config")
     ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c3a8n26,c3a8n27,"
-                                        "c3a16n26,c4,c5shard",
+                                        "c3a16n26,c3a128,c4,c4x,c5shard",
                     help="N=1: nested configurations")
     a = ap.parse_args()
     if a.config is None:
@@ -581,8 +581,8 @@ def run_extra(name, args, torch, dpg, steps_obj, peak):
     import datagen
     import oracle
     steps = max(3, min(args.steps, 8))
-    if name == "c4":
-        return run_join_extra(args, torch, dpg, steps_obj, peak, steps)
+    if name in ("c4", "c4x"):
+        return run_join_extra(args, torch, dpg, steps_obj, peak, steps, cfg=name)
     if name == "c5shard":
         return run_c5_shard(args, torch, dpg, steps_obj, peak, steps)
     log2n = 24
