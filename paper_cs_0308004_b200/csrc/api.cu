@@ -665,7 +665,7 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   if (ds != DPG_OK) return ds;
   if (radix) {
     p->hist_in_smem = 0;
-    p->grid_distribute = (uint32_t)sm;     // cooperative passes: one CTA per SM
+    p->grid_distribute = 3u * (uint32_t)sm;   // cooperative passes: up to three CTAs per SM
     p->dist_radix = radix_passes(K);
   }
   uint64_t gp = std::min<uint64_t>(K, (uint64_t)sm);
@@ -1438,7 +1438,7 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
   const bool timed = timing_begin(st, &pe);
   cudaError_t e = p.dist_radix
                       ? launch_radix_distribute(rids, n_out, n_src, p.log2_run, d.K, w.tmp,
-                                                (uint64_t*)w.pairs, w.counts, gbar + 16,
+                                                (uint64_t*)w.pairs, w.counts, gbar + 8,
                                                 w.run_start, sm, st, &nl, status)
                       : launch_distribute(d, false, st, &nl);
   if (e == cudaSuccess)
@@ -1811,7 +1811,7 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
   if (ds != DPG_OK) return ds;
   if (opt && opt->hist_mode == 3 && !t_bounds) {   // radix passes (reading A24)
     p.dist_radix = radix_passes(K);
-    p.grid_distribute = (uint32_t)sm;
+    p.grid_distribute = 3u * (uint32_t)sm;
     p.hist_in_smem = 0;
     p.pair_bytes = 8;
   }
@@ -1829,7 +1829,7 @@ dpg_status_t dpg_distribute(const uint32_t* rids, uint64_t n_out, uint64_t n_src
     cudaError_t e = gs == DPG_OK ? cudaSuccess : cudaErrorMemoryAllocation;
     if (e == cudaSuccess)
       e = launch_radix_distribute(rids, n_out, n_src, log2_run, (uint32_t)K, w.tmp,
-                                  (uint64_t*)w.pairs, w.counts, gbar + 16, w.run_start, sm, st,
+                                  (uint64_t*)w.pairs, w.counts, gbar + 8, w.run_start, sm, st,
                                   &nl, status);
     if (e == cudaSuccess)
       e = launch_radix_unpack((const uint64_t*)w.pairs, n_out, log2_run, w.run_start, (uint32_t)K,

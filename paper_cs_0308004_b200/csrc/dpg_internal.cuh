@@ -112,7 +112,9 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
 // publishes the next epoch; the others wait for the epoch word (a different
 // cache line from the count, so the waiters do not slow the arrivals).
 // w[0] = count, w[32] = epoch; both only grow (zero at allocation).  All
-// launches sharing w must use the same grid size G.
+// launches sharing w must use the same grid size G: the per-stream workspace
+// (persist_ws) keeps three word pairs -- gbar + 0 and gbar + 16 for kernels
+// of one CTA per SM, gbar + 8 for path 2's radix passes (sort.cu, 3 CTAs per SM).
 __device__ __forceinline__ void grid_barrier_mono(uint32_t* w, uint32_t G) {
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -65,8 +65,8 @@ struct SortPassArgs {
   uint32_t byte;         // key byte of this pass (0 = most significant)
   uint32_t* counts;      // [grid * 256]
   uint32_t* gbar;        // monotonic grid barrier words
-  // Phase I as radix passes (launch_radix_distribute): shift >= 0 takes the
-  // digit (key word >> shift) & 255 instead of key byte `byte`; SRC passes
+  // Phase I as radix passes (launch_radix_distribute, template SH): the digit
+  // is (key word >> shift) & 255 instead of key byte `byte`; SRC passes
   // read the rid list and form the key word (rid << 32) | position, a rid
   // >= n_src becoming 0xFFFFFFFF (reported at its position).
   int32_t shift;
@@ -75,8 +75,17 @@ struct SortPassArgs {
   unsigned long long* status;
 };
 
-static constexpr int kSKpt = 16;                         // elements per lane in a tile
-static constexpr uint32_t kSTile = kSThreads * kSKpt;    // 8192 elements per tile
+// Elements per lane of a tile and CTAs per SM.  The key sorts (dpg_sort_rids,
+// the DPG-Sort join): 16 per lane (8192-element tiles), one CTA per SM.  Path
+// 2's Phase I passes (launch_radix_distribute): 4 per lane, three CTAs of 512
+// threads per SM (<= 42 registers, ~55 KB of shared memory each), so one
+// CTA's barriers and digit scans overlap the others' memory traffic -- 1.3-1.5x
+// faster there, 1.5x slower for the 1 Mi-key sort of config 2, whose CTAs
+// hold about one tile each (profiles/r02_radix_occupancy.md).
+static constexpr int kSKpt = 16;
+static constexpr uint32_t kSTile = kSThreads * kSKpt;
+static constexpr int kRKpt = 4, kRCtas = 3;
+static constexpr uint32_t kRTile = kSThreads * kRKpt;
 
 __device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, uint32_t byte) {
   return byte < 8 ? (uint32_t)(hi >> (8 * (7 - byte))) & 255u : (lo >> (8 * (11 - byte))) & 255u;
@@ -100,20 +109,21 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 // is packed in the low half of the key word, numeric keys <= 4 bytes).
 //   count   the CTA's digit counts, a grid barrier, every CTA derives its
 //           bucket bases (smaller digits first, then earlier CTAs);
-//   place   the chunk in tiles of 8192: warp w takes the tile's elements
-//           [512 w, 512 w + 512) into registers (16 per lane, index order =
+//   place   the chunk in tiles of 512 KPT: warp w takes the tile's elements
+//           [32 KPT w, 32 KPT (w + 1)) into registers (KPT per lane, index order =
 //           (k, lane)), counts them per digit (warp-private counters), the
 //           16 x 256 counters become per-warp offsets into a
 //           shared-memory staging area in digit order, and every element goes
 //           to its stable position there (rank among equal digits of the same
 //           32 elements from ballots); the staged tile then leaves as one
 //           contiguous run per digit.  Four CTA barriers per tile.
-template <bool LO, bool RID, bool SRC>
-__global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
+template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
+__global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a) {
+  constexpr uint32_t kTile = kSThreads * KPT;
   extern __shared__ __align__(16) uint8_t sdyn[];
-  uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kSTile]
-  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * kSTile);   // [kSTile] (LO)
-  uint32_t* sr = sl + (LO ? kSTile : 0);                           // [kSTile] (RID)
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kTile]
+  uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * kTile);    // [kTile] (LO)
+  uint32_t* sr = sl + (LO ? kTile : 0);                            // [kTile] (RID)
   __shared__ uint32_t hist[256];       // CTA counts
   __shared__ uint32_t gbase[256];      // first global slot of this CTA's block of digit d
   __shared__ uint32_t run[256];        // elements of digit d written so far (this CTA)
@@ -128,8 +138,9 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   const uint64_t hi = min_u64(a.n, lo + a.chunk);
   const uint32_t byte = a.byte;
   const int32_t shift = a.shift;
+  // (SH, a compile-time choice: the key sorts' inner loops keep byte digits)
   auto dig = [&](uint64_t kh, uint32_t kl) -> uint32_t {
-    return shift >= 0 ? (uint32_t)(kh >> shift) & 255u : digit_of(kh, kl, byte);
+    return SH ? (uint32_t)(kh >> shift) & 255u : digit_of(kh, kl, byte);
   };
   // SRC: the key word of element i (rid << 32 | i; 0xFFFFFFFF for a bad rid)
   auto src_word = [&](uint64_t i, uint32_t r) -> uint64_t {
@@ -198,15 +209,15 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
   }
   __syncthreads();
 
-  const uint32_t wb = warp * 512;
-  uint64_t kh[kSKpt];
-  uint32_t kl[kSKpt], rd[kSKpt];
+  const uint32_t wb = warp * 32 * KPT;
+  uint64_t kh[KPT];
+  uint32_t kl[KPT], rd[KPT];
   // the warp's 512 elements of the tile at t0 into registers (index order =
   // (k, lane)); issued for the next tile before the current one is written out
   auto load_tile = [&](uint64_t t0) {
-    const uint32_t cnt = (uint32_t)min_u64(kSTile, hi > t0 ? hi - t0 : 0);
+    const uint32_t cnt = (uint32_t)min_u64(kTile, hi > t0 ? hi - t0 : 0);
 #pragma unroll
-    for (int k = 0; k < kSKpt; ++k) {
+    for (int k = 0; k < KPT; ++k) {
       const uint32_t e = wb + k * 32 + lane;
       kh[k] = 0;
       kl[k] = 0;
@@ -221,15 +232,15 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     }
   };
   load_tile(lo);
-  for (uint64_t t0 = lo; t0 < hi; t0 += kSTile) {
-    const uint32_t cnt = (uint32_t)min_u64(kSTile, hi - t0);
+  for (uint64_t t0 = lo; t0 < hi; t0 += kTile) {
+    const uint32_t cnt = (uint32_t)min_u64(kTile, hi - t0);
     // ---- count the warp's elements per digit ----
     uint32_t* wo = woff[warp];
 #pragma unroll
     for (int k = 0; k < 8; ++k) wo[k * 32 + lane] = 0;
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kSKpt; ++k)
+    for (int k = 0; k < KPT; ++k)
       if (wb + k * 32 + lane < cnt) atomicAdd(&wo[dig(kh[k], kl[k])], 1u);
     __syncthreads();
     // ---- per-digit tile totals, their scan (staging bases), per-warp offsets ----
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
     // ---- place every element at its stable staging position ----
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int k = 0; k < kSKpt; ++k) {
+    for (int k = 0; k < KPT; ++k) {
       const bool on = wb + k * 32 + lane < cnt;
       const uint32_t d = dig(kh[k], kl[k]);
       const uint32_t pm = match_digit(d, __ballot_sync(0xffffffffu, on));
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_sort_pass(SortPassArgs a) {
       if (on && (pm & lt) == 0) wo[d] += __popc(pm);
       __syncwarp();
     }
-    load_tile(t0 + kSTile);     // in flight during the write-out
+    load_tile(t0 + kTile);     // in flight during the write-out
     __syncthreads();
     // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
     // p - tl[d]: consecutive threads, consecutive slots of one digit run ----
@@ -311,14 +322,14 @@ __global__ void k_unpack(const uint64_t* __restrict__ khi, uint64_t n, uint32_t*
   }
 }
 
-template <bool LO, bool RID, bool SRC = false>
+template <bool LO, bool RID, bool SRC = false, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
 static cudaError_t set_pass_smem() {
   static int set_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_dev == dev) return cudaSuccess;
-  const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSTile;
-  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC>,
+  const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSThreads * KPT;
+  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC, KPT, MINB, SH>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) set_dev = dev;
   return e;
@@ -362,7 +373,8 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   const bool lo_w = key_bytes > 8;
   if (e == cudaSuccess)
     e = packed ? set_pass_smem<false, false>() : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
-  const uint64_t chunk = ((n + sm - 1) / sm + kSTile - 1) / kSTile * kSTile;
+  const int grid = sm;
+  const uint64_t chunk = ((n + grid - 1) / grid + kSTile - 1) / kSTile * kSTile;
   const uint32_t dyn = (8 + (lo_w ? 4 : 0) + (packed ? 0 : 4)) * kSTile;
   const void* fn = packed ? (const void*)k_sort_pass<false, false, false>
                           : lo_w ? (const void*)k_sort_pass<true, true, false>
@@ -387,7 +399,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     s.status = nullptr;
     void* params[] = {&s};
     ++*nl;
-    e = cudaLaunchCooperativeKernel(fn, dim3(sm), dim3(kSThreads), params, dyn, st);
+    e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
   }
   if (e == cudaSuccess && packed) {
     // the sorted (key, rid) words of the last pass: rids (and keys) out
@@ -409,7 +421,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
 // contiguous run per digit from a shared-memory staged tile.  out[n] (8-byte
 // elements (rid << 32) | position, by run, positions ascending inside a run;
 // a rid >= n_src is 0xFFFFFFFF and sorts last, into run K-1 at the latest),
-// tmp[n] a ping-pong buffer (P >= 2), counts[256 * sm], then run_start[K+1]
+// tmp[n] a ping-pong buffer (P >= 2), counts[256 * 3 * sm], then run_start[K+1]
 // from the boundaries of the sorted runs.
 __global__ void k_run_bounds(const uint64_t* __restrict__ e, uint64_t n, uint32_t s,
                              uint32_t bits, uint32_t K, uint32_t* __restrict__ rs) {
@@ -437,10 +449,11 @@ cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n
                                     uint32_t* gbar, uint32_t* run_start, int sm, cudaStream_t st,
                                     uint32_t* nl, unsigned long long* status) {
   const uint32_t P = radix_passes(K);
-  cudaError_t e = set_pass_smem<false, false, true>();
-  if (e == cudaSuccess) e = set_pass_smem<false, false, false>();
-  const uint64_t chunk = ((n + sm - 1) / sm + kSTile - 1) / kSTile * kSTile;
-  const uint32_t dyn = 8 * kSTile;
+  const int grid = kRCtas * sm;
+  cudaError_t e = set_pass_smem<false, false, true, kRKpt, kRCtas, true>();
+  if (e == cudaSuccess) e = set_pass_smem<false, false, false, kRKpt, kRCtas, true>();
+  const uint64_t chunk = ((n + grid - 1) / grid + kRTile - 1) / kRTile * kRTile;
+  const uint32_t dyn = 8 * kRTile;
   const uint64_t* in = nullptr;
   for (uint32_t k = 0; k < P && e == cudaSuccess; ++k) {
     uint64_t* o = ((P - 1 - k) % 2 == 0) ? out : tmp;
@@ -458,9 +471,9 @@ cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n
     a.status = status;
     void* params[] = {&a};
     ++*nl;
-    e = cudaLaunchCooperativeKernel(k ? (const void*)k_sort_pass<false, false, false>
-                                      : (const void*)k_sort_pass<false, false, true>,
-                                    dim3(sm), dim3(kSThreads), params, dyn, st);
+    const void* fn = k ? (const void*)k_sort_pass<false, false, false, kRKpt, kRCtas, true>
+                       : (const void*)k_sort_pass<false, false, true, kRKpt, kRCtas, true>;
+    e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
     in = o;
   }
   if (e == cudaSuccess) {

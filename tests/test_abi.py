@@ -104,7 +104,7 @@ def test_plan_run_length(dpg, rec, n, L, K, path):
     # passes of 8 bits over the run index (8-byte elements carrying the rid)
     if m["num_runs"] > 24576:
         assert m["dist_radix"] == (int(m["num_runs"] - 1).bit_length() + 7) // 8
-        assert m["pair_bytes"] == 8 and m["grid_distribute"] == 148
+        assert m["pair_bytes"] == 8 and m["grid_distribute"] == 3 * 148
     else:
         assert m["dist_radix"] == 0
     r = dpg.dpg_plan(rec, n, n, 0, 148, path=2, hist_mode=3)
