@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N=1: only the headline config")
     ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c3a8n26,c3a8n27,"
-                                        "c3a16n26,c3a128,c4,c4x,c5shard",
+                                        "c3a16n26,c3a128,c4r256,c4,c4x,c5shard",
                     help="N=1: nested configurations")
     a = ap.parse_args()
     if a.config is None:
@@ -449,6 +449,10 @@ def roofline_for(dpg, plan_path, res_dpg, n_src, n_out, rec, pay, peak, peak_src
         per = {"k_dpg_fused": (ph[1] + ph[0], n_out * (2 * rec + 4))}
     else:
         per = {f"path {plan_path} probe-gather": (ph[1], n_src * rec + n_out * (rec + 8))}
+        if plan_path == 2 and ph[0] > 0:
+            # Phase I: the rid list read, the 8-byte pairs written (the radix passes'
+            # intermediate round trips are not algorithmic)
+            per["path 2 Phase I (distribute)"] = (ph[0], n_out * (4 + 8))
     kernel = max(per, key=lambda k: per[k][0])
     ms, by = per[kernel]
     achieved = by / (ms * 1e-3) / 1e9 if ms > 0 else None
@@ -585,6 +589,8 @@ def run_extra(name, args, torch, dpg, steps_obj, peak):
         return run_join_extra(args, torch, dpg, steps_obj, peak, steps, cfg=name)
     if name == "c5shard":
         return run_c5_shard(args, torch, dpg, steps_obj, peak, steps)
+    if name.startswith("c4r"):                # config 4's retrieval shape with rec-byte records
+        return run_c4r_extra(name, args, torch, dpg, steps_obj, peak, steps)
     log2n = 24
     if "n" in name[3:]:                       # e.g. c3a8n26: config 3's shape at 2^26 records
         name, log2n = name.split("n")[0], int(name.split("n")[1])
@@ -616,6 +622,37 @@ def run_extra(name, args, torch, dpg, steps_obj, peak):
                              "ms": res["direct_windowed"]["ms"]},
          "dpg_over_naive": res["naive"]["ms"] / d["ms"], "parity_sampled_ok": ok,
          "roofline": roofline_for(dpg, d["plan_path"], d, n, n, rec, 0, peak, "", name)}
+    del out, src, rids
+    return r
+
+
+def run_c4r_extra(name, args, torch, dpg, steps_obj, peak, steps):
+    """Config 4's retrieval shape with wider dimension records (c4r256: 2^26
+    uniform foreign keys into 2^24 x 256-byte records; four rids per record on
+    average, the join's fan-in): DPG vs the direct gather."""
+    import datagen
+    import oracle
+    rec = int(name[3:])
+    n_src, n = 1 << 24, 1 << 26
+    sid = datagen.STREAMS[("c4", "dim")]
+    src = torch.empty((n_src, rec), dtype=torch.uint8, device="cuda")
+    datagen.random_bytes_cuda(src.view(-1), sid)
+    rids_h = datagen.uniform(n, n_src, datagen.STREAMS[("c4", "fk")])
+    rids = torch.from_numpy(rids_h.view(np.int32)).cuda()
+    res, out, alg = measure_retrieval(torch, dpg, steps_obj, src, rids, steps, args.warmup)
+    dpg.dpg_sync_status()
+    idx_fn = lambda i: oracle.retrieve_generated(rec, n_src, sid, rids_h[i].astype(np.uint64))
+    ok = sampled_ok(out, idx_fn, n, k=512)
+    d = res["dpg"]
+    r = {"workload": f"c4r{rec}: 67,108,864 uniform rids into 16,777,216 x {rec} B "
+                     "(config 4's fan-in, retrieval only)",
+         "plan_path": d["plan_path"], "value": d["value"], "frac_of_hbm_peak": d["value"] / peak,
+         "ms": d["ms"], "ms_kernels": d["ms_kernels"], "phases_ms": d["phases_ms"],
+         "naive": {"value": res["naive"]["value"], "ms": res["naive"]["ms"]},
+         "direct_windowed": {"value": res["direct_windowed"]["value"],
+                             "ms": res["direct_windowed"]["ms"]},
+         "dpg_over_naive": res["naive"]["ms"] / d["ms"], "parity_sampled_ok": ok,
+         "roofline": roofline_for(dpg, d["plan_path"], d, n_src, n, rec, 0, peak, "", name)}
     del out, src, rids
     return r
 
