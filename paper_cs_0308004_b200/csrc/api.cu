@@ -634,12 +634,14 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   const uint64_t L = 1ull << s;
   const uint64_t K = (nsrc + L - 1) >> s;
   if (K >= (1ull << 31)) return DPG_ERR_UNSUPPORTED;
-  // Phase I: counting distribute with per-CTA run histograms in shared memory
-  // while K counters fit, else stable radix passes over the run index (their
-  // 8-byte elements carry the rid; reading A24)
+  // Phase I: stable radix passes over the run index (their 8-byte elements
+  // carry the rid; reading A24) for large lists or when the K run counters
+  // exceed shared memory, else the counting distribute with per-CTA run
+  // histograms in shared memory (its fixed cost is lower: 56 vs 107 us at
+  // 1 Mi rids; 560 vs 400 us at 16 Mi, profiles/r02_radix_occupancy.md)
   const uint32_t hm = opt ? opt->hist_mode : 0;
   if (hm == 3 && pay) return DPG_ERR_UNSUPPORTED;
-  const bool radix = pay == 0 && (hm == 3 || (hm == 0 && K > kHistSmemMax));
+  const bool radix = pay == 0 && (hm == 3 || (hm == 0 && (K > kHistSmemMax || n_out >= (4ull << 20))));
   const uint32_t pb = radix ? 8u : pair_bytes_for(s);
   // Pair chunk per stage: the expected rids of a run with Poisson slack (at
   // least 2L) when it fits, else 2L, 1.5L, L, ...; a heavier run is processed
