@@ -689,7 +689,7 @@ struct Workspace {
 
 dpg_status_t alloc_workspace(const dpg_plan_t& p, uint64_t n_out, cudaStream_t st, Workspace* w) {
   const uint64_t K = p.num_runs, G = p.grid_distribute;
-  const uint64_t M = (p.dist_radix ? 256 : K) * G;   // counts: per (run or digit, CTA)
+  const uint64_t M = p.dist_radix ? 256 * G + 256 : K * G;   // counts: per (run or digit, CTA)
   const uint64_t ntiles = (M + 4095) / 4096;
   uint64_t off_counts = 0;
   uint64_t off_rs = align_up(off_counts + M * 4, 256);

@@ -63,7 +63,7 @@ struct SortPassArgs {
   uint64_t n;
   uint64_t chunk;        // elements per CTA (multiple of the tile)
   uint32_t byte;         // key byte of this pass (0 = most significant)
-  uint32_t* counts;      // [grid * 256]
+  uint32_t* counts;      // [grid * 256 + 256]
   uint32_t* gbar;        // monotonic grid barrier words
   // Phase I as radix passes (launch_radix_distribute, template SH): the digit
   // is (key word >> shift) & 255 instead of key byte `byte`; SRC passes
@@ -173,25 +173,37 @@ __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a) {
   __syncthreads();
   for (uint32_t d = tid; d < 256; d += kSThreads) a.counts[c * 256 + d] = hist[d];
   grid_barrier_mono(a.gbar, G);
-  // ---- bases: the CTA rows of counts read coalesced, 8 loads in flight ----
-  if (tid < 256) {
-    uint32_t tot = 0, pre = 0;
-    uint32_t q = 0;
-    for (; q + 8 <= G; q += 8) {
-      uint32_t x[8];
+  // ---- bases, in two steps.  (1) CTA c scans the CTA counts of digits c,
+  // c + G, ... (a column prefix over the CTAs, written in place) and writes
+  // the digit's total; (2) after a second barrier every CTA reads its own row
+  // of column prefixes and the 256 totals.  (Each CTA summing all G rows
+  // itself read G^2 * 256 words per pass: 50 M at G = 444.) ----
+  uint32_t* tot_w = a.counts + (uint64_t)G * 256;   // [256] digit totals
+  for (uint32_t d = c; d < 256; d += G) {
+    uint32_t carry = 0;
+    for (uint32_t q0 = 0; q0 < G; q0 += kSThreads) {
+      const uint32_t q = q0 + tid;
+      const uint32_t v = q < G ? __ldcg(a.counts + (uint64_t)q * 256 + d) : 0u;
+      uint32_t x = v;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldcg(a.counts + (q + u) * 256 + tid);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        tot += x[u];
-        if (q + u < c) pre += x[u];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
       }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      uint32_t off = carry;
+      for (int w = 0; w < warp; ++w) off += wsum[w];
+      if (q < G) a.counts[(uint64_t)q * 256 + d] = off + x - v;
+      for (int w = 0; w < kSWarps; ++w) carry += wsum[w];
+      __syncthreads();
     }
-    for (; q < G; ++q) {
-      const uint32_t x = __ldcg(a.counts + q * 256 + tid);
-      tot += x;
-      if (q < c) pre += x;
-    }
+    if (tid == 0) tot_w[d] = carry;
+  }
+  grid_barrier_mono(a.gbar, G);
+  if (tid < 256) {
+    const uint32_t tot = __ldcg(tot_w + tid);
+    const uint32_t pre = __ldcg(a.counts + (uint64_t)c * 256 + tid);
     uint32_t y = tot;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -421,7 +433,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
 // contiguous run per digit from a shared-memory staged tile.  out[n] (8-byte
 // elements (rid << 32) | position, by run, positions ascending inside a run;
 // a rid >= n_src is 0xFFFFFFFF and sorts last, into run K-1 at the latest),
-// tmp[n] a ping-pong buffer (P >= 2), counts[256 * 3 * sm], then run_start[K+1]
+// tmp[n] a ping-pong buffer (P >= 2), counts[256 * 3 * sm + 256], then run_start[K+1]
 // from the boundaries of the sorted runs.
 __global__ void k_run_bounds(const uint64_t* __restrict__ e, uint64_t n, uint32_t s,
                              uint32_t bits, uint32_t K, uint32_t* __restrict__ rs) {
@@ -511,7 +523,7 @@ cudaError_t launch_radix_unpack(const uint64_t* e, uint64_t n, uint32_t s, const
 
 uint64_t sort_ws_bytes(uint64_t n, int sm) {
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
-  return 2 * al(8 * n) + 2 * al(4 * n) + al(4 * n) + al(256ull * 4 * sm) + 256;
+  return 2 * al(8 * n) + 2 * al(4 * n) + al(4 * n) + al(256ull * 4 * sm + 1024) + 256;
 }
 
 // DPG-Sort join, last step: out row j = a[j] (a_bytes, the moved
