@@ -16,9 +16,10 @@
  * the L2 or shared memory: a source within the L2 budget is one
  * run, staged into the L2 by TMA bulk copies and probed in output order
  * (path 3); larger sources are cut into shared-memory runs whose probe
- * writes each record straight to its destination (paths 1/2) or into K
- * L2-sized runs with an INTERNAL file (path 5, chosen after a skew sample or
- * for very large sources).  dpg_plan_t.path below lists the plans.
+ * writes each record straight to its destination (paths 1/2; path 2 also
+ * after a skew sample), into K L2-sized runs with an INTERNAL file (path 5,
+ * very large sources), or -- small records -- into three sequential passes
+ * (path 6).  dpg_plan_t.path below lists the plans.
  *
  * Conventions (all entry points):
  *  - Pointers named src/rids/dst/fact/fk_col/dim/out are DEVICE pointers
@@ -70,7 +71,7 @@ typedef enum {
 typedef void *dpg_stream_t; /* a cudaStream_t */
 
 /* Execution plan chosen for one call (host-side; no GPU needed; the skew
- * sample of dpg_retrieve may still switch path 1 to path 5 at run time,
+ * sample of dpg_retrieve may still switch path 1 to path 2 at run time,
  * dpg_last_path).  Run length L = 2^log2_run records (runs sized
  * to the cache, power of two, identified by the high-order bits of the
  * rid): the whole source for path 3, one shared-memory stage for paths 1/2,
@@ -88,7 +89,9 @@ typedef struct {
     uint32_t hist_in_smem;  /* 1: per-CTA run histogram in shared memory        */
     uint32_t pay_bytes;     /* payload bytes carried per pair (join: fact row)  */
     uint32_t path;          /* 1 = one persistent cooperative kernel (fused.cu)
-                               2 = distribute kernels + probe-gather kernel
+                               2 = distribute kernels (counting, or stable
+                                   radix passes: dist_radix) + probe-gather
+                                   kernel over work items (run, chunk)
                                3 = one L2-resident run (l2run.cu): the source
                                    fits the L2 budget, K = 1; Phase II loads it
                                    into L2, Phase III probes it in rid order
@@ -98,7 +101,12 @@ typedef struct {
                                    Phase III (one cooperative kernel)
                                5 = K L2 runs (l2k.cu): Phase I distribute
                                    kernel, K staged probes into INTERNAL,
-                                   Phase III gather                            */
+                                   Phase III gather
+                               6 = three sequential passes (seq3.cu), small
+                                   records: tile-sorted RID_RUN, run probes
+                                   into a tile-major INTERNAL, tile gathers
+                               7 = two levels: owner super-runs, path 6 in
+                                   each, one gather back                       */
     uint32_t nstages;       /* shared-memory stages of the probe-gather pipeline */
     uint32_t stage_bytes;   /* bytes per stage                                  */
     uint32_t gather;        /* 1 = probe writes rows straight to dst (rows are
@@ -481,8 +489,9 @@ uint32_t dpg_last_launch_count(void);
  * (section 2.3: 65,536 rids at evenly spaced positions, counted
  * per group of runs; one stream synchronisation); when the estimated rids
  * beyond the runs' fixed capacity exceed 2% of the input, the call runs the
- * count-based L2 runs (path 5) instead, whose run sizes are exact.  (Not
- * while the stream is being captured into a CUDA graph: no sampling then.) */
+ * multi-kernel plan (path 2) instead, whose run sizes are exact and whose
+ * heavy runs are split into work items over all SMs.  (Not while the stream
+ * is being captured into a CUDA graph: no sampling then.) */
 uint32_t dpg_last_path(void);
 
 /* Phase timing (bench.py's roofline): while enabled, every dpg_retrieve /
