@@ -651,10 +651,15 @@ def test_skew_check_switches_plan(dpg):
     items); a uniform list keeps the fixed runs."""
     for cfg, want in (("c4x", 2), ("c4", 1)):
         w = datagen.make(cfg, scale=4)
-        d = dpg.dpg_fk_join(dev(w["fact"]), dev(w["fk"]), dev(w["dim"]))
+        d = dpg.dpg_retrieve(dev(w["dim"]), dev(w["fk"]))
         assert dpg.last_path() == want, cfg
         got = host(d)
-        assert np.array_equal(got, oracle.fk_join(w["fact"], w["fk"], w["dim"])), cfg
+        assert np.array_equal(got, oracle.retrieve(w["dim"], w["fk"])), cfg
+    # the join on a dimension table beyond the L2 builds its rows in path 6
+    w = datagen.make("c4x", scale=4)
+    got = host(dpg.dpg_fk_join(dev(w["fact"]), dev(w["fk"]), dev(w["dim"])))
+    assert dpg.last_path() == 6
+    assert np.array_equal(got, oracle.fk_join(w["fact"], w["fk"], w["dim"]))
 
 
 # --------------------------------------------------------------------------

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--stage-kb", default="")
     ap.add_argument("--twolevel", action="store_true", help="also time path 7")
+    ap.add_argument("--clusters", default="", help="also path 6 with these cluster sizes, e.g. 2,4")
     args = ap.parse_args()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -83,6 +84,16 @@ def main():
                              f" [{ph[0]:.0f}/{ph[1]:.0f}/{ph[2]:.0f}]")
                 except dpg.DPGError as e:
                     line += f"  nbuf{nb} -- {e}"
+            for cl in [int(x) for x in args.clusters.split(",") if x]:
+                out.zero_()
+                try:
+                    t, ph = timed(lambda: dpg.dpg_retrieve(src, rids, dst=out, path=6, cluster=cl),
+                                  phases=True)
+                    ok = torch.equal(out, want)
+                    line += (f"  cl{cl} {t:7.1f}us {'ok' if ok else 'BAD'}"
+                             f" [{ph[0]:.0f}/{ph[1]:.0f}/{ph[2]:.0f}]")
+                except dpg.DPGError as e:
+                    line += f"  cl{cl} -- {e}"
             if args.twolevel:
                 out.zero_()
                 try:
