@@ -143,6 +143,14 @@ __global__ void __launch_bounds__(k3DistThreads) k3_distribute(Seq3Args a) {
     // count: run b = rid >> s; invalid rids go to bucket K
     for (uint32_t q = tid; q < n4; q += nth) {
       const uint4 r4 = srid4[q];
+      if (q < nfull && max(max(r4.x, r4.y), max(r4.z, r4.w)) <= rid_max) {
+        // (the common case, without per-rid branches: four valid rids)
+        atomicAdd(&hist[r4.x >> sh], 1u);
+        atomicAdd(&hist[r4.y >> sh], 1u);
+        atomicAdd(&hist[r4.z >> sh], 1u);
+        atomicAdd(&hist[r4.w >> sh], 1u);
+        continue;
+      }
       const uint32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
       if (q < nfull) {
 #pragma unroll
@@ -173,6 +181,18 @@ __global__ void __launch_bounds__(k3DistThreads) k3_distribute(Seq3Args a) {
     uint2* tinv4 = reinterpret_cast<uint2*>(a.tinv + i0);   // i0 % 4 == 0 (T % 16 == 0)
     for (uint32_t q = tid; q < n4; q += nth) {
       const uint4 r4 = srid4[q];
+      if (!DBG && q < nfull && max(max(r4.x, r4.y), max(r4.z, r4.w)) <= rid_max) {
+        const uint32_t s0 = atomicAdd(&scur[r4.x >> sh], 1u);
+        const uint32_t s1 = atomicAdd(&scur[r4.y >> sh], 1u);
+        const uint32_t s2 = atomicAdd(&scur[r4.z >> sh], 1u);
+        const uint32_t s3 = atomicAdd(&scur[r4.w >> sh], 1u);
+        sloc[s0] = (uint16_t)(r4.x & lmask);
+        sloc[s1] = (uint16_t)(r4.y & lmask);
+        sloc[s2] = (uint16_t)(r4.z & lmask);
+        sloc[s3] = (uint16_t)(r4.w & lmask);
+        tinv4[q] = make_uint2(s0 | (s1 << 16), s2 | (s3 << 16));
+        continue;
+      }
       const uint32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
       const uint32_t kn = q < nfull ? 4u : nt - 4 * q;
       uint32_t sl[4];
