@@ -515,7 +515,7 @@ def run_single(args):
                                              max(3, args.steps // 2), launches=dpg.last_launch_count)
         sort_res = {"ms_per_sort": med(tot), "records_per_s": n_out / (med(tot) * 1e-3),
                     "launches_per_sort": nl / max(3, args.steps // 2), "parity_sampled_ok": srt_ok,
-                    "what": "dpg_sort: 10-byte keys at offset 0, stable LSD radix sort + dpg_retrieve"}
+                    "what": "dpg_sort: 10-byte keys at offset 0, stable radix passes on the 4-byte prefix + fix-up of equal-prefix groups (full LSD sort if a group exceeds 32) + dpg_retrieve"}
 
     # end to end through the host-buffer C-ABI entry (PCIe copies inside)
     e2e = None

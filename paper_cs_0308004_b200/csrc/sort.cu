@@ -17,6 +17,7 @@
 //            (stable), which makes the LSD sort correct.
 //   phase 3  dpg_retrieve of the records in the sorted rid order (api.cu).
 #include <cstring>
+#include <utility>
 
 #include "dpg_internal.cuh"
 
@@ -29,7 +30,8 @@ __global__ void k_sort_extract(const uint8_t* __restrict__ src, uint32_t rec, ui
                                uint32_t key_off, uint32_t key_bytes, uint64_t* __restrict__ khi,
                                uint32_t* __restrict__ klo, uint32_t* __restrict__ rid,
                                const uint32_t* __restrict__ keys_u32, uint64_t key_limit,
-                               unsigned long long* status) {
+                               unsigned long long* status, const uint32_t* cond = nullptr) {
+  if (cond && *(volatile const uint32_t*)cond == 0) return;   // (the fallback, not needed)
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     if (keys_u32) {
@@ -73,6 +75,7 @@ struct SortPassArgs {
   const uint32_t* rids_in;
   uint64_t n_src;
   unsigned long long* status;
+  const uint32_t* cond;   // non-null: the pass runs only if *cond != 0 (the key sort's fallback)
 };
 
 // Elements per lane of a tile and CTAs per SM.  The key sorts (dpg_sort_rids,
@@ -120,6 +123,7 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
 __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a) {
   constexpr uint32_t kTile = kSThreads * KPT;
+  if (a.cond && *(volatile const uint32_t*)a.cond == 0) return;   // every CTA alike
   extern __shared__ __align__(16) uint8_t sdyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kTile]
   uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * kTile);    // [kTile] (LO)
@@ -334,6 +338,55 @@ __global__ void k_unpack(const uint64_t* __restrict__ khi, uint64_t n, uint32_t*
   }
 }
 
+// The key sort's prefix step: after stable passes over the first four key
+// bytes, elements with equal 4-byte prefixes are adjacent and in rid order;
+// each group of up to kFixMax elements is ordered by the remaining key bytes
+// (ties keep rid order) by the thread at its start, and rids_out receives the
+// sorted rids.  A longer group sets *overflow: the full sort then runs.
+constexpr uint32_t kFixMax = 32;
+__global__ void k_sort_fixup(const uint64_t* __restrict__ khi, const uint32_t* __restrict__ klo,
+                             const uint32_t* __restrict__ rid, uint64_t n, bool lo_w,
+                             uint32_t* __restrict__ rids_out, uint32_t* __restrict__ overflow) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t kj = khi[j];
+    const uint32_t pj = (uint32_t)(kj >> 32);
+    if (j > 0 && (uint32_t)(khi[j - 1] >> 32) == pj) continue;       // not a group start
+    uint32_t g = 1;
+    while (j + g < n && g <= kFixMax && (uint32_t)(khi[j + g] >> 32) == pj) ++g;
+    if (g == 1) {
+      rids_out[j] = rid[j];
+      continue;
+    }
+    if (g > kFixMax) {
+      atomicOr(overflow, 1u);
+      continue;
+    }
+    uint64_t k[kFixMax];
+    uint32_t l[kFixMax], r[kFixMax];
+    for (uint32_t e = 0; e < g; ++e) {
+      k[e] = khi[j + e];
+      l[e] = lo_w ? klo[j + e] : 0u;
+      r[e] = rid[j + e];
+    }
+    for (uint32_t e = 1; e < g; ++e) {      // insertion sort: stable, g <= 32
+      const uint64_t ke = k[e];
+      const uint32_t le = l[e], re = r[e];
+      uint32_t f = e;
+      while (f > 0 && (k[f - 1] > ke || (k[f - 1] == ke && l[f - 1] > le))) {
+        k[f] = k[f - 1];
+        l[f] = l[f - 1];
+        r[f] = r[f - 1];
+        --f;
+      }
+      k[f] = ke;
+      l[f] = le;
+      r[f] = re;
+    }
+    for (uint32_t e = 0; e < g; ++e) rids_out[j + e] = r[e];
+  }
+}
+
 template <bool LO, bool RID, bool SRC = false, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
 static cudaError_t set_pass_smem() {
   static int set_dev = -1;
@@ -360,6 +413,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   uint32_t* rid0 = reinterpret_cast<uint32_t*>(p);
   p += al(4 * n);
   uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(p + al(256ull * 4 * sm + 1024));
   // numeric keys (<= 4 bytes): the rid rides in the low half of the key word;
   // only the key bytes a key below key_limit can have nonzero are sorted on
   const bool packed = keys_u32 != nullptr;
@@ -369,50 +423,85 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
     for (uint64_t m = key_limit > 0 ? key_limit - 1 : 0; m; m >>= 8) ++kb;
     first = 4 - max(kb, 1u);
   }
-  const uint32_t passes = key_bytes - first;
-  uint32_t* rid[2] = {rid0, rids_out};
-  // the passes alternate buffers; start so that the last pass lands in rids_out
-  if (passes % 2 == 0) {
-    uint32_t* t = rid[0];
-    rid[0] = rid[1];
-    rid[1] = t;
-  }
-  ++*nl;
-  const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 255) / 256, (uint64_t)sm * 8));
-  k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0],
-                                    keys_u32, key_limit, status);
-  cudaError_t e = cudaGetLastError();
   const bool lo_w = key_bytes > 8;
-  if (e == cudaSuccess)
-    e = packed ? set_pass_smem<false, false>() : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
+  const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 255) / 256, (uint64_t)sm * 8));
   const int grid = sm;
   const uint64_t chunk = ((n + grid - 1) / grid + kSTile - 1) / kSTile * kSTile;
   const uint32_t dyn = (8 + (lo_w ? 4 : 0) + (packed ? 0 : 4)) * kSTile;
   const void* fn = packed ? (const void*)k_sort_pass<false, false, false>
                           : lo_w ? (const void*)k_sort_pass<true, true, false>
                                  : (const void*)k_sort_pass<false, true, false>;
-  uint32_t in = 0;
-  for (int byte = (int)key_bytes - 1; byte >= (int)first && e == cudaSuccess; --byte, in ^= 1) {
-    SortPassArgs s;
-    s.khi_in = khi[in];
-    s.klo_in = klo[in];
-    s.rid_in = rid[in];
-    s.khi_out = khi[in ^ 1];
-    s.klo_out = klo[in ^ 1];
-    s.rid_out = rid[in ^ 1];
-    s.n = n;
-    s.chunk = chunk;
-    s.byte = (uint32_t)byte;
-    s.counts = counts;
-    s.gbar = gbar;
-    s.shift = -1;
-    s.rids_in = nullptr;
-    s.n_src = 0;
-    s.status = nullptr;
-    void* params[] = {&s};
+  cudaError_t e = packed ? set_pass_smem<false, false>()
+                         : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
+  // the passes over key bytes [last, first) in LSD order, rid[] ping-ponging so
+  // that the last pass lands in rid[0] ^ (passes odd)
+  auto run_passes = [&](uint32_t lo_byte, uint32_t hi_byte, uint32_t* const rid[2],
+                        const uint32_t* cond) {
+    uint32_t in = 0;
+    for (int byte = (int)hi_byte - 1; byte >= (int)lo_byte && e == cudaSuccess; --byte, in ^= 1) {
+      SortPassArgs sa;
+      std::memset(&sa, 0, sizeof(sa));
+      sa.khi_in = khi[in];
+      sa.klo_in = klo[in];
+      sa.rid_in = rid[in];
+      sa.khi_out = khi[in ^ 1];
+      sa.klo_out = klo[in ^ 1];
+      sa.rid_out = rid[in ^ 1];
+      sa.n = n;
+      sa.chunk = chunk;
+      sa.byte = (uint32_t)byte;
+      sa.counts = counts;
+      sa.gbar = gbar;
+      sa.shift = -1;
+      sa.cond = cond;
+      void* params[] = {&sa};
+      ++*nl;
+      e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
+    }
+    return in;
+  };
+  // Keys longer than 4 bytes (the Datamation 10-byte keys): four
+  // passes sort by the 4-byte prefix, the short groups of equal prefixes are
+  // finished by k_sort_fixup; only if some group is longer (few distinct
+  // prefixes) do the extraction and all key_bytes passes run (launched
+  // always, each returning at once unless the fixup set the flag).
+  if (!packed && key_bytes > 4 && e == cudaSuccess) {
+    uint32_t* rid_p[2] = {rid0, rids_out};          // 4 passes: the result in rid0
     ++*nl;
-    e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
+    k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid_p[0],
+                                      nullptr, 0, status);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemsetAsync(overflow, 0, 4, st);
+    run_passes(0, 4, rid_p, nullptr);
+    if (e == cudaSuccess) {
+      ++*nl;
+      k_sort_fixup<<<g, 256, 0, st>>>(khi[0], klo[0], rid_p[0], n, lo_w, rids_out, overflow);
+      e = cudaGetLastError();
+    }
+    uint32_t* rid_f[2] = {rid0, rids_out};
+    if (key_bytes % 2 == 0) std::swap(rid_f[0], rid_f[1]);   // the last pass lands in rids_out
+    if (e == cudaSuccess) {
+      ++*nl;
+      k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid_f[0],
+                                        nullptr, 0, status, overflow);
+      e = cudaGetLastError();
+    }
+    run_passes(0, key_bytes, rid_f, overflow);
+    if (e == cudaSuccess && keys_out) {
+      // (keys_out is only requested with packed numeric keys)
+      e = cudaErrorInvalidValue;
+    }
+    return e;
   }
+  const uint32_t passes = key_bytes - first;
+  uint32_t* rid[2] = {rid0, rids_out};
+  // the passes alternate buffers; start so that the last pass lands in rids_out
+  if (passes % 2 == 0) std::swap(rid[0], rid[1]);
+  ++*nl;
+  k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0],
+                                    keys_u32, key_limit, status);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  run_passes(first, key_bytes, rid, nullptr);
   if (e == cudaSuccess && packed) {
     // the sorted (key, rid) words of the last pass: rids (and keys) out
     ++*nl;

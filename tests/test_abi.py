@@ -194,3 +194,12 @@ def test_bounds_entry_points_host_checks(dpg):
         dpg.DPG_ERR_INVALID_ARG
     assert lib.dpg_skew_partition(r, 10, 100, 4, 40000, 0, out, ctypes.byref(n_runs), None) == \
         dpg.DPG_ERR_UNSUPPORTED
+
+
+def test_library_has_no_undefined_internal_symbols(dpg):
+    """Every internal (namespace dpg) function the translation units call is
+    defined in the library: an undefined one would only fail at dlopen on the
+    GPU box."""
+    out = subprocess.check_output(["nm", "-D", "--undefined-only", dpg.LIB_PATH], text=True)
+    missing = [line.split()[-1] for line in out.splitlines() if "_ZN3dpg" in line]
+    assert not missing, missing

@@ -588,6 +588,33 @@ def test_dpg_sort_rejects_bad_keys(dpg):
             dpg.dpg_sort(s, off, kb)
 
 
+@pytest.mark.parametrize("case", ["groups", "boundary32", "boundary33", "one_prefix", "mixed"])
+def test_dpg_sort_prefix_groups_and_fallback(dpg, case):
+    """Keys longer than 4 bytes sort by their 4-byte prefix, then the short
+    groups of equal prefixes by the rest (k_sort_fixup); a group longer than 32
+    makes the full sort run instead.  Both against the oracle's stable sort."""
+    rng = np.random.default_rng(len(case))
+    n, kb = 200_003, 10
+    src = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    if case == "groups":            # ~20 records per prefix, ties in the rest too
+        src[:, :4] = np.repeat(rng.integers(0, 256, (n // 20 + 1, 4)), 20, axis=0)[:n]
+        src[:, 4:6] = rng.integers(0, 2, (n, 2))
+    elif case in ("boundary32", "boundary33"):
+        g = 32 if case == "boundary32" else 33
+        src[:g, :4] = 7                                   # one group of exactly g
+        src[g:, :4] = rng.integers(8, 256, (n - g, 4))
+    elif case == "one_prefix":
+        src[:, :4] = 42                                   # one group: the full sort
+    else:
+        src[::1000, :4] = 1                               # one long group among short ones
+    want = oracle.sort_rids(src, 0, kb)
+    got = host(dpg.dpg_sort_rids(dev(src), 0, kb)).view(np.uint32)
+    assert np.array_equal(got, want)
+    for off, k2 in ((3, 5), (0, 12), (2, 9)):            # odd / even byte counts, lo word
+        want = oracle.sort_rids(src, off, k2)
+        assert np.array_equal(host(dpg.dpg_sort_rids(dev(src), off, k2)).view(np.uint32), want)
+
+
 def test_dpg_sort_many_tiles(dpg):
     """Chunks of several staging tiles per CTA (n > 148 x 8192)."""
     rng = np.random.default_rng(99)
