@@ -76,6 +76,7 @@ struct SortPassArgs {
   uint64_t n_src;
   unsigned long long* status;
   const uint32_t* cond;   // non-null: the pass runs only if *cond != 0 (the key sort's fallback)
+  uint32_t npasses;       // passes in this launch (0 = 1): bytes byte, byte - 1, ...
 };
 
 // Elements per lane of a tile and CTAs per SM.  The key sorts (dpg_sort_rids,
@@ -120,10 +121,10 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 //           to its stable position there (rank among equal digits of the same
 //           32 elements from ballots); the staged tile then leaves as one
 //           contiguous run per digit.  Four CTA barriers per tile.
-template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
-__global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a) {
+template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC, bool MP = false>
+__global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) {
   constexpr uint32_t kTile = kSThreads * KPT;
-  if (a.cond && *(volatile const uint32_t*)a.cond == 0) return;   // every CTA alike
+  if (a0.cond && *(volatile const uint32_t*)a0.cond == 0) return;   // every CTA alike
   extern __shared__ __align__(16) uint8_t sdyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kTile]
   uint32_t* sl = reinterpret_cast<uint32_t*>(sdyn + 8 * kTile);    // [kTile] (LO)
@@ -138,188 +139,207 @@ __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a) {
   __shared__ uint32_t wsum[kSWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
-  const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
-  const uint64_t hi = min_u64(a.n, lo + a.chunk);
-  const uint32_t byte = a.byte;
-  const int32_t shift = a.shift;
-  // (SH, a compile-time choice: the key sorts' inner loops keep byte digits)
-  auto dig = [&](uint64_t kh, uint32_t kl) -> uint32_t {
-    return SH ? (uint32_t)(kh >> shift) & 255u : digit_of(kh, kl, byte);
-  };
-  // SRC: the key word of element i (rid << 32 | i; 0xFFFFFFFF for a bad rid)
-  auto src_word = [&](uint64_t i, uint32_t r) -> uint64_t {
-    return (uint64_t)(r < a.n_src ? r : 0xFFFFFFFFu) << 32 | (uint32_t)i;
-  };
-  for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
-  __syncthreads();
-  // ---- count (only the key word that holds the digit is read) ----
-  for (uint64_t i0 = lo + tid; i0 < hi; i0 += 16 * kSThreads) {
-    uint32_t dg[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const uint64_t i = i0 + u * kSThreads;
-      dg[u] = 256;
-      if (SRC) {
-        if (i < hi) {
-          const uint32_t r = __ldcg(a.rids_in + i);
-          if (r >= a.n_src) report_bad(a.status, i);
-          dg[u] = dig(src_word(i, r), 0u);
-        }
-      } else if (i < hi) {
-        dg[u] = (!LO || byte < 8) ? dig(__ldcg(a.khi_in + i), 0u)
-                                  : digit_of(0ull, __ldcg(a.klo_in + i), byte);
-      }
+  // MP (npasses > 1): consecutive passes in one launch (key bytes byte,
+  // byte - 1, ...), the buffers swapping after each, a grid barrier between
+  // passes.  (Only the key sort's fallback uses it: the per-pass argument copy
+  // costs registers, ~20 % per pass on the DPG-Sort join's 64 Mi keys.)
+  const uint32_t np = MP ? max(1u, a0.npasses) : 1u;
+  for (uint32_t ps = 0; ps < np; ++ps) {
+    SortPassArgs a = a0;
+    if (ps & 1) {
+      a.khi_in = a0.khi_out;
+      a.klo_in = a0.klo_out;
+      a.rid_in = a0.rid_out;
+      a.khi_out = const_cast<uint64_t*>(a0.khi_in);
+      a.klo_out = const_cast<uint32_t*>(a0.klo_in);
+      a.rid_out = const_cast<uint32_t*>(a0.rid_in);
     }
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      if (dg[u] < 256) atomicAdd(&hist[dg[u]], 1u);
-  }
-  __syncthreads();
-  for (uint32_t d = tid; d < 256; d += kSThreads) a.counts[c * 256 + d] = hist[d];
-  grid_barrier_mono(a.gbar, G);
-  // ---- bases, in two steps.  (1) CTA c scans the CTA counts of digits c,
-  // c + G, ... (a column prefix over the CTAs, written in place) and writes
-  // the digit's total; (2) after a second barrier every CTA reads its own row
-  // of column prefixes and the 256 totals.  (Each CTA summing all G rows
-  // itself read G^2 * 256 words per pass: 50 M at G = 444.) ----
-  uint32_t* tot_w = a.counts + (uint64_t)G * 256;   // [256] digit totals
-  for (uint32_t d = c; d < 256; d += G) {
-    uint32_t carry = 0;
-    for (uint32_t q0 = 0; q0 < G; q0 += kSThreads) {
-      const uint32_t q = q0 + tid;
-      const uint32_t v = q < G ? __ldcg(a.counts + (uint64_t)q * 256 + d) : 0u;
-      uint32_t x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += t;
-      }
-      if (lane == 31) wsum[warp] = x;
-      __syncthreads();
-      uint32_t off = carry;
-      for (int w = 0; w < warp; ++w) off += wsum[w];
-      if (q < G) a.counts[(uint64_t)q * 256 + d] = off + x - v;
-      for (int w = 0; w < kSWarps; ++w) carry += wsum[w];
-      __syncthreads();
-    }
-    if (tid == 0) tot_w[d] = carry;
-  }
-  grid_barrier_mono(a.gbar, G);
-  if (tid < 256) {
-    const uint32_t tot = __ldcg(tot_w + tid);
-    const uint32_t pre = __ldcg(a.counts + (uint64_t)c * 256 + tid);
-    uint32_t y = tot;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
-      if (lane >= d) y += t;
-    }
-    if (lane == 31) wsum[warp] = y;
-    gbase[tid] = y - tot + pre;
-  }
-  __syncthreads();
-  if (tid < 256) {
-    uint32_t off = 0;
-    for (int w = 0; w < warp; ++w) off += wsum[w];
-    gbase[tid] += off;
-  }
-  __syncthreads();
-
-  const uint32_t wb = warp * 32 * KPT;
-  uint64_t kh[KPT];
-  uint32_t kl[KPT], rd[KPT];
-  // the warp's 512 elements of the tile at t0 into registers (index order =
-  // (k, lane)); issued for the next tile before the current one is written out
-  auto load_tile = [&](uint64_t t0) {
-    const uint32_t cnt = (uint32_t)min_u64(kTile, hi > t0 ? hi - t0 : 0);
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const uint32_t e = wb + k * 32 + lane;
-      kh[k] = 0;
-      kl[k] = 0;
-      rd[k] = 0;
-      if (SRC && e < cnt) {
-        kh[k] = src_word(t0 + e, __ldcs(a.rids_in + t0 + e));
-      } else if (e < cnt) {
-        kh[k] = __ldcs(a.khi_in + t0 + e);
-        if (LO) kl[k] = __ldcs(a.klo_in + t0 + e);
-        if (RID) rd[k] = __ldcs(a.rid_in + t0 + e);
-      }
-    }
-  };
-  load_tile(lo);
-  for (uint64_t t0 = lo; t0 < hi; t0 += kTile) {
-    const uint32_t cnt = (uint32_t)min_u64(kTile, hi - t0);
-    // ---- count the warp's elements per digit ----
-    uint32_t* wo = woff[warp];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) wo[k * 32 + lane] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < KPT; ++k)
-      if (wb + k * 32 + lane < cnt) atomicAdd(&wo[dig(kh[k], kl[k])], 1u);
+    a.byte = a0.byte - ps;
+    a.shift = a0.shift + 8 * (int32_t)ps;
+    if (ps) grid_barrier_mono(a.gbar, G);   // the previous pass's rows, from every CTA
+    const uint64_t lo = min_u64(a.n, (uint64_t)c * a.chunk);
+    const uint64_t hi = min_u64(a.n, lo + a.chunk);
+    const uint32_t byte = a.byte;
+    const int32_t shift = a.shift;
+    // (SH, a compile-time choice: the key sorts' inner loops keep byte digits)
+    auto dig = [&](uint64_t kh, uint32_t kl) -> uint32_t {
+      return SH ? (uint32_t)(kh >> shift) & 255u : digit_of(kh, kl, byte);
+    };
+    // SRC: the key word of element i (rid << 32 | i; 0xFFFFFFFF for a bad rid)
+    auto src_word = [&](uint64_t i, uint32_t r) -> uint64_t {
+      return (uint64_t)(r < a.n_src ? r : 0xFFFFFFFFu) << 32 | (uint32_t)i;
+    };
+    for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
     __syncthreads();
-    // ---- per-digit tile totals, their scan (staging bases), per-warp offsets ----
-    if (tid < 256) {
-      uint32_t s2 = 0;
-#pragma unroll
-      for (int w = 0; w < kSWarps; ++w) {
-        const uint32_t x = woff[w][tid];
-        woff[w][tid] = s2;
-        s2 += x;
+    // ---- count (only the key word that holds the digit is read) ----
+    for (uint64_t i0 = lo + tid; i0 < hi; i0 += 16 * kSThreads) {
+      uint32_t dg[16];
+  #pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const uint64_t i = i0 + u * kSThreads;
+        dg[u] = 256;
+        if (SRC) {
+          if (i < hi) {
+            const uint32_t r = __ldcg(a.rids_in + i);
+            if (r >= a.n_src) report_bad(a.status, i);
+            dg[u] = dig(src_word(i, r), 0u);
+          }
+        } else if (i < hi) {
+          dg[u] = (!LO || byte < 8) ? dig(__ldcg(a.khi_in + i), 0u)
+                                    : digit_of(0ull, __ldcg(a.klo_in + i), byte);
+        }
       }
-      tt[tid] = s2;
-      uint32_t y = s2;
-#pragma unroll
+  #pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (dg[u] < 256) atomicAdd(&hist[dg[u]], 1u);
+    }
+    __syncthreads();
+    for (uint32_t d = tid; d < 256; d += kSThreads) a.counts[c * 256 + d] = hist[d];
+    grid_barrier_mono(a.gbar, G);
+    // ---- bases, in two steps.  (1) CTA c scans the CTA counts of digits c,
+    // c + G, ... (a column prefix over the CTAs, written in place) and writes
+    // the digit's total; (2) after a second barrier every CTA reads its own row
+    // of column prefixes and the 256 totals.  (Each CTA summing all G rows
+    // itself read G^2 * 256 words per pass: 50 M at G = 444.) ----
+    uint32_t* tot_w = a.counts + (uint64_t)G * 256;   // [256] digit totals
+    for (uint32_t d = c; d < 256; d += G) {
+      uint32_t carry = 0;
+      for (uint32_t q0 = 0; q0 < G; q0 += kSThreads) {
+        const uint32_t q = q0 + tid;
+        const uint32_t v = q < G ? __ldcg(a.counts + (uint64_t)q * 256 + d) : 0u;
+        uint32_t x = v;
+  #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += t;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        uint32_t off = carry;
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+        if (q < G) a.counts[(uint64_t)q * 256 + d] = off + x - v;
+        for (int w = 0; w < kSWarps; ++w) carry += wsum[w];
+        __syncthreads();
+      }
+      if (tid == 0) tot_w[d] = carry;
+    }
+    grid_barrier_mono(a.gbar, G);
+    if (tid < 256) {
+      const uint32_t tot = __ldcg(tot_w + tid);
+      const uint32_t pre = __ldcg(a.counts + (uint64_t)c * 256 + tid);
+      uint32_t y = tot;
+  #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
         if (lane >= d) y += t;
       }
       if (lane == 31) wsum[warp] = y;
-      tl[tid] = y - s2;
+      gbase[tid] = y - tot + pre;
     }
     __syncthreads();
     if (tid < 256) {
       uint32_t off = 0;
       for (int w = 0; w < warp; ++w) off += wsum[w];
-      tl[tid] += off;
-      delta[tid] = gbase[tid] + run[tid] - tl[tid];
+      gbase[tid] += off;
     }
     __syncthreads();
-    // ---- place every element at its stable staging position ----
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const bool on = wb + k * 32 + lane < cnt;
-      const uint32_t d = dig(kh[k], kl[k]);
-      const uint32_t pm = match_digit(d, __ballot_sync(0xffffffffu, on));
-      if (on) {
-        const uint32_t pos = tl[d] + wo[d] + __popc(pm & lt);
-        sk[pos] = kh[k];
-        if (LO) sl[pos] = kl[k];
-        if (RID) sr[pos] = rd[k];
+
+    const uint32_t wb = warp * 32 * KPT;
+    uint64_t kh[KPT];
+    uint32_t kl[KPT], rd[KPT];
+    // the warp's 512 elements of the tile at t0 into registers (index order =
+    // (k, lane)); issued for the next tile before the current one is written out
+    auto load_tile = [&](uint64_t t0) {
+      const uint32_t cnt = (uint32_t)min_u64(kTile, hi > t0 ? hi - t0 : 0);
+  #pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const uint32_t e = wb + k * 32 + lane;
+        kh[k] = 0;
+        kl[k] = 0;
+        rd[k] = 0;
+        if (SRC && e < cnt) {
+          kh[k] = src_word(t0 + e, __ldcs(a.rids_in + t0 + e));
+        } else if (e < cnt) {
+          kh[k] = __ldcs(a.khi_in + t0 + e);
+          if (LO) kl[k] = __ldcs(a.klo_in + t0 + e);
+          if (RID) rd[k] = __ldcs(a.rid_in + t0 + e);
+        }
       }
+    };
+    load_tile(lo);
+    for (uint64_t t0 = lo; t0 < hi; t0 += kTile) {
+      const uint32_t cnt = (uint32_t)min_u64(kTile, hi - t0);
+      // ---- count the warp's elements per digit ----
+      uint32_t* wo = woff[warp];
+  #pragma unroll
+      for (int k = 0; k < 8; ++k) wo[k * 32 + lane] = 0;
       __syncwarp();
-      if (on && (pm & lt) == 0) wo[d] += __popc(pm);
-      __syncwarp();
+  #pragma unroll
+      for (int k = 0; k < KPT; ++k)
+        if (wb + k * 32 + lane < cnt) atomicAdd(&wo[dig(kh[k], kl[k])], 1u);
+      __syncthreads();
+      // ---- per-digit tile totals, their scan (staging bases), per-warp offsets ----
+      if (tid < 256) {
+        uint32_t s2 = 0;
+  #pragma unroll
+        for (int w = 0; w < kSWarps; ++w) {
+          const uint32_t x = woff[w][tid];
+          woff[w][tid] = s2;
+          s2 += x;
+        }
+        tt[tid] = s2;
+        uint32_t y = s2;
+  #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, y, d);
+          if (lane >= d) y += t;
+        }
+        if (lane == 31) wsum[warp] = y;
+        tl[tid] = y - s2;
+      }
+      __syncthreads();
+      if (tid < 256) {
+        uint32_t off = 0;
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+        tl[tid] += off;
+        delta[tid] = gbase[tid] + run[tid] - tl[tid];
+      }
+      __syncthreads();
+      // ---- place every element at its stable staging position ----
+      const uint32_t lt = lanemask_lt();
+  #pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const bool on = wb + k * 32 + lane < cnt;
+        const uint32_t d = dig(kh[k], kl[k]);
+        const uint32_t pm = match_digit(d, __ballot_sync(0xffffffffu, on));
+        if (on) {
+          const uint32_t pos = tl[d] + wo[d] + __popc(pm & lt);
+          sk[pos] = kh[k];
+          if (LO) sl[pos] = kl[k];
+          if (RID) sr[pos] = rd[k];
+        }
+        __syncwarp();
+        if (on && (pm & lt) == 0) wo[d] += __popc(pm);
+        __syncwarp();
+      }
+      load_tile(t0 + kTile);     // in flight during the write-out
+      __syncthreads();
+      // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
+      // p - tl[d]: consecutive threads, consecutive slots of one digit run ----
+      for (uint32_t p = tid; p < cnt; p += kSThreads) {
+        const uint64_t k = sk[p];
+        const uint32_t l = LO ? sl[p] : 0u;
+        const uint32_t d = dig(k, l);
+        const uint32_t slot = delta[d] + p;
+        __stcg(a.khi_out + slot, k);
+        if (LO) __stcg(a.klo_out + slot, l);
+        if (RID) __stcg(a.rid_out + slot, sr[p]);
+      }
+      __syncthreads();
+      if (tid < 256) run[tid] += tt[tid];
+      // (the next tile's first barrier orders this update before the next write-out)
     }
-    load_tile(t0 + kTile);     // in flight during the write-out
-    __syncthreads();
-    // ---- write out: staged slot p of digit d goes to gbase[d] + run[d] +
-    // p - tl[d]: consecutive threads, consecutive slots of one digit run ----
-    for (uint32_t p = tid; p < cnt; p += kSThreads) {
-      const uint64_t k = sk[p];
-      const uint32_t l = LO ? sl[p] : 0u;
-      const uint32_t d = dig(k, l);
-      const uint32_t slot = delta[d] + p;
-      __stcg(a.khi_out + slot, k);
-      if (LO) __stcg(a.klo_out + slot, l);
-      if (RID) __stcg(a.rid_out + slot, sr[p]);
-    }
-    __syncthreads();
-    if (tid < 256) run[tid] += tt[tid];
-    // (the next tile's first barrier orders this update before the next write-out)
-  }
+  }   // passes
 }
 
 __global__ void k_keys_u32(const uint64_t* __restrict__ khi, uint64_t n, uint32_t* __restrict__ out) {
@@ -387,14 +407,15 @@ __global__ void k_sort_fixup(const uint64_t* __restrict__ khi, const uint32_t* _
   }
 }
 
-template <bool LO, bool RID, bool SRC = false, int KPT = kSKpt, int MINB = 1, bool SH = SRC>
+template <bool LO, bool RID, bool SRC = false, int KPT = kSKpt, int MINB = 1, bool SH = SRC,
+          bool MP = false>
 static cudaError_t set_pass_smem() {
   static int set_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_dev == dev) return cudaSuccess;
   const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSThreads * KPT;
-  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC, KPT, MINB, SH>,
+  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC, KPT, MINB, SH, MP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) set_dev = dev;
   return e;
@@ -431,14 +452,20 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   const void* fn = packed ? (const void*)k_sort_pass<false, false, false>
                           : lo_w ? (const void*)k_sort_pass<true, true, false>
                                  : (const void*)k_sort_pass<false, true, false>;
+  const void* fn_mp = lo_w ? (const void*)k_sort_pass<true, true, false, kSKpt, 1, false, true>
+                           : (const void*)k_sort_pass<false, true, false, kSKpt, 1, false, true>;
   cudaError_t e = packed ? set_pass_smem<false, false>()
                          : lo_w ? set_pass_smem<true, true>() : set_pass_smem<false, true>();
-  // the passes over key bytes [last, first) in LSD order, rid[] ping-ponging so
-  // that the last pass lands in rid[0] ^ (passes odd)
+  if (e == cudaSuccess && !packed)
+    e = lo_w ? set_pass_smem<true, true, false, kSKpt, 1, false, true>()
+             : set_pass_smem<false, true, false, kSKpt, 1, false, true>();
+  // the passes over key bytes [lo_byte, hi_byte) in LSD order, in one
+  // launch, the buffers ping-ponging: the last pass lands in index (passes odd)
+  // (one launch per pass; one launch for all of them with `one_launch`)
   auto run_passes = [&](uint32_t lo_byte, uint32_t hi_byte, uint32_t* const rid[2],
-                        const uint32_t* cond) {
+                        const uint32_t* cond, bool one_launch) {
     uint32_t in = 0;
-    for (int byte = (int)hi_byte - 1; byte >= (int)lo_byte && e == cudaSuccess; --byte, in ^= 1) {
+    for (uint32_t byte = hi_byte; byte > lo_byte && e == cudaSuccess; --byte, in ^= 1) {
       SortPassArgs sa;
       std::memset(&sa, 0, sizeof(sa));
       sa.khi_in = khi[in];
@@ -449,16 +476,18 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
       sa.rid_out = rid[in ^ 1];
       sa.n = n;
       sa.chunk = chunk;
-      sa.byte = (uint32_t)byte;
+      sa.byte = byte - 1;
       sa.counts = counts;
       sa.gbar = gbar;
       sa.shift = -1;
       sa.cond = cond;
+      sa.npasses = one_launch ? hi_byte - lo_byte : 1;
       void* params[] = {&sa};
       ++*nl;
-      e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
+      e = cudaLaunchCooperativeKernel(one_launch ? fn_mp : fn, dim3(grid), dim3(kSThreads), params,
+                                      dyn, st);
+      if (one_launch) break;
     }
-    return in;
   };
   // Keys longer than 4 bytes (the Datamation 10-byte keys): four
   // passes sort by the 4-byte prefix, the short groups of equal prefixes are
@@ -472,7 +501,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
                                       nullptr, 0, status);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemsetAsync(overflow, 0, 4, st);
-    run_passes(0, 4, rid_p, nullptr);
+    run_passes(0, 4, rid_p, nullptr, false);
     if (e == cudaSuccess) {
       ++*nl;
       k_sort_fixup<<<g, 256, 0, st>>>(khi[0], klo[0], rid_p[0], n, lo_w, rids_out, overflow);
@@ -486,7 +515,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
                                         nullptr, 0, status, overflow);
       e = cudaGetLastError();
     }
-    run_passes(0, key_bytes, rid_f, overflow);
+    run_passes(0, key_bytes, rid_f, overflow, true);
     if (e == cudaSuccess && keys_out) {
       // (keys_out is only requested with packed numeric keys)
       e = cudaErrorInvalidValue;
@@ -501,7 +530,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid[0],
                                     keys_u32, key_limit, status);
   if (e == cudaSuccess) e = cudaGetLastError();
-  run_passes(first, key_bytes, rid, nullptr);
+  run_passes(first, key_bytes, rid, nullptr, false);
   if (e == cudaSuccess && packed) {
     // the sorted (key, rid) words of the last pass: rids (and keys) out
     ++*nl;
