@@ -195,6 +195,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_dpg_fused(FusedArgs a) {
         const uint32_t j = j0 + u * blockDim.x;
         r[u] = j < tspan ? rid_at(j) : 0xFFFFFFFFu;
       }
+      uint32_t rmax = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) rmax = max(rmax, r[u]);
+      if (j0 + (U - 1) * blockDim.x < tspan && rmax < a.n_src) {
+        // (the common case, without per-rid branches: U valid rids)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          rank[j0 + u * blockDim.x] = (uint16_t)atomicAdd(&hc[r[u] >> a.s], 1u);
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t j = j0 + u * blockDim.x;
