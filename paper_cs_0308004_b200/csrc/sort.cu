@@ -77,6 +77,9 @@ struct SortPassArgs {
   unsigned long long* status;
   const uint32_t* cond;   // non-null: the pass runs only if *cond != 0 (the key sort's fallback)
   uint32_t npasses;       // passes in this launch (0 = 1): bytes byte, byte - 1, ...
+  // RB passes: run_start[K+1] of the runs (rid >> rb_s, rb_bits digits) of the output
+  uint32_t* run_start;
+  uint32_t rb_s, rb_bits, rb_K;
 };
 
 // Elements per lane of a tile and CTAs per SM.  The key sorts (dpg_sort_rids,
@@ -121,7 +124,8 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 //           to its stable position there (rank among equal digits of the same
 //           32 elements from ballots); the staged tile then leaves as one
 //           contiguous run per digit.  Four CTA barriers per tile.
-template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC, bool MP = false>
+template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = SRC, bool MP = false,
+          bool RB = false>
 __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) {
   constexpr uint32_t kTile = kSThreads * KPT;
   if (a0.cond && *(volatile const uint32_t*)a0.cond == 0) return;   // every CTA alike
@@ -137,6 +141,9 @@ __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) 
   __shared__ uint32_t tt[256];         // elements of digit d in the current tile
   __shared__ uint32_t delta[256];      // gbase + run - tl: staged position -> global slot
   __shared__ uint32_t wsum[kSWarps];
+  // RB (the last radix pass of path 2's Phase I): run boundaries while writing
+  __shared__ uint32_t lastb[RB ? 256 : 1];     // run of the last element of digit d written
+  __shared__ uint32_t dslot[RB ? 256 : 1], drun[RB ? 256 : 1], ndef;   // deferred firsts
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = blockIdx.x, G = gridDim.x;
   // MP (npasses > 1): consecutive passes in one launch (key bytes byte,
@@ -170,6 +177,13 @@ __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) 
       return (uint64_t)(r < a.n_src ? r : 0xFFFFFFFFu) << 32 | (uint32_t)i;
     };
     for (uint32_t d = tid; d < 256; d += kSThreads) { hist[d] = 0; run[d] = 0; }
+    if (RB && tid == 0) ndef = 0;
+    // (RB) the run of an element: its truncated run digits, capped at K
+    auto run_of = [&](uint64_t k) -> uint32_t {
+      uint32_t b = (uint32_t)(k >> 32) >> a.rb_s;
+      if (a.rb_bits < 32) b &= (1u << a.rb_bits) - 1u;
+      return min(b, a.rb_K);
+    };
     __syncthreads();
     // ---- count (only the key word that holds the digit is read) ----
     for (uint64_t i0 = lo + tid; i0 < hi; i0 += 16 * kSThreads) {
@@ -334,10 +348,45 @@ __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) 
         __stcg(a.khi_out + slot, k);
         if (LO) __stcg(a.klo_out + slot, l);
         if (RID) __stcg(a.rid_out + slot, sr[p]);
+        if (RB) {
+          // run_start[b'] = slot for the runs b' in (run of the previous
+          // element, b]; the previous element is the staged one before, or
+          // this CTA's last of digit d; the CTA's first of digit d waits for
+          // the end of the pass (its predecessor is another CTA's)
+          const uint32_t b = run_of(k);
+          uint32_t bp = 0;
+          bool known = true;
+          if (p > tl[d]) {
+            bp = run_of(sk[p - 1]);
+          } else if (run[d] > 0) {
+            bp = lastb[d];
+          } else {
+            known = false;
+            const uint32_t q = atomicAdd(&ndef, 1u);
+            dslot[q] = slot;
+            drun[q] = b;
+          }
+          if (known)
+            for (uint32_t bb = bp + 1; bb <= b; ++bb) a.run_start[bb] = slot;
+          if (slot + 1 == a.n)
+            for (uint32_t bb = b + 1; bb <= a.rb_K; ++bb) a.run_start[bb] = (uint32_t)a.n;
+        }
       }
       __syncthreads();
-      if (tid < 256) run[tid] += tt[tid];
+      if (tid < 256) {
+        if (RB && tt[tid]) lastb[tid] = run_of(sk[tl[tid] + tt[tid] - 1]);
+        run[tid] += tt[tid];
+      }
       // (the next tile's first barrier orders this update before the next write-out)
+    }
+    if (RB) {
+      // the deferred firsts: their predecessors, written by other CTAs
+      grid_barrier_mono(a.gbar, G);
+      for (uint32_t q = tid; q < ndef; q += kSThreads) {
+        const uint32_t slot = dslot[q], b = drun[q];
+        const uint32_t b0 = slot ? run_of(__ldcg(a.khi_out + slot - 1)) + 1 : 0u;
+        for (uint32_t bb = b0; bb <= b; ++bb) a.run_start[bb] = slot;
+      }
     }
   }   // passes
 }
@@ -408,14 +457,14 @@ __global__ void k_sort_fixup(const uint64_t* __restrict__ khi, const uint32_t* _
 }
 
 template <bool LO, bool RID, bool SRC = false, int KPT = kSKpt, int MINB = 1, bool SH = SRC,
-          bool MP = false>
+          bool MP = false, bool RB = false>
 static cudaError_t set_pass_smem() {
   static int set_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_dev == dev) return cudaSuccess;
   const int dyn = (8 + (LO ? 4 : 0) + (RID ? 4 : 0)) * kSThreads * KPT;
-  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC, KPT, MINB, SH, MP>,
+  const cudaError_t e = cudaFuncSetAttribute(k_sort_pass<LO, RID, SRC, KPT, MINB, SH, MP, RB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) set_dev = dev;
   return e;
@@ -551,23 +600,8 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
 // contiguous run per digit from a shared-memory staged tile.  out[n] (8-byte
 // elements (rid << 32) | position, by run, positions ascending inside a run;
 // a rid >= n_src is 0xFFFFFFFF and sorts last, into run K-1 at the latest),
-// tmp[n] a ping-pong buffer (P >= 2), counts[256 * 3 * sm + 256], then run_start[K+1]
-// from the boundaries of the sorted runs.
-__global__ void k_run_bounds(const uint64_t* __restrict__ e, uint64_t n, uint32_t s,
-                             uint32_t bits, uint32_t K, uint32_t* __restrict__ rs) {
-  auto run = [&](uint64_t j) -> uint32_t {
-    uint32_t b = (uint32_t)(e[j] >> 32) >> s;
-    if (bits < 32) b &= (1u << bits) - 1u;
-    return min(b, K);
-  };
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t lo = j == 0 ? 0u : run(j - 1) + 1u;
-    const uint32_t hi = j == n ? K : run(j);
-    for (uint32_t b = lo; b <= hi; ++b) rs[b] = (uint32_t)j;
-  }
-}
-
+// tmp[n] a ping-pong buffer (P >= 2), counts[256 * 3 * sm + 256]; the last
+// pass also writes run_start[K+1] from the boundaries of the sorted runs (RB).
 uint32_t radix_passes(uint64_t K) {
   uint32_t bits = 0;
   for (uint64_t m = K > 1 ? K - 1 : 0; m; m >>= 1) ++bits;
@@ -579,9 +613,19 @@ cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n
                                     uint32_t* gbar, uint32_t* run_start, int sm, cudaStream_t st,
                                     uint32_t* nl, unsigned long long* status) {
   const uint32_t P = radix_passes(K);
+  if (n == 0) return cudaMemsetAsync(run_start, 0, ((uint64_t)K + 1) * 4, st);
   const int grid = kRCtas * sm;
-  cudaError_t e = set_pass_smem<false, false, true, kRKpt, kRCtas, true>();
-  if (e == cudaSuccess) e = set_pass_smem<false, false, false, kRKpt, kRCtas, true>();
+  // the pass kinds: first (reads the rids) / later, and the last one also
+  // writes the run boundaries (RB)
+  const void* f_first = P == 1
+      ? (const void*)k_sort_pass<false, false, true, kRKpt, kRCtas, true, false, true>
+      : (const void*)k_sort_pass<false, false, true, kRKpt, kRCtas, true, false, false>;
+  const void* f_mid = (const void*)k_sort_pass<false, false, false, kRKpt, kRCtas, true, false, false>;
+  const void* f_last = (const void*)k_sort_pass<false, false, false, kRKpt, kRCtas, true, false, true>;
+  cudaError_t e = set_pass_smem<false, false, true, kRKpt, kRCtas, true, false, true>();
+  if (e == cudaSuccess) e = set_pass_smem<false, false, true, kRKpt, kRCtas, true, false, false>();
+  if (e == cudaSuccess) e = set_pass_smem<false, false, false, kRKpt, kRCtas, true, false, false>();
+  if (e == cudaSuccess) e = set_pass_smem<false, false, false, kRKpt, kRCtas, true, false, true>();
   const uint64_t chunk = ((n + grid - 1) / grid + kRTile - 1) / kRTile * kRTile;
   const uint32_t dyn = 8 * kRTile;
   const uint64_t* in = nullptr;
@@ -599,18 +643,15 @@ cudaError_t launch_radix_distribute(const uint32_t* rids, uint64_t n, uint64_t n
     a.rids_in = rids;
     a.n_src = n_src;
     a.status = status;
+    a.run_start = run_start;
+    a.rb_s = s;
+    a.rb_bits = 8 * P;
+    a.rb_K = K;
     void* params[] = {&a};
     ++*nl;
-    const void* fn = k ? (const void*)k_sort_pass<false, false, false, kRKpt, kRCtas, true>
-                       : (const void*)k_sort_pass<false, false, true, kRKpt, kRCtas, true>;
+    const void* fn = k == 0 ? f_first : k + 1 == P ? f_last : f_mid;
     e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSThreads), params, dyn, st);
     in = o;
-  }
-  if (e == cudaSuccess) {
-    ++*nl;
-    const uint32_t g = (uint32_t)max_u64(1, min_u64((n + 256) / 256, (uint64_t)sm * 8));
-    k_run_bounds<<<g, 256, 0, st>>>(out, n, s, 8 * P, K, run_start);
-    e = cudaGetLastError();
   }
   return e;
 }
