@@ -305,12 +305,24 @@ dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t
 /* End-to-end entry with HOST buffers: copies src and rids host->device,
  * runs dpg_retrieve, copies dst device->host and synchronises `stream`.
  * Host buffers should be pinned for full PCIe bandwidth.  Device buffers are
- * library-owned and cached across calls, per device (dpg_release_cache frees
- * them).  dpg_release_cache also frees the per-stream workspaces and trims
- * the library's memory pool (it synchronises every device). */
+ * library-owned and cached across calls, per (device, stream)
+ * (dpg_release_cache frees them).  dpg_release_cache also frees the
+ * per-stream workspaces and trims the library's memory pool (it synchronises
+ * every device). */
 dpg_status_t dpg_retrieve_host(const void *src_host, size_t rec_bytes, uint64_t n_src,
                                const uint32_t *rids_host, uint64_t n_out, void *dst_host,
                                dpg_stream_t stream);
+
+/* dpg_retrieve_host without the final synchronisation: the copies and the
+ * retrieval are enqueued on `stream` and dst_host is complete once the stream
+ * reaches the call (the caller synchronises).  Host buffers must be pinned
+ * and stay valid until then.  Calls on different streams use different
+ * device buffers, so a caller alternating two streams overlaps one call's
+ * device->host copy with the next call's host->device copy (PCIe is full
+ * duplex). */
+dpg_status_t dpg_retrieve_host_async(const void *src_host, size_t rec_bytes, uint64_t n_src,
+                                     const uint32_t *rids_host, uint64_t n_out, void *dst_host,
+                                     dpg_stream_t stream);
 void dpg_release_cache(void);
 
 /* Batch lookup of keys in a hash index (section 4).  The index

@@ -46,6 +46,7 @@ EXPORTED = (
     "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
     "dpg_phase_times_ex", "dpg_retrieve_dist_loopback", "dpg_fk_join_direct",
     "dpg_skew_partition", "dpg_retrieve_bounds", "dpg_distribute_bounds",
+    "dpg_retrieve_host_async",
 )
 
 
@@ -89,6 +90,7 @@ _sigs = {
     "dpg_distribute": [_P, _U, _U, ctypes.c_uint32, _P, _P, _P, _P],
     "dpg_scatter_rows": [_P, _S, _P, _U, _P, _U, _P],
     "dpg_retrieve_host": [_P, _S, _U, _P, _U, _P, _P],
+    "dpg_retrieve_host_async": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_sync_status": [_P, _P],
     "dpg_retrieve_direct_ex": [_P, _S, _U, _P, _U, _P, _P, _I],
     "dpg_l2_prefetch": [_P, _U, _P],
@@ -471,15 +473,18 @@ def dpg_scatter_rows(rows, pos, dst, stream=None):
     return dst
 
 
-def dpg_retrieve_host(src, rids, dst, stream=None):
+def dpg_retrieve_host(src, rids, dst, stream=None, synchronize=True):
     """End-to-end retrieval with HOST tensors (pinned for full PCIe speed):
-    H2D of src and rids, DPG on the GPU, D2H of dst, synchronise."""
+    H2D of src and rids, DPG on the GPU, D2H of dst, synchronise.  With
+    synchronize=False (dpg_retrieve_host_async) the work is only enqueued on
+    `stream`; dst is complete once the stream is synchronised."""
     for t, n in ((src, "src"), (rids, "rids"), (dst, "dst")):
         if t.is_cuda or not t.is_contiguous():
             raise ValueError(f"{n} must be a contiguous host tensor")
     n_src, rec = src.shape
-    _check(_lib.dpg_retrieve_host(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(),
-                                  dst.data_ptr(), _stream_ptr(stream)), "dpg_retrieve_host")
+    fn = _lib.dpg_retrieve_host if synchronize else _lib.dpg_retrieve_host_async
+    _check(fn(src.data_ptr(), rec, n_src, rids.data_ptr(), rids.numel(), dst.data_ptr(),
+              _stream_ptr(stream)), "dpg_retrieve_host")
     return dst
 
 

@@ -2085,32 +2085,51 @@ dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
   return DPG_ERR_RID_RANGE;
 }
 
-// ---- end-to-end entry with host buffers --------------------------------------
-static std::mutex g_host_mu;
-// device buffers of dpg_retrieve_host, cached per device
-static void* g_host_buf[64][3] = {};
-static size_t g_host_cap[64][3] = {};
-
-static dpg_status_t host_buf(int k, size_t bytes, void** out) {
+// ---- end-to-end entries with host buffers -------------------------------------
+// Device buffers of dpg_retrieve_host(_async), cached per (device, stream):
+// calls on one stream reuse them in stream order; calls on different streams
+// (the asynchronous entry, pipelined) each have their own.  A buffer that has
+// to grow is freed stream-ordered (work already queued may still read it).
+struct HostBufs {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DPG_ERR_CUDA;
-  if (g_host_cap[dev][k] < bytes) {
-    if (g_host_buf[dev][k]) cudaFree(g_host_buf[dev][k]);
-    g_host_buf[dev][k] = nullptr;
-    g_host_cap[dev][k] = 0;
-    if (cudaMalloc(&g_host_buf[dev][k], bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return DPG_ERR_OOM;
-    }
-    g_host_cap[dev][k] = bytes;
+  cudaStream_t st = nullptr;
+  void* buf[3] = {nullptr, nullptr, nullptr};
+  size_t cap[3] = {0, 0, 0};
+};
+static std::mutex g_host_mu;
+static std::vector<HostBufs> g_host_bufs;
+
+static dpg_status_t host_bufs(cudaStream_t st, const size_t bytes[3], void* out[3]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DPG_ERR_CUDA;
+  HostBufs* h = nullptr;
+  for (auto& x : g_host_bufs)
+    if (x.dev == dev && x.st == st) h = &x;
+  if (!h) {
+    g_host_bufs.emplace_back();
+    h = &g_host_bufs.back();
+    h->dev = dev;
+    h->st = st;
   }
-  *out = g_host_buf[dev][k];
+  for (int k = 0; k < 3; ++k) {
+    if (h->cap[k] < bytes[k]) {
+      if (h->buf[k]) cudaFreeAsync(h->buf[k], st);
+      h->buf[k] = nullptr;
+      h->cap[k] = 0;
+      if (ws_malloc(&h->buf[k], bytes[k], st) != cudaSuccess) {
+        cudaGetLastError();
+        return DPG_ERR_OOM;
+      }
+      h->cap[k] = bytes[k];
+    }
+    out[k] = h->buf[k];
+  }
   return DPG_OK;
 }
 
-dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t n_src,
-                               const uint32_t* rids_host, uint64_t n_out, void* dst_host,
-                               dpg_stream_t stream) {
+dpg_status_t dpg_retrieve_host_async(const void* src_host, size_t rec_bytes, uint64_t n_src,
+                                     const uint32_t* rids_host, uint64_t n_out, void* dst_host,
+                                     dpg_stream_t stream) {
   if (rec_bytes == 0) return DPG_ERR_INVALID_ARG;
   if (n_out == 0) return DPG_OK;
   if (!src_host || !rids_host || !dst_host || n_src == 0) return DPG_ERR_INVALID_ARG;
@@ -2120,33 +2139,38 @@ dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t 
     return DPG_ERR_INVALID_ARG;
   std::lock_guard<std::mutex> lk(g_host_mu);
   cudaStream_t st = (cudaStream_t)stream;
-  void *s = nullptr, *r = nullptr, *d = nullptr;
-  dpg_status_t x;
-  if ((x = host_buf(0, sb, &s)) != DPG_OK) return x;
-  if ((x = host_buf(1, n_out * 4, &r)) != DPG_OK) return x;
-  if ((x = host_buf(2, db, &d)) != DPG_OK) return x;
-  cudaError_t e = cudaMemcpyAsync(s, src_host, sb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(r, rids_host, n_out * 4, cudaMemcpyHostToDevice, st);
+  void* b[3];
+  const size_t bytes[3] = {sb, n_out * 4, db};
+  dpg_status_t x = host_bufs(st, bytes, b);
+  if (x != DPG_OK) return x;
+  cudaError_t e = cudaMemcpyAsync(b[0], src_host, sb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(b[1], rids_host, n_out * 4, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_status(e);
-  dpg_status_t ds = dpg_retrieve(s, rec_bytes, n_src, (const uint32_t*)r, n_out, d, stream);
+  dpg_status_t ds = dpg_retrieve(b[0], rec_bytes, n_src, (const uint32_t*)b[1], n_out, b[2], stream);
   if (ds != DPG_OK) return ds;
-  e = cudaMemcpyAsync(dst_host, d, db, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  return cuda_status(e);
+  return cuda_status(cudaMemcpyAsync(dst_host, b[2], db, cudaMemcpyDeviceToHost, st));
+}
+
+dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t n_src,
+                               const uint32_t* rids_host, uint64_t n_out, void* dst_host,
+                               dpg_stream_t stream) {
+  dpg_status_t s = dpg_retrieve_host_async(src_host, rec_bytes, n_src, rids_host, n_out,
+                                           dst_host, stream);
+  if (s != DPG_OK) return s;
+  return cuda_status(cudaStreamSynchronize((cudaStream_t)stream));
 }
 
 void dpg_release_cache(void) {
   std::lock_guard<std::mutex> lk(g_host_mu);
   int cur = 0;
   cudaGetDevice(&cur);
-  for (int d = 0; d < 64; ++d)
-    for (int k = 0; k < 3; ++k) {
-      if (!g_host_buf[d][k]) continue;
-      cudaSetDevice(d);
-      cudaFree(g_host_buf[d][k]);
-      g_host_buf[d][k] = nullptr;
-      g_host_cap[d][k] = 0;
-    }
+  for (auto& h : g_host_bufs) {
+    cudaSetDevice(h.dev);
+    cudaDeviceSynchronize();           // (the stream may be gone: free synchronously)
+    for (int k = 0; k < 3; ++k)
+      if (h.buf[k]) cudaFree(h.buf[k]);
+  }
+  g_host_bufs.clear();
   cudaSetDevice(cur);
   cudaGetLastError();
   release_persist_ws();

@@ -544,6 +544,26 @@ def test_host_entry_end_to_end(dpg):
     assert np.array_equal(dst.numpy(), oracle.retrieve(w["src"], w["rids"]))
 
 
+def test_host_entry_async_two_streams(dpg):
+    """dpg_retrieve_host_async on two streams in turn (each stream its own
+    device buffers), inputs changing between calls, sizes growing (buffers
+    re-allocated stream-ordered): every output equals the oracle's."""
+    rng = np.random.default_rng(12)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = []
+    for i, (n_src, n_out, rec) in enumerate([(5000, 7000, 12), (40000, 30000, 12),
+                                             (3000, 90000, 40), (100000, 100000, 8)]):
+        src = torch.from_numpy(rng.integers(0, 256, (n_src, rec), dtype=np.uint8)).pin_memory()
+        rids = torch.from_numpy(rng.integers(0, n_src, n_out).astype(np.int32)).pin_memory()
+        dst = torch.empty((n_out, rec), dtype=torch.uint8).pin_memory()
+        dpg.dpg_retrieve_host(src, rids, dst, stream=streams[i % 2], synchronize=False)
+        jobs.append((src, rids, dst))
+    torch.cuda.synchronize()
+    for src, rids, dst in jobs:
+        assert np.array_equal(dst.numpy(), oracle.retrieve(src.numpy(), rids.numpy().view(np.uint32)))
+    dpg.dpg_release_cache()
+
+
 def test_scatter_rows(dpg):
     rng = np.random.default_rng(3)
     rows = rng.integers(0, 256, (5000, 36), dtype=np.uint8)
