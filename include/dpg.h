@@ -305,8 +305,9 @@ dpg_status_t dpg_scatter_rows(const void *rows, size_t rec_bytes, const uint32_t
 /* End-to-end entry with HOST buffers: copies src and rids host->device,
  * runs dpg_retrieve, copies dst device->host and synchronises `stream`.
  * Host buffers should be pinned for full PCIe bandwidth.  Device buffers are
- * library-owned and cached across calls, per (device, stream)
- * (dpg_release_cache frees them).  dpg_release_cache also frees the
+ * library-owned and cached across calls, per (device, stream), for the 8 most
+ * recently used streams (an older entry is freed after a device
+ * synchronisation; dpg_release_cache frees them all).  dpg_release_cache also frees the
  * per-stream workspaces and trims the library's memory pool (it synchronises
  * every device). */
 dpg_status_t dpg_retrieve_host(const void *src_host, size_t rec_bytes, uint64_t n_src,

@@ -2086,10 +2086,11 @@ dpg_status_t dpg_sync_status(dpg_stream_t stream, uint64_t* first_bad_index) {
 }
 
 // ---- end-to-end entries with host buffers -------------------------------------
-// Device buffers of dpg_retrieve_host(_async), cached per (device, stream):
-// calls on one stream reuse them in stream order; calls on different streams
-// (the asynchronous entry, pipelined) each have their own.  A buffer that has
-// to grow is freed stream-ordered (work already queued may still read it).
+// Device buffers of dpg_retrieve_host(_async), cached per (device, stream),
+// the kWsCached most recently used streams: calls on one stream reuse them in
+// stream order; calls on different streams (the asynchronous entry,
+// pipelined) each have their own.  A buffer that has to grow is freed
+// stream-ordered (work already queued may still read it).
 struct HostBufs {
   int dev = 0;
   cudaStream_t st = nullptr;
@@ -2102,15 +2103,33 @@ static std::vector<HostBufs> g_host_bufs;
 static dpg_status_t host_bufs(cudaStream_t st, const size_t bytes[3], void* out[3]) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DPG_ERR_CUDA;
-  HostBufs* h = nullptr;
-  for (auto& x : g_host_bufs)
-    if (x.dev == dev && x.st == st) h = &x;
-  if (!h) {
+  size_t at = g_host_bufs.size();
+  for (size_t q = 0; q < g_host_bufs.size(); ++q)
+    if (g_host_bufs[q].dev == dev && g_host_bufs[q].st == st) at = q;
+  if (at == g_host_bufs.size()) {
+    // at most kWsCached streams keep buffers: the oldest entry goes (freed
+    // synchronously -- its stream may no longer exist)
+    if (g_host_bufs.size() >= kWsCached) {
+      HostBufs& o = g_host_bufs.front();
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(o.dev);
+      cudaDeviceSynchronize();
+      for (int k = 0; k < 3; ++k)
+        if (o.buf[k]) cudaFree(o.buf[k]);
+      cudaSetDevice(cur);
+      cudaGetLastError();
+      g_host_bufs.erase(g_host_bufs.begin());
+    }
     g_host_bufs.emplace_back();
-    h = &g_host_bufs.back();
-    h->dev = dev;
-    h->st = st;
+    g_host_bufs.back().dev = dev;
+    g_host_bufs.back().st = st;
+    at = g_host_bufs.size() - 1;
+  } else if (at + 1 != g_host_bufs.size()) {
+    std::rotate(g_host_bufs.begin() + at, g_host_bufs.begin() + at + 1, g_host_bufs.end());
+    at = g_host_bufs.size() - 1;                 // most recently used last
   }
+  HostBufs* h = &g_host_bufs[at];
   for (int k = 0; k < 3; ++k) {
     if (h->cap[k] < bytes[k]) {
       if (h->buf[k]) cudaFreeAsync(h->buf[k], st);

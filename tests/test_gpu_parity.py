@@ -561,6 +561,18 @@ def test_host_entry_async_two_streams(dpg):
     torch.cuda.synchronize()
     for src, rids, dst in jobs:
         assert np.array_equal(dst.numpy(), oracle.retrieve(src.numpy(), rids.numpy().view(np.uint32)))
+    # more streams than the library caches buffers for (least recently used go)
+    many = [torch.cuda.Stream() for _ in range(11)]
+    jobs = []
+    for i, st in enumerate(many * 2):
+        src = torch.from_numpy(rng.integers(0, 256, (2000 + i, 16), dtype=np.uint8)).pin_memory()
+        rids = torch.from_numpy(rng.integers(0, 2000, 3000).astype(np.int32)).pin_memory()
+        dst = torch.empty((3000, 16), dtype=torch.uint8).pin_memory()
+        dpg.dpg_retrieve_host(src, rids, dst, stream=st, synchronize=False)
+        jobs.append((src, rids, dst))
+    torch.cuda.synchronize()
+    for src, rids, dst in jobs:
+        assert np.array_equal(dst.numpy(), oracle.retrieve(src.numpy(), rids.numpy().view(np.uint32)))
     dpg.dpg_release_cache()
 
 
