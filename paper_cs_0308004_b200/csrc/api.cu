@@ -167,9 +167,11 @@ bool plan_fused(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   const uint32_t pos_bits = bit_length(n_out - 1);
   const bool force8 = opt && opt->pair_bytes == 8;
   // Gather mode: rows that are whole 32-byte sectors go straight to dst;
-  // rows that straddle sectors may go through INTERNAL (a scattered
-  // partial-sector write costs a DRAM read-modify-write on this HBM).
-  uint32_t gather = 1;
+  // rows that straddle sectors go through INTERNAL and a Phase III gather (a
+  // scattered partial-sector write costs a DRAM read-modify-write on this
+  // HBM): 16 Mi x 48 B 1.04 ms (path 2 took 1.69), 100 B 2.07 vs
+  // 2.13 ms, 64 B stays direct-to-dst (0.92 vs 1.58 ms; profiles/r02_gather_mode.md)
+  uint32_t gather = rec % 32 == 0 ? 1 : 2;
   if (opt && opt->gather) gather = opt->gather;
   auto fits = [&](uint32_t s, dpg_plan_t* q) -> bool {
     const uint64_t L = 1ull << s;
@@ -999,7 +1001,21 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
     for (uint32_t q = 0; q < sg.n; ++q) al4 = al4 && ((uintptr_t)sg.out[q] % 4 == 0);
     const bool agr_ok = rec % 4 == 0 && rec >= 8 && rec <= 116 && al4 && (uintptr_t)src % 4 == 0;
     if (p.path == 1 && pay == 0) {
-      p.gather = 1;
+      if (p.gather != 1) {
+        // the fused probe writes segment rows only in its direct-to-dst mode
+        dpg_options_t o;
+        if (opt) o = *opt; else std::memset(&o, 0, sizeof(o));
+        o.path = 1;
+        o.gather = 1;
+        dpg_plan_t q;
+        if (make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK) {
+          p = q;
+        } else {
+          o.path = 2;
+          o.gather = 0;
+          if (make_plan(rec, n_src, n_out, 0, &o, sm, &p) != DPG_OK) return DPG_ERR_UNSUPPORTED;
+        }
+      }
     } else if (p.path == 2 && pay == 0) {
     } else if (p.path == 5 && agr_ok) {
     } else if (agr_ok && n_src * rec <= ((uint64_t)1 << 32)) {
@@ -1011,10 +1027,8 @@ dpg_status_t run_dpg(const void* src, uint64_t rec, uint64_t n_src, const uint32
                  // the shared-memory runs, which write rows anywhere: fused, else multi-kernel
                  dpg_options_t o{};
                  o.path = 1;
-                 if (make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK) {
-                   q.gather = 1;
-                   return true;
-                 }
+                 o.gather = 1;
+                 if (make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK) return true;
                  o.path = 2;
                  return make_plan(rec, n_src, n_out, 0, &o, sm, &q) == DPG_OK;
                }()) {

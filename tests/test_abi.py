@@ -138,6 +138,8 @@ def test_plan_l2_run_rule(dpg, rec, n, auto_path):
 
 def test_plan_pair_packing_and_overrides(dpg):
     c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20, path=1)
+    assert c2["gather"] == 2 and c2["pair_bytes"] == 2                # rows straddle sectors
+    c2 = dpg.dpg_plan(100, 1 << 20, 1 << 20, path=1, gather=1)
     assert c2["gather"] == 1 and c2["pair_bytes"] == 4                # 9 + 20 bits packed
     assert c2["slot_pairs"] == 672                                    # CAP = L + L/4 + 32
     assert dpg.dpg_plan(100, 1 << 20, 1 << 20, gather=2)["pair_bytes"] == 2   # u16 locals
