@@ -205,3 +205,14 @@ def test_library_has_no_undefined_internal_symbols(dpg):
     out = subprocess.check_output(["nm", "-D", "--undefined-only", dpg.LIB_PATH], text=True)
     missing = [line.split()[-1] for line in out.splitlines() if "_ZN3dpg" in line]
     assert not missing, missing
+
+
+def test_host_entries_validate_before_cuda(dpg):
+    lib = dpg.raw_lib()
+    p = ctypes.c_void_p(0x10000)
+    for fn in (lib.dpg_retrieve_host, lib.dpg_retrieve_host_async):
+        assert fn(p, 0, 10, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG      # rec == 0
+        assert fn(p, 8, 10, p, 0, p, None) == dpg.DPG_OK                    # nothing to do
+        assert fn(None, 8, 10, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG
+        assert fn(p, 8, 0, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG       # n_src == 0
+        assert fn(p, 1 << 40, 1 << 30, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG   # overflow
