@@ -2189,7 +2189,7 @@ dpg_status_t dpg_retrieve_host(const void* src_host, size_t rec_bytes, uint64_t 
                                dpg_stream_t stream) {
   dpg_status_t s = dpg_retrieve_host_async(src_host, rec_bytes, n_src, rids_host, n_out,
                                            dst_host, stream);
-  if (s != DPG_OK) return s;
+  if (s != DPG_OK || n_out == 0) return s;
   return cuda_status(cudaStreamSynchronize((cudaStream_t)stream));
 }
 
