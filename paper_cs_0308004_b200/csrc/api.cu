@@ -598,8 +598,10 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
   // window gather takes runs faster as K L2-sized runs than as the
   // multi-kernel shared-memory runs (the config-5 owner shard, 2^27 x 100 B:
   // 11.4 vs 14.7 ms per 2^26 rids, profiles/r01_c5_owner_plans.txt)
+  // (not for rows of whole 32-byte sectors, which path 2 writes straight to
+  // their rows: 2^26 x 64 B 3.98 ms vs 6.34 ms, profiles/r02_sweep_final.md)
   if (want_path == 0 && !overrides && pay == 0 && rec % 4 == 0 && rec >= 8 && rec <= 116 &&
-      n_src * rec >= 8 * current_l2_bytes() &&
+      rec % 32 != 0 && n_src * rec >= 8 * current_l2_bytes() &&
       plan_l2k(rec, n_src, n_out, pay, false, 0, sm, current_l2_bytes(), p))
     return DPG_OK;
   std::memset(p, 0, sizeof(*p));
