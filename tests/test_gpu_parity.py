@@ -647,6 +647,19 @@ def test_dpg_sort_prefix_groups_and_fallback(dpg, case):
         assert np.array_equal(host(dpg.dpg_sort_rids(dev(src), off, k2)).view(np.uint32), want)
 
 
+@pytest.mark.parametrize("kb", [5, 6, 7, 8, 9, 11, 12])
+@pytest.mark.parametrize("alpha", [2, 16, 256])
+def test_dpg_sort_key_lengths_and_alphabets(dpg, kb, alpha):
+    """Every key length past the 4-byte prefix, over small and large byte
+    alphabets (few distinct prefixes -> the full sort; many -> the fix-up)."""
+    rng = np.random.default_rng(kb * 1000 + alpha)
+    n = 30_011
+    src = rng.integers(0, alpha, (n, 16), dtype=np.uint8)
+    off = 16 - kb
+    got = host(dpg.dpg_sort_rids(dev(src), off, kb)).view(np.uint32)
+    assert np.array_equal(got, oracle.sort_rids(src, off, kb))
+
+
 def test_dpg_sort_many_tiles(dpg):
     """Chunks of several staging tiles per CTA (n > 148 x 8192)."""
     rng = np.random.default_rng(99)
