@@ -493,6 +493,21 @@ def _compare_chunked(out, want_fn, n, chunk=1 << 20):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("log2n,kind", [(24, "perm"), (23, "repl"), (26, "repl")])
+def test_four_byte_records_full_size(dpg, log2n, kind):
+    """4-byte records at 8 Mi - 64 Mi (the automatic plan is path 6 even when
+    the source fits the L2 budget): every row against the oracle."""
+    n = 1 << log2n
+    src, rids = _case(log2n, n, 4, n, kind)
+    s, r = dev(src), dev(rids)
+    out = dpg.dpg_retrieve(s, r)
+    assert dpg.last_path() == 6
+    torch.cuda.synchronize()
+    _compare_chunked(out, lambda k, e: oracle.retrieve(src, rids[k:e]), n)
+    dpg.dpg_sync_status()
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("variant", ["c3a", "c3b"])
 @pytest.mark.parametrize("rec", datagen.C3_RECS)
 def test_config_3_full_size(dpg, variant, rec):
