@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N=1: only the headline config")
-    ap.add_argument("--extras", default="c2L,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c3a8n26,c3a8n27,"
+    ap.add_argument("--extras", default="c2L,c3a4,c3a8,c3a16,c3a32,c3a64,c3a256,c3b8,c3a4n26,c3a8n26,c3a8n27,"
                                         "c3a16n26,c3a128,c4r256,c4,c4x,c5shard",
                     help="N=1: nested configurations")
     a = ap.parse_args()
