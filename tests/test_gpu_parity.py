@@ -493,6 +493,39 @@ def _compare_chunked(out, want_fn, n, chunk=1 << 20):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("rec,n_src", [(4, 1 << 31), (16, 1 << 28)])
+def test_maximum_rid_lists(dpg, rec, n_src):
+    """More than 2^31 output rows (the 32-bit rid list's range: positions and
+    pair indices past 2^31), on the automatic plan and the direct gather;
+    sampled rows -- the first and last, those around 2^31 and random ones --
+    against the oracle evaluated on the generated source."""
+    n = (1 << 31) + 4099
+    sid = datagen.STREAMS[("c3", "src")]
+    src = torch.empty(n_src * rec, dtype=torch.uint8, device="cuda")
+    datagen.random_bytes_cuda(src, sid)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(rec)
+    rids = torch.randint(0, n_src, (n,), device="cuda", generator=g, dtype=torch.int64)
+    rids = rids.to(torch.int32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(rec)
+    idx = np.unique(np.concatenate([np.arange(1000), np.arange(n - 1000, n),
+                                    np.arange((1 << 31) - 1000, (1 << 31) + 1000),
+                                    rng.integers(0, n, 3000)]))
+    ti = torch.from_numpy(idx).cuda()
+    r_h = rids[ti].cpu().numpy().view(np.uint32)
+    want = oracle.retrieve_generated(rec, n_src, sid, r_h.astype(np.uint64))
+    out = dpg.dpg_retrieve(src.view(n_src, rec), rids)
+    path = dpg.last_path()
+    dpg.dpg_sync_status()
+    assert np.array_equal(out[ti].cpu().numpy(), want), path
+    dpg.dpg_retrieve_direct(src.view(n_src, rec), rids, dst=out)
+    assert np.array_equal(out[ti].cpu().numpy(), want)
+    del out, rids, src
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("log2n,kind", [(24, "perm"), (23, "repl"), (26, "repl")])
 def test_four_byte_records_full_size(dpg, log2n, kind):
     """4-byte records at 8 Mi - 64 Mi (the automatic plan is path 6 even when
