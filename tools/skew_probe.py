@@ -7,6 +7,7 @@ a hot set (90% of the rids on 1% of the records), floor(n_src u^6) ("zipf":
   auto         dpg_retrieve (plan + skew check; path 5 when the sample shows skew)
   p1 / p2      the fused / multi-kernel plan on high-bit runs (path 1 / 2)
   p1g2         path 1 with Fig. 1's INTERNAL file and a Phase III gather (gather=2)
+  p6 / p7      the three sequential passes / two DPG levels
   p2r / p2g    path 2 with Phase I as radix passes / global-atomic counting (hist_mode 3 / 2)
   p5           the K L2 runs (path 5)
   bounds       dpg_retrieve_bounds over runs from dpg_skew_partition (the
@@ -97,7 +98,7 @@ def main():
             line += f"  auto(p{dpg.last_path()}) {t:8.1f}{'' if ok else ' MISMATCH'}"
             variants = [("p1", dict(path=1)), ("p1g2", dict(path=1, gather=2)), ("p2", dict(path=2)),
                         ("p2r", dict(path=2, hist_mode=3)), ("p2g", dict(path=2, hist_mode=2)),
-                        ("p5", dict(path=5))]
+                        ("p5", dict(path=5)), ("p6", dict(path=6)), ("p7", dict(path=7))]
             for name, kw in variants:
                 if name not in args.variants.split(","):
                     continue
