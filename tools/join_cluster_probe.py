@@ -1,9 +1,15 @@
 """Config 4's DPG-Move join on path 6 with each cluster size (0 = the plan's
 choice): time and Phase I / II / III (ms).  python tools/join_cluster_probe.py"""
-import sys, os, time
-sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
-import numpy as np, torch
-import datagen, paper_cs_0308004_b200 as dpg
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen  # noqa: E402
+import paper_cs_0308004_b200 as dpg  # noqa: E402
+
 w = datagen.make("c4")
 fact = torch.from_numpy(w["fact"]).cuda(); fk = torch.from_numpy(w["fk"].view(np.int32)).cuda(); dim = torch.from_numpy(w["dim"]).cuda()
 out = torch.empty((w["fk"].size, 80), dtype=torch.uint8, device="cuda")
