@@ -113,9 +113,13 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t on) {
 
 // One counting-sort pass over key byte a.byte.  LO: the key has a
 // low word (key bytes 8..11); RID: the rid travels in its own array (else it
-// is packed in the low half of the key word, numeric keys <= 4 bytes).
-//   count   the CTA's digit counts, a grid barrier, every CTA derives its
-//           bucket bases (smaller digits first, then earlier CTAs);
+// is packed in the low half of the key word, numeric keys <= 4 bytes).  SRC /
+// SH: path 2's radix Phase I (the first pass reads the rid list; the digit is
+// a shifted byte of the rid); MP: several passes in one launch; RB: the last
+// radix pass also writes the run boundaries.
+//   count   the CTA's digit counts, a grid barrier, the bucket bases by a
+//           column scan per digit and a second barrier (smaller digits first,
+//           then earlier CTAs);
 //   place   the chunk in tiles of 512 KPT: warp w takes the tile's elements
 //           [32 KPT w, 32 KPT (w + 1)) into registers (KPT per lane, index order =
 //           (k, lane)), counts them per digit (warp-private counters), the
