@@ -436,19 +436,21 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   if (cl == 0) {
     // automatic: one CTA per run, or a cluster of 2-4 sharing the run through
     // distributed shared memory while one CTA's runs would leave pieces
-    // (tile, run) of fewer than 4 entries on average -- measured: the remote
+    // (tile, run) of fewer than 3 entries on average -- measured: the remote
     // lookups cost more than the shorter pieces save unless the pieces are
     // that short (profiles/r02_seq3_cluster.md)
     const uint64_t T0 = std::min<uint64_t>(32768, (220ull << 10) / (rec + 2));
     cl = 1;
     // (records of <= 16 bytes; a remote lookup of a 32-byte record already
     // costs more than it saves -- DSMEM moves ~20 B per cycle per SM)
-    while (rec <= 16 && cl < 4 && ((T0 * cl) << ls) < 4 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
+    while (rec <= 16 && cl < 4 && ((T0 * cl) << ls) < 3 * n_src && ls + (cl == 2 ? 1u : 0u) < 15)
       cl *= 2;
-    // more runs than Phase I takes (8192), or pieces of under one entry:
-    // larger runs, whatever the record
+    // more runs than Phase I takes (8192), or pieces of under two entries
+    // (one from 32-byte records on): larger runs, whatever the record
+    // (2^26 x 12 / 16 / 24 B: 2143 -> 2021, 1738 -> 1701, 3301 -> 2913 us)
     auto runs = [&](uint32_t c) { return (n_src + ((uint64_t)c << ls) - 1) / ((uint64_t)c << ls); };
-    while (cl < 8 && (runs(cl) > 8192 || runs(cl) * ((n_out + T0 - 1) / T0) > n_out) &&
+    const uint64_t min_piece = rec < 32 ? 2 : 1;
+    while (cl < 8 && (runs(cl) > 8192 || min_piece * runs(cl) * ((n_out + T0 - 1) / T0) > n_out) &&
            ls + bit_length(cl) < 17)
       cl *= 2;
   }
