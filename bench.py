@@ -565,6 +565,7 @@ def run_single(args):
             except Exception as e:  # noqa: BLE001 -- a failed extra is reported, not fatal
                 extras[name] = {"error": repr(e)}
             torch.cuda.empty_cache()
+            dpg.dpg_release_cache()      # each nested configuration starts from an empty pool
 
     line = {
         "metric": METRIC, "value": d["value"], "unit": "GB/s", "n_gpus": 1,
