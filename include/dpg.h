@@ -418,6 +418,21 @@ dpg_status_t dpg_retrieve_dist_loopback(int P, const void *const *src_shards, si
                                         const uint64_t *n_out, void *const *dst,
                                         dpg_stream_t stream);
 
+/* The exchange's arithmetic (host only, no CUDA): for the P x (P + 1) count
+ * matrix C (host, row-major; C[q][o] = rows of rank q whose rids rank o owns,
+ * o < P; C[q][P] = rank q's rows), rank `me`'s plan -- roff[P+1]: where the
+ * requests from each requester q start in me's receive buffer (requester
+ * order); soff[P+1]: where me's requests to each owner start in its own
+ * request list (owner order); win_row[P]: the row of requester q's window at
+ * which me's replies to q start (q's window holds the replies owner by
+ * owner); *n_req: the requests me receives; *cap: the largest rank's rows
+ * (each window's capacity).  dpg_retrieve_dist and
+ * dpg_retrieve_dist_loopback compute exactly this.  P in [1, 64], 0 <= me < P,
+ * else DPG_ERR_INVALID_ARG. */
+dpg_status_t dpg_exchange_plan(const uint64_t *counts, int P, int me, uint64_t *roff,
+                               uint64_t *soff, uint64_t *win_row, uint64_t *n_req,
+                               uint64_t *cap);
+
 /* Receive windows for the fused multi-GPU exchange (one process per GPU on
  * one node).  dpg_ipc_alloc: a device buffer of `bytes` on the current device
  * (library-owned until dpg_ipc_free) and its 64-byte CUDA IPC handle, to be

@@ -46,7 +46,7 @@ EXPORTED = (
     "dpg_retrieve_direct_ex", "dpg_l2_prefetch", "dpg_partition", "dpg_last_path",
     "dpg_phase_times_ex", "dpg_retrieve_dist_loopback", "dpg_fk_join_direct",
     "dpg_skew_partition", "dpg_retrieve_bounds", "dpg_distribute_bounds",
-    "dpg_retrieve_host_async",
+    "dpg_retrieve_host_async", "dpg_exchange_plan",
 )
 
 
@@ -91,6 +91,7 @@ _sigs = {
     "dpg_scatter_rows": [_P, _S, _P, _U, _P, _U, _P],
     "dpg_retrieve_host": [_P, _S, _U, _P, _U, _P, _P],
     "dpg_retrieve_host_async": [_P, _S, _U, _P, _U, _P, _P],
+    "dpg_exchange_plan": [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P],
     "dpg_sync_status": [_P, _P],
     "dpg_retrieve_direct_ex": [_P, _S, _U, _P, _U, _P, _P, _I],
     "dpg_l2_prefetch": [_P, _U, _P],
@@ -401,6 +402,24 @@ def dpg_distribute_bounds(rids, n_src: int, bounds, log2_run: int, stream=None):
                                       ctypes.addressof(K), _stream_ptr(stream)),
            "dpg_distribute_bounds")
     return pairs[:n_out], rs
+
+
+def dpg_exchange_plan(counts, me: int) -> dict:
+    """The multi-GPU exchange's offsets for rank `me` from the P x (P+1) count
+    matrix (host, no GPU): roff, soff (P+1 each), win_row (P), n_req, cap."""
+    import numpy as np
+    C = np.ascontiguousarray(np.asarray(counts), dtype=np.uint64)
+    P = C.shape[0]
+    if C.shape != (P, P + 1):
+        raise ValueError("counts must be P x (P + 1)")
+    roff = np.zeros(P + 1, np.uint64)
+    soff = np.zeros(P + 1, np.uint64)
+    win = np.zeros(P, np.uint64)
+    n_req, cap = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(_lib.dpg_exchange_plan(C.ctypes.data, P, me, roff.ctypes.data, soff.ctypes.data,
+                                  win.ctypes.data, ctypes.addressof(n_req), ctypes.addressof(cap)),
+           "dpg_exchange_plan")
+    return {"roff": roff, "soff": soff, "win_row": win, "n_req": n_req.value, "cap": cap.value}
 
 
 def dpg_partition(rids, n_src_total: int, log2_span: int, parts: int, stream=None):

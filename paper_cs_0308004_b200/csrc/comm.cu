@@ -267,6 +267,24 @@ using namespace dpg;
 
 extern "C" {
 
+dpg_status_t dpg_exchange_plan(const uint64_t* counts, int P, int me, uint64_t* roff,
+                               uint64_t* soff, uint64_t* win_row, uint64_t* n_req,
+                               uint64_t* cap) {
+  if (!counts || !roff || !soff || !win_row || !n_req || !cap || P < 1 || P > 64 || me < 0 ||
+      me >= P)
+    return DPG_ERR_INVALID_ARG;
+  const std::vector<uint64_t> C(counts, counts + (uint64_t)P * (P + 1));
+  const ExchangePlan x = exchange_plan(C, P, me);
+  for (int q = 0; q <= P; ++q) {
+    roff[q] = x.roff[q];
+    soff[q] = x.soff[q];
+  }
+  for (int q = 0; q < P; ++q) win_row[q] = x.win_row[q];
+  *n_req = x.n_req;
+  *cap = x.cap;
+  return DPG_OK;
+}
+
 dpg_status_t dpg_get_unique_id(uint8_t id[128]) {
 #ifdef DPG_NO_NCCL
   (void)id;
