@@ -317,6 +317,9 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
   }
   __syncthreads();
   const uint64_t pol_first = policy_evict_first();
+  // the next run, prefetched into L2 while this one is probed, is kept there
+  // until its bulk copy reads it (evict_first lost ~half of it at 2^26 records)
+  const uint64_t pol_keep = policy_evict_last();
   const uint64_t L = 1ull << a.s;
   const uint64_t Ls = L / CL;                     // records of one CTA's slice
   const uint32_t ls_shift = a.s - (CL == 8 ? 3 : CL == 4 ? 2 : CL == 2 ? 1 : 0);
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
         const uint64_t rn = ((uint64_t)bn << a.s) + cr * Ls;
         const uint32_t nb = rn < a.n_src ? (uint32_t)(min_u64(Ls, a.n_src - rn) * rec) & ~15u : 0u;
         for (uint32_t off = 0; off < nb; off += 32768)
-          bulk_prefetch_l2(a.src + rn * rec + off, min(32768u, nb - off), pol_first);
+          bulk_prefetch_l2(a.src + rn * rec + off, min(32768u, nb - off), pol_keep);
       }
     }
     for (uint32_t t = bulk + tid; t < bytes; t += blockDim.x) stage[t] = gsrc[t];   // < 16 B
