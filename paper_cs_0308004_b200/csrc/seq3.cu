@@ -423,7 +423,9 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
             if (a.dbg & 0x20000) {
               if (l[u] == 0xFFFFFFFFu) reinterpret_cast<W*>(a.internal)[0] = v;
             } else {
-              reinterpret_cast<W*>(a.internal + (uint64_t)sl[u] * rec)[w] = v;
+              // (streaming store: INTERNAL is read back only after the whole
+              // Phase II, so it need not displace the staged runs' lines)
+              __stcs(reinterpret_cast<W*>(a.internal + (uint64_t)sl[u] * rec) + w, v);
             }
           }
         }
