@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -216,3 +217,25 @@ def test_host_entries_validate_before_cuda(dpg):
         assert fn(None, 8, 10, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG
         assert fn(p, 8, 0, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG       # n_src == 0
         assert fn(p, 1 << 40, 1 << 30, p, 10, p, None) == dpg.DPG_ERR_INVALID_ARG   # overflow
+
+
+def test_fuzz_cases_reach_every_plan(dpg):
+    """The randomised GPU parity cases (test_gpu_fuzz.py) are only worth
+    their run time if every forced plan accepts some of them and the
+    automatic planner picks more than one path: checked here with the host
+    planner."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import test_gpu_fuzz as fz
+    ran = {name: 0 for name, _ in fz.VARIANTS}
+    auto = set()
+    for (_, rec, _, n_src, n_out, _) in fz._cases():
+        for name, o in fz.VARIANTS:
+            try:
+                p = dpg.dpg_plan(rec, n_src, n_out, **fz._opts(name, o, n_src))
+            except dpg.DPGError:
+                continue
+            ran[name] += 1
+            if name == "auto":
+                auto.add(p["path"])
+    assert min(ran.values()) >= 10, ran
+    assert {1, 3, 6} <= auto, auto
