@@ -207,3 +207,84 @@ def test_fk_join_fuzz(dpg, k, fb, rec, n_dim, n_fact, with_bad):
             continue
         assert np.array_equal(got[ok], want), name
         assert (got[~ok] == CANARY).all(), name
+
+
+@pytest.mark.parametrize("k,rec,kind,n_src,n_out,n_bad", _cases()[:48:3])
+def test_bounds_segments_host_fuzz(dpg, k, rec, kind, n_src, n_out, n_bad):
+    """The other retrieval entry points on the same random problems: DPG over
+    random run boundaries (dpg_retrieve_bounds, section 2.3), the output split
+    into random segments at odd byte offsets (dpg_retrieve_segments), and the
+    host-buffer entry (dpg_retrieve_host)."""
+    src, rids, bad = _problem(k, rec, kind, n_src, n_out, n_bad)
+    ok = np.ones(n_out, bool)
+    ok[bad] = False
+    want = np.full((n_out, rec), CANARY, np.uint8)
+    want[ok] = oracle.retrieve(src, rids[ok])
+    rng = np.random.default_rng(9000 + k)
+    s, r = dev(src), dev(rids)
+
+    def settle():
+        if bad.size:
+            with pytest.raises(dpg.DPGError) as e:
+                dpg.dpg_sync_status()
+            assert e.value.index == int(bad.min())
+        else:
+            dpg.dpg_sync_status()
+
+    # random run boundaries: strictly increasing cuts inside (0, n_src)
+    nb = int(rng.integers(1, min(64, n_src) + 1))
+    cuts = np.unique(rng.integers(1, n_src, nb - 1)) if n_src > 1 else np.zeros(0, np.int64)
+    bounds = np.concatenate([[0], cuts, [n_src]]).astype(np.uint32)
+    d = torch.full((n_out, rec), CANARY, dtype=torch.uint8, device="cuda")
+    try:
+        dpg.dpg_retrieve_bounds(s, r, bounds, dst=d)
+    except dpg.DPGError as e:
+        assert e.status == dpg.DPG_ERR_UNSUPPORTED, e     # a run too large for shared memory
+    else:
+        settle()
+        assert np.array_equal(d.cpu().numpy(), want), "bounds"
+    # random segments (some empty), each at a byte offset of 0..3
+    nseg = int(rng.integers(1, 6))
+    sizes = np.diff(np.sort(np.concatenate([[0, n_out], rng.integers(0, n_out + 1, nseg - 1)])))
+    shifts = rng.integers(0, 4, nseg)
+    bufs = [torch.full((int(n) * rec + 8,), CANARY, dtype=torch.uint8, device="cuda")
+            for n in sizes]
+    dpg.dpg_retrieve_segments(s, r, [int(n) for n in sizes],
+                              [b.data_ptr() + int(o) for b, o in zip(bufs, shifts)])
+    settle()
+    row = 0
+    for n, b, o in zip(sizes, bufs, shifts):
+        h = b.cpu().numpy()
+        assert (h[:o] == CANARY).all() and (h[o + n * rec:] == CANARY).all(), "segment bounds"
+        assert np.array_equal(h[o:o + n * rec].reshape(n, rec), want[row:row + n]), "segments"
+        row += n
+    # host buffers in and out
+    hs = torch.from_numpy(src).pin_memory()
+    hr = torch.from_numpy(rids.view(np.int32)).pin_memory()
+    hd = torch.full((n_out, rec), CANARY, dtype=torch.uint8).pin_memory()
+    dpg.dpg_retrieve_host(hs, hr, hd)
+    settle()
+    if not bad.size:                      # (a bad rid's row in a host dst is unspecified)
+        assert np.array_equal(hd.numpy(), want), "host"
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_sort_fuzz(dpg, k):
+    """dpg_sort / dpg_sort_rids on random record sizes, key offsets and
+    lengths, with key alphabets from all-equal to full bytes (ties resolved
+    by rid: the stable order)."""
+    rng = np.random.default_rng(7000 + k)
+    rec = int(rng.integers(1, 130))
+    kb = int(rng.integers(1, min(rec, 12) + 1))
+    off = int(rng.integers(0, rec - kb + 1))
+    n = int(np.exp(rng.uniform(0, np.log(1 << 21))))
+    alpha = [1, 2, 4, 26, 256][k % 5]
+    src = rng.integers(0, 256, (n, rec), dtype=np.uint8)
+    src[:, off:off + kb] = rng.integers(0, alpha, (n, kb), dtype=np.uint8)
+    want = oracle.sort_rids(src, off, kb)
+    got = dpg.dpg_sort_rids(dev(src), off, kb)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), want)
+    out = dpg.dpg_sort(dev(src), off, kb)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.sort(src, off, kb))
