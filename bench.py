@@ -516,6 +516,18 @@ def run_single(args):
         sort_res = {"ms_per_sort": med(tot), "records_per_s": n_out / (med(tot) * 1e-3),
                     "launches_per_sort": nl / max(3, args.steps // 2), "parity_sampled_ok": srt_ok,
                     "what": "dpg_sort: 10-byte keys at offset 0, stable radix passes on the 4-byte prefix + fix-up of equal-prefix groups (full LSD sort if a group exceeds 32) + dpg_retrieve"}
+        # the paper's comparison: the same phases 1-2, phase 3 by
+        # the direct gather ("standard" key-pointer sort)
+        srids = torch.empty(n_out, dtype=torch.int32, device="cuda")
+
+        def naive_sort():
+            dpg.dpg_sort_rids(src, 0, 10, rids=srids)
+            dpg.dpg_retrieve_direct(src, srids, dst=out)
+        naive_sort()
+        torch.cuda.synchronize()
+        ntot, _, _, _, _ = steps_obj.run(naive_sort, max(3, args.steps // 2))
+        sort_res["naive_phase3_ms_per_sort"] = med(ntot)
+        sort_res["dpg_over_naive"] = med(ntot) / med(tot)
 
     # end to end through the host-buffer C-ABI entries (PCIe copies inside):
     # the asynchronous entry on two streams in turn, so one step's device->host
