@@ -6,6 +6,8 @@
 
 #include "../../include/dpg.h"
 
+#include <utility>
+
 namespace dpg {
 
 __host__ __device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -130,6 +132,21 @@ __device__ __forceinline__ void grid_barrier_mono(uint32_t* w, uint32_t G) {
     }
   }
   __syncthreads();
+}
+
+// Programmatic dependent launch (PDL) between the kernels of one plan: a
+// kernel launched by launch_pdl may be scheduled while its stream predecessor
+// is still finishing (its CTAs take SMs as the predecessor's CTAs exit, which
+// hides the launch gap, ~2-4 us per kernel boundary); it calls pdl_wait()
+// before it touches anything earlier kernels wrote (griddepcontrol.wait
+// returns once the predecessor grid has completed and its writes are
+// visible; a no-op for an ordinary launch).  pdl_trigger() lets the
+// dependent grid be scheduled before this one ends.  Dependents are only
+// scheduled once every CTA of this grid has triggered or exited, so a grid's
+// own CTAs are all resident first.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -957,5 +974,34 @@ __device__ __forceinline__ void agr_pipeline(uint32_t nt, F group, S split, uint
     slot = slot == 2 ? 0 : slot + 1;
   }
   cp_async_wait<0>();
+}
+
+// Launch `k` with programmatic stream serialisation (PDL, see pdl_wait) when
+// `pdl`, on clusters of `cluster` CTAs when > 1.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, uint32_t smem,
+                              cudaStream_t st, bool pdl, uint32_t cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 }  // namespace dpg

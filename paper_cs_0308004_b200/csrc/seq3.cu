@@ -52,6 +52,12 @@ static constexpr uint16_t kNoSlot = 0xFFFF;
 
 // ---- Phase I: distribute each tile into its runs ----------------------------
 static constexpr int k3DistThreads = 512;
+// the plan's kernels after the first are launched with PDL (pdl_wait), no
+// early trigger: each starts as its predecessor's CTAs exit, hiding the launch
+// gap (path 6, 4 launches: -5 to -9 us per call; triggering at kernel start
+// was slower, up to +100 us at 32-byte records: profiles/r02_pdl.md).  The
+// tuning flag 0x100000 launches them plainly (A/B)
+static bool seq3_pdl(const Seq3Args& a) { return !(a.dbg & 0x100000u); }
 
 uint32_t seq3_dist_smem(uint32_t T, uint32_t K) {
   return (uint32_t)(256 + (uint64_t)T * 4 + (((uint64_t)T * 2 + 15) & ~15ull) +
@@ -229,6 +235,7 @@ __global__ void k3_transpose(const uint16_t* __restrict__ in, uint16_t* __restri
                              uint32_t rows, uint32_t cols) {
   __shared__ uint16_t tile[32][33];
   const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  pdl_wait();
   for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
     const uint32_t r = r0 + y, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[y][threadIdx.x] = in[(uint64_t)r * cols + c];
@@ -249,8 +256,10 @@ cudaError_t launch_seq3_distribute(const Seq3Args& a, uint32_t grid, cudaStream_
   kern<<<grid, k3DistThreads, smem, st>>>(a);
   ++*nl;
   dim3 tg((a.K + 1 + 31) / 32, (a.nsub + 31) / 32);
-  k3_transpose<<<tg, dim3(32, 8), 0, st>>>(a.pre, a.preT, a.nsub, a.K + 1);
+  e = launch_pdl(k3_transpose, tg, dim3(32, 8), 0, st, seq3_pdl(a), 1, a.pre, a.preT, a.nsub,
+                 a.K + 1);
   ++*nl;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -306,6 +315,7 @@ __global__ void __launch_bounds__(k3ProbeThreads, 1) k3_probe(Seq3Args a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   uint32_t* reg = reinterpret_cast<uint32_t*>(smp + 256) + warp * k3Reg;
   uint8_t* stage = smp + 256 + (k3ProbeThreads / 32) * k3Reg * 4;
+  pdl_wait();
   const uint32_t cr = CL > 1 ? cluster_ctarank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const uint8_t* sbase[CL];
@@ -447,10 +457,9 @@ static cudaError_t launch_probe_wc(const Seq3Args& a, uint32_t grid, uint32_t sm
   cudaError_t e = cudaFuncSetAttribute(k3_probe<WB, M, CL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (CL == 1) {
-    k3_probe<WB, M, 1><<<grid, k3ProbeThreads, smem, st>>>(a);
-    return cudaSuccess;
-  }
+  if (CL == 1)
+    return launch_pdl(k3_probe<WB, M, 1>, dim3(grid), dim3(k3ProbeThreads), smem, st,
+                      seq3_pdl(a), 1, a);
   // clusters of CL CTAs, as many as can be resident at once
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -472,8 +481,8 @@ static cudaError_t launch_probe_wc(const Seq3Args& a, uint32_t grid, uint32_t sm
   }
   const uint32_t runs = a.K;
   const uint32_t ncl = (uint32_t)std::max(1, std::min<int>(nclusters, (int)std::max(1u, runs)));
-  cfg.gridDim = dim3(ncl * CL);
-  return cudaLaunchKernelEx(&cfg, k3_probe<WB, M, CL>, a);
+  return launch_pdl(k3_probe<WB, M, CL>, dim3(ncl * CL), dim3(k3ProbeThreads), smem, st,
+                    seq3_pdl(a), CL, a);
 }
 
 template <int WB, int M>
@@ -542,6 +551,7 @@ __global__ void __launch_bounds__(k3GatherThreads, 1)
     for (uint32_t k = 0; k < nbuf; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
   }
+  pdl_wait();
   __syncthreads();
   const uint64_t pol_first = policy_evict_first();
   auto issue = [&](uint32_t t, uint32_t k) {
@@ -613,7 +623,9 @@ cudaError_t launch_seq3_gather(const Seq3Args& a, uint32_t W, uint32_t grid, uin
   case WB:                                                                                    \
     e = cudaFuncSetAttribute(k3_gather<WB>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                              (int)smem);                                                      \
-    if (e == cudaSuccess) k3_gather<WB><<<grid, k3GatherThreads, smem, st>>>(a, fr, mp, nbuf); \
+    if (e == cudaSuccess)                                                                     \
+      e = launch_pdl(k3_gather<WB>, dim3(grid), dim3(k3GatherThreads), smem, st, seq3_pdl(a),  \
+                     1, a, fr, mp, nbuf);                                                      \
     break;
   switch (W) {
     DPG_SEQ3_GATHER(4)
