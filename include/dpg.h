@@ -535,9 +535,12 @@ void dpg_phase_timing(int enable);
  * it off. */
 void dpg_debug_phase_stamps(void *device_buf);
 
-/* Tuning experiments only: code-generation variants of the fused kernel that
- * do not change any result (store cache policies, reservation order).  0 is
- * the default and what every other caller gets. */
+/* Tuning experiments only (tools/): code-generation and launch variants (store
+ * cache policies, reservation order, ring geometry, bit 18: plain launches
+ * instead of programmatic dependent launch between a plan's kernels) and, for
+ * timing experiments, bits that skip work and so change the result (bits 20
+ * and 21 of the window gather).  0 is the default and what every other caller
+ * gets. */
 void dpg_debug_flags(uint32_t flags);
 dpg_status_t dpg_phase_times(double *distribute_ms, double *probe_gather_ms, uint32_t *calls);
 /* Same record split by phase: Phase I (distribute), Phase II (probe) and

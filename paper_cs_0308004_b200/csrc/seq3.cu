@@ -56,8 +56,8 @@ static constexpr int k3DistThreads = 512;
 // early trigger: each starts as its predecessor's CTAs exit, hiding the launch
 // gap (path 6, 4 launches: -5 to -9 us per call; triggering at kernel start
 // was slower, up to +100 us at 32-byte records: profiles/r02_pdl.md).  The
-// tuning flag 0x100000 launches them plainly (A/B)
-static bool seq3_pdl(const Seq3Args& a) { return !(a.dbg & 0x100000u); }
+// tuning flag 0x40000 launches them plainly (A/B)
+static bool seq3_pdl(const Seq3Args& a) { return !(a.dbg & 0x40000u); }
 
 uint32_t seq3_dist_smem(uint32_t T, uint32_t K) {
   return (uint32_t)(256 + (uint64_t)T * 4 + (((uint64_t)T * 2 + 15) & ~15ull) +

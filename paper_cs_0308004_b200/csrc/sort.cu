@@ -31,6 +31,7 @@ __global__ void k_sort_extract(const uint8_t* __restrict__ src, uint32_t rec, ui
                                uint32_t* __restrict__ klo, uint32_t* __restrict__ rid,
                                const uint32_t* __restrict__ keys_u32, uint64_t key_limit,
                                unsigned long long* status, const uint32_t* cond = nullptr) {
+  pdl_wait();                                                 // (launched with PDL: launch_pdl)
   if (cond && *(volatile const uint32_t*)cond == 0) return;   // (the fallback, not needed)
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -132,6 +133,7 @@ template <bool LO, bool RID, bool SRC, int KPT = kSKpt, int MINB = 1, bool SH = 
           bool RB = false>
 __global__ void __launch_bounds__(kSThreads, MINB) k_sort_pass(SortPassArgs a0) {
   constexpr uint32_t kTile = kSThreads * KPT;
+  pdl_wait();                                                        // (sort_coop_launch)
   if (a0.cond && *(volatile const uint32_t*)a0.cond == 0) return;   // every CTA alike
   extern __shared__ __align__(16) uint8_t sdyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sdyn);                // [kTile]
@@ -420,6 +422,7 @@ constexpr uint32_t kFixMax = 32;
 __global__ void k_sort_fixup(const uint64_t* __restrict__ khi, const uint32_t* __restrict__ klo,
                              const uint32_t* __restrict__ rid, uint64_t n, bool lo_w,
                              uint32_t* __restrict__ rids_out, uint32_t* __restrict__ overflow) {
+  pdl_wait();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t kj = khi[j];
@@ -472,6 +475,34 @@ static cudaError_t set_pass_smem() {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) set_dev = dev;
   return e;
+}
+
+extern uint32_t g_debug_flags;
+
+// A sort pass: a cooperative launch (grid barriers), with PDL after the
+// previous kernel of the sort (pdl_wait) unless the tuning flag 0x40000 asks
+// for plain launches (A/B: profiles/r02_pdl.md)
+static bool sort_pdl() { return !(g_debug_flags & 0x40000u); }
+static cudaError_t sort_coop_launch(const void* fn, int grid, void** params, uint32_t dyn,
+                                    cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  unsigned na = 0;
+  at[na].id = cudaLaunchAttributeCooperative;
+  at[na].val.cooperative = 1;
+  ++na;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelExC(&cfg, fn, params);
 }
 
 cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint32_t key_off,
@@ -537,8 +568,7 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
       sa.npasses = one_launch ? hi_byte - lo_byte : 1;
       void* params[] = {&sa};
       ++*nl;
-      e = cudaLaunchCooperativeKernel(one_launch ? fn_mp : fn, dim3(grid), dim3(kSThreads), params,
-                                      dyn, st);
+      e = sort_coop_launch(one_launch ? fn_mp : fn, grid, params, dyn, st, sort_pdl());
       if (one_launch) break;
     }
   };
@@ -549,24 +579,29 @@ cudaError_t launch_sort_rids(const uint8_t* src, uint32_t rec, uint64_t n, uint3
   // always, each returning at once unless the fixup set the flag).
   if (!packed && key_bytes > 4 && e == cudaSuccess) {
     uint32_t* rid_p[2] = {rid0, rids_out};          // 4 passes: the result in rid0
-    ++*nl;
-    k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid_p[0],
-                                      nullptr, 0, status);
-    e = cudaGetLastError();
+    // (the flag is cleared first, so that the kernels follow one another:
+    // PDL links kernel to kernel)
     if (e == cudaSuccess) e = cudaMemsetAsync(overflow, 0, 4, st);
+    ++*nl;
+    if (e == cudaSuccess) {
+      k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid_p[0],
+                                        nullptr, 0, status);
+      e = cudaGetLastError();
+    }
     run_passes(0, 4, rid_p, nullptr, false);
     if (e == cudaSuccess) {
       ++*nl;
-      k_sort_fixup<<<g, 256, 0, st>>>(khi[0], klo[0], rid_p[0], n, lo_w, rids_out, overflow);
-      e = cudaGetLastError();
+      e = launch_pdl(k_sort_fixup, dim3(g), dim3(256), 0, st, sort_pdl(), 1,
+                     (const uint64_t*)khi[0], (const uint32_t*)klo[0], (const uint32_t*)rid_p[0],
+                     n, lo_w, rids_out, overflow);
     }
     uint32_t* rid_f[2] = {rid0, rids_out};
     if (key_bytes % 2 == 0) std::swap(rid_f[0], rid_f[1]);   // the last pass lands in rids_out
     if (e == cudaSuccess) {
       ++*nl;
-      k_sort_extract<<<g, 256, 0, st>>>(src, rec, n, key_off, key_bytes, khi[0], klo[0], rid_f[0],
-                                        nullptr, 0, status, overflow);
-      e = cudaGetLastError();
+      e = launch_pdl(k_sort_extract, dim3(g), dim3(256), 0, st, sort_pdl(), 1, src, rec, n,
+                     key_off, key_bytes, khi[0], klo[0], rid_f[0], (const uint32_t*)nullptr,
+                     (uint64_t)0, status, (const uint32_t*)overflow);
     }
     run_passes(0, key_bytes, rid_f, overflow, true);
     if (e == cudaSuccess && keys_out) {

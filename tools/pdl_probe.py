@@ -1,6 +1,6 @@
 """A/B of programmatic dependent launch between a plan's kernels: the same
 retrieval timed (L2 flushed before each step, CUDA events, no phase events)
-with PDL (default) and with the tuning flag 0x100000 (plain launches),
+with PDL (default) and with the tuning flag 0x40000 (plain launches),
 interleaved.  python tools/pdl_probe.py [--cases c3a4,c3a8,...]"""
 import argparse
 import ctypes
@@ -40,7 +40,7 @@ for name in a.cases.split(","):
     rids = torch.randperm(n, device="cuda", generator=g).to(torch.int32)
     out = torch.empty_like(src)
     want = dpg.dpg_retrieve_direct(src, rids)
-    FL = [0, 0x100000]
+    FL = [0, 0x40000]
     res = {f: [] for f in FL}
     for rep in range(3):
         for flag in FL:
