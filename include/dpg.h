@@ -17,8 +17,9 @@
  * run, staged into the L2 by TMA bulk copies and probed in output order
  * (path 3); larger sources are cut into shared-memory runs whose probe
  * writes each record straight to its destination (paths 1/2; path 2 also
- * after a skew sample), into K L2-sized runs with an INTERNAL file (path 5,
- * very large sources), or -- small records -- into three sequential passes
+ * after a skew sample), into K L2-sized runs with an INTERNAL file (path 5:
+ * records in 4-byte words of 36..116 bytes, and very large sources), or --
+ * small records -- into three sequential passes
  * (path 6).  dpg_plan_t.path below lists the plans.
  *
  * Conventions (all entry points):

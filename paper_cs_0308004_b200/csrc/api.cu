@@ -599,6 +599,15 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
       return DPG_OK;
     if (want_path == 5) return DPG_ERR_UNSUPPORTED;
   }
+  // Beyond the L2, records of 36..116 bytes in 4-byte words (a multiple of
+  // 4, not of 8) run faster as K L2 runs than as the fused shared-memory runs
+  // (2^24 x 100 B: 1889 vs 2093 us, 2^24 x 36 B: 921 vs 1117, 2^22 x 52 B:
+  // 271 vs 338); with 8- or 16-byte words the fused kernel stays ahead
+  // (2^24 x 72 B: 1549 vs 2026 us; profiles/r02_l2k_vs_fused.md)
+  if (want_path == 0 && !overrides && pay == 0 && rec % 8 == 4 && rec >= 36 && rec <= 116 &&
+      n_out >= n_src / 2 &&
+      plan_l2k(rec, n_src, n_out, pay, false, 0, sm, current_l2_bytes(), p))
+    return DPG_OK;
   if (want_path != 2 && !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
       plan_fused(rec, n_src, n_out, pay, opt, sm, p))
     return DPG_OK;
