@@ -608,7 +608,14 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
       n_out >= n_src / 2 &&
       plan_l2k(rec, n_src, n_out, pay, false, 0, sm, current_l2_bytes(), p))
     return DPG_OK;
-  if (want_path != 2 && !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
+  // Sources of >= 6 L2s with power-of-two records of >= 128 bytes: the
+  // multi-kernel runs beat the fused kernel (2^23 x 128 B: 653 vs 741 us,
+  // 2^22 x 256 B: 492 vs 644; at half those sources the fused kernel is
+  // ahead: 312 vs 351, 245 vs 271; profiles/r02_l2k_vs_fused.md)
+  const bool big_pow2 = want_path == 0 && !overrides && pay == 0 && rec >= 128 &&
+                        (rec & (rec - 1)) == 0 && n_src * rec >= 6 * current_l2_bytes();
+  if (want_path != 2 && !big_pow2 &&
+      !(opt && (opt->grid_distribute || opt->grid_probe || opt->hist_mode)) &&
       plan_fused(rec, n_src, n_out, pay, opt, sm, p))
     return DPG_OK;
   if (want_path == 1) return DPG_ERR_UNSUPPORTED;

@@ -28,7 +28,7 @@ for sh in a.shapes.split(","):
     want = dpg.dpg_retrieve_direct(src, rids)
     line = [f"2^{lg} x {rec} B ({n * rec / 2**30:.2f} GiB):"]
     for name, kw in (("auto", {}), ("p1", {"path": 1, "gather": 2}), ("p5", {"path": 5}),
-                     ("direct", None)):
+                     ("p2", {"path": 2}), ("p6", {"path": 6}), ("direct", None)):
         fn = (lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)) if kw is None else \
             (lambda kw=kw: dpg.dpg_retrieve(src, rids, dst=out, **kw))
         try:
