@@ -562,11 +562,14 @@ dpg_status_t make_plan(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pa
     if (plan_l2pair(rec, n_src, n_out, pay, true, sm, current_l2_bytes(), p)) return DPG_OK;
     return DPG_ERR_UNSUPPORTED;
   }
-  // Records of <= 8 bytes in lists of >= 8 Mi rids take the three sequential
-  // passes even when the source fits the L2 budget: the one staged L2 run
-  // re-reads lines it could not keep (16 Mi x 4 B: path 6 166 us, path 3 273,
-  // the direct gather 192; 8 Mi x 8 B: 110 / 150 / 85; profiles/r02_sweep_final.md)
-  if (want_path == 0 && !overrides && rec <= 8 && n_out >= (8ull << 20) &&
+  // Records of <= 8 bytes in lists of >= 4 Mi rids (>= 2 Mi for 5..8-byte
+  // records) take the three sequential passes even when the source fits the
+  // L2 budget: the one staged L2 run re-reads lines it could not keep (16 Mi
+  // x 4 B: path 6 166 us, path 3 273, the direct gather 192; 8 Mi x 8 B: 110 /
+  // 150 / 85; profiles/r02_sweep_final.md; 4 Mi x 4 B: 49 / 68 / 52, 2 Mi x
+  // 8 B: 36 / 41 / 23, but 2 Mi x 4 B: 47 / 39 / 30, 1 Mi x 8 B: 32 / 25 / 14,
+  // profiles/r02_l2k_vs_fused.md)
+  if (want_path == 0 && !overrides && rec <= 8 && n_out >= ((rec > 4 ? 2ull : 4ull) << 20) &&
       plan_seq3(rec, n_src, n_out, pay, opt, sm, p))
     return DPG_OK;
   if (want_path == 3 || (want_path == 0 && !overrides)) {

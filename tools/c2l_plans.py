@@ -14,6 +14,7 @@ import paper_cs_0308004_b200 as dpg  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--shapes", default="23:100,24:100,25:100,24:72,25:48,24:116,26:36,24:52")
+ap.add_argument("--variants", default="auto,p1,p5,p2,p6,p3,direct")
 a = ap.parse_args()
 fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
@@ -27,8 +28,10 @@ for sh in a.shapes.split(","):
     out = torch.empty_like(src)
     want = dpg.dpg_retrieve_direct(src, rids)
     line = [f"2^{lg} x {rec} B ({n * rec / 2**30:.2f} GiB):"]
-    for name, kw in (("auto", {}), ("p1", {"path": 1, "gather": 2}), ("p5", {"path": 5}),
-                     ("p2", {"path": 2}), ("p6", {"path": 6}), ("direct", None)):
+    for name, kw in [v for v in (("auto", {}), ("p1", {"path": 1, "gather": 2}),
+                                 ("p5", {"path": 5}), ("p2", {"path": 2}), ("p6", {"path": 6}),
+                                 ("p3", {"path": 3}), ("direct", None))
+                     if v[0] in a.variants.split(",")]:
         fn = (lambda: dpg.dpg_retrieve_direct(src, rids, dst=out)) if kw is None else \
             (lambda kw=kw: dpg.dpg_retrieve(src, rids, dst=out, **kw))
         try:
