@@ -15,6 +15,8 @@ import paper_cs_0308004_b200 as dpg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--shapes", default="23:100,24:100,25:100,24:72,25:48,24:116,26:36,24:52")
 ap.add_argument("--variants", default="auto,p1,p5,p2,p6,p3,direct")
+ap.add_argument("--fan", type=float, default=1.0,
+                help="n_out = fan * n_src; != 1: rids uniform with replacement")
 a = ap.parse_args()
 fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
@@ -24,8 +26,12 @@ for sh in a.shapes.split(","):
     g = torch.Generator(device="cuda")
     g.manual_seed(0)
     src = torch.randint(0, 256, (n, rec), dtype=torch.uint8, device="cuda", generator=g)
-    rids = torch.randperm(n, device="cuda", generator=g).to(torch.int32)
-    out = torch.empty_like(src)
+    if a.fan == 1.0:
+        rids = torch.randperm(n, device="cuda", generator=g).to(torch.int32)
+    else:
+        rids = torch.randint(0, n, (max(1, int(n * a.fan)),), device="cuda",
+                             generator=g).to(torch.int32)
+    out = torch.empty((rids.numel(), rec), dtype=torch.uint8, device="cuda")
     want = dpg.dpg_retrieve_direct(src, rids)
     line = [f"2^{lg} x {rec} B ({n * rec / 2**30:.2f} GiB):"]
     for name, kw in [v for v in (("auto", {}), ("p1", {"path": 1, "gather": 2}),
