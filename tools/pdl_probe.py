@@ -16,7 +16,8 @@ import paper_cs_0308004_b200 as dpg  # noqa: E402
 CASES = {"c3a4": (1 << 24, 4, {}), "c3a8": (1 << 24, 8, {}), "c3a16": (1 << 24, 16, {}),
          "c3a32": (1 << 24, 32, {}), "n26r8": (1 << 26, 8, {}), "n26r4": (1 << 26, 4, {}),
          "c3a256": (1 << 24, 256, {}), "c3a128": (1 << 24, 128, {}),
-         "c2L": (1 << 24, 100, {})}
+         "c2L": (1 << 24, 100, {}), "c2": (1 << 20, 100, {}), "n23r68": (1 << 23, 68, {}),
+         "n24r36": (1 << 24, 36, {})}
 ap = argparse.ArgumentParser()
 ap.add_argument("--cases", default="c3a4,c3a8,c3a16,c3a32,n26r8,c3a256")
 ap.add_argument("--steps", type=int, default=20)
