@@ -18,6 +18,7 @@ L2 flushed before every rep; CUDA events on the current stream; median.
                                [--kinds exp,hot,zipf,uniform] [--runs 1024,8192] [--sample 32768]
 """
 import argparse
+import ctypes
 import os
 import sys
 
@@ -40,7 +41,12 @@ def main():
     ap.add_argument("--sample", type=int, default=32768)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--variants", default="p2,p5", help="of p1,p2,p2r,p5")
+    ap.add_argument("--dbg", type=lambda x: int(x, 0), default=0, help="dpg_debug_flags (tuning A/B)")
     args = ap.parse_args()
+    lib = dpg.raw_lib()
+    lib.dpg_debug_flags.argtypes = [ctypes.c_uint32]
+    lib.dpg_debug_flags.restype = None
+    lib.dpg_debug_flags(args.dbg)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
