@@ -20,6 +20,7 @@ using namespace dpg;
 namespace dpg {
 
 constexpr uint32_t kSmemLimit = 232448;   // 227 KB dynamic smem per CTA (sm_100)
+constexpr uint64_t kSmemPerSm = 233472;   // 228 KB per SM (each CTA also reserves 1 KB)
 constexpr uint32_t kBarBytes = 128;
 constexpr uint32_t kHistSmemMax = 24576;  // runs whose per-CTA histogram lives in smem
 
@@ -484,6 +485,16 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
     T = tile_for(220ull << 10);
     nbuf = 1;
   }
+  // Phase I occupancy: where one Phase I CTA would fill an SM's shared memory
+  // (4-byte records: T rids + T offsets ~ 117 KB), a tile up to 20 % smaller
+  // lets two CTAs share the SM, one's rid load overlapping the other's counting
+  // (16 Mi x 4 B: Phase I 59 -> 48 us, the call 149 -> 140 us; 2^26 x 4 B:
+  // 643 -> 628 us; profiles/r02_s3_p6dist.md)
+  if (kSmemPerSm / (seq3_dist_smem((uint32_t)T, (uint32_t)K) + 1024) < 2) {
+    uint64_t T2 = T;
+    while (T2 >= 16 && 2 * (seq3_dist_smem((uint32_t)T2, (uint32_t)K) + 1024) > kSmemPerSm) T2 -= 16;
+    if (T2 >= 16 && T2 * 10 >= T * 8) T = T2;
+  }
   if (opt && opt->grid_distribute) T = std::max<uint64_t>(16, std::min<uint64_t>(T, opt->grid_distribute * 16ull));
   if (T < 16) return false;
   const uint64_t nsub = (n_out + T - 1) / T;
@@ -491,7 +502,7 @@ bool plan_seq3(uint64_t rec, uint64_t n_src, uint64_t n_out, uint64_t pay,
   if (!forced && K * nsub > n_out) return false;
   if (nsub * (K + 1) > (1ull << 31)) return false;
   const uint32_t dsm = seq3_dist_smem((uint32_t)T, (uint32_t)K);
-  const uint64_t dctas = std::max<uint64_t>(1, std::min<uint64_t>(4, kSmemLimit / (dsm + 1024)));
+  const uint64_t dctas = std::max<uint64_t>(1, std::min<uint64_t>(4, kSmemPerSm / (dsm + 1024)));
   std::memset(p, 0, sizeof(*p));
   p->path = 6;
   p->log2_run = s;
