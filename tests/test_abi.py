@@ -239,3 +239,22 @@ def test_fuzz_cases_reach_every_plan(dpg):
                 auto.add(p["path"])
     assert min(ran.values()) >= 10, ran
     assert {1, 3, 6} <= auto, auto
+
+
+@pytest.mark.parametrize("rec,n", [(4, 1 << 24), (4, 1 << 26), (8, 1 << 24), (16, 1 << 24), (8, 1 << 26)])
+def test_plan_seq3_phase1_occupancy(dpg, rec, n):
+    """Path 6's tile: Phase III's buffer bounds it; where one Phase I CTA
+    (T rids + T 16-bit offsets + two K+1 count columns, seq3.cu) would fill an
+    SM's 228 KB, the tile shrinks by at most 20 % so that two share it
+    (profiles/r02_s3_p6dist.md)."""
+    p = dpg.dpg_plan(rec, n, n, 0, 148)
+    assert p["path"] == 6
+    T, K = p["tile"], p["num_runs"]
+    assert T % 16 == 0
+    smem = 256 + 4 * T + ((2 * T + 15) & ~15) + 2 * ((K + 1) * 4 + 16)
+    per_sm = 233472 // (smem + 1024)
+    assert per_sm >= 1 and p["grid_distribute"] == min(-(-n // T), min(4, per_sm) * 148)
+    if rec == 4:                                  # 117 KB at the buffer's tile: shrunk to two per SM
+        assert per_sm == 2
+        full = min(32768, (110 << 10) // (rec + 2)) & ~15
+        assert 0.8 * full <= T < full
