@@ -87,6 +87,26 @@ def test_seq3_default_geometry_many_runs(dpg):
     assert np.array_equal(got, oracle.retrieve(src, rids))
 
 
+@pytest.mark.parametrize("n_src,n_out,s,kind", [(300_000, 300_000, 9, "perm"), (1 << 20, 777_777, 11, "repl"),
+                                                 (1 << 24, 1 << 24, 15, "perm")])
+def test_seq3_phase1_shrunk_tile(dpg, n_src, n_out, s, kind):
+    """4-byte records with hundreds of runs: the plan shrinks the tile so that
+    two Phase I CTAs share an SM (profiles/r02_s3_p6dist.md); several tiles,
+    the last one ragged; the last case is config 3's 4-byte permutation."""
+    rec = 4
+    src, rids = _case(n_src + s, n_src, rec, n_out, kind)
+    p = dpg.dpg_plan(rec, n_src, n_out, path=6, log2_run=s)
+    full = min(32768, (110 << 10) // (rec + 2)) & ~15
+    nsub = -(-n_out // p["tile"])
+    assert p["path"] == 6 and 0.8 * full <= p["tile"] < full and p["grid_distribute"] == min(nsub, 296)
+    assert n_out % p["tile"] != 0 and n_out > p["tile"]
+    out = torch.full((n_out, rec), 0xA5, dtype=torch.uint8, device="cuda")
+    dpg.dpg_retrieve(dev(src), dev(rids), dst=out, path=6, log2_run=s)
+    assert dpg.last_path() == 6
+    assert np.array_equal(host(out), oracle.retrieve(src, rids))
+    dpg.dpg_sync_status()
+
+
 def test_seq3_invalid_rids(dpg):
     """rid >= n_src: the row is left unwritten (canary kept), every other row
     is right, and the smallest offending position is reported (reading A6)."""

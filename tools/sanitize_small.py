@@ -31,6 +31,12 @@ for kw in (dict(path=2, hist_mode=3, log2_run=3), dict(path=2, log2_run=4), dict
            dict(path=1, log2_run=5)):
     got = dpg.dpg_retrieve(S, R, **kw).cpu().numpy()
     assert np.array_equal(got, want), kw
+# path 6 with 4-byte records and a tile shrunk for two Phase I CTAs per SM
+s4 = rng.integers(0, 256, (300000, 4), dtype=np.uint8)
+r4 = rng.permutation(300000).astype(np.uint32)
+assert dpg.dpg_plan(4, 300000, 300000, path=6, log2_run=9)["tile"] < 18768
+got = dpg.dpg_retrieve(dev(s4), dev(r4), path=6, log2_run=9).cpu().numpy()
+assert np.array_equal(got, s4[r4])
 b = dpg.dpg_skew_partition(R, n_src, 64, sample_size=4096, seed=3)
 got = dpg.dpg_retrieve_bounds(S, R, b).cpu().numpy()
 assert np.array_equal(got, want)
